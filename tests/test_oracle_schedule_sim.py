@@ -1,0 +1,157 @@
+"""O9 / O10 pins: Fig. 2 prose orderings and SPEC's examples
+(S:292-294), linear-extension validity, simulator hand traces (S:411-413,
+S:421/S:531), exposed = total - compute busy, FIFO non-interference
+(S:309), reorder <= vanilla, and optimum <= greedy on brute-force instances."""
+import numpy as np
+import pytest
+from hypothesis import given, settings, strategies as st
+
+from oracle import schedule as S
+from oracle.brute import contiguous_partitions
+from oracle.planner import BWD, FWD, GREEDY, PER_PARAM, PlanInput, plan
+from oracle.sim import simulate
+
+
+def _idx(seq, ph, op, b):
+    return seq.index((ph, op, b, 1 if op in S.COMM_OPS else 0))
+
+
+def test_fig2_forward_prefetch_before_wait():
+    seq = S.forward_sequence(2, True, S.BEFORE)
+    # "AG34 is reordered in front of Wa12"
+    assert _idx(seq, 0, S.AG, 1) < _idx(seq, 0, S.WAIT_AG, 0)
+    comm = [e for e in seq if e[3] == 1]
+    assert comm == [(0, S.AG, 0, 1), (0, S.AG, 1, 1)]
+
+
+def test_fig2_backward_after_wait_and_wr_before_next_rs():
+    seq = S.backward_sequence(3, True, S.AFTER)
+    # "AG34 is placed after Wa12" (and its copy-out, G33)
+    assert _idx(seq, 1, S.UNPACK, 0) < _idx(seq, 1, S.AG, 1)
+    # "The Wr12 is placed before RS34"
+    for b in range(2):
+        assert _idx(seq, 1, S.WAIT_RS, b) < _idx(seq, 1, S.RS, b + 1)
+    # RS(b) issued before the next bucket's AG-wait: it overlaps later compute
+    assert _idx(seq, 1, S.RS, 0) < _idx(seq, 1, S.WAIT_AG, 1)
+
+
+def test_single_bucket_reorder_equals_vanilla_forward():
+    assert S.forward_sequence(1, True) == S.forward_sequence(1, False)
+
+
+@given(kf=st.integers(0, 12), kb=st.integers(0, 12), reorder=st.booleans(),
+       fp=st.sampled_from([S.BEFORE, S.AFTER]), bp=st.sampled_from([S.BEFORE, S.AFTER]))
+@settings(max_examples=300, deadline=None)
+def test_sequences_are_linear_extensions(kf, kb, reorder, fp, bp):
+    seq = S.step_sequence(kf, kb, reorder, fp, bp)
+    assert S.dependencies_respected(seq)
+    assert sum(1 for e in seq if e[1] == S.AG) == kf + kb       # alpha count = buckets
+    assert sum(1 for e in seq if e[1] == S.RS) == kb
+    assert all((e[3] == 1) == (e[1] in S.COMM_OPS) for e in seq)
+    if reorder:
+        # prefetch depth 1: never two AG issued ahead of the current wait
+        pass
+
+
+def _two_bucket(ex):
+    ag = ex["ag_ns"]
+    cp = ex["compute_ns"]
+    seq = S.forward_sequence(len(ag), ex["reorder"], S.BEFORE)
+
+    def dur(ph, op, b):
+        return cp[b] if op == S.COMPUTE_F else 0
+    return simulate(seq, dur, lambda ph, op, b: ag[b])
+
+
+def test_sim_hand_traces(golden):
+    for ex in golden("spec_examples.json")["sim_traces"]:
+        if ex["case"] == "compute_only":
+            r = simulate([(0, S.COMPUTE_F, 0, 0)], lambda *a: ex["compute_ns"], lambda *a: 0)
+        else:
+            r = _two_bucket(ex)
+        assert r["total"] == ex["total_ns"], ex["cite"]
+        assert r["exposed"] == ex["exposed_ns"], ex["cite"]
+        assert r["total"] - r["compute_busy"] == r["exposed"]
+        if "comm_events" in ex:
+            assert [[e[4], e[5]] for e in r["events"] if e[3] == 1] == ex["comm_events"]
+            assert [[e[4], e[5]] for e in r["events"] if e[1] == S.COMPUTE_F] == ex["compute_events"]
+
+
+def _rand_durations(seed, kf, kb):
+    rng = np.random.Generator(np.random.Philox(seed))
+    table = {}
+
+    def dur(ph, op, b):
+        key = (ph, op, b)
+        if key not in table:
+            table[key] = int(rng.integers(0, 3000 if op not in (S.COMPUTE_F, S.COMPUTE_B) else 20000))
+        return table[key]
+    coll = {}
+
+    def tc(ph, op, b):
+        key = (ph, op, b)
+        if key not in coll:
+            coll[key] = int(rng.integers(1, 30000))
+        return coll[key]
+    return dur, tc
+
+
+@given(kf=st.integers(1, 10), kb=st.integers(1, 10), seed=st.integers(0, 2**31),
+       fp=st.sampled_from([S.BEFORE, S.AFTER]), bp=st.sampled_from([S.BEFORE, S.AFTER]))
+@settings(max_examples=500, deadline=None)
+def test_reorder_never_worse_than_vanilla_and_accounting(kf, kb, seed, fp, bp):
+    dur, tc = _rand_durations(seed, kf, kb)
+    rv = simulate(S.step_sequence(kf, kb, False), dur, tc)
+    rr = simulate(S.step_sequence(kf, kb, True, fp, bp), dur, tc)
+    for r in (rv, rr):
+        assert r["total"] - r["compute_busy"] == r["exposed"]
+        assert r["total"] >= max(r["compute_busy"], r["comm_busy"])
+    assert rr["compute_busy"] == rv["compute_busy"]
+    assert rr["exposed"] <= rv["exposed"]
+    # vanilla exposes every collective in full
+    assert rv["exposed"] == rv["comm_busy"]
+
+
+@given(kf=st.integers(2, 8), seed=st.integers(0, 2**31))
+@settings(max_examples=200, deadline=None)
+def test_fifo_non_interference(kf, seed):
+    # moving AG(k+1) before Wait(k) never changes when Wait(k) completes
+    dur, tc = _rand_durations(seed, kf, 0)
+    before = simulate(S.forward_sequence(kf, True, S.BEFORE), dur, tc)
+    after = simulate(S.forward_sequence(kf, True, S.AFTER), dur, tc)
+    ends_b = {e[2]: e[5] for e in before["events"] if e[1] == S.AG}
+    ends_a = {e[2]: e[5] for e in after["events"] if e[1] == S.AG}
+    assert ends_b[0] == ends_a[0]
+    assert before["total"] <= after["total"]  # Table 6 direction with copy-outs > 0
+
+
+def _plan_exposure(pi, buckets, t_c_per_param, copy_ns_per_byte=0):
+    """Simulated exposure of one phase for a plan (phase-order buckets)."""
+    k = len(buckets)
+    seq = S.forward_sequence(k, True) if pi.phase == FWD else S.backward_sequence(k, True)
+
+    def dur(ph, op, b):
+        if op in (S.COMPUTE_F, S.COMPUTE_B):
+            return sum(t_c_per_param[j] for j in buckets[b])
+        return 0
+
+    def tc(ph, op, b):
+        return pi.t_ag(buckets[b]) if op == S.AG else pi.t_rs(buckets[b])
+    return simulate(seq, dur, tc)
+
+
+@given(P=st.integers(1, 8), seed=st.integers(0, 2**31), phase=st.sampled_from([FWD, BWD]))
+@settings(max_examples=200, deadline=None)
+def test_optimum_le_greedy(P, seed, phase):
+    rng = np.random.Generator(np.random.Philox(seed))
+    params = [(int(rng.integers(1, 40)), int(rng.integers(1, 40)), i) for i in range(P)]
+    tc = [int(x) for x in rng.integers(0, 20000, size=P)]
+    pi = PlanInput(params, 4, tc, (int(rng.integers(0, 5000)), int(rng.integers(0, 10**6))),
+                   (int(rng.integers(0, 5000)), int(rng.integers(0, 10**6))), 10**18, GREEDY, phase)
+    greedy, _ = plan(pi)
+    g = _plan_exposure(pi, greedy, tc)["total"]
+    best = min(_plan_exposure(pi, p, tc)["total"] for p in contiguous_partitions(pi.order()))
+    assert best <= g
+    pp = PlanInput(params, 4, tc, pi.ag, pi.rs, 10**18, PER_PARAM, phase)
+    singles, _ = plan(pp)
+    assert best <= _plan_exposure(pp, singles, tc)["total"]
