@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""Benchmark of the SimpleFSDP hot path on B200 -- one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one pass of the whole hot path for one rank of a Llama-3-8B FSDP
+job (BASELINE.json configs[1]: bf16 params, fp32 reduce, per-transformer-block
+buckets = MANUAL wrapping, reordered with the Table 6 default placements):
+forward all-gathers (pack K1, NCCL AG, unpack K3) and backward re-gathers,
+gradient pack (K4), NCCL reduce-scatter, copy-out (K6) for all 35 buckets.
+
+* N = 1 (default): one GPU holds rank 0 of an 8-way job (layout world 8,
+  "1 GPU (pack/unpack only)" in BASELINE.json) -- every kernel runs at the
+  8-GPU per-rank size; the collectives are absent because there are no peers.
+* N > 1 (torchrun): one process per GPU, an NCCL communicator of N ranks,
+  real in-place all-gather / reduce-scatter on a high-priority comm stream,
+  a calibrated compute proxy per bucket (--tokens, default 1024 tokens/GPU).
+
+value = sum over ranks of the full bucket bytes the step's collectives carry
+(forward AG + backward AG in bf16, RS in fp32) / step time, in GB/s.  Inputs
+(64.3 GB of bucket traffic per rank-step) are far larger than the 126 MB L2.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "AG/RS bus GB/s and exposed-comm ms/step, Llama-3-8B shards, 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="8b")
+    ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--plan", default="manual", choices=["manual", "greedy", "per_param", "size_cap"])
+    ap.add_argument("--sim-world", type=int, default=8, help="layout world size at N=1")
+    ap.add_argument("--tokens", type=int, default=None, help="proxy compute tokens/GPU (0 = none)")
+    ap.add_argument("--no-reorder", action="store_true")
+    ap.add_argument("--fwd-placement", default="before", choices=["before", "after"])
+    ap.add_argument("--bwd-placement", default="after", choices=["before", "after"])
+    ap.add_argument("--mem-limit", type=float, default=2e9)
+    ap.add_argument("--alpha-ns", type=int, default=20000)
+    ap.add_argument("--beta-fs", type=int, default=1500)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--proxy-ctas", type=int, default=1)
+    ap.add_argument("--proxy-smem", type=int, default=0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(int(r[0]) for r in self.rows if r[0].isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": int(self.rows[0][1]) if self.rows[0][1].isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(op_name):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/ncu_traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(op_name)
+    except (OSError, ValueError):
+        return None
+
+
+# --------------------------------------------------------------- CPU oracle
+def cpu_oracle_sample(world, seconds_hint=20.0):
+    """The oracle as it stands, on a bounded sample of the same workload:
+    whole 8B-block tensors (attention_norm, wq, wk, wv, wo, ffn_norm) at world
+    N -- forward AG (shard + pack all ranks + gather + unpack), the backward
+    re-gather, and the bucketed RS (pack every rank, rank-order sum, copy-out).
+    Returns (GB/s in the bench's unit, seconds, sample description)."""
+    import numpy as np
+    from oracle import collectives as OC
+    from workloads import llama
+    from workloads.data import grad_tensor, param_tensor
+
+    specs = [s for s in llama("8b", n_layers=1, with_embeddings=False)
+             if s.name.split(".")[-2] in ("attention_norm", "wq", "wk", "wv", "wo", "ffn_norm")]
+    params = [param_tensor(s, "bf16", 1 + i) for i, s in enumerate(specs)]
+    grads = [[grad_tensor(s, "bf16", 2, r) for s in specs] for r in range(world)]
+    t0 = time.perf_counter()
+    OC.bucketed_all_gather(params, world, 16)           # forward
+    OC.bucketed_all_gather(params, world, 16)           # backward re-gather
+    OC.bucketed_reduce_scatter(grads, world, 16)
+    dt = time.perf_counter() - t0
+    from oracle.layout import bucket_layout
+    dims = [(s.dim0, s.row_numel) for s in specs]
+    ag = world * bucket_layout(dims, world, 2, 16)[1]
+    rs = world * bucket_layout(dims, world, 4, 16)[1]
+    n = sum(s.dim0 * s.row_numel for s in specs)
+    desc = ("oracle (NumPy, 1 thread) on %d tensors / %.1f M params of one Llama-3-8B block at N=%d: "
+            "fwd AG + bwd AG + RS, all %d simulated ranks" % (len(specs), n / 1e6, world, world))
+    del np
+    return (2 * ag + rs) / dt / 1e9, dt, desc
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    world = args.sim_world if args.gpus == 1 else args.gpus
+    t0 = time.perf_counter()
+    vals = []
+    for _ in range(args.warmup + args.steps):
+        v, dt, desc = cpu_oracle_sample(world)
+        vals.append((v, dt))
+    timed = vals[args.warmup:]
+    v = sum(x[0] for x in timed) / len(timed)
+    ms = 1e3 * sum(x[1] for x in timed) / len(timed)
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "GB/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": "llama3-8b FSDP rank step sample (see cpu_baseline.sample)",
+                       "world": world, "plan": "one bucket of the sampled tensors"},
+            "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": desc, "host_cpus": os.cpu_count()},
+            "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": round(time.perf_counter() - t0, 1)}
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------------- ours
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_00284_b200 as F
+    from paper_2411_00284_b200 import _lib as L
+    from paper_2411_00284_b200 import harness as H
+    from workloads import llama
+    from workloads.compute_model import per_param_compute_ns
+
+    assert torch.cuda.is_available(), "bench.py needs a B200"
+    torch.cuda.set_device(local)
+    multi = args.gpus > 1
+    if multi:
+        assert world_env == args.gpus, "launch with torchrun --nproc-per-node %d" % args.gpus
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = [F.nccl_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        world = args.gpus
+        ctx = F.Ctx(world, rank, local, nccl_uid=uid[0])
+    else:
+        world = args.sim_world
+        ctx = F.Ctx(world, 0, local)   # layout-only: rank 0 of a simulated `world`-way job
+    tokens = args.tokens if args.tokens is not None else (1024 if multi else 0)
+
+    specs = llama(args.model, n_layers=args.layers)
+    t_fwd, t_bwd = per_param_compute_ns(specs, tokens) if tokens else ([0] * len(specs), [0] * len(specs))
+    mode = {"manual": L.PLAN_MANUAL, "greedy": L.PLAN_GREEDY, "per_param": L.PLAN_PER_PARAM,
+            "size_cap": L.PLAN_SIZE_CAP}[args.plan]
+    link = (args.alpha_ns, args.beta_fs)
+    fplan, bplan = H.plans_for(specs, world, mode, t_fwd, t_bwd, link, link, int(args.mem_limit))
+    st = H.RankState(specs, world, rank if multi else 0, fplan, bplan, ctx, seed=1234 + rank)
+    compute = torch.cuda.Stream()
+    comm = torch.cuda.Stream(priority=-1)
+    cs, ms = compute.cuda_stream, comm.cuda_stream
+
+    pf = pb = None
+    if tokens:
+        nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
+        pf = H.proxy_iters(H.bucket_times(fplan, t_fwd), nspi)
+        pb = H.proxy_iters(H.bucket_times(bplan, t_bwd), nspi)
+    flags = 0 if args.no_reorder else L.SCHED_REORDER
+    if args.fwd_placement == "before":
+        flags |= L.SCHED_FWD_AG_BEFORE_WAIT
+    if args.bwd_placement == "before":
+        flags |= L.SCHED_BWD_AG_BEFORE_WAIT
+
+    def step(extra=0):
+        return st.step(flags | extra, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem)
+
+    def barrier():
+        if multi:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if not multi:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step(L.SCHED_TIMING)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reports = []
+    with ClockSampler(local) as clk:
+        ev0.record(compute)
+        for _ in range(args.steps):
+            reports.append(step(L.SCHED_TIMING))
+        ev1.record(compute)
+        barrier()
+    ms_step = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+
+    # compute-stream-only baseline: same ops, no collective, no wait
+    for _ in range(2):
+        step(L.SCHED_NO_COMM)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(compute)
+    for _ in range(args.steps):
+        step(L.SCHED_NO_COMM)
+    e1.record(compute)
+    barrier()
+    ms_compute = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+
+    ag_b, rs_b = st.step_bytes()
+    ranks = world_env if multi else 1
+    value = ranks * (ag_b + rs_b) / (ms_step * 1e-3) / 1e9
+
+    # per-op device time from the timed steps' events -> dominant data kernel
+    op_ns = [sum(r["op_ns"][i] for r in reports) for i in range(L.N_OPS)]
+    op_cnt = [sum(r["op_count"][i] for r in reports) for i in range(L.N_OPS)]
+    kbytes = st.kernel_bytes()
+    names = {L.OP_PACK_AG: "fsdp_ag_pack_kernel", L.OP_UNPACK: "fsdp_ag_unpack_kernel",
+             L.OP_PACK_RS: "fsdp_rs_pack_kernel", L.OP_COPYOUT_RS: "fsdp_rs_copyout_kernel"}
+    dom = max(kbytes, key=lambda op: op_ns[op])
+    peak, peak_src = measured_peak_hbm()
+    achieved = kbytes[dom] * args.steps / (op_ns[dom] * 1e-9) / 1e9
+    per_kernel = {names[op]: {"GB/s": round(kbytes[op] * args.steps / (op_ns[op] * 1e-9) / 1e9, 1),
+                              "ms_per_step": round(op_ns[op] / args.steps / 1e6, 3),
+                              "launches_per_step": op_cnt[op] // args.steps,
+                              "bytes_per_step": kbytes[op]} for op in kbytes if op_ns[op] > 0}
+    launches = sum(r["kernel_launches"] for r in reports)
+    coll_ms = {"ag_ms_per_step": round(op_ns[L.OP_AG] / args.steps / 1e6, 3),
+               "rs_ms_per_step": round(op_ns[L.OP_RS] / args.steps / 1e6, 3)}
+    busbw = None
+    if multi and op_ns[L.OP_AG] > 0:
+        busbw = {"ag": round((world - 1) / world * ag_b * args.steps / (op_ns[L.OP_AG] * 1e-9) / 1e9, 1),
+                 "rs": round((world - 1) / world * rs_b * args.steps / (op_ns[L.OP_RS] * 1e-9) / 1e9, 1)}
+
+    # e2e through the public call with host buffers: H2D of the rank's
+    # parameter shards, the step, D2H of the fp32 gradient shards.
+    e2e = None
+    if not args.no_e2e:
+        h_sh = torch.empty(st.shard_buf.numel(), dtype=torch.uint8, pin_memory=True)
+        h_gs = torch.empty(st.gshard_buf.numel(), dtype=torch.uint8, pin_memory=True)
+        h_sh.copy_(st.shard_buf)
+        barrier()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(compute):
+            x0.record(compute)
+            for _ in range(args.e2e_steps):
+                st.shard_buf.copy_(h_sh, non_blocking=True)
+                step()
+                h_gs.copy_(st.gshard_buf, non_blocking=True)
+            x1.record(compute)
+        barrier()
+        e2e_ms = max_over_ranks(x0.elapsed_time(x1) / args.e2e_steps)
+        e2e = {"value": round(ranks * (ag_b + rs_b) / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+               "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(h_sh.numel()),
+               "d2h_bytes_per_step": int(h_gs.numel())}
+        del h_sh, h_gs
+
+    cpu = None
+    if rank == 0 and not multi and not args.no_cpu_baseline:
+        v, dt, desc = cpu_oracle_sample(world)
+        cpu = {"value": round(v, 3), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc,
+               "seconds": round(dt, 2), "host_cpus": os.cpu_count()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {
+                "workload": ("llama3-8b FSDP rank step, %s plan, %s" % (args.plan, "reorder fwd-%s/bwd-%s" % (
+                    args.fwd_placement, args.bwd_placement) if not args.no_reorder else "vanilla order")) +
+                (", 1 GPU = rank 0 of a simulated %d-way job (pack/unpack only, no peers)" % world if not multi
+                 else ", %d ranks over NCCL" % world),
+                "model": "llama3-8b shapes (Table 2; vocab 128256, 8 KV heads)", "layout_world": world,
+                "buckets_fwd": len(fplan), "buckets_bwd": len(bplan), "param_dtype": "bf16",
+                "reduce_dtype": "fp32", "proxy_tokens_per_gpu": tokens,
+                "value_def": "sum over ranks of full AG(fwd)+AG(bwd)+RS bucket bytes per second of step time",
+                "bytes_per_rank_step": ag_b + rs_b, "l2": "inputs > L2 (126 MB): 64 GB of bucket traffic per step",
+                "parallelism": "fsdp%d" % world if multi else "fsdp1 (simulated %d)" % world},
+            "exposed_comm_ms": round(ms_step - ms_compute, 3), "compute_stream_ms": round(ms_compute, 3),
+            "collectives": coll_ms, "busbw_GBps": busbw, "kernels": per_kernel,
+            "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": ncu_traffic(names[dom]),
+                         "algorithmic_bytes_per_launch": kbytes[dom] // max(1, op_cnt[dom] // args.steps)},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    ctx_close = getattr(ctx, "close", None)
+    del st
+    if ctx_close:
+        ctx_close()
+    if multi:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

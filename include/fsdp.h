@@ -1,0 +1,333 @@
+/*
+ * fsdp.h -- C ABI of the B200-native SimpleFSDP data-parallel hot path.
+ *
+ * The method (arXiv 2411.00284, "SimpleFSDP"; citations P:<line> are lines of
+ * the paper's LaTeX source PAPER.md, S:<line> lines of SPEC.md):
+ *   - shard every parameter along dim 0 across N devices;
+ *   - all-gather the parameters before forward use, release them, all-gather
+ *     them again before backward use;
+ *   - reduce-scatter the gradients with an average after backward, in
+ *     reduce_dtype;
+ *   - bucket the collectives and reorder them for prefetch
+ *     (P:182-193), with manual or greedy auto wrapping (Alg. 1).
+ *
+ * Conventions (all entry points):
+ *   - Every function returns fsdp_status; nothing throws or aborts across the
+ *     ABI.  On failure fsdp_last_error() returns a thread-local message that
+ *     stays valid until the next fsdp_* call on the same thread.
+ *   - Arguments are validated before anything is enqueued: a failing call
+ *     enqueues nothing.
+ *   - "device" pointers are CUDA device pointers of the ctx's device; "host"
+ *     pointers are ordinary host memory.  fsdp_stream_t is a cudaStream_t.
+ *   - The caller owns every large device buffer (shards, full parameters,
+ *     full gradients, gradient shards, staging).  The library owns only the
+ *     ctx, bucket handles and their small device run tables, each released by
+ *     the matching *_destroy.  The library never frees caller memory; caller
+ *     pointers bound in fsdp_bucket_create must outlive the bucket.
+ *   - All device work is stream-ordered and asynchronous; only
+ *     fsdp_run_schedule with FSDP_SCHED_TIMING and fsdp_proxy_calibrate
+ *     synchronise.  A ctx is not thread-safe; distinct ctxs are independent.
+ *   - There is no CPU fallback: a call that needs the GPU fails with
+ *     FSDP_ERR_CUDA when no device is present.  Host-only calls
+ *     (fsdp_shard with NULL data pointers, fsdp_plan_buckets, fsdp_layout,
+ *     fsdp_run_schedule with FSDP_SCHED_DRY_RUN on a NULL ctx) work without one.
+ */
+#ifndef FSDP_B200_FSDP_H
+#define FSDP_B200_FSDP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSDP_ABI_VERSION 1
+
+typedef void* fsdp_stream_t; /* cudaStream_t */
+
+typedef enum {
+  FSDP_OK = 0,
+  FSDP_ERR_INVALID_ARG = 1,
+  FSDP_ERR_CUDA = 2,
+  FSDP_ERR_NCCL = 3,
+  FSDP_ERR_OOM = 4,
+  FSDP_ERR_UNSUPPORTED = 5
+} fsdp_status;
+
+typedef enum { FSDP_BF16 = 0, FSDP_FP32 = 1 } fsdp_dtype; /* param_dtype / grad dtype */
+
+const char* fsdp_last_error(void);
+int32_t fsdp_abi_version(void);
+
+/* One parameter p_j of shape [dim0, ...]; row_numel = product of the other
+ * dims (1 for 1-D tensors).  module_id tags the wrapping module;
+ * array index = forward-use order. */
+typedef struct {
+  int64_t dim0;
+  int64_t row_numel;
+  int32_t module_id;
+  int32_t reserved; /* must be 0 */
+} fsdp_param_desc;
+
+/* Rank r's dim-0 shard: shard_rows = c = ceil(dim0/N); the rank owns rows
+ * [row_begin, row_begin + valid_rows) with valid_rows = clamp(dim0 - r*c, 0, c)
+ * and row_begin = min(r*c, dim0); shard_numel = c * row_numel.  Rows past
+ * valid_rows are padding and hold +0. */
+typedef struct {
+  int64_t shard_rows;
+  int64_t row_begin;
+  int64_t valid_rows;
+  int64_t shard_numel;
+} fsdp_shard_info;
+
+/* ---------------------------------------------------------------- context */
+typedef struct fsdp_ctx fsdp_ctx;
+
+/* Writes a 128-byte NCCL unique id (host memory) for an owned communicator. */
+fsdp_status fsdp_nccl_get_unique_id(void* uid128);
+
+/* Creates the per-rank context on cuda_device.
+ *   nccl_uid (host, 128 B) non-NULL : the ctx owns a new NCCL communicator of
+ *                                     `world` ranks (collective call: every rank
+ *                                     must call it with the same uid);
+ *   borrowed_comm non-NULL          : use this ncclComm_t (never destroyed here);
+ *   both NULL                       : layout-only ctx for rank `rank` of a
+ *                                     simulated world: ISSUE runs only the pack,
+ *                                     WAIT only the copy-out, no collective.
+ * world >= 1, 0 <= rank < world.  A ctx with a communicator issues its
+ * collectives at every world size (at world 1 NCCL's in-place collectives are
+ * local no-ops); a layout-only ctx never issues one. */
+fsdp_status fsdp_ctx_create(fsdp_ctx** out, int32_t world, int32_t rank, int32_t cuda_device,
+                            const void* nccl_uid, void* borrowed_comm);
+fsdp_status fsdp_ctx_destroy(fsdp_ctx* ctx);
+
+/* ------------------------------------------------------------ 1. fsdp_shard
+ * P:69 "partitioned per the number of devices ... Each device only holds one of
+ * the partitions"; P:133 Shard(0) DTensors.  Always fills *info.  If both
+ * full_dev ([dim0, row_numel] row-major, dtype dt) and shard_dev
+ * ([shard_rows, row_numel], dtype dt) are non-NULL, also enqueues on `stream`
+ * the copy of the owned rows and the zero fill of the padding rows (kernel
+ * K0).  Exactly one NULL pointer is FSDP_ERR_INVALID_ARG. */
+fsdp_status fsdp_shard(int32_t world, int32_t rank, const fsdp_param_desc* p, fsdp_dtype dt,
+                       const void* full_dev, void* shard_dev, fsdp_shard_info* info,
+                       fsdp_stream_t stream);
+
+/* ---------------------------------------------------- 2. fsdp_plan_buckets
+ * Bucket plan for one phase.  Modes:
+ *   PER_PARAM : singletons (the unbucketed baseline);
+ *   MANUAL    : one bucket per wrapped module: maximal runs of
+ *               equal module_id in the phase's execution order;
+ *   SIZE_CAP  : GREEDY with the time constraint disabled;
+ *   GREEDY    : Algorithm 1, Table 1 variables:
+ *     forward  : merge q_i iff T_AG(open + q_i) <= T_c and M(open) + M_i <= M_max
+ *     backward : merge q_i iff T_RS(b_{j-2}) + T_AG(open + q_i) <= T_c and the same memory test
+ *     T(n) = alpha_ns + ceil(n * beta_fs_per_byte / 1e6), n = N * segment
+ *     bytes of the bucket in its dtype; T_c = sum of t_compute_ns over the
+ *     previously closed bucket (0 before the first close); M_i = mem_bytes[i]
+ *     or, if mem_bytes is NULL, the padded gathered bytes N * c_i * row_numel_i
+ *     * sizeof(param_dtype); ties merge.
+ * The phase execution order is forward-use order (FWD) or its reverse (BWD).
+ * Output: bucket_begin[0..n_buckets] (caller array of n_params + 1) holds
+ * positions in the phase order: bucket b = positions [bucket_begin[b],
+ * bucket_begin[b+1]); the forward index of position k is k (FWD) or
+ * n_params - 1 - k (BWD).  trace (nullable, n_params - 1 records) receives one
+ * record per decision i = 2..P (GREEDY / SIZE_CAP fill every field; other
+ * modes fill param and accept only).  Host-only. */
+typedef struct {
+  int64_t alpha_ns;
+  int64_t beta_fs_per_byte;
+} fsdp_link;
+
+typedef enum {
+  FSDP_PLAN_PER_PARAM = 0,
+  FSDP_PLAN_MANUAL = 1,
+  FSDP_PLAN_SIZE_CAP = 2,
+  FSDP_PLAN_GREEDY = 3
+} fsdp_plan_mode;
+
+typedef enum { FSDP_PHASE_FWD = 0, FSDP_PHASE_BWD = 1 } fsdp_phase;
+
+typedef struct {
+  const fsdp_param_desc* params; /* n_params, forward order */
+  const int64_t* t_compute_ns;   /* n_params, this phase's T_ci, by forward index */
+  const int64_t* mem_bytes;      /* n_params or NULL (see above) */
+  fsdp_link ag;
+  fsdp_link rs;
+  int64_t mem_max_bytes;
+  int32_t n_params;
+  int32_t world;
+  int32_t align_bytes;  /* layout alignment A >= 1 (16 default) */
+  int32_t mode;         /* fsdp_plan_mode */
+  int32_t phase;        /* fsdp_phase */
+  int32_t param_dtype;  /* fsdp_dtype of the all-gather */
+  int32_t reduce_bytes; /* bytes per reduce_dtype element: 4 (fp32) */
+  int32_t reserved;
+} fsdp_plan_in;
+
+typedef struct {
+  int64_t t_lhs_ns; /* T_AG(open + q_i) (+ T_RS(b_{j-2}) in BWD) */
+  int64_t t_rhs_ns; /* T_c */
+  int64_t m_lhs;    /* M(open) + M_i */
+  int64_t m_rhs;    /* M_max */
+  int32_t param;    /* forward index of q_i */
+  int32_t accept;   /* 1 = merged into the open bucket */
+} fsdp_plan_trace;
+
+fsdp_status fsdp_plan_buckets(const fsdp_plan_in* in, int32_t* bucket_begin, int32_t* n_buckets,
+                              fsdp_plan_trace* trace);
+
+/* Bucket layout, host-only: for k members (forward order) of
+ * elem_bytes-byte elements at world N, offs[j] = byte offset of member j in a
+ * rank segment, *seg_bytes = segment size; off_1 = 0, off_{j+1} =
+ * align(off_j + c_j * row_numel_j * elem_bytes), seg = align(end of last). */
+fsdp_status fsdp_layout(const fsdp_param_desc* members, int32_t k, int32_t world, int32_t elem_bytes,
+                        int32_t align_bytes, int64_t* offs, int64_t* seg_bytes);
+
+/* ------------------------------------------------------------ buckets
+ * Binds the device pointers of one bucket's members once (parameters do not
+ * move) and builds its device run tables.  Layouts: all-gather segment in
+ * param_dtype, reduce-scatter segment in fp32 (reduce_dtype).
+ * Pointer arrays have k entries; an array may be NULL if the step that
+ * uses it is never called: shards (AG ISSUE), fulls (AG WAIT), full_grads
+ * (RS ISSUE), grad_shards (RS WAIT); fsdp_run_schedule needs all four for
+ * backward buckets and the first two for forward buckets.  shards[j]: [c_j, R_j] param_dtype; fulls[j]: [d_j, R_j] param_dtype;
+ * full_grads[j]: [d_j, R_j] grad_dtype; grad_shards[j]: [c_j, R_j] fp32.
+ * The ctx must outlive the bucket. */
+typedef struct fsdp_bucket fsdp_bucket;
+
+typedef struct {
+  const fsdp_param_desc* params; /* k member descriptors, forward order */
+  void* const* shards;
+  void* const* fulls;
+  const void* const* full_grads;
+  void* const* grad_shards;
+  int32_t k;
+  int32_t align_bytes;
+  int32_t param_dtype; /* fsdp_dtype */
+  int32_t grad_dtype;  /* fsdp_dtype of full_grads */
+} fsdp_bucket_desc;
+
+fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc* desc, fsdp_bucket** out,
+                               int64_t* ag_seg_bytes, int64_t* rs_seg_bytes);
+fsdp_status fsdp_bucket_destroy(fsdp_bucket* b);
+
+/* ------------------------------------------ 3. fsdp_allgather_bucket
+ * copy-in ("flattens and concatenates"), one all-gather AG + wait Wa,
+ * copy-out "based on their original tensor size".
+ *   FSDP_ISSUE : on `compute`, K1 packs this rank's shards into segment `rank`
+ *                of ag_staging (pads zeroed); then on `comm`, after the pack,
+ *                an in-place ncclAllGather fills every segment.
+ *   FSDP_WAIT  : `compute` waits for the all-gather, then K3 copies the valid
+ *                rows of every segment into the full parameters.
+ * ag_staging: device, world * ag_seg_bytes, 16-B aligned.  The caller must not
+ * re-ISSUE into the same staging before the previous WAIT was enqueued.
+ * Layout-only ctx: ISSUE = pack only, WAIT = copy-out only. */
+enum { FSDP_ISSUE = 1, FSDP_WAIT = 2 };
+fsdp_status fsdp_allgather_bucket(fsdp_ctx* ctx, fsdp_bucket* b, void* ag_staging,
+                                  fsdp_stream_t compute, fsdp_stream_t comm, uint32_t flags);
+
+/* ------------------------------------- 4. fsdp_reduce_scatter_bucket
+ * split each gradient "into chunks based on world size", concatenate
+ * chunk q of every member into segment q, one reduce-scatter RS + wait Wr that
+ * averages, read out the gradient shards.
+ *   FSDP_ISSUE : on `compute`, K4 writes fp32(grad) * fl32(1/N) of chunk q into
+ *                segment q of rs_staging (pads +0.0); then on `comm` an in-place
+ *                fp32 ncclReduceScatter(sum) leaves rank r's average in segment r.
+ *   FSDP_WAIT  : `compute` waits, then K6 copies segment `rank` into grad_shards.
+ * rs_staging: device, world * rs_seg_bytes, 16-B aligned.
+ * Layout-only ctx: ISSUE = pack only, WAIT = copy-out of segment `rank` only. */
+fsdp_status fsdp_reduce_scatter_bucket(fsdp_ctx* ctx, fsdp_bucket* b, void* rs_staging,
+                                       fsdp_stream_t compute, fsdp_stream_t comm, uint32_t flags);
+
+/* ------------------------------------------------ 5. fsdp_run_schedule
+ * One training step's communication path (Table 6):
+ *   reorder on : forward prefetch depth 1 -- AG(k+1) before (default) or after
+ *                Wa(k) and its copy-out; backward AG(j+1) after (default) or
+ *                before Wa(j); Wr(j-1) before RS(j); first AG and last RS exposed;
+ *   reorder off: vanilla -- every collective right before its own wait.
+ * Buckets are given in each phase's execution order; bucket b uses staging
+ * slot b % 2 (ag_staging[2], rs_staging[2], each >= world * the largest
+ * segment).  Compute of bucket b = compute-proxy kernel K7 with
+ * proxy_iters_{fwd,bwd}[b] iterations (NULL or 0 = none).
+ * The op sequence is written to report->log (if non-NULL) in host enqueue
+ * order as (phase, op, bucket, stream) with op codes FSDP_OP_*; stream 0 =
+ * compute, 1 = comm.
+ * Flags:
+ *   FSDP_SCHED_REORDER            prefetch reordering (else vanilla)
+ *   FSDP_SCHED_FWD_AG_BEFORE_WAIT forward AG(k+1) before Wa(k) (else after)
+ *   FSDP_SCHED_BWD_AG_BEFORE_WAIT backward AG(j+1) before Wa(j) (else after)
+ *   FSDP_SCHED_NO_COMM            run every compute-stream op but no collective
+ *                                 and no wait (the compute-only baseline)
+ *   FSDP_SCHED_DRY_RUN            write the log only, enqueue nothing (ctx may be NULL)
+ *   FSDP_SCHED_TIMING             CUDA events around every op; synchronises at
+ *                                 the end and fills step_ns, op_ns/op_count and
+ *                                 log[i].ns */
+enum {
+  FSDP_OP_PACK_AG = 0, FSDP_OP_AG = 1, FSDP_OP_WAIT_AG = 2, FSDP_OP_UNPACK = 3,
+  FSDP_OP_COMPUTE_F = 4, FSDP_OP_COMPUTE_B = 5, FSDP_OP_PACK_RS = 6, FSDP_OP_RS = 7,
+  FSDP_OP_WAIT_RS = 8, FSDP_OP_COPYOUT_RS = 9, FSDP_N_OPS = 10
+};
+enum {
+  FSDP_SCHED_REORDER = 1u,
+  FSDP_SCHED_FWD_AG_BEFORE_WAIT = 2u,
+  FSDP_SCHED_BWD_AG_BEFORE_WAIT = 4u,
+  FSDP_SCHED_NO_COMM = 8u,
+  FSDP_SCHED_DRY_RUN = 16u,
+  FSDP_SCHED_TIMING = 32u
+};
+
+typedef struct {
+  fsdp_bucket* const* fwd;      /* n_fwd handles, forward execution order */
+  fsdp_bucket* const* bwd;      /* n_bwd handles, backward execution order */
+  const int64_t* proxy_iters_fwd; /* n_fwd or NULL */
+  const int64_t* proxy_iters_bwd; /* n_bwd or NULL */
+  void* ag_staging[2];
+  void* rs_staging[2];
+  fsdp_stream_t compute;
+  fsdp_stream_t comm;
+  int32_t n_fwd;
+  int32_t n_bwd;
+  uint32_t flags;
+  int32_t proxy_ctas_per_sm; /* K7 footprint: CTAs per SM (>= 1) */
+  int32_t proxy_smem_bytes;  /* K7 footprint: dynamic shared memory per CTA */
+  int32_t reserved;
+} fsdp_schedule;
+
+typedef struct {
+  int64_t ns;     /* TIMING: event-measured duration of this op, else -1 */
+  int32_t phase;  /* 0 forward, 1 backward */
+  int32_t op;     /* FSDP_OP_* */
+  int32_t bucket; /* index in the phase's execution order */
+  int32_t stream; /* 0 compute, 1 comm */
+} fsdp_log_entry;
+
+typedef struct {
+  fsdp_log_entry* log; /* caller array or NULL */
+  int32_t log_capacity;
+  int32_t log_len;     /* entries written (sequence length) */
+  int64_t step_ns;     /* TIMING: first to last compute-stream event */
+  int64_t op_ns[FSDP_N_OPS];    /* TIMING: summed ns per op code */
+  int32_t op_count[FSDP_N_OPS]; /* ops per code in this step */
+  int32_t kernel_launches;      /* library kernels enqueued by this step */
+  int32_t collectives;          /* NCCL collectives enqueued by this step */
+} fsdp_step_report;
+
+fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, fsdp_step_report* out);
+
+/* ----------------------------------------------- compute proxy (K7)
+ * A measurement device, not a method step: stands in for the layer compute
+ * that the paper's reordering overlaps communication with, so that
+ * exposed communication is measurable.  Persistent grid of ctas_per_sm CTAs
+ * per SM x 256 threads running `iters` iterations of a dependent FMA chain,
+ * each CTA holding smem_bytes of dynamic shared memory. */
+fsdp_status fsdp_proxy_launch(fsdp_ctx* ctx, int64_t iters, int32_t ctas_per_sm, int32_t smem_bytes,
+                              fsdp_stream_t stream);
+/* Times fsdp_proxy_launch(iters) on `stream` (median of `reps`) and writes the
+ * measured ns; synchronises. */
+fsdp_status fsdp_proxy_calibrate(fsdp_ctx* ctx, int64_t iters, int32_t ctas_per_sm, int32_t smem_bytes,
+                                 int32_t reps, fsdp_stream_t stream, int64_t* ns_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSDP_B200_FSDP_H */

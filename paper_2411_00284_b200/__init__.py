@@ -1,0 +1,23 @@
+"""B200-native SimpleFSDP (arXiv 2411.00284) data-parallel hot path.
+
+The product is the C-ABI library ``libfsdp_b200.so`` (include/fsdp.h):
+fsdp_shard, fsdp_plan_buckets, fsdp_allgather_bucket, fsdp_reduce_scatter_bucket,
+fsdp_run_schedule.  ``paper_2411_00284_b200.fsdp`` exposes the same names to
+Python (marshalling only).  Any use of the API loads the built library and
+raises ImportError if it is missing: there is no CPU fallback.  (Attributes are
+resolved lazily so that ``python -m paper_2411_00284_b200.build`` can run
+before the library exists.)
+"""
+_API = ("Bucket", "Ctx", "abi_version", "allgather_bucket", "layout", "nccl_get_unique_id",
+        "plan_buckets", "proxy_calibrate", "proxy_launch", "reduce_scatter_bucket", "run_schedule",
+        "shard")
+
+
+def __getattr__(name):
+    if name in _API:
+        from . import fsdp
+        return getattr(fsdp, name)
+    if name.isupper() or name == "FsdpError":
+        from . import _lib
+        return getattr(_lib, name)
+    raise AttributeError(name)

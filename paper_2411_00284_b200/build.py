@@ -1,0 +1,94 @@
+"""Builds libfsdp_b200.so in-tree (sm_100a only).
+
+    python -m paper_2411_00284_b200.build [--verbose]
+
+Kernels (csrc/*.cu) are compiled by nvcc with
+``-gencode arch=compute_100a,code=sm_100a -lineinfo``; the host core
+(csrc/*.cc) by g++; the library links the CUDA runtime statically and NCCL
+dynamically from the same ``nvidia-nccl`` wheel torch loads (so a communicator
+borrowed from torch's ProcessGroupNCCL is valid here, and an owned one uses
+the same libnccl instance).  No torch headers or libraries are involved.
+"""
+import glob
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+BUILD = os.path.join(PKG, "_build")
+LIB = os.path.join(PKG, "libfsdp_b200.so")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def cuda_home():
+    for c in (os.environ.get("CUDA_HOME"), "/usr/local/cuda"):
+        if c and os.path.exists(os.path.join(c, "bin", "nvcc")):
+            return c
+    nvcc = shutil.which("nvcc")
+    if nvcc:
+        return os.path.dirname(os.path.dirname(nvcc))
+    raise RuntimeError("nvcc not found")
+
+
+def nccl_dirs():
+    import nvidia.nccl  # the wheel torch links against
+    base = os.path.dirname(nvidia.nccl.__file__) if nvidia.nccl.__file__ else list(nvidia.nccl.__path__)[0]
+    inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+    if not os.path.exists(os.path.join(inc, "nccl.h")) or not os.path.exists(os.path.join(lib, "libnccl.so.2")):
+        raise RuntimeError("NCCL headers/library not found under %s" % base)
+    return inc, lib
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("build step failed: %s" % " ".join(cmd[:3]))
+    return r.stdout + r.stderr
+
+
+def _stale(out, deps):
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(verbose=False, force=False):
+    cuda = cuda_home()
+    nvcc = os.path.join(cuda, "bin", "nvcc")
+    inc_nccl, lib_nccl = nccl_dirs()
+    os.makedirs(BUILD, exist_ok=True)
+    headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
+    incs = ["-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc_nccl, "-I", os.path.join(cuda, "include")]
+    objs = []
+    ptxas_log = []
+    for src in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
+        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [src] + headers):
+            out = _run([nvcc, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v",
+                        "-Xcompiler", "-fPIC", *incs, "-c", src, "-o", obj], verbose)
+            ptxas_log.append(out)
+    for src in sorted(glob.glob(os.path.join(CSRC, "*.cc"))):
+        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [src] + headers):
+            _run(["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-Wno-unused-parameter",
+                  *incs, "-c", src, "-o", obj], verbose)
+    if force or _stale(LIB, objs):
+        _run([nvcc, "-shared", *ARCH, "-o", LIB, *objs, "-L", lib_nccl, "-l:libnccl.so.2",
+              "-Xlinker", "-rpath," + lib_nccl, "-cudart", "static"], verbose)
+    if ptxas_log:
+        with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
+            f.write("\n".join(ptxas_log))
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv))

@@ -1,0 +1,243 @@
+// Bucket handles and the per-bucket collectives:
+//   fsdp_allgather_bucket      -- AG bucketing, P:177 (copy-in, AG + Wa, copy-out)
+//   fsdp_reduce_scatter_bucket -- RS bucketing, P:179 (chunk/concat, RS + Wr avg, read-out)
+// Copies are the sm_100a kernels of kernels.cu on the compute stream; the
+// collectives are in-place NCCL calls on the comm stream, ordered by events.
+#include <cstring>
+
+#include "internal.h"
+
+using namespace fsdp;
+
+namespace {
+
+cudaStream_t comm_stream(fsdp_ctx* c, fsdp_stream_t s) {
+  if (s) return static_cast<cudaStream_t>(s);
+  if (!c->own_comm_stream) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&c->own_comm_stream, cudaStreamNonBlocking, hi);
+  }
+  return c->own_comm_stream;
+}
+
+void destroy_bucket(fsdp_bucket* b) {
+  release(&b->ag_pack);
+  release(&b->ag_unpack);
+  release(&b->rs_pack);
+  release(&b->rs_copyout);
+  for (cudaEvent_t* e : {&b->ev_ag_packed, &b->ev_ag_done, &b->ev_rs_packed, &b->ev_rs_done})
+    if (*e) cudaEventDestroy(*e);
+  delete b;
+}
+
+}  // namespace
+
+extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc* d, fsdp_bucket** out,
+                                          int64_t* ag_seg_bytes, int64_t* rs_seg_bytes) {
+  if (!ctx || !d || !out) return fail(FSDP_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  const int32_t k = d->k;
+  if (k < 1 || !d->params) return fail(FSDP_ERR_INVALID_ARG, "bucket needs >= 1 member");
+  if (d->align_bytes < 1) return fail(FSDP_ERR_INVALID_ARG, "align_bytes < 1");
+  const int32_t ep = dtype_bytes(d->param_dtype), eg = dtype_bytes(d->grad_dtype);
+  if (!ep || !eg) return fail(FSDP_ERR_INVALID_ARG, "unsupported dtype");
+  for (int32_t j = 0; j < k; ++j) {
+    const fsdp_param_desc& p = d->params[j];
+    if (p.dim0 < 1 || p.row_numel < 1 || p.reserved != 0)
+      return fail(FSDP_ERR_INVALID_ARG, "bad param descriptor");
+    if (d->shards && !d->shards[j]) return fail(FSDP_ERR_INVALID_ARG, "NULL shard pointer");
+    if (d->fulls && !d->fulls[j]) return fail(FSDP_ERR_INVALID_ARG, "NULL full pointer");
+    if (d->full_grads && !d->full_grads[j]) return fail(FSDP_ERR_INVALID_ARG, "NULL grad pointer");
+    if (d->grad_shards && !d->grad_shards[j])
+      return fail(FSDP_ERR_INVALID_ARG, "NULL grad shard pointer");
+  }
+  const int32_t N = ctx->world, r = ctx->rank;
+  std::vector<int64_t> ag_off(k), rs_off(k);
+  int64_t ag_seg = 0, rs_seg = 0;
+  layout(d->params, k, N, ep, d->align_bytes, ag_off.data(), &ag_seg);
+  layout(d->params, k, N, 4, d->align_bytes, rs_off.data(), &rs_seg);
+
+  TableBuilder pack, unpack, rpack, rcopy;
+  for (int32_t j = 0; j < k; ++j) {
+    const fsdp_param_desc& p = d->params[j];
+    const ShardRows own = shard_rows(p.dim0, N, r);
+    const int64_t R = p.row_numel;
+    const int64_t ag_end = (j + 1 < k) ? ag_off[j + 1] : ag_seg;
+    const int64_t rs_end = (j + 1 < k) ? rs_off[j + 1] : rs_seg;
+    if (d->shards) {
+      // K1: this rank's whole padded shard into segment r, alignment gap zeroed.
+      const uint64_t dst = static_cast<uint64_t>(r * ag_seg + ag_off[j]);
+      const int64_t nb = own.c * R * ep;
+      pack.copy(reinterpret_cast<uint64_t>(d->shards[j]), dst, nb);
+      pack.zero(dst + nb, ag_end - ag_off[j] - nb);
+    }
+    for (int32_t q = 0; q < N; ++q) {
+      const ShardRows s = shard_rows(p.dim0, N, q);
+      if (d->fulls && s.v > 0) {
+        // K3: valid rows of rank q's chunk -> rows [q c, q c + v) of the full param.
+        unpack.copy(static_cast<uint64_t>(q * ag_seg + ag_off[j]),
+                    reinterpret_cast<uint64_t>(d->fulls[j]) + static_cast<uint64_t>(s.begin * R * ep),
+                    s.v * R * ep);
+      }
+      if (d->full_grads) {
+        // K4: rows of chunk q, widened and scaled, into segment q; pads +0.0.
+        const uint64_t dst = static_cast<uint64_t>(q * rs_seg + rs_off[j]);
+        const uint64_t src = reinterpret_cast<uint64_t>(d->full_grads[j]) +
+                             static_cast<uint64_t>(s.begin * R * eg);
+        if (eg == 2) rpack.widen(src, dst, s.v * R);
+        else rpack.scale(src, dst, s.v * R);
+        rpack.zero(dst + s.v * R * 4, rs_end - rs_off[j] - s.v * R * 4);
+      }
+    }
+    if (d->grad_shards) {
+      // K6: own segment r -> fp32 gradient shard [c, R].
+      rcopy.copy(static_cast<uint64_t>(r * rs_seg + rs_off[j]),
+                 reinterpret_cast<uint64_t>(d->grad_shards[j]), own.c * R * 4);
+    }
+  }
+  FSDP_CUDA_TRY(cudaSetDevice(ctx->device));
+  fsdp_bucket* b = new fsdp_bucket();
+  b->ctx = ctx;
+  b->k = k;
+  b->ag_seg = ag_seg;
+  b->rs_seg = rs_seg;
+  b->param_bytes = ep;
+  b->grad_bytes = eg;
+  b->has_shards = d->shards != nullptr;
+  b->has_fulls = d->fulls != nullptr;
+  b->has_grads = d->full_grads != nullptr;
+  b->has_gshards = d->grad_shards != nullptr;
+  fsdp_status st = FSDP_OK;
+  if (st == FSDP_OK) st = upload(pack, &b->ag_pack);
+  if (st == FSDP_OK) st = upload(unpack, &b->ag_unpack);
+  if (st == FSDP_OK) st = upload(rpack, &b->rs_pack);
+  if (st == FSDP_OK) st = upload(rcopy, &b->rs_copyout);
+  for (cudaEvent_t* e : {&b->ev_ag_packed, &b->ev_ag_done, &b->ev_rs_packed, &b->ev_rs_done}) {
+    if (st != FSDP_OK) break;
+    cudaError_t err = cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+    if (err != cudaSuccess) st = fail(FSDP_ERR_CUDA, cudaGetErrorString(err));
+  }
+  if (st != FSDP_OK) {
+    destroy_bucket(b);
+    return st;
+  }
+  if (ag_seg_bytes) *ag_seg_bytes = ag_seg;
+  if (rs_seg_bytes) *rs_seg_bytes = rs_seg;
+  *out = b;
+  return FSDP_OK;
+}
+
+extern "C" fsdp_status fsdp_bucket_destroy(fsdp_bucket* b) {
+  if (!b) return FSDP_OK;
+  cudaSetDevice(b->ctx->device);
+  destroy_bucket(b);
+  return FSDP_OK;
+}
+
+namespace fsdp {
+
+// Shared by the public calls and the schedule executor.  `launches` and
+// `colls` count enqueued kernels / collectives.
+fsdp_status ag_issue(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, cudaStream_t ms,
+                     bool with_comm, int* launches, int* colls) {
+  FSDP_CUDA_TRY(launch_table(KK_AG_PACK, b->ag_pack, staging, 1.0f, cs, c->max_ctas));
+  if (b->ag_pack.n && launches) ++*launches;
+  if (with_comm && c->comm) {
+    FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_packed, cs));
+    FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_ag_packed, 0));
+    // In place: sendbuff = recvbuff + rank * sendcount (bytes as ncclInt8).
+    FSDP_NCCL_TRY(ncclAllGather(staging + c->rank * b->ag_seg, staging, static_cast<size_t>(b->ag_seg),
+                                ncclInt8, c->comm, ms));
+    FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_done, ms));
+    if (colls) ++*colls;
+  }
+  return FSDP_OK;
+}
+
+fsdp_status ag_wait(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm) {
+  if (with_comm && c->comm) FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, b->ev_ag_done, 0));
+  return FSDP_OK;
+}
+
+fsdp_status ag_unpack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, int* launches) {
+  FSDP_CUDA_TRY(launch_table(KK_AG_UNPACK, b->ag_unpack, staging, 1.0f, cs, c->max_ctas));
+  if (b->ag_unpack.n && launches) ++*launches;
+  return FSDP_OK;
+}
+
+fsdp_status rs_issue(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, cudaStream_t ms,
+                     bool with_comm, int* launches, int* colls) {
+  const float inv = 1.0f / static_cast<float>(c->world);  // fl32(1/N), correctly rounded
+  FSDP_CUDA_TRY(launch_table(KK_RS_PACK, b->rs_pack, staging, inv, cs, c->max_ctas));
+  if (b->rs_pack.n && launches) ++*launches;
+  if (with_comm && c->comm) {
+    FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_packed, cs));
+    FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_rs_packed, 0));
+    // In place: recvbuff = sendbuff + rank * recvcount; sum of pre-scaled fp32.
+    const size_t cnt = static_cast<size_t>(b->rs_seg / 4);
+    FSDP_NCCL_TRY(ncclReduceScatter(staging, staging + c->rank * b->rs_seg, cnt, ncclFloat32, ncclSum,
+                                    c->comm, ms));
+    FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_done, ms));
+    if (colls) ++*colls;
+  }
+  return FSDP_OK;
+}
+
+fsdp_status rs_wait(fsdp_ctx* c, fsdp_bucket* b, cudaStream_t cs, bool with_comm) {
+  if (with_comm && c->comm) FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, b->ev_rs_done, 0));
+  return FSDP_OK;
+}
+
+fsdp_status rs_copyout(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, int* launches) {
+  FSDP_CUDA_TRY(launch_table(KK_RS_COPYOUT, b->rs_copyout, staging, 1.0f, cs, c->max_ctas));
+  if (b->rs_copyout.n && launches) ++*launches;
+  return FSDP_OK;
+}
+
+cudaStream_t resolve_comm(fsdp_ctx* c, fsdp_stream_t s) { return comm_stream(c, s); }
+
+}  // namespace fsdp
+
+static fsdp_status check_call(fsdp_ctx* c, fsdp_bucket* b, void* staging, uint32_t flags) {
+  if (!c || !b || !staging) return fail(FSDP_ERR_INVALID_ARG, "NULL argument");
+  if (b->ctx != c) return fail(FSDP_ERR_INVALID_ARG, "bucket belongs to another ctx");
+  if (reinterpret_cast<uintptr_t>(staging) % 16) return fail(FSDP_ERR_INVALID_ARG, "staging not 16-B aligned");
+  if (!flags || (flags & ~3u)) return fail(FSDP_ERR_INVALID_ARG, "flags must be ISSUE and/or WAIT");
+  return FSDP_OK;
+}
+
+extern "C" fsdp_status fsdp_allgather_bucket(fsdp_ctx* c, fsdp_bucket* b, void* staging,
+                                             fsdp_stream_t compute, fsdp_stream_t comm, uint32_t flags) {
+  FSDP_TRY(check_call(c, b, staging, flags));
+  if ((flags & FSDP_ISSUE) && !b->has_shards) return fail(FSDP_ERR_INVALID_ARG, "ISSUE needs bound shards");
+  if ((flags & FSDP_WAIT) && !b->has_fulls) return fail(FSDP_ERR_INVALID_ARG, "WAIT needs bound fulls");
+  FSDP_CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t cs = static_cast<cudaStream_t>(compute);
+  cudaStream_t ms = resolve_comm(c, comm);
+  char* st = static_cast<char*>(staging);
+  if (flags & FSDP_ISSUE) FSDP_TRY(ag_issue(c, b, st, cs, ms, true, nullptr, nullptr));
+  if (flags & FSDP_WAIT) {
+    FSDP_TRY(ag_wait(c, b, st, cs, true));
+    FSDP_TRY(ag_unpack(c, b, st, cs, nullptr));
+  }
+  return FSDP_OK;
+}
+
+extern "C" fsdp_status fsdp_reduce_scatter_bucket(fsdp_ctx* c, fsdp_bucket* b, void* staging,
+                                                  fsdp_stream_t compute, fsdp_stream_t comm,
+                                                  uint32_t flags) {
+  FSDP_TRY(check_call(c, b, staging, flags));
+  if ((flags & FSDP_ISSUE) && !b->has_grads) return fail(FSDP_ERR_INVALID_ARG, "ISSUE needs bound full_grads");
+  if ((flags & FSDP_WAIT) && !b->has_gshards) return fail(FSDP_ERR_INVALID_ARG, "WAIT needs bound grad_shards");
+  FSDP_CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t cs = static_cast<cudaStream_t>(compute);
+  cudaStream_t ms = resolve_comm(c, comm);
+  char* st = static_cast<char*>(staging);
+  if (flags & FSDP_ISSUE) FSDP_TRY(rs_issue(c, b, st, cs, ms, true, nullptr, nullptr));
+  if (flags & FSDP_WAIT) {
+    FSDP_TRY(rs_wait(c, b, cs, true));
+    FSDP_TRY(rs_copyout(c, b, st, cs, nullptr));
+  }
+  return FSDP_OK;
+}

@@ -1,0 +1,138 @@
+// Internal declarations of the B200-native SimpleFSDP hot path.
+// Not part of the ABI; see include/fsdp.h for the public contract.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "fsdp.h"
+
+namespace fsdp {
+
+// ----------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+fsdp_status fail(fsdp_status st, const std::string& msg);
+
+#define FSDP_CUDA_TRY(expr)                                                              \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return ::fsdp::fail(e_ == cudaErrorMemoryAllocation ? FSDP_ERR_OOM : FSDP_ERR_CUDA, \
+                          std::string(#expr) + ": " + cudaGetErrorString(e_));           \
+  } while (0)
+
+#define FSDP_NCCL_TRY(expr)                                                              \
+  do {                                                                                   \
+    ncclResult_t r_ = (expr);                                                            \
+    if (r_ != ncclSuccess)                                                               \
+      return ::fsdp::fail(FSDP_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+#define FSDP_TRY(expr)                 \
+  do {                                 \
+    fsdp_status s_ = (expr);           \
+    if (s_ != FSDP_OK) return s_;      \
+  } while (0)
+
+// ------------------------------------------------------------ shard math
+struct ShardRows {
+  int64_t c, begin, v;  // rows per rank, first owned row, owned rows
+};
+ShardRows shard_rows(int64_t d, int32_t world, int32_t rank);
+int64_t align_up(int64_t x, int64_t a);
+int32_t dtype_bytes(int32_t dt);  // 0 if unknown
+// Segment layout of k members (forward order): offsets and segment bytes.
+void layout(const fsdp_param_desc* m, int32_t k, int32_t world, int64_t elem_bytes, int64_t align,
+            int64_t* offs, int64_t* seg);
+
+// ------------------------------------------------------------ run tables
+// A chunk is <= kChunkBytes of destination data processed by one CTA.
+// Addresses are absolute device addresses, or offsets from the staging base
+// passed at launch for the side a kernel treats as relative.
+constexpr uint32_t kChunkBytes = 32 * 1024;
+
+enum ChunkOp : uint32_t {
+  OP_COPY = 0,   // n units of `unit` bytes
+  OP_ZERO = 1,   // n units of `unit` bytes at dst
+  OP_WIDEN = 2,  // bf16 -> fp32 * scale; unit 16: n groups of 8 elems, unit 2: n elems
+  OP_SCALE = 3,  // fp32 * scale;        unit 16: n groups of 4 elems, unit 4: n elems
+};
+
+struct Chunk {
+  uint64_t src;
+  uint64_t dst;
+  uint32_t n;
+  uint32_t op_unit;  // op | unit << 8
+};
+static_assert(sizeof(Chunk) == 24, "chunk layout");
+
+// Builder that splits runs into chunks (host side).
+struct TableBuilder {
+  std::vector<Chunk> chunks;
+  int64_t bytes_moved = 0;  // algorithmic bytes (read + write)
+  void copy(uint64_t src, uint64_t dst, int64_t bytes);
+  void zero(uint64_t dst, int64_t bytes);
+  void widen(uint64_t src, uint64_t dst, int64_t elems);  // bf16 -> f32 * s
+  void scale(uint64_t src, uint64_t dst, int64_t elems);  // f32 -> f32 * s
+};
+
+struct DevTable {
+  Chunk* d = nullptr;
+  int32_t n = 0;
+  int64_t bytes_moved = 0;
+};
+fsdp_status upload(const TableBuilder& tb, DevTable* out);
+void release(DevTable* t);
+
+// Kernel launchers (kernels.cu).  `base` is the staging buffer for the side
+// that is relative; grid = min(n, max_ctas).
+enum KernelKind { KK_SHARD = 0, KK_AG_PACK, KK_AG_UNPACK, KK_RS_PACK, KK_RS_COPYOUT };
+cudaError_t launch_table(KernelKind kind, const DevTable& t, char* base, float scale, cudaStream_t s,
+                         int max_ctas);
+cudaError_t launch_proxy(int64_t iters, int grid, int smem, float* sink, cudaStream_t s);
+int device_sm_count(int device);
+
+// Per-bucket steps shared by the public calls and the schedule executor
+// (bucket.cc).  `launches` / `colls` (nullable) count enqueued kernels and
+// collectives; with_comm = false skips the collective and the event wait.
+}  // namespace fsdp
+struct fsdp_ctx;
+struct fsdp_bucket;
+namespace fsdp {
+fsdp_status ag_issue(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, cudaStream_t ms,
+                     bool with_comm, int* launches, int* colls);
+fsdp_status ag_wait(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm);
+fsdp_status ag_unpack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, int* launches);
+fsdp_status rs_issue(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, cudaStream_t ms,
+                     bool with_comm, int* launches, int* colls);
+fsdp_status rs_wait(fsdp_ctx* c, fsdp_bucket* b, cudaStream_t cs, bool with_comm);
+fsdp_status rs_copyout(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, int* launches);
+cudaStream_t resolve_comm(fsdp_ctx* c, fsdp_stream_t s);
+}  // namespace fsdp
+
+struct fsdp_ctx {
+  int32_t world = 1, rank = 0, device = 0;
+  ncclComm_t comm = nullptr;
+  bool owns_comm = false;
+  cudaStream_t own_comm_stream = nullptr;
+  int sm_count = 148;
+  int max_ctas = 148 * 8;
+  float* sink = nullptr;
+  std::vector<cudaEvent_t> timing_events;  // pool for FSDP_SCHED_TIMING
+};
+
+struct fsdp_bucket {
+  fsdp_ctx* ctx = nullptr;
+  int32_t k = 0;
+  int64_t ag_seg = 0, rs_seg = 0;
+  int32_t param_bytes = 2, grad_bytes = 2;
+  // which pointer arrays were bound: K1 shards, K3 fulls, K4 full_grads, K6 grad_shards
+  bool has_shards = false, has_fulls = false, has_grads = false, has_gshards = false;
+  fsdp::DevTable ag_pack, ag_unpack, rs_pack, rs_copyout;
+  cudaEvent_t ev_ag_packed = nullptr, ev_ag_done = nullptr;
+  cudaEvent_t ev_rs_packed = nullptr, ev_rs_done = nullptr;
+};

@@ -1,0 +1,302 @@
+// fsdp_run_schedule: the reordered (Table 6) or vanilla op
+// sequence of one training step, executed on a compute and a comm stream.
+// Also the compute proxy (K7) launch and calibration.
+#include <algorithm>
+#include <vector>
+
+#include "internal.h"
+
+using namespace fsdp;
+
+namespace {
+
+struct Op {
+  int32_t phase, op, bucket;
+};
+
+bool is_comm(int32_t op) { return op == FSDP_OP_AG || op == FSDP_OP_RS; }
+
+// Forward: prefetch depth 1; AG(k+1) before Wa(k) or after Wa(k) and its
+// copy-out.  Vanilla: AG(k) right before Wa(k).
+void forward_ops(std::vector<Op>& s, int32_t K, bool reorder, bool before) {
+  if (!reorder) {
+    for (int32_t b = 0; b < K; ++b)
+      for (int32_t op : {FSDP_OP_PACK_AG, FSDP_OP_AG, FSDP_OP_WAIT_AG, FSDP_OP_UNPACK, FSDP_OP_COMPUTE_F})
+        s.push_back({0, op, b});
+    return;
+  }
+  if (K > 0) {
+    s.push_back({0, FSDP_OP_PACK_AG, 0});
+    s.push_back({0, FSDP_OP_AG, 0});
+  }
+  for (int32_t b = 0; b < K; ++b) {
+    auto prefetch = [&] {
+      if (b + 1 < K) {
+        s.push_back({0, FSDP_OP_PACK_AG, b + 1});
+        s.push_back({0, FSDP_OP_AG, b + 1});
+      }
+    };
+    if (before) prefetch();
+    s.push_back({0, FSDP_OP_WAIT_AG, b});
+    s.push_back({0, FSDP_OP_UNPACK, b});
+    if (!before) prefetch();
+    s.push_back({0, FSDP_OP_COMPUTE_F, b});
+  }
+}
+
+// Backward: re-gather with AG(j+1) after (default) or before Wa(j);
+// "Wr12 is placed before RS34": Wr(j-1) and its read-out precede RS(j).
+void backward_ops(std::vector<Op>& s, int32_t K, bool reorder, bool before) {
+  if (!reorder) {
+    for (int32_t b = 0; b < K; ++b)
+      for (int32_t op : {FSDP_OP_PACK_AG, FSDP_OP_AG, FSDP_OP_WAIT_AG, FSDP_OP_UNPACK, FSDP_OP_COMPUTE_B,
+                         FSDP_OP_PACK_RS, FSDP_OP_RS, FSDP_OP_WAIT_RS, FSDP_OP_COPYOUT_RS})
+        s.push_back({1, op, b});
+    return;
+  }
+  if (K > 0) {
+    s.push_back({1, FSDP_OP_PACK_AG, 0});
+    s.push_back({1, FSDP_OP_AG, 0});
+  }
+  for (int32_t b = 0; b < K; ++b) {
+    auto prefetch = [&] {
+      if (b + 1 < K) {
+        s.push_back({1, FSDP_OP_PACK_AG, b + 1});
+        s.push_back({1, FSDP_OP_AG, b + 1});
+      }
+    };
+    if (before) prefetch();
+    s.push_back({1, FSDP_OP_WAIT_AG, b});
+    s.push_back({1, FSDP_OP_UNPACK, b});
+    if (!before) prefetch();
+    s.push_back({1, FSDP_OP_COMPUTE_B, b});
+    s.push_back({1, FSDP_OP_PACK_RS, b});
+    if (b >= 1) {
+      s.push_back({1, FSDP_OP_WAIT_RS, b - 1});
+      s.push_back({1, FSDP_OP_COPYOUT_RS, b - 1});
+    }
+    s.push_back({1, FSDP_OP_RS, b});
+  }
+  if (K > 0) {
+    s.push_back({1, FSDP_OP_WAIT_RS, K - 1});
+    s.push_back({1, FSDP_OP_COPYOUT_RS, K - 1});
+  }
+}
+
+int64_t max_seg(fsdp_bucket* const* bs, int32_t n, bool ag) {
+  int64_t m = 0;
+  for (int32_t i = 0; i < n; ++i) m = std::max(m, ag ? bs[i]->ag_seg : bs[i]->rs_seg);
+  return m;
+}
+
+fsdp_status grow_events(fsdp_ctx* c, size_t n) {
+  while (c->timing_events.size() < n) {
+    cudaEvent_t e;
+    FSDP_CUDA_TRY(cudaEventCreate(&e));
+    c->timing_events.push_back(e);
+  }
+  return FSDP_OK;
+}
+
+}  // namespace
+
+extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, fsdp_step_report* out) {
+  if (!s) return fail(FSDP_ERR_INVALID_ARG, "NULL schedule");
+  const uint32_t known = FSDP_SCHED_REORDER | FSDP_SCHED_FWD_AG_BEFORE_WAIT | FSDP_SCHED_BWD_AG_BEFORE_WAIT |
+                         FSDP_SCHED_NO_COMM | FSDP_SCHED_DRY_RUN | FSDP_SCHED_TIMING;
+  if (s->flags & ~known) return fail(FSDP_ERR_INVALID_ARG, "unknown schedule flag");
+  if (s->n_fwd < 0 || s->n_bwd < 0) return fail(FSDP_ERR_INVALID_ARG, "negative bucket count");
+  const bool dry = s->flags & FSDP_SCHED_DRY_RUN;
+  const bool timing = (s->flags & FSDP_SCHED_TIMING) && !dry;
+  const bool with_comm = !(s->flags & FSDP_SCHED_NO_COMM);
+
+  std::vector<Op> seq;
+  seq.reserve(5 * s->n_fwd + 9 * s->n_bwd + 4);
+  const bool reorder = s->flags & FSDP_SCHED_REORDER;
+  forward_ops(seq, s->n_fwd, reorder, s->flags & FSDP_SCHED_FWD_AG_BEFORE_WAIT);
+  backward_ops(seq, s->n_bwd, reorder, s->flags & FSDP_SCHED_BWD_AG_BEFORE_WAIT);
+
+  if (out) {
+    if (out->log && out->log_capacity < static_cast<int32_t>(seq.size()))
+      return fail(FSDP_ERR_INVALID_ARG, "log_capacity smaller than the step's op sequence");
+    out->log_len = static_cast<int32_t>(seq.size());
+    out->step_ns = -1;
+    out->kernel_launches = 0;
+    out->collectives = 0;
+    for (int i = 0; i < FSDP_N_OPS; ++i) {
+      out->op_ns[i] = timing ? 0 : -1;
+      out->op_count[i] = 0;
+    }
+    for (size_t i = 0; i < seq.size(); ++i) {
+      out->op_count[seq[i].op]++;
+      if (out->log) {
+        fsdp_log_entry& e = out->log[i];
+        e.ns = -1;
+        e.phase = seq[i].phase;
+        e.op = seq[i].op;
+        e.bucket = seq[i].bucket;
+        e.stream = is_comm(seq[i].op) ? 1 : 0;
+      }
+    }
+  }
+  if (dry) return FSDP_OK;
+
+  // ---- validation before any enqueue
+  if (!ctx) return fail(FSDP_ERR_INVALID_ARG, "NULL ctx");
+  if ((s->n_fwd && !s->fwd) || (s->n_bwd && !s->bwd)) return fail(FSDP_ERR_INVALID_ARG, "NULL bucket array");
+  for (int32_t i = 0; i < s->n_fwd; ++i)
+    if (!s->fwd[i] || s->fwd[i]->ctx != ctx || !s->fwd[i]->has_shards || !s->fwd[i]->has_fulls)
+      return fail(FSDP_ERR_INVALID_ARG, "forward bucket missing, foreign or without AG pointers");
+  for (int32_t i = 0; i < s->n_bwd; ++i)
+    if (!s->bwd[i] || s->bwd[i]->ctx != ctx || !s->bwd[i]->has_shards || !s->bwd[i]->has_fulls ||
+        !s->bwd[i]->has_grads || !s->bwd[i]->has_gshards)
+      return fail(FSDP_ERR_INVALID_ARG, "backward bucket missing, foreign or without AG/RS pointers");
+  if ((s->n_fwd || s->n_bwd) && (!s->ag_staging[0] || !s->ag_staging[1]))
+    return fail(FSDP_ERR_INVALID_ARG, "NULL AG staging slot");
+  if (s->n_bwd && (!s->rs_staging[0] || !s->rs_staging[1]))
+    return fail(FSDP_ERR_INVALID_ARG, "NULL RS staging slot");
+  for (int i = 0; i < 2; ++i)
+    if (reinterpret_cast<uintptr_t>(s->ag_staging[i]) % 16 || reinterpret_cast<uintptr_t>(s->rs_staging[i]) % 16)
+      return fail(FSDP_ERR_INVALID_ARG, "staging slot not 16-B aligned");
+  if (s->proxy_ctas_per_sm < 0 || s->proxy_smem_bytes < 0)
+    return fail(FSDP_ERR_INVALID_ARG, "bad proxy footprint");
+  (void)max_seg;  // slot sizes are the caller's contract (>= world * largest segment)
+
+  FSDP_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t cs = static_cast<cudaStream_t>(s->compute);
+  cudaStream_t ms = resolve_comm(ctx, s->comm);
+  const int proxy_grid = ctx->sm_count * std::max(1, s->proxy_ctas_per_sm);
+  if (timing) FSDP_TRY(grow_events(ctx, 2 * seq.size() + 2));
+  cudaEvent_t* ev = timing ? ctx->timing_events.data() : nullptr;
+  if (timing) FSDP_CUDA_TRY(cudaEventRecord(ev[0], cs));
+
+  int launches = 0, colls = 0;
+  for (size_t i = 0; i < seq.size(); ++i) {
+    const Op& o = seq[i];
+    fsdp_bucket* b = (o.phase == 0 ? s->fwd : s->bwd)[o.bucket];
+    char* ag_st = static_cast<char*>(s->ag_staging[o.bucket & 1]);
+    char* rs_st = static_cast<char*>(s->rs_staging[o.bucket & 1]);
+    const bool comm_op = is_comm(o.op);
+    const bool skipped = !with_comm && (comm_op || o.op == FSDP_OP_WAIT_AG || o.op == FSDP_OP_WAIT_RS);
+    cudaStream_t on = comm_op ? ms : cs;
+    if (timing && !skipped) {
+      if (comm_op) {
+        // start after the pack this collective depends on
+        FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, o.op == FSDP_OP_AG ? b->ev_ag_packed : b->ev_rs_packed, 0));
+      }
+      FSDP_CUDA_TRY(cudaEventRecord(ev[2 + 2 * i], on));
+    }
+    switch (o.op) {
+      case FSDP_OP_PACK_AG: {
+        FSDP_CUDA_TRY(launch_table(KK_AG_PACK, b->ag_pack, ag_st, 1.0f, cs, ctx->max_ctas));
+        if (b->ag_pack.n) ++launches;
+        if (with_comm && ctx->comm) FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_packed, cs));
+        break;
+      }
+      case FSDP_OP_AG:
+        if (with_comm && ctx->comm) {
+          FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_ag_packed, 0));
+          FSDP_NCCL_TRY(ncclAllGather(ag_st + ctx->rank * b->ag_seg, ag_st, static_cast<size_t>(b->ag_seg),
+                                      ncclInt8, ctx->comm, ms));
+          FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_done, ms));
+          ++colls;
+        }
+        break;
+      case FSDP_OP_WAIT_AG: FSDP_TRY(ag_wait(ctx, b, ag_st, cs, with_comm)); break;
+      case FSDP_OP_UNPACK: FSDP_TRY(ag_unpack(ctx, b, ag_st, cs, &launches)); break;
+      case FSDP_OP_COMPUTE_F:
+      case FSDP_OP_COMPUTE_B: {
+        const int64_t* it = o.op == FSDP_OP_COMPUTE_F ? s->proxy_iters_fwd : s->proxy_iters_bwd;
+        if (it && it[o.bucket] > 0) {
+          FSDP_CUDA_TRY(launch_proxy(it[o.bucket], proxy_grid, s->proxy_smem_bytes, ctx->sink, cs));
+          ++launches;
+        }
+        break;
+      }
+      case FSDP_OP_PACK_RS: {
+        const float inv = 1.0f / static_cast<float>(ctx->world);
+        FSDP_CUDA_TRY(launch_table(KK_RS_PACK, b->rs_pack, rs_st, inv, cs, ctx->max_ctas));
+        if (b->rs_pack.n) ++launches;
+        if (with_comm && ctx->comm) FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_packed, cs));
+        break;
+      }
+      case FSDP_OP_RS:
+        if (with_comm && ctx->comm) {
+          FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_rs_packed, 0));
+          FSDP_NCCL_TRY(ncclReduceScatter(rs_st, rs_st + ctx->rank * b->rs_seg, static_cast<size_t>(b->rs_seg / 4),
+                                          ncclFloat32, ncclSum, ctx->comm, ms));
+          FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_done, ms));
+          ++colls;
+        }
+        break;
+      case FSDP_OP_WAIT_RS: FSDP_TRY(rs_wait(ctx, b, cs, with_comm)); break;
+      case FSDP_OP_COPYOUT_RS: FSDP_TRY(rs_copyout(ctx, b, rs_st, cs, &launches)); break;
+    }
+    if (timing && !skipped) FSDP_CUDA_TRY(cudaEventRecord(ev[3 + 2 * i], on));
+  }
+  if (timing) FSDP_CUDA_TRY(cudaEventRecord(ev[1], cs));
+
+  if (out) {
+    out->kernel_launches = launches;
+    out->collectives = colls;
+  }
+  if (timing) {
+    FSDP_CUDA_TRY(cudaEventSynchronize(ev[1]));
+    float ms_total = 0.f;
+    FSDP_CUDA_TRY(cudaEventElapsedTime(&ms_total, ev[0], ev[1]));
+    if (out) {
+      out->step_ns = static_cast<int64_t>(ms_total * 1e6);
+      for (size_t i = 0; i < seq.size(); ++i) {
+        const Op& o = seq[i];
+        const bool skipped = !with_comm && (is_comm(o.op) || o.op == FSDP_OP_WAIT_AG || o.op == FSDP_OP_WAIT_RS);
+        if (skipped) continue;
+        float t = 0.f;
+        FSDP_CUDA_TRY(cudaEventElapsedTime(&t, ev[2 + 2 * i], ev[3 + 2 * i]));
+        const int64_t ns = static_cast<int64_t>(t * 1e6);
+        out->op_ns[o.op] += ns;
+        if (out->log) out->log[i].ns = ns;
+      }
+    }
+  }
+  return FSDP_OK;
+}
+
+extern "C" fsdp_status fsdp_proxy_launch(fsdp_ctx* ctx, int64_t iters, int32_t ctas_per_sm, int32_t smem_bytes,
+                                         fsdp_stream_t stream) {
+  if (!ctx || iters < 0 || ctas_per_sm < 1 || smem_bytes < 0)
+    return fail(FSDP_ERR_INVALID_ARG, "bad proxy arguments");
+  FSDP_CUDA_TRY(cudaSetDevice(ctx->device));
+  if (iters == 0) return FSDP_OK;
+  FSDP_CUDA_TRY(launch_proxy(iters, ctx->sm_count * ctas_per_sm, smem_bytes, ctx->sink,
+                             static_cast<cudaStream_t>(stream)));
+  return FSDP_OK;
+}
+
+extern "C" fsdp_status fsdp_proxy_calibrate(fsdp_ctx* ctx, int64_t iters, int32_t ctas_per_sm, int32_t smem_bytes,
+                                            int32_t reps, fsdp_stream_t stream, int64_t* ns_out) {
+  if (!ctx || iters < 1 || ctas_per_sm < 1 || smem_bytes < 0 || reps < 1 || !ns_out)
+    return fail(FSDP_ERR_INVALID_ARG, "bad calibration arguments");
+  FSDP_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaEvent_t a, b;
+  FSDP_CUDA_TRY(cudaEventCreate(&a));
+  FSDP_CUDA_TRY(cudaEventCreate(&b));
+  std::vector<float> t;
+  fsdp_status status = FSDP_OK;
+  for (int32_t r = 0; r < reps + 1 && status == FSDP_OK; ++r) {  // first rep warms up
+    cudaError_t e = cudaEventRecord(a, st);
+    if (e == cudaSuccess) e = launch_proxy(iters, ctx->sm_count * ctas_per_sm, smem_bytes, ctx->sink, st);
+    if (e == cudaSuccess) e = cudaEventRecord(b, st);
+    if (e == cudaSuccess) e = cudaEventSynchronize(b);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, a, b);
+    if (e != cudaSuccess) status = fail(FSDP_ERR_CUDA, std::string("proxy calibration: ") + cudaGetErrorString(e));
+    if (r > 0) t.push_back(ms);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (status != FSDP_OK) return status;
+  std::sort(t.begin(), t.end());
+  *ns_out = static_cast<int64_t>(t[t.size() / 2] * 1e6);
+  return FSDP_OK;
+}

@@ -1,0 +1,175 @@
+"""Python names for the C ABI (include/fsdp.h).  Marshalling only.
+
+Pointers are plain integers (e.g. ``tensor.data_ptr()``), streams are
+``torch.cuda.Stream.cuda_stream`` integers (0 = legacy default stream).  No
+logic of the method lives here: sharding, layout, planning, scheduling and all
+data movement happen in libfsdp_b200.so.
+"""
+import ctypes as C
+
+from . import _lib as L
+from ._lib import check
+
+
+def abi_version():
+    return L.lib.fsdp_abi_version()
+
+
+def nccl_get_unique_id():
+    buf = (C.c_uint8 * 128)()
+    check(L.lib.fsdp_nccl_get_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+def shard(world, rank, desc, dtype, full_ptr=None, shard_ptr=None, stream=0):
+    """fsdp_shard: metadata always, K0 copy when both pointers are given."""
+    d = L.descs([desc])
+    info = L.ShardInfo()
+    check(L.lib.fsdp_shard(world, rank, d, dtype, full_ptr, shard_ptr, C.byref(info), stream or None))
+    return dict(shard_rows=info.shard_rows, row_begin=info.row_begin, valid_rows=info.valid_rows,
+                shard_numel=info.shard_numel)
+
+
+def layout(members, world, elem_bytes, align=16):
+    d = L.descs(members)
+    offs = (C.c_int64 * len(members))()
+    seg = C.c_int64()
+    check(L.lib.fsdp_layout(d, len(members), world, elem_bytes, align, offs, C.byref(seg)))
+    return list(offs), seg.value
+
+
+def plan_buckets(params, world, t_compute_ns, ag, rs, mem_max, mode, phase, param_dtype=L.BF16,
+                 align=16, mem_bytes=None, reduce_bytes=4, want_trace=False):
+    """fsdp_plan_buckets.  params: (dim0, row_numel, module_id) in forward order.
+    Returns (buckets, trace): buckets = lists of forward indices in the phase's
+    execution order; trace = list of dicts (one per decision) if requested."""
+    params = list(params)
+    P = len(params)
+    d = L.descs(params)
+    tc = L.i64_array(t_compute_ns) if t_compute_ns is not None else None
+    mb = L.i64_array(mem_bytes) if mem_bytes is not None else None
+    pin = L.PlanIn()
+    pin.params = d
+    pin.t_compute_ns = tc
+    pin.mem_bytes = mb
+    pin.ag = L.Link(int(ag[0]), int(ag[1]))
+    pin.rs = L.Link(int(rs[0]), int(rs[1]))
+    pin.mem_max_bytes = int(mem_max)
+    pin.n_params, pin.world, pin.align_bytes = P, world, align
+    pin.mode, pin.phase, pin.param_dtype, pin.reduce_bytes, pin.reserved = mode, phase, param_dtype, reduce_bytes, 0
+    bb = (C.c_int32 * (P + 1))()
+    nb = C.c_int32()
+    tr = (L.PlanTrace * max(P - 1, 1))() if want_trace else None
+    check(L.lib.fsdp_plan_buckets(C.byref(pin), bb, C.byref(nb), tr))
+    order = list(range(P)) if phase == L.PHASE_FWD else list(range(P - 1, -1, -1))
+    buckets = [order[bb[b]:bb[b + 1]] for b in range(nb.value)]
+    trace = None
+    if want_trace:
+        trace = [dict(param=t.param, t_lhs=t.t_lhs_ns, t_rhs=t.t_rhs_ns, m_lhs=t.m_lhs, m_rhs=t.m_rhs,
+                      accept=bool(t.accept)) for t in tr[:P - 1]]
+    return buckets, trace
+
+
+class Ctx:
+    """fsdp_ctx_create / fsdp_ctx_destroy."""
+
+    def __init__(self, world, rank, device=0, nccl_uid=None, borrowed_comm=None):
+        self.world, self.rank, self.device = world, rank, device
+        h = C.c_void_p()
+        uid = None
+        if nccl_uid is not None:
+            uid = (C.c_uint8 * 128).from_buffer_copy(nccl_uid)
+        check(L.lib.fsdp_ctx_create(C.byref(h), world, rank, device,
+                                    C.cast(uid, C.c_void_p) if uid is not None else None,
+                                    borrowed_comm))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            check(L.lib.fsdp_ctx_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Bucket:
+    """fsdp_bucket_create / fsdp_bucket_destroy.  Pointer lists hold ints."""
+
+    def __init__(self, ctx, params, shards=None, fulls=None, full_grads=None, grad_shards=None,
+                 param_dtype=L.BF16, grad_dtype=L.BF16, align=16):
+        self.ctx = ctx
+        self._keep = [L.descs(params), L.ptr_array(shards), L.ptr_array(fulls),
+                      L.ptr_array(full_grads), L.ptr_array(grad_shards)]
+        d = L.BucketDesc()
+        d.params, d.shards, d.fulls, d.full_grads, d.grad_shards = self._keep
+        d.k, d.align_bytes, d.param_dtype, d.grad_dtype = len(params), align, param_dtype, grad_dtype
+        h = C.c_void_p()
+        ag, rs = C.c_int64(), C.c_int64()
+        check(L.lib.fsdp_bucket_create(ctx.h, C.byref(d), C.byref(h), C.byref(ag), C.byref(rs)))
+        self.h = h
+        self.ag_seg, self.rs_seg = ag.value, rs.value
+
+    def close(self):
+        if self.h:
+            check(L.lib.fsdp_bucket_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def allgather_bucket(ctx, bucket, staging_ptr, compute=0, comm=0, flags=L.ISSUE | L.WAIT):
+    check(L.lib.fsdp_allgather_bucket(ctx.h, bucket.h, staging_ptr, compute or None, comm or None, flags))
+
+
+def reduce_scatter_bucket(ctx, bucket, staging_ptr, compute=0, comm=0, flags=L.ISSUE | L.WAIT):
+    check(L.lib.fsdp_reduce_scatter_bucket(ctx.h, bucket.h, staging_ptr, compute or None, comm or None, flags))
+
+
+def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0, comm=0, flags=0,
+                 proxy_iters_fwd=None, proxy_iters_bwd=None, proxy_ctas_per_sm=1, proxy_smem_bytes=0,
+                 n_fwd=None, n_bwd=None, want_log=True):
+    """fsdp_run_schedule.  fwd / bwd: Bucket lists in execution order (or
+    counts via n_fwd / n_bwd with FSDP_SCHED_DRY_RUN and ctx=None).  Returns the
+    step report as a dict (log as a list of (phase, op, bucket, stream, ns))."""
+    nf = len(fwd) if fwd is not None else (n_fwd or 0)
+    nb = len(bwd) if bwd is not None else (n_bwd or 0)
+    s = L.Schedule()
+    fw = L.ptr_array([b.h.value for b in fwd]) if fwd else None
+    bw = L.ptr_array([b.h.value for b in bwd]) if bwd else None
+    pf = L.i64_array(proxy_iters_fwd)
+    pb = L.i64_array(proxy_iters_bwd)
+    s.fwd, s.bwd, s.proxy_iters_fwd, s.proxy_iters_bwd = fw, bw, pf, pb
+    s.ag_staging[0], s.ag_staging[1] = ag_staging
+    s.rs_staging[0], s.rs_staging[1] = rs_staging
+    s.compute, s.comm = compute or None, comm or None
+    s.n_fwd, s.n_bwd, s.flags = nf, nb, flags
+    s.proxy_ctas_per_sm, s.proxy_smem_bytes, s.reserved = proxy_ctas_per_sm, proxy_smem_bytes, 0
+    cap = 5 * nf + 9 * nb + 4
+    log = (L.LogEntry * cap)() if want_log else None
+    rep = L.StepReport()
+    rep.log, rep.log_capacity = log, cap if want_log else 0
+    check(L.lib.fsdp_run_schedule(ctx.h if ctx is not None else None, C.byref(s), C.byref(rep)))
+    out = dict(step_ns=rep.step_ns, op_ns=list(rep.op_ns), op_count=list(rep.op_count),
+               kernel_launches=rep.kernel_launches, collectives=rep.collectives, log_len=rep.log_len)
+    if want_log:
+        out["log"] = [(e.phase, e.op, e.bucket, e.stream, e.ns) for e in log[:rep.log_len]]
+    return out
+
+
+def proxy_launch(ctx, iters, ctas_per_sm=1, smem_bytes=0, stream=0):
+    check(L.lib.fsdp_proxy_launch(ctx.h, int(iters), ctas_per_sm, smem_bytes, stream or None))
+
+
+def proxy_calibrate(ctx, iters, ctas_per_sm=1, smem_bytes=0, reps=5, stream=0):
+    ns = C.c_int64()
+    check(L.lib.fsdp_proxy_calibrate(ctx.h, int(iters), ctas_per_sm, smem_bytes, reps, stream or None,
+                                     C.byref(ns)))
+    return ns.value

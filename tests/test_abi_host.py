@@ -1,0 +1,147 @@
+"""CPU tests of the C ABI: the library loads and exports every symbol
+include/fsdp.h declares; host-only entry points (shard metadata, layout,
+plan, dry-run schedule) are bit-exact / sequence-equal against the oracle.
+No GPU needed: these calls never touch the device."""
+import os
+import re
+
+import numpy as np
+import pytest
+from hypothesis import given, settings, strategies as st
+
+import paper_2411_00284_b200 as F
+from paper_2411_00284_b200 import _lib as L
+from oracle import schedule as OS
+from oracle.layout import bucket_layout
+from oracle.planner import BWD, FWD, GREEDY, MANUAL, PER_PARAM, SIZE_CAP, PlanInput, plan
+from oracle.shard import shard_rows
+from workloads import llama, toy_mlp
+from workloads.compute_model import per_param_compute_ns
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+MODES = {PER_PARAM: L.PLAN_PER_PARAM, MANUAL: L.PLAN_MANUAL, SIZE_CAP: L.PLAN_SIZE_CAP, GREEDY: L.PLAN_GREEDY}
+PHASES = {FWD: L.PHASE_FWD, BWD: L.PHASE_BWD}
+
+
+def test_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "fsdp.h")).read()
+    declared = set(re.findall(r"\b(fsdp_[a-z_0-9]+)\s*\(", hdr))
+    assert declared == set(L.EXPORTED)
+    for name in declared:
+        assert hasattr(L.lib, name), name
+    assert F.abi_version() == 1
+
+
+@given(d=st.integers(1, 10**6), world=st.integers(1, 64), data=st.data())
+@settings(max_examples=300, deadline=None)
+def test_shard_metadata_matches_oracle(d, world, data):
+    r = data.draw(st.integers(0, world - 1))
+    info = F.shard(world, r, (d, 7, 0), L.BF16)
+    c, begin, v = shard_rows(d, world, r)
+    assert (info["shard_rows"], info["row_begin"], info["valid_rows"], info["shard_numel"]) == (c, begin, v, 7 * c)
+
+
+def test_shard_rejects_bad_args():
+    with pytest.raises(F.FsdpError):
+        F.shard(2, 2, (10, 1, 0), L.BF16)
+    with pytest.raises(F.FsdpError):
+        F.shard(2, 0, (0, 1, 0), L.BF16)
+    with pytest.raises(F.FsdpError):
+        F.shard(2, 0, (4, 1, 0), L.BF16, full_ptr=1234, shard_ptr=None)
+
+
+@given(dims=st.lists(st.tuples(st.integers(1, 500), st.integers(1, 300)), min_size=1, max_size=12),
+       world=st.integers(1, 9), e=st.sampled_from([2, 4]), a=st.sampled_from([1, 2, 16, 256]))
+@settings(max_examples=300, deadline=None)
+def test_layout_matches_oracle(dims, world, e, a):
+    offs, seg = F.layout([(d, r, 0) for d, r in dims], world, e, a)
+    o2, s2 = bucket_layout(dims, world, e, a)
+    assert offs == o2 and seg == s2
+
+
+def _both_plans(pi, param_dtype):
+    ob, otr = plan(pi)
+    cb, ctr = F.plan_buckets(pi.params, pi.world, pi.t_compute_ns, pi.ag, pi.rs, pi.mem_max,
+                             MODES[pi.mode], PHASES[pi.phase], param_dtype=param_dtype, align=pi.align,
+                             mem_bytes=pi.mem_bytes, reduce_bytes=pi.reduce_bytes, want_trace=True)
+    return ob, otr, cb, ctr
+
+
+def _assert_same(ob, otr, cb, ctr, mode):
+    assert cb == ob
+    if mode in (GREEDY, SIZE_CAP):
+        assert [dict(param=t["param"], t_lhs=t["t_lhs"], t_rhs=t["t_rhs"], m_lhs=t["m_lhs"],
+                     m_rhs=t["m_rhs"], accept=t["accept"]) for t in ctr] == otr
+    else:
+        assert [(t["param"], t["accept"]) for t in ctr] == [(t["param"], t["accept"]) for t in otr]
+
+
+@given(P=st.integers(1, 40), world=st.integers(1, 9), seed=st.integers(0, 2**31),
+       phase=st.sampled_from([FWD, BWD]), mode=st.sampled_from([PER_PARAM, MANUAL, SIZE_CAP, GREEDY]),
+       bf16=st.booleans(), a=st.sampled_from([1, 16]))
+@settings(max_examples=500, deadline=None)
+def test_plan_bit_exact_fuzz(P, world, seed, phase, mode, bf16, a):
+    rng = np.random.Generator(np.random.Philox(seed))
+    params = [(int(rng.integers(1, 300)), int(rng.integers(1, 200)), int(rng.integers(0, 4)))
+              for _ in range(P)]
+    tc = [int(x) for x in rng.integers(0, 200000, size=P)]
+    mem = None if rng.integers(0, 2) else [int(x) for x in rng.integers(1, 10**6, size=P)]
+    pi = PlanInput(params, world, tc, (int(rng.integers(0, 20000)), int(rng.integers(0, 10**6))),
+                   (int(rng.integers(0, 20000)), int(rng.integers(0, 10**6))),
+                   int(rng.integers(1, 4 * 10**6)), mode, phase, param_bytes=2 if bf16 else 4,
+                   align=a, mem_bytes=mem)
+    _assert_same(*_both_plans(pi, L.BF16 if bf16 else L.FP32), mode)
+
+
+@pytest.mark.parametrize("model", ["8b", "70b"])
+@pytest.mark.parametrize("tokens", [1024, 8192])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_plan_bit_exact_llama(model, tokens, world):
+    ps = llama(model)
+    params = [(p.dim0, p.row_numel, p.module_id) for p in ps]
+    f, b = per_param_compute_ns(ps, tokens)
+    # alpha/beta of an NVLink-class link: 20 us, 1.5 ps/B (~670 GB/s)
+    for phase, tc in ((FWD, f), (BWD, b)):
+        for mode, mmax in ((GREEDY, 2 * 10**9), (GREEDY, 10**18), (SIZE_CAP, 500 * 10**6), (MANUAL, 0)):
+            pi = PlanInput(params, world, tc, (20000, 1500), (20000, 1500), mmax, mode, phase)
+            _assert_same(*_both_plans(pi, L.BF16), mode)
+
+
+def test_plan_hand_examples(golden):
+    for key, phase in (("forward", FWD), ("backward", BWD)):
+        ex = golden("alg1_hand_examples.json")[key]
+        pi = PlanInput([(1, 500000, i) for i in range(7)], 1, [ex["t_c_ns"]] * 7, (10000, ex["beta_ag_fs"]),
+                       (10000, ex["beta_rs_fs"]), 3_000_000, GREEDY, phase, mem_bytes=[10**6] * 7)
+        ob, otr, cb, ctr = _both_plans(pi, L.BF16)
+        _assert_same(ob, otr, cb, ctr, GREEDY)
+        pos = {j: k + 1 for k, j in enumerate(pi.order())}
+        assert [[pos[j] for j in bb] for bb in cb] == ex["buckets"]
+
+
+def test_plan_rejects_bad_input():
+    with pytest.raises(F.FsdpError):
+        F.plan_buckets([], 2, [], (0, 0), (0, 0), 0, L.PLAN_GREEDY, L.PHASE_FWD)
+    with pytest.raises(F.FsdpError):
+        F.plan_buckets([(0, 1, 0)], 2, [0], (0, 0), (0, 0), 0, L.PLAN_GREEDY, L.PHASE_FWD)
+
+
+@given(kf=st.integers(0, 40), kb=st.integers(0, 40), reorder=st.booleans(), fb=st.booleans(), bb=st.booleans())
+@settings(max_examples=200, deadline=None)
+def test_dry_run_schedule_log_equals_oracle(kf, kb, reorder, fb, bb):
+    flags = L.SCHED_DRY_RUN | (L.SCHED_REORDER if reorder else 0)
+    flags |= (L.SCHED_FWD_AG_BEFORE_WAIT if fb else 0) | (L.SCHED_BWD_AG_BEFORE_WAIT if bb else 0)
+    rep = F.run_schedule(None, None, None, flags=flags, n_fwd=kf, n_bwd=kb)
+    got = [e[:4] for e in rep["log"]]
+    want = OS.step_sequence(kf, kb, reorder, OS.BEFORE if fb else OS.AFTER, OS.BEFORE if bb else OS.AFTER)
+    assert got == want
+    assert all(e[4] == -1 for e in rep["log"])
+
+
+def test_toy_plan_parity():
+    ps = toy_mlp()
+    params = [(p.dim0, p.row_numel, p.module_id) for p in ps]
+    tc = [20000 if p.row_numel > 1 else 0 for p in ps]
+    for phase in (FWD, BWD):
+        for mode in (PER_PARAM, MANUAL, GREEDY):
+            pi = PlanInput(params, 2, tc, (10000, 1000), (10000, 1000), 10**9, mode, phase, param_bytes=4)
+            _assert_same(*_both_plans(pi, L.FP32), mode)

@@ -1,0 +1,336 @@
+"""-m gpu parity: the CUDA path (through the C ABI) against the oracle,
+element by element on the same seeded inputs.
+
+1-GPU simulated ranks: one layout-only ctx per simulated rank;
+every rank's K1 pack writes its own segment of one shared staging buffer,
+which is then exactly the buffer an all-gather would leave on every rank, so
+K3 on it is checked bit-exactly against the oracle.  For the reduce-scatter,
+each rank's K4 output is checked bit-exactly, the collective's sum is taken by
+the oracle's rank-order reduce_scatter (standing in for NCCL), written into
+each rank's own segment, and K6 is checked bit-exactly.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2411_00284_b200 as F
+from paper_2411_00284_b200 import _lib as L
+from oracle import collectives as OC
+from oracle import schedule as OS
+from oracle.layout import bucket_layout
+from oracle.shard import shard, shard_rows
+from workloads import llama, toy_mlp
+from workloads.data import EDGE_BF16_BITS, EDGE_F32_BITS, grad_tensor, param_tensor
+from workloads.shapes import ParamSpec
+
+from .gpu_util import DevArray, bits
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "-m gpu tests need a CUDA device"
+    torch.cuda.init()
+
+
+def _np(dt):
+    return np.uint16 if dt == L.BF16 else np.float32
+
+
+def _esize(dt):
+    return 2 if dt == L.BF16 else 4
+
+
+def _specs_from_dims(dims):
+    return [ParamSpec("p%d" % i, d, r, 0) for i, (d, r) in enumerate(dims)]
+
+
+def _shard_on_device(full_devs, params, world, rank, dt):
+    out = []
+    for p, fd in zip(params, full_devs):
+        d, r = p.shape
+        c, _, _ = shard_rows(d, world, rank)
+        sd = DevArray(nbytes=c * r * _esize(dt), fill=0xAB, dtype=_np(dt), shape=(c, r))
+        info = F.shard(world, rank, (d, r, 0), dt, fd.ptr, sd.ptr)
+        assert info["shard_rows"] == c
+        out.append(sd)
+    return out
+
+
+def sim_allgather(params, world, dt, align=16, check_all_ranks=True):
+    """Shard (K0) -> pack (K1) per simulated rank -> unpack (K3); compare."""
+    dims = [p.shape for p in params]
+    descs = [(d, r, 0) for d, r in dims]
+    full_devs = [DevArray(p) for p in params]
+    ctxs = [F.Ctx(world, r) for r in range(world)]
+    shards = [_shard_on_device(full_devs, params, world, r, dt) for r in range(world)]
+    for r in (range(world) if check_all_ranks else [0, world - 1]):
+        for p, s in zip(params, shards[r]):
+            assert np.array_equal(bits(s.get()), bits(shard(p, world, r)))
+    outs = {r: [DevArray(nbytes=p.nbytes, fill=0x5A, dtype=p.dtype, shape=p.shape) for p in params]
+            for r in {0, world - 1}}
+    buckets = [F.Bucket(ctxs[r], descs, shards=[s.ptr for s in shards[r]],
+                        fulls=[o.ptr for o in outs[r]] if r in outs else None,
+                        param_dtype=dt, grad_dtype=dt, align=align) for r in range(world)]
+    _, seg = bucket_layout(dims, world, _esize(dt), align)
+    assert buckets[0].ag_seg == seg
+    staging = DevArray(nbytes=world * seg, fill=0xCD)
+    for r in range(world):
+        F.allgather_bucket(ctxs[r], buckets[r], staging.ptr, flags=L.ISSUE)
+    for r in outs:
+        F.allgather_bucket(ctxs[r], buckets[r], staging.ptr, flags=L.WAIT)
+    g_ref, fulls_ref = OC.bucketed_all_gather(params, world, align)
+    assert np.array_equal(staging.get(), g_ref)           # raw buffer incl. zero pads
+    for r in outs:
+        for o, p in zip(outs[r], params):
+            assert np.array_equal(bits(o.get()), bits(p))  # all_gather(shard(p)) == p
+    return True
+
+
+def sim_reduce_scatter(grads_per_rank, world, gdt, align=16):
+    """K4 per simulated rank (bit-exact), oracle sum in rank order, K6 (bit-exact)."""
+    dims = [g.shape for g in grads_per_rank[0]]
+    descs = [(d, r, 0) for d, r in dims]
+    _, seg = bucket_layout(dims, world, 4, align)
+    ctxs = [F.Ctx(world, r) for r in range(world)]
+    gdev = [[DevArray(g) for g in gs] for gs in grads_per_rank]
+    gsh = [[DevArray(nbytes=-(-d // world) * r * 4, fill=0x77, dtype=np.float32, shape=(-(-d // world), r))
+            for d, r in dims] for _ in range(world)]
+    buckets = [F.Bucket(ctxs[r], descs, full_grads=[g.ptr for g in gdev[r]], grad_shards=[g.ptr for g in gsh[r]],
+                        param_dtype=gdt, grad_dtype=gdt, align=align) for r in range(world)]
+    assert buckets[0].rs_seg == seg
+    stag = [DevArray(nbytes=world * seg, fill=0xEF, dtype=np.float32) for _ in range(world)]
+    for r in range(world):
+        F.reduce_scatter_bucket(ctxs[r], buckets[r], stag[r].ptr, flags=L.ISSUE)
+    ins_ref, outs_ref, shards_ref = OC.bucketed_reduce_scatter(grads_per_rank, world, align)
+    packed = [s.get() for s in stag]
+    for r in range(world):
+        assert np.array_equal(bits(packed[r]), bits(ins_ref[r]))
+    # the collective (NCCL on real GPUs): rank-order fp32 sum of the device-packed inputs
+    outs = OC.reduce_scatter(packed, world)
+    for q in range(world):
+        host = stag[q].get()
+        host[q * seg // 4:(q + 1) * seg // 4] = outs[q]
+        stag[q].t[stag[q].off:stag[q].off + stag[q].nbytes].copy_(torch.from_numpy(host.view(np.uint8).copy()))
+        F.reduce_scatter_bucket(ctxs[q], buckets[q], stag[q].ptr, flags=L.WAIT)
+    for q in range(world):
+        for j in range(len(dims)):
+            assert np.array_equal(bits(gsh[q][j].get()), bits(shards_ref[q][j]))
+    return True
+
+
+# ---------------------------------------------------------------- all-gather
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("dt", [L.FP32, L.BF16])
+def test_toy_mlp_allgather(world, dt):
+    params = [param_tensor(p, "f32" if dt == L.FP32 else "bf16", 100 + i) for i, p in enumerate(toy_mlp())]
+    assert sim_allgather(params, world, dt)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_shapes_allgather(seed):
+    rng = np.random.Generator(np.random.Philox(seed))
+    world = int(rng.integers(2, 9))
+    k = int(rng.integers(1, 13))
+    dims = [(int(rng.integers(1, 300)), int(rng.integers(1, 70))) for _ in range(k)]
+    dt = L.BF16 if seed % 2 else L.FP32
+    align = 1 if seed % 3 == 0 else 16
+    params = [param_tensor(s, "bf16" if dt == L.BF16 else "f32", seed * 31 + i)
+              for i, s in enumerate(_specs_from_dims(dims))]
+    assert sim_allgather(params, world, dt, align)
+
+
+def test_edge_values_allgather():
+    p = [np.tile(EDGE_BF16_BITS, 7).reshape(-1, 1), np.tile(EDGE_F32_BITS, 3).view(np.uint16).reshape(-1, 4)]
+    assert sim_allgather(p, 3, L.BF16)
+
+
+def test_llama8b_block_allgather_full_size():
+    # BASELINE configs[1] bucket: one 8B transformer block, bf16, N = 8 (436.2 MB gathered)
+    specs = llama("8b", n_layers=1, with_embeddings=False)
+    params = [param_tensor(s, "bf16", 7 + i) for i, s in enumerate(specs)]
+    assert sim_allgather(params, 8, L.BF16, check_all_ranks=False)
+
+
+# ------------------------------------------------------------ reduce-scatter
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("gdt", [L.FP32, L.BF16])
+def test_toy_mlp_reduce_scatter(world, gdt):
+    specs = toy_mlp()
+    g = [[grad_tensor(s, "f32" if gdt == L.FP32 else "bf16", 3, r) for s in specs] for r in range(world)]
+    assert sim_reduce_scatter(g, world, gdt)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_shapes_reduce_scatter(seed):
+    rng = np.random.Generator(np.random.Philox(1000 + seed))
+    world = int(rng.integers(2, 9))
+    dims = [(int(rng.integers(1, 200)), int(rng.integers(1, 50))) for _ in range(int(rng.integers(1, 9)))]
+    kind = "exact" if seed % 2 else "normal"
+    g = [[grad_tensor(s, "bf16", seed, r, kind) for s in _specs_from_dims(dims)] for r in range(world)]
+    assert sim_reduce_scatter(g, world, L.BF16, align=1 if seed % 3 == 0 else 16)
+
+
+def test_edge_values_reduce_scatter():
+    # +-0, subnormals, +-inf, NaN: widen + scale on device vs oracle; NaN by class
+    g = [[np.tile(EDGE_BF16_BITS, 5).reshape(-1, 3)] for _ in range(2)]
+    dims = [g[0][0].shape]
+    _, seg = bucket_layout(dims, 2, 4, 16)
+    ctx = F.Ctx(2, 0)
+    gd = DevArray(g[0][0])
+    b = F.Bucket(ctx, [(dims[0][0], dims[0][1], 0)], full_grads=[gd.ptr],
+                 grad_shards=[DevArray(nbytes=4 * 3 * 10).ptr], param_dtype=L.BF16, grad_dtype=L.BF16)
+    st = DevArray(nbytes=2 * seg, fill=0xEF, dtype=np.float32)
+    F.reduce_scatter_bucket(ctx, b, st.ptr, flags=L.ISSUE)
+    got = st.get()
+    ref = OC.rs_pack(g[0], 2, 16)
+    nan = np.isnan(ref)
+    assert np.array_equal(np.isnan(got), nan)
+    assert np.array_equal(bits(got[~nan]), bits(ref[~nan]))
+
+
+def test_llama8b_block_rs_pack_full_size():
+    # K4 on the full 8B block at N = 8 for two ranks, bit-exact; copy-out checked on rank 0
+    specs = llama("8b", n_layers=1, with_embeddings=False)
+    world = 8
+    dims = [(s.dim0, s.row_numel) for s in specs]
+    _, seg = bucket_layout(dims, world, 4, 16)
+    for r in (0, 5):
+        g = [grad_tensor(s, "bf16", 11, r) for s in specs]
+        ctx = F.Ctx(world, r)
+        gd = [DevArray(x) for x in g]
+        gs = [DevArray(nbytes=-(-d // world) * R * 4, dtype=np.float32, shape=(-(-d // world), R)) for d, R in dims]
+        b = F.Bucket(ctx, [(d, R, 0) for d, R in dims], full_grads=[x.ptr for x in gd],
+                     grad_shards=[x.ptr for x in gs], param_dtype=L.BF16, grad_dtype=L.BF16)
+        st = DevArray(nbytes=world * seg, fill=0xEF, dtype=np.float32)
+        F.reduce_scatter_bucket(ctx, b, st.ptr, flags=L.ISSUE | L.WAIT)  # layout-only: pack then copy-out
+        packed = st.get()
+        assert np.array_equal(bits(packed), bits(OC.rs_pack(g, world, 16)))
+        # with no collective the own segment holds this rank's pre-scaled chunk
+        own = packed[r * seg // 4:(r + 1) * seg // 4]
+        for j, sh in enumerate(OC.rs_copyout(own, dims, world, 16)):
+            assert np.array_equal(bits(gs[j].get()), bits(sh))
+        del gd, gs, st, b, ctx
+        torch.cuda.empty_cache()
+
+
+def test_405b_layer_allgather_64bit_offsets():
+    # BASELINE configs[4]: one 405B layer as one bucket at N = 8 (6.38 GB gathered,
+    # byte offsets beyond 2^32).  Filled on device; checked by the property
+    # all_gather(shard(p)) == p at full size plus oracle-computed sampled bytes.
+    specs = llama("405b", n_layers=1, with_embeddings=False)
+    world = 8
+    dims = [(s.dim0, s.row_numel) for s in specs]
+    descs = [(d, R, 0) for d, R in dims]
+    offs, seg = bucket_layout(dims, world, 2, 16)
+    assert world * seg > 2 ** 32
+    gen = torch.Generator(device="cuda").manual_seed(405)
+    fulls_src = [torch.randint(-32768, 32767, (d, R), dtype=torch.int16, device="cuda", generator=gen) for d, R in dims]
+    ctxs = [F.Ctx(world, r) for r in range(world)]
+    staging = torch.full((world * seg,), 0xCD, dtype=torch.uint8, device="cuda")
+    out = [torch.empty_like(x) for x in fulls_src]
+    buckets = []
+    for r in range(world):
+        sh = []
+        for (d, R), src in zip(dims, fulls_src):
+            c = -(-d // world)
+            s = torch.empty((c, R), dtype=torch.int16, device="cuda")
+            F.shard(world, r, (d, R, 0), L.BF16, src.data_ptr(), s.data_ptr())
+            sh.append(s)
+        b = F.Bucket(ctxs[r], descs, shards=[s.data_ptr() for s in sh],
+                     fulls=[o.data_ptr() for o in out], param_dtype=L.BF16)
+        F.allgather_bucket(ctxs[r], b, staging.data_ptr(), flags=L.ISSUE)
+        buckets.append((b, sh))
+    F.allgather_bucket(ctxs[0], buckets[0][0], staging.data_ptr(), flags=L.WAIT)
+    torch.cuda.synchronize()
+    for o, s in zip(out, fulls_src):
+        assert torch.equal(o, s)
+    # sampled staging bytes, located one by one with the oracle's layout
+    rng = np.random.Generator(np.random.Philox(9))
+    st16 = staging.view(torch.int16)
+    for _ in range(200):
+        q = int(rng.integers(0, world))
+        j = int(rng.integers(0, len(dims)))
+        d, R = dims[j]
+        c, begin, v = shard_rows(d, world, q)
+        row = int(rng.integers(0, c))
+        col = int(rng.integers(0, R))
+        pos = (q * seg + offs[j]) // 2 + row * R + col
+        want = int(fulls_src[j][begin + row, col]) if row < v else 0
+        assert int(st16[pos]) == want
+
+
+# ------------------------------------------------------------------ schedule
+def _schedule_case(world_comm):
+    specs = toy_mlp()
+    params = [param_tensor(p, "bf16", 50 + i) for i, p in enumerate(specs)]
+    grads = [grad_tensor(p, "bf16", 51, 0) for p in specs]
+    descs = [(p.dim0, p.row_numel, p.module_id) for p in specs]
+    if world_comm:
+        ctx = F.Ctx(1, 0, 0, nccl_uid=F.nccl_get_unique_id())
+    else:
+        ctx = F.Ctx(1, 0)
+    fb, _ = F.plan_buckets(descs, 1, [0] * 8, (0, 0), (0, 0), 0, L.PLAN_MANUAL, L.PHASE_FWD)
+    bb, _ = F.plan_buckets(descs, 1, [0] * 8, (0, 0), (0, 0), 0, L.PLAN_MANUAL, L.PHASE_BWD)
+    shards = [DevArray(p) for p in params]            # world 1: shard == param
+    fulls = [DevArray(nbytes=p.nbytes, fill=0x11, dtype=np.uint16, shape=p.shape) for p in params]
+    gd = [DevArray(g) for g in grads]
+    gs = [DevArray(nbytes=g.size * 4, fill=0x22, dtype=np.float32, shape=g.shape) for g in grads]
+
+    def mk(members):
+        m = sorted(members)
+        return F.Bucket(ctx, [descs[j] for j in m], shards=[shards[j].ptr for j in m],
+                        fulls=[fulls[j].ptr for j in m], full_grads=[gd[j].ptr for j in m],
+                        grad_shards=[gs[j].ptr for j in m])
+    fwd = [mk(b) for b in fb]
+    bwd = [mk(b) for b in bb]
+    big_ag = max(b.ag_seg for b in fwd + bwd)
+    big_rs = max(b.rs_seg for b in bwd)
+    ag = [DevArray(nbytes=big_ag) for _ in range(2)]
+    rs = [DevArray(nbytes=big_rs) for _ in range(2)]
+    return ctx, params, grads, fulls, gs, fwd, bwd, ag, rs
+
+
+@pytest.mark.parametrize("world_comm", [False, True])
+@pytest.mark.parametrize("flags", [0, L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT,
+                                   L.SCHED_REORDER | L.SCHED_BWD_AG_BEFORE_WAIT, L.SCHED_REORDER])
+def test_schedule_executes_and_logs(world_comm, flags):
+    ctx, params, grads, fulls, gs, fwd, bwd, ag, rs = _schedule_case(world_comm)
+    s = torch.cuda.Stream()
+    c = torch.cuda.Stream(priority=-1)
+    rep = F.run_schedule(ctx, fwd, bwd, ag_staging=(ag[0].ptr, ag[1].ptr), rs_staging=(rs[0].ptr, rs[1].ptr),
+                         compute=s.cuda_stream, comm=c.cuda_stream, flags=flags | L.SCHED_TIMING,
+                         proxy_iters_fwd=[1000] * len(fwd), proxy_iters_bwd=[2000] * len(bwd))
+    torch.cuda.synchronize()
+    want = OS.step_sequence(len(fwd), len(bwd), bool(flags & L.SCHED_REORDER),
+                            OS.BEFORE if flags & L.SCHED_FWD_AG_BEFORE_WAIT else OS.AFTER,
+                            OS.BEFORE if flags & L.SCHED_BWD_AG_BEFORE_WAIT else OS.AFTER)
+    assert [e[:4] for e in rep["log"]] == want
+    assert rep["step_ns"] > 0
+    assert rep["collectives"] == (len(fwd) + 2 * len(bwd) if world_comm else 0)
+    for f, p in zip(fulls, params):
+        assert np.array_equal(f.get(), p)
+    for g_out, g in zip(gs, grads):
+        assert np.array_equal(bits(g_out.get()), bits(OC.bf16.widen(g)))
+    ctx.close()
+
+
+def test_proxy_calibration_scales():
+    ctx = F.Ctx(1, 0)
+    t1 = F.proxy_calibrate(ctx, 20000)
+    t2 = F.proxy_calibrate(ctx, 40000)
+    assert t1 > 0 and 1.6 < t2 / t1 < 2.4
+
+
+def test_abi_rejects_misaligned_staging_and_foreign_bucket():
+    ctx, ctx2 = F.Ctx(2, 0), F.Ctx(2, 1)
+    p = DevArray(np.zeros((4, 4), np.uint16))
+    b = F.Bucket(ctx, [(8, 4, 0)], shards=[p.ptr], fulls=[p.ptr])
+    st = DevArray(nbytes=1024)
+    with pytest.raises(F.FsdpError):
+        F.allgather_bucket(ctx, b, st.ptr + 2)
+    with pytest.raises(F.FsdpError):
+        F.allgather_bucket(ctx2, b, st.ptr)
+    with pytest.raises(F.FsdpError):
+        F.reduce_scatter_bucket(ctx, b, st.ptr)  # created without gradient pointers
