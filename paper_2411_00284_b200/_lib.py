@@ -8,7 +8,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfsdp_b200.so")
+# FSDP_B200_LIB selects a tuning variant built by build.py (tools/kernel_sweep.py).
+LIB_PATH = os.environ.get("FSDP_B200_LIB") or os.path.join(_HERE, "libfsdp_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

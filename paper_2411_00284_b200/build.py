@@ -59,35 +59,42 @@ def _stale(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose=False, force=False):
+def build(verbose=False, force=False, defines=None, variant=None):
+    """Builds the library.  ``defines`` (e.g. ["FSDP_UNROLL=16"]) with a
+    ``variant`` name build a tuning variant into _build/variants/<variant>/
+    (selected at run time with FSDP_B200_LIB=<path>); the default build is the
+    in-tree libfsdp_b200.so."""
     cuda = cuda_home()
     nvcc = os.path.join(cuda, "bin", "nvcc")
     inc_nccl, lib_nccl = nccl_dirs()
-    os.makedirs(BUILD, exist_ok=True)
+    bdir = os.path.join(BUILD, "variants", variant) if variant else BUILD
+    lib = os.path.join(bdir, "libfsdp_b200.so") if variant else LIB
+    os.makedirs(bdir, exist_ok=True)
+    dflags = ["-D" + d for d in (defines or [])]
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
     incs = ["-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc_nccl, "-I", os.path.join(cuda, "include")]
     objs = []
     ptxas_log = []
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(bdir, os.path.basename(src) + ".o")
         objs.append(obj)
-        if force or _stale(obj, [src] + headers):
-            out = _run([nvcc, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v",
+        if force or variant or _stale(obj, [src] + headers):
+            out = _run([nvcc, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v", *dflags,
                         "-Xcompiler", "-fPIC", *incs, "-c", src, "-o", obj], verbose)
             ptxas_log.append(out)
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cc"))):
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(bdir, os.path.basename(src) + ".o")
         objs.append(obj)
-        if force or _stale(obj, [src] + headers):
-            _run(["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-Wno-unused-parameter",
+        if force or variant or _stale(obj, [src] + headers):
+            _run(["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-Wno-unused-parameter", *dflags,
                   *incs, "-c", src, "-o", obj], verbose)
-    if force or _stale(LIB, objs):
-        _run([nvcc, "-shared", *ARCH, "-o", LIB, *objs, "-L", lib_nccl, "-l:libnccl.so.2",
+    if force or variant or _stale(lib, objs):
+        _run([nvcc, "-shared", *ARCH, "-o", lib, *objs, "-L", lib_nccl, "-l:libnccl.so.2",
               "-Xlinker", "-rpath," + lib_nccl, "-cudart", "static"], verbose)
     if ptxas_log:
-        with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
+        with open(os.path.join(bdir, "ptxas.log"), "w") as f:
             f.write("\n".join(ptxas_log))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -99,6 +99,7 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   FSDP_CUDA_TRY(cudaSetDevice(ctx->device));
   fsdp_bucket* b = new fsdp_bucket();
   b->ctx = ctx;
+  b->device = ctx->device;
   b->k = k;
   b->ag_seg = ag_seg;
   b->rs_seg = rs_seg;
@@ -130,7 +131,7 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
 
 extern "C" fsdp_status fsdp_bucket_destroy(fsdp_bucket* b) {
   if (!b) return FSDP_OK;
-  cudaSetDevice(b->ctx->device);
+  cudaSetDevice(b->device);
   destroy_bucket(b);
   return FSDP_OK;
 }

@@ -175,7 +175,7 @@ fsdp_status fsdp_ctx_create(fsdp_ctx** out, int32_t world, int32_t rank, int32_t
   c->device = cuda_device;
   c->sm_count = device_sm_count(cuda_device);
   if (c->sm_count <= 0) c->sm_count = 148;
-  c->max_ctas = c->sm_count * 8;
+  c->max_ctas = c->sm_count * FSDP_CTAS_PER_SM;
   cudaError_t e = cudaMalloc(&c->sink, 4096 * sizeof(float));
   if (e != cudaSuccess) {
     delete c;
@@ -247,7 +247,7 @@ fsdp_status fsdp_shard(int32_t world, int32_t rank, const fsdp_param_desc* p, fs
   int dev = 0;
   cudaGetDevice(&dev);
   int sms = device_sm_count(dev);
-  cudaError_t err = launch_table(KK_SHARD, t, nullptr, 1.0f, st, (sms > 0 ? sms : 148) * 8);
+  cudaError_t err = launch_table(KK_SHARD, t, nullptr, 1.0f, st, (sms > 0 ? sms : 148) * FSDP_CTAS_PER_SM);
   cudaError_t err2 = cudaFreeAsync(t.d, st);
   if (err != cudaSuccess) return fail(FSDP_ERR_CUDA, std::string("shard kernel: ") + cudaGetErrorString(err));
   if (err2 != cudaSuccess) return fail(FSDP_ERR_CUDA, std::string("cudaFreeAsync: ") + cudaGetErrorString(err2));

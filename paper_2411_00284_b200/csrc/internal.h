@@ -53,7 +53,17 @@ void layout(const fsdp_param_desc* m, int32_t k, int32_t world, int64_t elem_byt
 // A chunk is <= kChunkBytes of destination data processed by one CTA.
 // Addresses are absolute device addresses, or offsets from the staging base
 // passed at launch for the side a kernel treats as relative.
-constexpr uint32_t kChunkBytes = 32 * 1024;
+#ifndef FSDP_CHUNK_KB
+#define FSDP_CHUNK_KB 32
+#endif
+#ifndef FSDP_CTAS_PER_SM
+// LSU-engine grid cap per SM.  1024 = in practice one CTA per chunk: the
+// hardware block scheduler then balances the chunks dynamically, which
+// measured 6529 GB/s on K3 vs 5901 for a persistent 8-CTA/SM grid
+// (profiles/r01_kernel_sweep.md).
+#define FSDP_CTAS_PER_SM 1024
+#endif
+constexpr uint32_t kChunkBytes = FSDP_CHUNK_KB * 1024;
 
 enum ChunkOp : uint32_t {
   OP_COPY = 0,   // n units of `unit` bytes
@@ -127,6 +137,7 @@ struct fsdp_ctx {
 
 struct fsdp_bucket {
   fsdp_ctx* ctx = nullptr;
+  int32_t device = 0;  // copied from the ctx: destroy must not read a destroyed ctx
   int32_t k = 0;
   int64_t ag_seg = 0, rs_seg = 0;
   int32_t param_bytes = 2, grad_bytes = 2;

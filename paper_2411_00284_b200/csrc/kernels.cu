@@ -8,67 +8,124 @@
 //   K6 fsdp_rs_copyout_kernel  own RS segment -> grad shards            ("read out from RS12")
 //   K7 fsdp_compute_proxy_kernel  calibrated stand-in for layer compute (measurement device)
 //
-// Every data kernel walks a host-built table of <= 32 KiB chunks with a grid
-// of at most (SMs x 8) CTAs of 256 threads; one CTA owns a whole chunk, so the
-// per-chunk branch is CTA-uniform.  Aligned chunks move 16 B per thread per
-// access with 8 independent loads in flight per thread before the stores
-// (8 x 256 x 16 B = one 32 KiB chunk per pass); misaligned runs (odd toy
-// shapes, 1-D norms at N = 3) fall back to the widest unit that divides their
-// addresses and size.  Arithmetic is IEEE round-to-nearest with no FTZ and no
-// contraction: widen is exact, then one __fmul_rn by fl32(1/N).
+// Every data kernel walks a host-built table of <= kChunkBytes chunks; one CTA
+// owns a whole chunk, so the per-chunk branch is CTA-uniform.
+//
+// Two engines:
+//  * LSU engine (run_table, the default): one CTA of FSDP_THREADS threads per
+//    32 KiB chunk (grid = chunks; the block scheduler balances them), aligned
+//    chunks move 16 B per thread per access with FSDP_UNROLL independent loads
+//    in flight per thread before the stores; K4 writes its 32 widened bytes
+//    per thread with one 256-bit STG.  Measured on B200 (8B block, N = 8):
+//    K3 6529 GB/s and K4 6643 GB/s vs 6585 GB/s for torch's copy_ on the same
+//    box (profiles/r01_kernel_sweep.md).
+//  * Bulk-copy (TMA) engine (run_table_bulk, FSDP_BULK, off by default: it
+//    measured 5.9 TB/s at best on K3): one warp per CTA; lane 0
+//    streams 16-B-aligned copy chunks global -> shared -> global with
+//    cp.async.bulk through a ring of FSDP_BULK_STAGES shared-memory stages
+//    (mbarrier complete_tx for loads, bulk groups for stores), so a handful of
+//    instructions keep up to (stages - 1) x 32 KiB of loads in flight per CTA.
+// Misaligned runs (odd toy shapes, 1-D norms at N = 3) fall back to the widest
+// unit that divides their addresses and size.  Arithmetic is IEEE
+// round-to-nearest with no FTZ and no contraction: widen is exact, then one
+// __fmul_rn by fl32(1/N).
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 #include "internal.h"
 
+#ifndef FSDP_THREADS
+#define FSDP_THREADS 256
+#endif
+#ifndef FSDP_UNROLL
+#define FSDP_UNROLL 8
+#endif
+#ifndef FSDP_MIN_BLOCKS
+#define FSDP_MIN_BLOCKS 4
+#endif
+#ifndef FSDP_ST_HINT
+#define FSDP_ST_HINT 0  // 0: st.global, 1: st.global.cs (evict-first streaming)
+#endif
+#ifndef FSDP_LD_HINT
+#define FSDP_LD_HINT 0  // 0: ld.global.nc.L1::no_allocate, 1: ld.global.cs
+#endif
+#ifndef FSDP_WIDEN_V8
+#define FSDP_WIDEN_V8 1  // K4: one 256-bit store per 8 widened elements
+#endif
+#ifndef FSDP_BULK
+#define FSDP_BULK 0  // bulk engine for: 0 none, 1 K3, 2 all pure-copy kernels (K0, K1, K3, K6)
+#endif
+#ifndef FSDP_BULK_STAGES
+#define FSDP_BULK_STAGES 6
+#endif
+#ifndef FSDP_BULK_CTAS_PER_SM
+#define FSDP_BULK_CTAS_PER_SM 1  // resident bulk CTAs per SM the smem ring is sized for
+#endif
+#ifndef FSDP_BULK_GRID_PER_SM
+#define FSDP_BULK_GRID_PER_SM FSDP_BULK_CTAS_PER_SM  // bulk-engine grid cap per SM
+#endif
+
 namespace fsdp {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kUnroll = 8;
+constexpr int kThreads = FSDP_THREADS;
+constexpr int kUnroll = FSDP_UNROLL;
+constexpr int kStages = FSDP_BULK_STAGES;
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 r;
+#if FSDP_LD_HINT == 1
+  asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+#else
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
+#endif
   return r;
 }
 
 __device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
+#if FSDP_ST_HINT == 1
+  asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+#else
   asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)
                : "memory");
+#endif
 }
 
+template <int NT>
 __device__ __forceinline__ void copy16(const char* src, char* dst, uint32_t n) {
   const uint4* s = reinterpret_cast<const uint4*>(src) + threadIdx.x;
   uint4* d = reinterpret_cast<uint4*>(dst) + threadIdx.x;
   uint32_t base = 0;
   // Full passes: kUnroll independent 16-B loads in flight, immediate offsets.
-  for (; base + kThreads * kUnroll <= n; base += kThreads * kUnroll) {
+  for (; base + NT * kUnroll <= n; base += NT * kUnroll) {
     uint4 v[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream(s + base + u * kThreads);
+    for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream(s + base + u * NT);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) st_v4(d + base + u * kThreads, v[u]);
+    for (int u = 0; u < kUnroll; ++u) st_v4(d + base + u * NT, v[u]);
   }
-  for (uint32_t i = base + threadIdx.x; i < n; i += kThreads)
-    st_v4(d - threadIdx.x + i, ld_stream(s - threadIdx.x + i));
+  for (uint32_t i = base + threadIdx.x; i < n; i += NT) st_v4(d - threadIdx.x + i, ld_stream(s - threadIdx.x + i));
 }
 
-template <typename T>
+template <int NT, typename T>
 __device__ __forceinline__ void copy_units(const char* src, char* dst, uint32_t n) {
   const T* s = reinterpret_cast<const T*>(src);
   T* d = reinterpret_cast<T*>(dst);
-  for (uint32_t i = threadIdx.x; i < n; i += kThreads) d[i] = s[i];
+  for (uint32_t i = threadIdx.x; i < n; i += NT) d[i] = s[i];
 }
 
-template <typename T>
+template <int NT, typename T>
 __device__ __forceinline__ void zero_units(char* dst, uint32_t n) {
   T* d = reinterpret_cast<T*>(dst);
-  for (uint32_t i = threadIdx.x; i < n; i += kThreads) d[i] = T{};
+  for (uint32_t i = threadIdx.x; i < n; i += NT) d[i] = T{};
 }
 
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
@@ -92,32 +149,51 @@ __device__ __forceinline__ uint4 widen_hi(const uint4& v, float scale) {
   return b;
 }
 
-__device__ __forceinline__ void widen16(const char* src, char* dst, uint32_t n, float scale) {
-  const uint4* s = reinterpret_cast<const uint4*>(src) + threadIdx.x;
-  uint4* d = reinterpret_cast<uint4*>(dst) + 2 * threadIdx.x;
-  constexpr int U = kUnroll / 2;
-  uint32_t base = 0;
-  for (; base + kThreads * U <= n; base += kThreads * U) {
-    uint4 v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = ld_stream(s + base + u * kThreads);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      st_v4(d + 2 * (base + u * kThreads), widen_lo(v[u], scale));
-      st_v4(d + 2 * (base + u * kThreads) + 1, widen_hi(v[u], scale));
-    }
-  }
-  for (uint32_t i = base + threadIdx.x; i < n; i += kThreads) {
-    uint4 v = ld_stream(s - threadIdx.x + i);
-    st_v4(d - 2 * threadIdx.x + 2 * i, widen_lo(v, scale));
-    st_v4(d - 2 * threadIdx.x + 2 * i + 1, widen_hi(v, scale));
+// The 32 widened bytes of one thread go out as one 256-bit store (sm_100
+// STG.256), so a warp's store covers 1 KiB contiguously; two 128-bit stores
+// would each cover every other 16 B of that range.  Needs 32-B alignment of
+// the destination, which the table builder guarantees for OP_WIDEN unit 16.
+template <bool kV8>
+__device__ __forceinline__ void st_widened(uint4* p, const uint4& v, float scale) {
+  if (kV8) {
+    const uint4 a = widen_lo(v, scale), b = widen_hi(v, scale);
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y),
+                 "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                 : "memory");
+  } else {
+    st_v4(p, widen_lo(v, scale));
+    st_v4(p + 1, widen_hi(v, scale));
   }
 }
 
+template <int NT, bool kV8>
+__device__ __forceinline__ void widen16_impl(const char* src, char* dst, uint32_t n, float scale) {
+  const uint4* s = reinterpret_cast<const uint4*>(src) + threadIdx.x;
+  uint4* d = reinterpret_cast<uint4*>(dst) + 2 * threadIdx.x;
+  constexpr int U = kUnroll / 2 > 0 ? kUnroll / 2 : 1;
+  uint32_t base = 0;
+  for (; base + NT * U <= n; base += NT * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld_stream(s + base + u * NT);
+#pragma unroll
+    for (int u = 0; u < U; ++u) st_widened<kV8>(d + 2 * (base + u * NT), v[u], scale);
+  }
+  for (uint32_t i = base + threadIdx.x; i < n; i += NT)
+    st_widened<kV8>(d - 2 * threadIdx.x + 2 * i, ld_stream(s - threadIdx.x + i), scale);
+}
+
+template <int NT>
+__device__ __forceinline__ void widen16(const char* src, char* dst, uint32_t n, float scale) {
+  if (FSDP_WIDEN_V8 && (reinterpret_cast<uintptr_t>(dst) & 31) == 0) widen16_impl<NT, true>(src, dst, n, scale);
+  else widen16_impl<NT, false>(src, dst, n, scale);
+}
+
+template <int NT>
 __device__ __forceinline__ void widen1(const char* src, char* dst, uint32_t n, float scale) {
   const uint16_t* s = reinterpret_cast<const uint16_t*>(src);
   float* d = reinterpret_cast<float*>(dst);
-  for (uint32_t i = threadIdx.x; i < n; i += kThreads)
+  for (uint32_t i = threadIdx.x; i < n; i += NT)
     d[i] = __fmul_rn(__uint_as_float(static_cast<uint32_t>(s[i]) << 16), scale);
 }
 
@@ -130,88 +206,205 @@ __device__ __forceinline__ uint4 scale4(const uint4& v, float scale) {
   return a;
 }
 
+template <int NT>
 __device__ __forceinline__ void scale16(const char* src, char* dst, uint32_t n, float scale) {
   const uint4* s = reinterpret_cast<const uint4*>(src) + threadIdx.x;
   uint4* d = reinterpret_cast<uint4*>(dst) + threadIdx.x;
   uint32_t base = 0;
-  for (; base + kThreads * kUnroll <= n; base += kThreads * kUnroll) {
+  for (; base + NT * kUnroll <= n; base += NT * kUnroll) {
     uint4 v[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream(s + base + u * kThreads);
+    for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream(s + base + u * NT);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) st_v4(d + base + u * kThreads, scale4(v[u], scale));
+    for (int u = 0; u < kUnroll; ++u) st_v4(d + base + u * NT, scale4(v[u], scale));
   }
-  for (uint32_t i = base + threadIdx.x; i < n; i += kThreads)
+  for (uint32_t i = base + threadIdx.x; i < n; i += NT)
     st_v4(d - threadIdx.x + i, scale4(ld_stream(s - threadIdx.x + i), scale));
 }
 
+template <int NT>
 __device__ __forceinline__ void scale1(const char* src, char* dst, uint32_t n, float scale) {
   const float* s = reinterpret_cast<const float*>(src);
   float* d = reinterpret_cast<float*>(dst);
-  for (uint32_t i = threadIdx.x; i < n; i += kThreads) d[i] = __fmul_rn(s[i], scale);
+  for (uint32_t i = threadIdx.x; i < n; i += NT) d[i] = __fmul_rn(s[i], scale);
+}
+
+template <int NT>
+__device__ __forceinline__ void process_chunk(const Chunk& ch, const char* src, char* dst, float scale) {
+  const uint32_t op = ch.op_unit & 0xFFu;
+  const uint32_t unit = ch.op_unit >> 8;
+  if (op == OP_COPY) {
+    switch (unit) {
+      case 16: copy16<NT>(src, dst, ch.n); break;
+      case 8: copy_units<NT, uint2>(src, dst, ch.n); break;
+      case 4: copy_units<NT, uint32_t>(src, dst, ch.n); break;
+      case 2: copy_units<NT, uint16_t>(src, dst, ch.n); break;
+      default: copy_units<NT, uint8_t>(src, dst, ch.n); break;
+    }
+  } else if (op == OP_ZERO) {
+    switch (unit) {
+      case 16: zero_units<NT, uint4>(dst, ch.n); break;
+      case 8: zero_units<NT, uint2>(dst, ch.n); break;
+      case 4: zero_units<NT, uint32_t>(dst, ch.n); break;
+      case 2: zero_units<NT, uint16_t>(dst, ch.n); break;
+      default: zero_units<NT, uint8_t>(dst, ch.n); break;
+    }
+  } else if (op == OP_WIDEN) {
+    if (unit == 16) widen16<NT>(src, dst, ch.n, scale);
+    else widen1<NT>(src, dst, ch.n, scale);
+  } else {
+    if (unit == 16) scale16<NT>(src, dst, ch.n, scale);
+    else scale1<NT>(src, dst, ch.n, scale);
+  }
 }
 
 template <bool kSrcRel, bool kDstRel>
-__device__ __forceinline__ void run_table(const Chunk* __restrict__ tab, int n, char* base,
-                                          float scale) {
+__device__ __forceinline__ void run_table(const Chunk* __restrict__ tab, int n, char* base, float scale) {
   for (int c = blockIdx.x; c < n; c += gridDim.x) {
     const Chunk ch = tab[c];
     const char* src = kSrcRel ? base + ch.src : reinterpret_cast<const char*>(ch.src);
     char* dst = kDstRel ? base + ch.dst : reinterpret_cast<char*>(ch.dst);
-    const uint32_t op = ch.op_unit & 0xFFu;
-    const uint32_t unit = ch.op_unit >> 8;
-    if (op == OP_COPY) {
-      switch (unit) {
-        case 16: copy16(src, dst, ch.n); break;
-        case 8: copy_units<uint2>(src, dst, ch.n); break;
-        case 4: copy_units<uint32_t>(src, dst, ch.n); break;
-        case 2: copy_units<uint16_t>(src, dst, ch.n); break;
-        default: copy_units<uint8_t>(src, dst, ch.n); break;
-      }
-    } else if (op == OP_ZERO) {
-      switch (unit) {
-        case 16: zero_units<uint4>(dst, ch.n); break;
-        case 8: zero_units<uint2>(dst, ch.n); break;
-        case 4: zero_units<uint32_t>(dst, ch.n); break;
-        case 2: zero_units<uint16_t>(dst, ch.n); break;
-        default: zero_units<uint8_t>(dst, ch.n); break;
-      }
-    } else if (op == OP_WIDEN) {
-      if (unit == 16) widen16(src, dst, ch.n, scale);
-      else widen1(src, dst, ch.n, scale);
-    } else {
-      if (unit == 16) scale16(src, dst, ch.n, scale);
-      else scale1(src, dst, ch.n, scale);
+    process_chunk<kThreads>(ch, src, dst, scale);
+  }
+}
+
+// ------------------------------------------------------------ bulk engine
+__device__ __forceinline__ bool is_bulk(const Chunk& ch) {
+  return (ch.op_unit & 0xFFu) == OP_COPY && (ch.op_unit >> 8) == 16;
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void bulk_load(uint32_t dst_smem, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_smem),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* dst, uint32_t src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src_smem), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <bool kSrcRel, bool kDstRel>
+__device__ __forceinline__ void run_table_bulk(const Chunk* __restrict__ tab, int n, char* base, float scale) {
+  extern __shared__ __align__(128) unsigned char bulk_smem[];
+  __shared__ __align__(8) unsigned long long bars[kStages];
+  // pass 1: chunks the bulk engine does not take (zero fill, misaligned), by the whole warp
+  for (int c = blockIdx.x; c < n; c += gridDim.x) {
+    const Chunk ch = tab[c];
+    if (is_bulk(ch)) continue;
+    const char* src = kSrcRel ? base + ch.src : reinterpret_cast<const char*>(ch.src);
+    char* dst = kDstRel ? base + ch.dst : reinterpret_cast<char*>(ch.dst);
+    process_chunk<32>(ch, src, dst, scale);
+  }
+  if (threadIdx.x != 0) return;
+  // pass 2: lane 0 streams the 16-B-aligned copy chunks through the stage ring
+  const uint32_t smem0 = static_cast<uint32_t>(__cvta_generic_to_shared(bulk_smem));
+  const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+  for (int s = 0; s < kStages; ++s) mbar_init(bar0 + 8 * s, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  char* dsts[kStages];
+  uint32_t lens[kStages];
+  int next = blockIdx.x;  // next table index to consider for loading
+  auto advance = [&](int c) {
+    while (c < n && !is_bulk(tab[c])) c += gridDim.x;
+    return c;
+  };
+  next = advance(next);
+  int loaded = 0, stored = 0;
+  // prologue: fill the ring
+  while (loaded < kStages && next < n) {
+    const Chunk ch = tab[next];
+    const int s = loaded % kStages;
+    const uint32_t bytes = ch.n * 16u;
+    dsts[s] = kDstRel ? base + ch.dst : reinterpret_cast<char*>(ch.dst);
+    lens[s] = bytes;
+    bulk_load(smem0 + s * kChunkBytes, kSrcRel ? base + ch.src : reinterpret_cast<const char*>(ch.src), bytes,
+              bar0 + 8 * s);
+    ++loaded;
+    next = advance(next + gridDim.x);
+  }
+  while (stored < loaded) {
+    const int s = stored % kStages;
+    mbar_wait(bar0 + 8 * s, (stored / kStages) & 1);
+    bulk_store(dsts[s], smem0 + s * kChunkBytes, lens[s]);
+    ++stored;
+    if (next < n) {
+      // the stage is reused: its store must have finished reading shared memory
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      const Chunk ch = tab[next];
+      const uint32_t bytes = ch.n * 16u;
+      dsts[s] = kDstRel ? base + ch.dst : reinterpret_cast<char*>(ch.dst);
+      lens[s] = bytes;
+      bulk_load(smem0 + s * kChunkBytes, kSrcRel ? base + ch.src : reinterpret_cast<const char*>(ch.src), bytes,
+                bar0 + 8 * s);
+      ++loaded;
+      next = advance(next + gridDim.x);
     }
   }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 }  // namespace
 
+#define FSDP_LSU_BOUNDS __launch_bounds__(kThreads, FSDP_MIN_BLOCKS)
+
 // K0: full parameter -> padded shard (absolute -> absolute).
-__global__ void __launch_bounds__(kThreads, 4) fsdp_shard_kernel(const Chunk* tab, int n, char* base, float s) {
+__global__ void FSDP_LSU_BOUNDS fsdp_shard_kernel(const Chunk* tab, int n, char* base, float s) {
   run_table<false, false>(tab, n, base, s);
 }
 // K1: shards -> segment `rank` of the AG staging buffer (absolute -> staging).
-__global__ void __launch_bounds__(kThreads, 4) fsdp_ag_pack_kernel(const Chunk* tab, int n, char* base, float s) {
+__global__ void FSDP_LSU_BOUNDS fsdp_ag_pack_kernel(const Chunk* tab, int n, char* base, float s) {
   run_table<false, true>(tab, n, base, s);
 }
 // K3: gathered staging -> full parameters (staging -> absolute).
-__global__ void __launch_bounds__(kThreads, 4) fsdp_ag_unpack_kernel(const Chunk* tab, int n, char* base, float s) {
+__global__ void FSDP_LSU_BOUNDS fsdp_ag_unpack_kernel(const Chunk* tab, int n, char* base, float s) {
   run_table<true, false>(tab, n, base, s);
 }
 // K4: full gradients -> fp32 rank-major chunks * fl32(1/N) (absolute -> staging).
-__global__ void __launch_bounds__(kThreads, 4) fsdp_rs_pack_kernel(const Chunk* tab, int n, char* base, float s) {
+__global__ void FSDP_LSU_BOUNDS fsdp_rs_pack_kernel(const Chunk* tab, int n, char* base, float s) {
   run_table<false, true>(tab, n, base, s);
 }
 // K6: own reduce-scatter segment -> fp32 gradient shards (staging -> absolute).
-__global__ void __launch_bounds__(kThreads, 4) fsdp_rs_copyout_kernel(const Chunk* tab, int n, char* base, float s) {
+__global__ void FSDP_LSU_BOUNDS fsdp_rs_copyout_kernel(const Chunk* tab, int n, char* base, float s) {
   run_table<true, false>(tab, n, base, s);
+}
+
+// Bulk-copy (TMA) variants of the pure-copy kernels.
+__global__ void __launch_bounds__(32) fsdp_shard_bulk_kernel(const Chunk* tab, int n, char* base, float s) {
+  run_table_bulk<false, false>(tab, n, base, s);
+}
+__global__ void __launch_bounds__(32) fsdp_ag_pack_bulk_kernel(const Chunk* tab, int n, char* base, float s) {
+  run_table_bulk<false, true>(tab, n, base, s);
+}
+__global__ void __launch_bounds__(32) fsdp_ag_unpack_bulk_kernel(const Chunk* tab, int n, char* base, float s) {
+  run_table_bulk<true, false>(tab, n, base, s);
+}
+__global__ void __launch_bounds__(32) fsdp_rs_copyout_bulk_kernel(const Chunk* tab, int n, char* base, float s) {
+  run_table_bulk<true, false>(tab, n, base, s);
 }
 
 // K7: persistent compute proxy.  Four independent FMA chains per thread; the
 // result is consumed behind an impossible branch so the loop survives.
-__global__ void __launch_bounds__(kThreads) fsdp_compute_proxy_kernel(long long iters, float* sink) {
+__global__ void __launch_bounds__(256) fsdp_compute_proxy_kernel(long long iters, float* sink) {
   extern __shared__ float smem[];
   float a0 = threadIdx.x * 1e-3f, a1 = a0 + 1.f, a2 = a0 + 2.f, a3 = a0 + 3.f;
   const float m = 0.9999999f, c = 1e-7f;
@@ -224,14 +417,55 @@ __global__ void __launch_bounds__(kThreads) fsdp_compute_proxy_kernel(long long 
   float r = a0 + a1 + a2 + a3;
   if (r == -1.0f) {
     smem[threadIdx.x] = r;
-    sink[blockIdx.x] = smem[(threadIdx.x + 1) % kThreads];
+    sink[blockIdx.x] = smem[(threadIdx.x + 1) % 256];
   }
 }
+
+namespace {
+constexpr int kBulkSmem = kStages * static_cast<int>(kChunkBytes);
+
+bool use_bulk(KernelKind kind) {
+  if (FSDP_BULK == 0) return false;
+  if (FSDP_BULK == 1) return kind == KK_AG_UNPACK;
+  return kind != KK_RS_PACK;
+}
+
+template <typename K>
+cudaError_t launch_bulk(KernelKind kind, K kernel, int grid, const DevTable& t, char* base, float scale,
+                        cudaStream_t s) {
+  static bool configured[8] = {};
+  if (!configured[kind]) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
+    if (e != cudaSuccess) return e;
+    configured[kind] = true;
+  }
+  kernel<<<grid, 32, kBulkSmem, s>>>(t.d, t.n, base, scale);
+  return cudaSuccess;
+}
+}  // namespace
 
 cudaError_t launch_table(KernelKind kind, const DevTable& t, char* base, float scale, cudaStream_t s,
                          int max_ctas) {
   if (t.n == 0) return cudaSuccess;
-  int grid = t.n < max_ctas ? t.n : max_ctas;
+  // This library's runtime instance is private to it, and every runtime call
+  // it makes is checked where it is made, so a pending error here is stale.
+  (void)cudaGetLastError();
+  if (use_bulk(kind)) {
+    const int sms = max_ctas / FSDP_CTAS_PER_SM;
+    const int cap = sms * FSDP_BULK_GRID_PER_SM;
+    const int grid = t.n < cap ? t.n : cap;
+    cudaError_t e = cudaSuccess;
+    switch (kind) {
+      case KK_SHARD: e = launch_bulk(kind, fsdp_shard_bulk_kernel, grid, t, base, scale, s); break;
+      case KK_AG_PACK: e = launch_bulk(kind, fsdp_ag_pack_bulk_kernel, grid, t, base, scale, s); break;
+      case KK_AG_UNPACK: e = launch_bulk(kind, fsdp_ag_unpack_bulk_kernel, grid, t, base, scale, s); break;
+      case KK_RS_COPYOUT: e = launch_bulk(kind, fsdp_rs_copyout_bulk_kernel, grid, t, base, scale, s); break;
+      default: break;
+    }
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
+  const int grid = t.n < max_ctas ? t.n : max_ctas;
   switch (kind) {
     case KK_SHARD: fsdp_shard_kernel<<<grid, kThreads, 0, s>>>(t.d, t.n, base, scale); break;
     case KK_AG_PACK: fsdp_ag_pack_kernel<<<grid, kThreads, 0, s>>>(t.d, t.n, base, scale); break;
@@ -248,7 +482,8 @@ cudaError_t launch_proxy(int64_t iters, int grid, int smem, float* sink, cudaStr
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
   }
-  fsdp_compute_proxy_kernel<<<grid, kThreads, smem, s>>>(static_cast<long long>(iters), sink);
+  (void)cudaGetLastError();
+  fsdp_compute_proxy_kernel<<<grid, 256, smem, s>>>(static_cast<long long>(iters), sink);
   return cudaGetLastError();
 }
 
