@@ -358,6 +358,7 @@ def main():
             "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": ncu_traffic(names[dom]),
+                         "traffic_launch_algorithmic_bytes": ncu_traffic(names[dom] + "_algorithmic"),
                          "algorithmic_bytes_per_launch": kbytes[dom] // max(1, op_cnt[dom] // args.steps)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
