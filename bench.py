@@ -282,16 +282,17 @@ def main():
     # per-op device time from the timed steps' events -> dominant data kernel
     op_ns = [sum(r["op_ns"][i] for r in reports) for i in range(L.N_OPS)]
     op_cnt = [sum(r["op_count"][i] for r in reports) for i in range(L.N_OPS)]
-    kbytes = st.kernel_bytes()
+    kbytes, klaunch = st.kernel_bytes(), st.kernel_launches()
     names = {L.OP_PACK_AG: "fsdp_ag_pack_kernel", L.OP_UNPACK: "fsdp_ag_unpack_kernel",
              L.OP_PACK_RS: "fsdp_rs_pack_kernel", L.OP_COPYOUT_RS: "fsdp_rs_copyout_kernel"}
-    dom = max(kbytes, key=lambda op: op_ns[op])
+    live = [op for op in kbytes if kbytes[op] > 0 and op_ns[op] > 0]
+    dom = max(live, key=lambda op: op_ns[op])
     peak, peak_src = measured_peak_hbm()
     achieved = kbytes[dom] * args.steps / (op_ns[dom] * 1e-9) / 1e9
     per_kernel = {names[op]: {"GB/s": round(kbytes[op] * args.steps / (op_ns[op] * 1e-9) / 1e9, 1),
                               "ms_per_step": round(op_ns[op] / args.steps / 1e6, 3),
-                              "launches_per_step": op_cnt[op] // args.steps,
-                              "bytes_per_step": kbytes[op]} for op in kbytes if op_ns[op] > 0}
+                              "launches_per_step": klaunch[op],
+                              "bytes_per_step": kbytes[op]} for op in live}
     launches = sum(r["kernel_launches"] for r in reports)
     coll_ms = {"ag_ms_per_step": round(op_ns[L.OP_AG] / args.steps / 1e6, 3),
                "rs_ms_per_step": round(op_ns[L.OP_RS] / args.steps / 1e6, 3)}
@@ -359,7 +360,8 @@ def main():
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": ncu_traffic(names[dom]),
                          "traffic_launch_algorithmic_bytes": ncu_traffic(names[dom] + "_algorithmic"),
-                         "algorithmic_bytes_per_launch": kbytes[dom] // max(1, op_cnt[dom] // args.steps)},
+                         "algorithmic_bytes_per_launch": kbytes[dom] // max(1, klaunch[dom])},
+            "zero_copy": st.zero_copy(),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
         }

@@ -205,11 +205,41 @@ typedef struct {
   int32_t align_bytes;
   int32_t param_dtype; /* fsdp_dtype */
   int32_t grad_dtype;  /* fsdp_dtype of full_grads */
+  uint32_t flags;      /* FSDP_BUCKET_* below, 0 = plain pointers */
+  int32_t reserved;    /* must be 0 */
 } fsdp_bucket_desc;
+
+/* Bucket flags: the caller's storage already is this rank's segment (see
+ * "Segment-layout storage" below); validated, FSDP_ERR_INVALID_ARG if the
+ * pointers do not follow fsdp_layout's offsets. */
+enum { FSDP_BUCKET_SEGMENT_SHARDS = 1u, FSDP_BUCKET_SEGMENT_GRAD_SHARDS = 2u };
 
 fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc* desc, fsdp_bucket** out,
                                int64_t* ag_seg_bytes, int64_t* rs_seg_bytes);
 fsdp_status fsdp_bucket_destroy(fsdp_bucket* b);
+
+/* Segment-layout ("zero-copy") storage, FSDP_BUCKET_SEGMENT_SHARDS: the caller
+ * keeps this rank's shards at shards[j] == shards[0] + off_j (off_j = the AG
+ * segment offsets of fsdp_layout, shards[0] 16-B aligned), so the storage
+ * already is this rank's AG segment: ISSUE launches no pack kernel and the
+ * all-gather sends from the storage (out of place; a layout-only ctx's ISSUE
+ * then writes nothing); WAIT copies this rank's rows straight from it.
+ * FSDP_BUCKET_SEGMENT_GRAD_SHARDS: grad_shards[j] == grad_shards[0] + off'_j
+ * (RS segment offsets): the reduce-scatter of a ctx with a communicator writes
+ * the averaged gradients directly into the storage (WAIT launches no copy-out;
+ * a layout-only ctx still copies its own segment there).  fsdp_bucket_create
+ * zeroes the alignment-gap bytes between members of such storage once
+ * (synchronously, on the legacy stream).  Reported by fsdp_bucket_query. */
+typedef struct {
+  int64_t ag_seg_bytes;
+  int64_t rs_seg_bytes;
+  int64_t kernel_bytes[4]; /* algorithmic HBM bytes per launch of K1 pack, K3 unpack,
+                              K4 grad pack, K6 copy-out (0 = kernel not launched) */
+  int32_t kernel_chunks[4];
+  int32_t ag_zero_copy;
+  int32_t rs_zero_copy;
+} fsdp_bucket_info;
+fsdp_status fsdp_bucket_query(const fsdp_bucket* b, fsdp_bucket_info* out);
 
 /* ------------------------------------------ 3. fsdp_allgather_bucket
  * copy-in ("flattens and concatenates"), one all-gather AG + wait Wa,

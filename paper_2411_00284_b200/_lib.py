@@ -29,11 +29,12 @@ ISSUE, WAIT = 1, 2
 N_OPS = 10
 SCHED_REORDER, SCHED_FWD_AG_BEFORE_WAIT, SCHED_BWD_AG_BEFORE_WAIT = 1, 2, 4
 SCHED_NO_COMM, SCHED_DRY_RUN, SCHED_TIMING = 8, 16, 32
+BUCKET_SEGMENT_SHARDS, BUCKET_SEGMENT_GRAD_SHARDS = 1, 2
 
 EXPORTED = [
     "fsdp_last_error", "fsdp_abi_version", "fsdp_nccl_get_unique_id", "fsdp_ctx_create",
     "fsdp_ctx_destroy", "fsdp_shard", "fsdp_plan_buckets", "fsdp_layout", "fsdp_bucket_create",
-    "fsdp_bucket_destroy", "fsdp_allgather_bucket", "fsdp_reduce_scatter_bucket",
+    "fsdp_bucket_destroy", "fsdp_bucket_query", "fsdp_allgather_bucket", "fsdp_reduce_scatter_bucket",
     "fsdp_run_schedule", "fsdp_proxy_launch", "fsdp_proxy_calibrate",
 ]
 
@@ -70,7 +71,13 @@ class BucketDesc(C.Structure):
     _fields_ = [("params", C.POINTER(ParamDesc)), ("shards", C.POINTER(C.c_void_p)),
                 ("fulls", C.POINTER(C.c_void_p)), ("full_grads", C.POINTER(C.c_void_p)),
                 ("grad_shards", C.POINTER(C.c_void_p)), ("k", C.c_int32), ("align_bytes", C.c_int32),
-                ("param_dtype", C.c_int32), ("grad_dtype", C.c_int32)]
+                ("param_dtype", C.c_int32), ("grad_dtype", C.c_int32), ("flags", C.c_uint32),
+                ("reserved", C.c_int32)]
+
+
+class BucketInfo(C.Structure):
+    _fields_ = [("ag_seg_bytes", C.c_int64), ("rs_seg_bytes", C.c_int64), ("kernel_bytes", C.c_int64 * 4),
+                ("kernel_chunks", C.c_int32 * 4), ("ag_zero_copy", C.c_int32), ("rs_zero_copy", C.c_int32)]
 
 
 class Schedule(C.Structure):
@@ -110,6 +117,7 @@ _sigs = {
     "fsdp_bucket_create": (C.c_int, [_P, C.POINTER(BucketDesc), C.POINTER(_P), C.POINTER(C.c_int64),
                                      C.POINTER(C.c_int64)]),
     "fsdp_bucket_destroy": (C.c_int, [_P]),
+    "fsdp_bucket_query": (C.c_int, [_P, C.POINTER(BucketInfo)]),
     "fsdp_allgather_bucket": (C.c_int, [_P, _P, _P, _P, _P, C.c_uint32]),
     "fsdp_reduce_scatter_bucket": (C.c_int, [_P, _P, _P, _P, _P, C.c_uint32]),
     "fsdp_run_schedule": (C.c_int, [_P, C.POINTER(Schedule), C.POINTER(StepReport)]),

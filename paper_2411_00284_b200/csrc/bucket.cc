@@ -40,6 +40,8 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   const int32_t k = d->k;
   if (k < 1 || !d->params) return fail(FSDP_ERR_INVALID_ARG, "bucket needs >= 1 member");
   if (d->align_bytes < 1) return fail(FSDP_ERR_INVALID_ARG, "align_bytes < 1");
+  if (d->reserved != 0 || (d->flags & ~(FSDP_BUCKET_SEGMENT_SHARDS | FSDP_BUCKET_SEGMENT_GRAD_SHARDS)))
+    return fail(FSDP_ERR_INVALID_ARG, "unknown bucket flags");
   const int32_t ep = dtype_bytes(d->param_dtype), eg = dtype_bytes(d->grad_dtype);
   if (!ep || !eg) return fail(FSDP_ERR_INVALID_ARG, "unsupported dtype");
   for (int32_t j = 0; j < k; ++j) {
@@ -58,7 +60,33 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   layout(d->params, k, N, ep, d->align_bytes, ag_off.data(), &ag_seg);
   layout(d->params, k, N, 4, d->align_bytes, rs_off.data(), &rs_seg);
 
-  TableBuilder pack, unpack, rpack, rcopy;
+  // Segment-layout storage ("zero-copy"): if the caller keeps this rank's
+  // shards exactly where its AG segment would hold them (shards[j] ==
+  // shards[0] + off_j), the segment already exists in memory: ISSUE needs no
+  // pack (the all-gather sends from the storage, out of place) and WAIT reads
+  // this rank's rows straight from it.  Likewise gradient shards stored at
+  // grad_shards[0] + off'_j let the reduce-scatter write its result in place
+  // of the copy-out (with a communicator).  The alignment gaps of such
+  // storage are zeroed once here, so the bytes on the wire match the packed
+  // form.
+  const bool ag_zc = d->flags & FSDP_BUCKET_SEGMENT_SHARDS;
+  const bool rs_zc = d->flags & FSDP_BUCKET_SEGMENT_GRAD_SHARDS;
+  if ((ag_zc && !d->shards) || (rs_zc && !d->grad_shards))
+    return fail(FSDP_ERR_INVALID_ARG, "segment-layout flag without the matching pointer array");
+  if ((ag_zc && reinterpret_cast<uintptr_t>(d->shards[0]) % 16) ||
+      (rs_zc && reinterpret_cast<uintptr_t>(d->grad_shards[0]) % 16))
+    return fail(FSDP_ERR_INVALID_ARG, "segment-layout storage not 16-B aligned");
+  for (int32_t j = 0; j < k; ++j) {
+    if (ag_zc && reinterpret_cast<uintptr_t>(d->shards[j]) !=
+                     reinterpret_cast<uintptr_t>(d->shards[0]) + static_cast<uintptr_t>(ag_off[j]))
+      return fail(FSDP_ERR_INVALID_ARG, "FSDP_BUCKET_SEGMENT_SHARDS: shards do not follow the segment offsets");
+    if (rs_zc && reinterpret_cast<uintptr_t>(d->grad_shards[j]) !=
+                     reinterpret_cast<uintptr_t>(d->grad_shards[0]) + static_cast<uintptr_t>(rs_off[j]))
+      return fail(FSDP_ERR_INVALID_ARG,
+                  "FSDP_BUCKET_SEGMENT_GRAD_SHARDS: grad shards do not follow the segment offsets");
+  }
+
+  TableBuilder pack, unpack, rpack, rcopy, gaps;
   for (int32_t j = 0; j < k; ++j) {
     const fsdp_param_desc& p = d->params[j];
     const ShardRows own = shard_rows(p.dim0, N, r);
@@ -66,19 +94,30 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
     const int64_t ag_end = (j + 1 < k) ? ag_off[j + 1] : ag_seg;
     const int64_t rs_end = (j + 1 < k) ? rs_off[j + 1] : rs_seg;
     if (d->shards) {
-      // K1: this rank's whole padded shard into segment r, alignment gap zeroed.
-      const uint64_t dst = static_cast<uint64_t>(r * ag_seg + ag_off[j]);
       const int64_t nb = own.c * R * ep;
-      pack.copy(reinterpret_cast<uint64_t>(d->shards[j]), dst, nb);
-      pack.zero(dst + nb, ag_end - ag_off[j] - nb);
+      if (ag_zc) {
+        gaps.zero(reinterpret_cast<uint64_t>(d->shards[0]) + ag_off[j] + nb, ag_end - ag_off[j] - nb);
+      } else {
+        // K1: this rank's whole padded shard into segment r, alignment gap zeroed.
+        const uint64_t dst = static_cast<uint64_t>(r * ag_seg + ag_off[j]);
+        pack.copy(reinterpret_cast<uint64_t>(d->shards[j]), dst, nb);
+        pack.zero(dst + nb, ag_end - ag_off[j] - nb);
+      }
+    }
+    if (rs_zc) {
+      const int64_t nb = own.c * R * 4;
+      gaps.zero(reinterpret_cast<uint64_t>(d->grad_shards[0]) + rs_off[j] + nb, rs_end - rs_off[j] - nb);
     }
     for (int32_t q = 0; q < N; ++q) {
       const ShardRows s = shard_rows(p.dim0, N, q);
       if (d->fulls && s.v > 0) {
-        // K3: valid rows of rank q's chunk -> rows [q c, q c + v) of the full param.
-        unpack.copy(static_cast<uint64_t>(q * ag_seg + ag_off[j]),
-                    reinterpret_cast<uint64_t>(d->fulls[j]) + static_cast<uint64_t>(s.begin * R * ep),
-                    s.v * R * ep);
+        // K3: valid rows of rank q's chunk -> rows [q c, q c + v) of the full param
+        // (this rank's rows from its segment-layout storage when zero-copy).
+        const uint64_t dst = reinterpret_cast<uint64_t>(d->fulls[j]) + static_cast<uint64_t>(s.begin * R * ep);
+        if (ag_zc && q == r)
+          unpack.copy(reinterpret_cast<uint64_t>(d->shards[j]), dst, s.v * R * ep, kAbsSrc);
+        else
+          unpack.copy(static_cast<uint64_t>(q * ag_seg + ag_off[j]), dst, s.v * R * ep);
       }
       if (d->full_grads) {
         // K4: rows of chunk q, widened and scaled, into segment q; pads +0.0.
@@ -109,7 +148,22 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   b->has_fulls = d->fulls != nullptr;
   b->has_grads = d->full_grads != nullptr;
   b->has_gshards = d->grad_shards != nullptr;
+  b->ag_zero_copy = ag_zc;
+  b->rs_zero_copy = rs_zc;
+  b->shard_seg = ag_zc ? static_cast<char*>(d->shards[0]) : nullptr;
+  b->gshard_seg = rs_zc ? static_cast<char*>(d->grad_shards[0]) : nullptr;
   fsdp_status st = FSDP_OK;
+  if (!gaps.chunks.empty()) {
+    // one-time zero fill of the storage's alignment gaps (setup, synchronous)
+    DevTable g;
+    st = upload(gaps, &g);
+    if (st == FSDP_OK) {
+      cudaError_t e = launch_table(KK_SHARD, g, nullptr, 1.0f, nullptr, ctx->max_ctas);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
+      if (e != cudaSuccess) st = fail(FSDP_ERR_CUDA, std::string("gap fill: ") + cudaGetErrorString(e));
+    }
+    release(&g);
+  }
   if (st == FSDP_OK) st = upload(pack, &b->ag_pack);
   if (st == FSDP_OK) st = upload(unpack, &b->ag_unpack);
   if (st == FSDP_OK) st = upload(rpack, &b->rs_pack);
@@ -129,6 +183,22 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   return FSDP_OK;
 }
 
+extern "C" fsdp_status fsdp_bucket_query(const fsdp_bucket* b, fsdp_bucket_info* out) {
+  if (!b || !out) return fail(FSDP_ERR_INVALID_ARG, "NULL argument");
+  out->ag_seg_bytes = b->ag_seg;
+  out->rs_seg_bytes = b->rs_seg;
+  const fsdp::DevTable* t[4] = {&b->ag_pack, &b->ag_unpack, &b->rs_pack, &b->rs_copyout};
+  for (int i = 0; i < 4; ++i) {
+    out->kernel_bytes[i] = t[i]->n ? t[i]->bytes_moved : 0;
+    out->kernel_chunks[i] = t[i]->n;
+  }
+  // with a communicator and zero-copy RS storage the copy-out never launches
+  if (b->rs_zero_copy && b->ctx && b->ctx->comm) out->kernel_bytes[3] = 0;
+  out->ag_zero_copy = b->ag_zero_copy ? 1 : 0;
+  out->rs_zero_copy = b->rs_zero_copy ? 1 : 0;
+  return FSDP_OK;
+}
+
 extern "C" fsdp_status fsdp_bucket_destroy(fsdp_bucket* b) {
   if (!b) return FSDP_OK;
   cudaSetDevice(b->device);
@@ -138,26 +208,35 @@ extern "C" fsdp_status fsdp_bucket_destroy(fsdp_bucket* b) {
 
 namespace fsdp {
 
-// Shared by the public calls and the schedule executor.  `launches` and
-// `colls` count enqueued kernels / collectives.
-fsdp_status ag_issue(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, cudaStream_t ms,
-                     bool with_comm, int* launches, int* colls) {
-  FSDP_CUDA_TRY(launch_table(KK_AG_PACK, b->ag_pack, staging, 1.0f, cs, c->max_ctas));
-  if (b->ag_pack.n && launches) ++*launches;
-  if (with_comm && c->comm) {
-    FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_packed, cs));
-    FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_ag_packed, 0));
-    // In place: sendbuff = recvbuff + rank * sendcount (bytes as ncclInt8).
-    FSDP_NCCL_TRY(ncclAllGather(staging + c->rank * b->ag_seg, staging, static_cast<size_t>(b->ag_seg),
-                                ncclInt8, c->comm, ms));
-    FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_done, ms));
-    if (colls) ++*colls;
+// Per-bucket steps, shared by the public calls and the schedule executor.
+// `launches` / `colls` (nullable) count enqueued kernels / collectives;
+// with_comm = false (FSDP_SCHED_NO_COMM) skips collectives and waits.
+static bool comm_on(fsdp_ctx* c, bool with_comm) { return with_comm && c->comm != nullptr; }
+
+fsdp_status ag_pack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches) {
+  if (!b->ag_zero_copy) {
+    FSDP_CUDA_TRY(launch_table(KK_AG_PACK, b->ag_pack, staging, 1.0f, cs, c->max_ctas));
+    if (b->ag_pack.n && launches) ++*launches;
   }
+  // the collective starts after everything enqueued on compute so far
+  if (comm_on(c, with_comm)) FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_packed, cs));
   return FSDP_OK;
 }
 
-fsdp_status ag_wait(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm) {
-  if (with_comm && c->comm) FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, b->ev_ag_done, 0));
+fsdp_status ag_collective(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t ms, bool with_comm, int* colls) {
+  if (!comm_on(c, with_comm)) return FSDP_OK;
+  FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_ag_packed, 0));
+  // In place (sendbuff = recvbuff + rank * sendcount), or out of place from
+  // segment-layout shard storage; bytes as ncclInt8.
+  const char* send = b->ag_zero_copy ? b->shard_seg : staging + c->rank * b->ag_seg;
+  FSDP_NCCL_TRY(ncclAllGather(send, staging, static_cast<size_t>(b->ag_seg), ncclInt8, c->comm, ms));
+  FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_done, ms));
+  if (colls) ++*colls;
+  return FSDP_OK;
+}
+
+fsdp_status ag_wait(fsdp_ctx* c, fsdp_bucket* b, cudaStream_t cs, bool with_comm) {
+  if (comm_on(c, with_comm)) FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, b->ev_ag_done, 0));
   return FSDP_OK;
 }
 
@@ -167,30 +246,36 @@ fsdp_status ag_unpack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t c
   return FSDP_OK;
 }
 
-fsdp_status rs_issue(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, cudaStream_t ms,
-                     bool with_comm, int* launches, int* colls) {
+fsdp_status rs_pack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches) {
   const float inv = 1.0f / static_cast<float>(c->world);  // fl32(1/N), correctly rounded
   FSDP_CUDA_TRY(launch_table(KK_RS_PACK, b->rs_pack, staging, inv, cs, c->max_ctas));
   if (b->rs_pack.n && launches) ++*launches;
-  if (with_comm && c->comm) {
-    FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_packed, cs));
-    FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_rs_packed, 0));
-    // In place: recvbuff = sendbuff + rank * recvcount; sum of pre-scaled fp32.
-    const size_t cnt = static_cast<size_t>(b->rs_seg / 4);
-    FSDP_NCCL_TRY(ncclReduceScatter(staging, staging + c->rank * b->rs_seg, cnt, ncclFloat32, ncclSum,
-                                    c->comm, ms));
-    FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_done, ms));
-    if (colls) ++*colls;
-  }
+  if (comm_on(c, with_comm)) FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_packed, cs));
+  return FSDP_OK;
+}
+
+fsdp_status rs_collective(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t ms, bool with_comm, int* colls) {
+  if (!comm_on(c, with_comm)) return FSDP_OK;
+  FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_rs_packed, 0));
+  // fp32 sum of pre-scaled chunks; in place (recvbuff = sendbuff + rank *
+  // recvcount) or straight into segment-layout gradient-shard storage.
+  char* recv = b->rs_zero_copy ? b->gshard_seg : staging + c->rank * b->rs_seg;
+  FSDP_NCCL_TRY(ncclReduceScatter(staging, recv, static_cast<size_t>(b->rs_seg / 4), ncclFloat32, ncclSum,
+                                  c->comm, ms));
+  FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_done, ms));
+  if (colls) ++*colls;
   return FSDP_OK;
 }
 
 fsdp_status rs_wait(fsdp_ctx* c, fsdp_bucket* b, cudaStream_t cs, bool with_comm) {
-  if (with_comm && c->comm) FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, b->ev_rs_done, 0));
+  if (comm_on(c, with_comm)) FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, b->ev_rs_done, 0));
   return FSDP_OK;
 }
 
-fsdp_status rs_copyout(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, int* launches) {
+fsdp_status rs_copyout(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches) {
+  // with a communicator and segment-layout storage the collective already
+  // wrote the result in place: nothing to copy
+  if (b->rs_zero_copy && comm_on(c, with_comm)) return FSDP_OK;
   FSDP_CUDA_TRY(launch_table(KK_RS_COPYOUT, b->rs_copyout, staging, 1.0f, cs, c->max_ctas));
   if (b->rs_copyout.n && launches) ++*launches;
   return FSDP_OK;
@@ -217,9 +302,12 @@ extern "C" fsdp_status fsdp_allgather_bucket(fsdp_ctx* c, fsdp_bucket* b, void* 
   cudaStream_t cs = static_cast<cudaStream_t>(compute);
   cudaStream_t ms = resolve_comm(c, comm);
   char* st = static_cast<char*>(staging);
-  if (flags & FSDP_ISSUE) FSDP_TRY(ag_issue(c, b, st, cs, ms, true, nullptr, nullptr));
+  if (flags & FSDP_ISSUE) {
+    FSDP_TRY(ag_pack(c, b, st, cs, true, nullptr));
+    FSDP_TRY(ag_collective(c, b, st, ms, true, nullptr));
+  }
   if (flags & FSDP_WAIT) {
-    FSDP_TRY(ag_wait(c, b, st, cs, true));
+    FSDP_TRY(ag_wait(c, b, cs, true));
     FSDP_TRY(ag_unpack(c, b, st, cs, nullptr));
   }
   return FSDP_OK;
@@ -235,10 +323,13 @@ extern "C" fsdp_status fsdp_reduce_scatter_bucket(fsdp_ctx* c, fsdp_bucket* b, v
   cudaStream_t cs = static_cast<cudaStream_t>(compute);
   cudaStream_t ms = resolve_comm(c, comm);
   char* st = static_cast<char*>(staging);
-  if (flags & FSDP_ISSUE) FSDP_TRY(rs_issue(c, b, st, cs, ms, true, nullptr, nullptr));
+  if (flags & FSDP_ISSUE) {
+    FSDP_TRY(rs_pack(c, b, st, cs, true, nullptr));
+    FSDP_TRY(rs_collective(c, b, st, ms, true, nullptr));
+  }
   if (flags & FSDP_WAIT) {
     FSDP_TRY(rs_wait(c, b, cs, true));
-    FSDP_TRY(rs_copyout(c, b, st, cs, nullptr));
+    FSDP_TRY(rs_copyout(c, b, st, cs, true, nullptr));
   }
   return FSDP_OK;
 }

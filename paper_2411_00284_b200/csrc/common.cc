@@ -62,13 +62,13 @@ static void push(std::vector<Chunk>& v, uint64_t src, uint64_t dst, uint32_t n, 
   v.push_back(c);
 }
 
-void TableBuilder::copy(uint64_t src, uint64_t dst, int64_t bytes) {
+void TableBuilder::copy(uint64_t src, uint64_t dst, int64_t bytes, uint32_t flags) {
   if (bytes <= 0) return;
   bytes_moved += 2 * bytes;
   uint32_t u = unit_of(src, dst, static_cast<uint64_t>(bytes));
   for (int64_t off = 0; off < bytes; off += kChunkBytes) {
     int64_t nb = std::min<int64_t>(kChunkBytes, bytes - off);
-    push(chunks, src + off, dst + off, static_cast<uint32_t>(nb / u), OP_COPY, u);
+    push(chunks, src + off, dst + off, static_cast<uint32_t>(nb / u), OP_COPY | flags, u);
   }
 }
 

@@ -76,15 +76,19 @@ struct Chunk {
   uint64_t src;
   uint64_t dst;
   uint32_t n;
-  uint32_t op_unit;  // op | unit << 8
+  uint32_t op_unit;  // op | unit << 8 | kAbsSrc
 };
+// Chunk flag: src is an absolute address even in a kernel whose source side is
+// staging-relative (K3 reading this rank's rows straight from segment-layout
+// shard storage, see fsdp_bucket_create).
+constexpr uint32_t kAbsSrc = 1u << 16;
 static_assert(sizeof(Chunk) == 24, "chunk layout");
 
 // Builder that splits runs into chunks (host side).
 struct TableBuilder {
   std::vector<Chunk> chunks;
   int64_t bytes_moved = 0;  // algorithmic bytes (read + write)
-  void copy(uint64_t src, uint64_t dst, int64_t bytes);
+  void copy(uint64_t src, uint64_t dst, int64_t bytes, uint32_t flags = 0);
   void zero(uint64_t dst, int64_t bytes);
   void widen(uint64_t src, uint64_t dst, int64_t elems);  // bf16 -> f32 * s
   void scale(uint64_t src, uint64_t dst, int64_t elems);  // f32 -> f32 * s
@@ -113,14 +117,14 @@ int device_sm_count(int device);
 struct fsdp_ctx;
 struct fsdp_bucket;
 namespace fsdp {
-fsdp_status ag_issue(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, cudaStream_t ms,
-                     bool with_comm, int* launches, int* colls);
-fsdp_status ag_wait(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm);
+fsdp_status ag_pack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches);
+fsdp_status ag_collective(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t ms, bool with_comm, int* colls);
+fsdp_status ag_wait(fsdp_ctx* c, fsdp_bucket* b, cudaStream_t cs, bool with_comm);
 fsdp_status ag_unpack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, int* launches);
-fsdp_status rs_issue(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, cudaStream_t ms,
-                     bool with_comm, int* launches, int* colls);
+fsdp_status rs_pack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches);
+fsdp_status rs_collective(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t ms, bool with_comm, int* colls);
 fsdp_status rs_wait(fsdp_ctx* c, fsdp_bucket* b, cudaStream_t cs, bool with_comm);
-fsdp_status rs_copyout(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, int* launches);
+fsdp_status rs_copyout(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches);
 cudaStream_t resolve_comm(fsdp_ctx* c, fsdp_stream_t s);
 }  // namespace fsdp
 
@@ -143,6 +147,10 @@ struct fsdp_bucket {
   int32_t param_bytes = 2, grad_bytes = 2;
   // which pointer arrays were bound: K1 shards, K3 fulls, K4 full_grads, K6 grad_shards
   bool has_shards = false, has_fulls = false, has_grads = false, has_gshards = false;
+  // segment-layout ("zero-copy") storage, see fsdp_bucket_create
+  bool ag_zero_copy = false, rs_zero_copy = false;
+  char* shard_seg = nullptr;   // this rank's AG segment in shard storage
+  char* gshard_seg = nullptr;  // this rank's RS segment in grad-shard storage
   fsdp::DevTable ag_pack, ag_unpack, rs_pack, rs_copyout;
   cudaEvent_t ev_ag_packed = nullptr, ev_ag_done = nullptr;
   cudaEvent_t ev_rs_packed = nullptr, ev_rs_done = nullptr;

@@ -229,10 +229,15 @@ __device__ __forceinline__ void scale1(const char* src, char* dst, uint32_t n, f
   for (uint32_t i = threadIdx.x; i < n; i += NT) d[i] = __fmul_rn(s[i], scale);
 }
 
+template <bool kSrcRel>
+__device__ __forceinline__ const char* src_of(const Chunk& ch, char* base) {
+  return (kSrcRel && !(ch.op_unit & kAbsSrc)) ? base + ch.src : reinterpret_cast<const char*>(ch.src);
+}
+
 template <int NT>
 __device__ __forceinline__ void process_chunk(const Chunk& ch, const char* src, char* dst, float scale) {
   const uint32_t op = ch.op_unit & 0xFFu;
-  const uint32_t unit = ch.op_unit >> 8;
+  const uint32_t unit = (ch.op_unit >> 8) & 0xFFu;
   if (op == OP_COPY) {
     switch (unit) {
       case 16: copy16<NT>(src, dst, ch.n); break;
@@ -262,7 +267,7 @@ template <bool kSrcRel, bool kDstRel>
 __device__ __forceinline__ void run_table(const Chunk* __restrict__ tab, int n, char* base, float scale) {
   for (int c = blockIdx.x; c < n; c += gridDim.x) {
     const Chunk ch = tab[c];
-    const char* src = kSrcRel ? base + ch.src : reinterpret_cast<const char*>(ch.src);
+    const char* src = src_of<kSrcRel>(ch, base);
     char* dst = kDstRel ? base + ch.dst : reinterpret_cast<char*>(ch.dst);
     process_chunk<kThreads>(ch, src, dst, scale);
   }
@@ -270,7 +275,7 @@ __device__ __forceinline__ void run_table(const Chunk* __restrict__ tab, int n, 
 
 // ------------------------------------------------------------ bulk engine
 __device__ __forceinline__ bool is_bulk(const Chunk& ch) {
-  return (ch.op_unit & 0xFFu) == OP_COPY && (ch.op_unit >> 8) == 16;
+  return (ch.op_unit & 0xFFu) == OP_COPY && ((ch.op_unit >> 8) & 0xFFu) == 16;
 }
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -311,7 +316,7 @@ __device__ __forceinline__ void run_table_bulk(const Chunk* __restrict__ tab, in
   for (int c = blockIdx.x; c < n; c += gridDim.x) {
     const Chunk ch = tab[c];
     if (is_bulk(ch)) continue;
-    const char* src = kSrcRel ? base + ch.src : reinterpret_cast<const char*>(ch.src);
+    const char* src = src_of<kSrcRel>(ch, base);
     char* dst = kDstRel ? base + ch.dst : reinterpret_cast<char*>(ch.dst);
     process_chunk<32>(ch, src, dst, scale);
   }
@@ -337,7 +342,7 @@ __device__ __forceinline__ void run_table_bulk(const Chunk* __restrict__ tab, in
     const uint32_t bytes = ch.n * 16u;
     dsts[s] = kDstRel ? base + ch.dst : reinterpret_cast<char*>(ch.dst);
     lens[s] = bytes;
-    bulk_load(smem0 + s * kChunkBytes, kSrcRel ? base + ch.src : reinterpret_cast<const char*>(ch.src), bytes,
+    bulk_load(smem0 + s * kChunkBytes, src_of<kSrcRel>(ch, base), bytes,
               bar0 + 8 * s);
     ++loaded;
     next = advance(next + gridDim.x);
@@ -354,7 +359,7 @@ __device__ __forceinline__ void run_table_bulk(const Chunk* __restrict__ tab, in
       const uint32_t bytes = ch.n * 16u;
       dsts[s] = kDstRel ? base + ch.dst : reinterpret_cast<char*>(ch.dst);
       lens[s] = bytes;
-      bulk_load(smem0 + s * kChunkBytes, kSrcRel ? base + ch.src : reinterpret_cast<const char*>(ch.src), bytes,
+      bulk_load(smem0 + s * kChunkBytes, src_of<kSrcRel>(ch, base), bytes,
                 bar0 + 8 * s);
       ++loaded;
       next = advance(next + gridDim.x);

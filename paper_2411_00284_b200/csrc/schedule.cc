@@ -187,22 +187,9 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
       FSDP_CUDA_TRY(cudaEventRecord(ev[2 + 2 * i], on));
     }
     switch (o.op) {
-      case FSDP_OP_PACK_AG: {
-        FSDP_CUDA_TRY(launch_table(KK_AG_PACK, b->ag_pack, ag_st, 1.0f, cs, ctx->max_ctas));
-        if (b->ag_pack.n) ++launches;
-        if (with_comm && ctx->comm) FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_packed, cs));
-        break;
-      }
-      case FSDP_OP_AG:
-        if (with_comm && ctx->comm) {
-          FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_ag_packed, 0));
-          FSDP_NCCL_TRY(ncclAllGather(ag_st + ctx->rank * b->ag_seg, ag_st, static_cast<size_t>(b->ag_seg),
-                                      ncclInt8, ctx->comm, ms));
-          FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_done, ms));
-          ++colls;
-        }
-        break;
-      case FSDP_OP_WAIT_AG: FSDP_TRY(ag_wait(ctx, b, ag_st, cs, with_comm)); break;
+      case FSDP_OP_PACK_AG: FSDP_TRY(ag_pack(ctx, b, ag_st, cs, with_comm, &launches)); break;
+      case FSDP_OP_AG: FSDP_TRY(ag_collective(ctx, b, ag_st, ms, with_comm, &colls)); break;
+      case FSDP_OP_WAIT_AG: FSDP_TRY(ag_wait(ctx, b, cs, with_comm)); break;
       case FSDP_OP_UNPACK: FSDP_TRY(ag_unpack(ctx, b, ag_st, cs, &launches)); break;
       case FSDP_OP_COMPUTE_F:
       case FSDP_OP_COMPUTE_B: {
@@ -213,24 +200,10 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
         }
         break;
       }
-      case FSDP_OP_PACK_RS: {
-        const float inv = 1.0f / static_cast<float>(ctx->world);
-        FSDP_CUDA_TRY(launch_table(KK_RS_PACK, b->rs_pack, rs_st, inv, cs, ctx->max_ctas));
-        if (b->rs_pack.n) ++launches;
-        if (with_comm && ctx->comm) FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_packed, cs));
-        break;
-      }
-      case FSDP_OP_RS:
-        if (with_comm && ctx->comm) {
-          FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_rs_packed, 0));
-          FSDP_NCCL_TRY(ncclReduceScatter(rs_st, rs_st + ctx->rank * b->rs_seg, static_cast<size_t>(b->rs_seg / 4),
-                                          ncclFloat32, ncclSum, ctx->comm, ms));
-          FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_done, ms));
-          ++colls;
-        }
-        break;
+      case FSDP_OP_PACK_RS: FSDP_TRY(rs_pack(ctx, b, rs_st, cs, with_comm, &launches)); break;
+      case FSDP_OP_RS: FSDP_TRY(rs_collective(ctx, b, rs_st, ms, with_comm, &colls)); break;
       case FSDP_OP_WAIT_RS: FSDP_TRY(rs_wait(ctx, b, cs, with_comm)); break;
-      case FSDP_OP_COPYOUT_RS: FSDP_TRY(rs_copyout(ctx, b, rs_st, cs, &launches)); break;
+      case FSDP_OP_COPYOUT_RS: FSDP_TRY(rs_copyout(ctx, b, rs_st, cs, with_comm, &launches)); break;
     }
     if (timing && !skipped) FSDP_CUDA_TRY(cudaEventRecord(ev[3 + 2 * i], on));
   }

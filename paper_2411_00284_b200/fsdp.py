@@ -100,18 +100,28 @@ class Bucket:
     """fsdp_bucket_create / fsdp_bucket_destroy.  Pointer lists hold ints."""
 
     def __init__(self, ctx, params, shards=None, fulls=None, full_grads=None, grad_shards=None,
-                 param_dtype=L.BF16, grad_dtype=L.BF16, align=16):
+                 param_dtype=L.BF16, grad_dtype=L.BF16, align=16, flags=0):
         self.ctx = ctx
         self._keep = [L.descs(params), L.ptr_array(shards), L.ptr_array(fulls),
                       L.ptr_array(full_grads), L.ptr_array(grad_shards)]
         d = L.BucketDesc()
         d.params, d.shards, d.fulls, d.full_grads, d.grad_shards = self._keep
         d.k, d.align_bytes, d.param_dtype, d.grad_dtype = len(params), align, param_dtype, grad_dtype
+        d.flags, d.reserved = flags, 0
         h = C.c_void_p()
         ag, rs = C.c_int64(), C.c_int64()
         check(L.lib.fsdp_bucket_create(ctx.h, C.byref(d), C.byref(h), C.byref(ag), C.byref(rs)))
         self.h = h
         self.ag_seg, self.rs_seg = ag.value, rs.value
+
+    def query(self):
+        """fsdp_bucket_query: segment sizes, zero-copy flags, per-kernel
+        algorithmic bytes per launch (K1, K3, K4, K6; 0 = not launched)."""
+        i = L.BucketInfo()
+        check(L.lib.fsdp_bucket_query(self.h, C.byref(i)))
+        return dict(ag_seg=i.ag_seg_bytes, rs_seg=i.rs_seg_bytes, kernel_bytes=list(i.kernel_bytes),
+                    kernel_chunks=list(i.kernel_chunks), ag_zero_copy=bool(i.ag_zero_copy),
+                    rs_zero_copy=bool(i.rs_zero_copy))
 
     def close(self):
         if self.h:

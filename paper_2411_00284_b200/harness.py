@@ -34,7 +34,7 @@ def _carve(sizes, align=ALIGN):
 
 class RankState:
     def __init__(self, specs, world, rank, fwd_plan, bwd_plan, ctx, param_dtype=L.BF16,
-                 device="cuda", seed=0, fill=True):
+                 device="cuda", seed=0, fill=True, segment_storage=True):
         self.specs, self.world, self.rank, self.ctx = specs, world, rank, ctx
         self.descs = [(p.dim0, p.row_numel, p.module_id) for p in specs]
         self.param_dtype = param_dtype
@@ -44,9 +44,17 @@ class RankState:
         c = [-(-p.dim0 // world) for p in specs]
         self.shard_numel = [c[j] * specs[j].row_numel for j in range(P)]
         self.full_numel = [p.dim0 * p.row_numel for p in specs]
-        self.shard_offs, tot = _carve([n * ep for n in self.shard_numel])
-        self.shard_buf = torch.empty(tot, dtype=torch.uint8, device=device)
-        self.gs_offs, tot_g = _carve([n * 4 for n in self.shard_numel])
+        if segment_storage:
+            # shards stored in the forward plan's AG segment layout, gradient
+            # shards in the backward plan's RS segment layout: the library
+            # detects it (fsdp_bucket_create) and drops the pack (K1) and,
+            # with a communicator, the copy-out (K6)
+            self.shard_offs, tot = self._segment_offsets(fwd_plan, ep)
+            self.gs_offs, tot_g = self._segment_offsets(bwd_plan, 4)
+        else:
+            self.shard_offs, tot = _carve([n * ep for n in self.shard_numel])
+            self.gs_offs, tot_g = _carve([n * 4 for n in self.shard_numel])
+        self.shard_buf = torch.zeros(tot, dtype=torch.uint8, device=device)
         self.gshard_buf = torch.zeros(tot_g, dtype=torch.uint8, device=device)
         # slots sized to the largest bucket of either phase
         buckets = list(fwd_plan) + list(bwd_plan)
@@ -60,6 +68,12 @@ class RankState:
             self._fill_normal(self.shard_buf, 0.02, g, param_dtype)
             for t in self.grad_slots:
                 self._fill_normal(t, 1e-3, g, L.BF16)
+            # shard padding rows hold +0 (fsdp_shard contract)
+            for j, p in enumerate(specs):
+                v = max(0, min(p.dim0 - rank * c[j], c[j]))
+                if v < c[j]:
+                    o = self.shard_offs[j] + v * p.row_numel * ep
+                    self.shard_buf[o:self.shard_offs[j] + self.shard_numel[j] * ep].zero_()
         sp = self.shard_buf.data_ptr()
         gp = self.gshard_buf.data_ptr()
         self.fwd, self.bwd = [], []
@@ -69,6 +83,11 @@ class RankState:
                 m = sorted(members)
                 offs, _ = _carve([self.full_numel[j] * ep for j in m])
                 goffs, _ = _carve([self.full_numel[j] * 2 for j in m])
+                flags = 0
+                if self._follows_segment(m, self.shard_offs, ep):
+                    flags |= L.BUCKET_SEGMENT_SHARDS
+                if phase == 1 and self._follows_segment(m, self.gs_offs, 4):
+                    flags |= L.BUCKET_SEGMENT_GRAD_SHARDS
                 fbase = self.full_slots[b % 2].data_ptr()
                 gbase = self.grad_slots[b % 2].data_ptr()
                 bk = F.Bucket(ctx, [self.descs[j] for j in m],
@@ -76,7 +95,7 @@ class RankState:
                               fulls=[fbase + o for o in offs],
                               full_grads=[gbase + o for o in goffs] if phase == 1 else None,
                               grad_shards=[gp + self.gs_offs[j] for j in m] if phase == 1 else None,
-                              param_dtype=param_dtype, grad_dtype=L.BF16)
+                              param_dtype=param_dtype, grad_dtype=L.BF16, flags=flags)
                 bk.members = m
                 out.append(bk)
                 max_ag = max(max_ag, bk.ag_seg)
@@ -84,6 +103,23 @@ class RankState:
         self.ag_st = [torch.zeros(world * max_ag + ALIGN, dtype=torch.uint8, device=device) for _ in range(2)]
         self.rs_st = [torch.zeros(world * max(max_rs, 16) + ALIGN, dtype=torch.uint8, device=device)
                       for _ in range(2)]
+
+    def _segment_offsets(self, plan, elem_bytes):
+        """Per-parameter byte offsets placing each bucket's members at the
+        library's segment offsets (fsdp_layout), buckets 256-B aligned."""
+        offs = [None] * len(self.specs)
+        cur = 0
+        for members in plan:
+            m = sorted(members)
+            moffs, seg = F.layout([self.descs[j] for j in m], self.world, elem_bytes, 16)
+            for j, o in zip(m, moffs):
+                offs[j] = cur + o
+            cur += (seg + ALIGN - 1) // ALIGN * ALIGN
+        return offs, max(cur, ALIGN)
+
+    def _follows_segment(self, members, offs, elem_bytes):
+        moffs, _ = F.layout([self.descs[j] for j in members], self.world, elem_bytes, 16)
+        return all(offs[j] - offs[members[0]] == o for j, o in zip(members, moffs)) and offs[members[0]] % 16 == 0
 
     @staticmethod
     def _fill_normal(buf, std, gen, dtype):
@@ -111,18 +147,39 @@ class RankState:
         return ag, rs
 
     def kernel_bytes(self):
-        """Algorithmic HBM bytes per step of each data kernel:
-        K1 read+write of the rank's shard, K3 read+write of the valid rows,
-        K4 2 B read + 4 B write per gradient element, K6 4 + 4 B per shard element."""
-        ep = self.ep
-        k1 = k3 = k4 = k6 = 0
-        for b in self.fwd + self.bwd:
-            k1 += sum(2 * self.shard_numel[j] * ep for j in b.members)
-            k3 += sum(2 * self.full_numel[j] * ep for j in b.members)
-        for b in self.bwd:
-            k4 += sum(6 * self.full_numel[j] for j in b.members)
-            k6 += sum(8 * self.shard_numel[j] for j in b.members)
-        return {L.OP_PACK_AG: k1, L.OP_UNPACK: k3, L.OP_PACK_RS: k4, L.OP_COPYOUT_RS: k6}
+        """Algorithmic HBM bytes per step of each data kernel, as the library's
+        run tables define them (fsdp_bucket_query): K1 2 x shard
+        bytes, K3 2 x valid full bytes, K4 6 B per gradient element, K6 8 B per
+        shard element (+ the few pad bytes zeroed).  A kernel that does not run
+        (zero-copy storage) counts 0."""
+        tot = {L.OP_PACK_AG: 0, L.OP_UNPACK: 0, L.OP_PACK_RS: 0, L.OP_COPYOUT_RS: 0}
+        for phase, bs in ((0, self.fwd), (1, self.bwd)):
+            for b in bs:
+                kb = b.query()["kernel_bytes"]
+                tot[L.OP_PACK_AG] += kb[0]
+                tot[L.OP_UNPACK] += kb[1]
+                if phase == 1:
+                    tot[L.OP_PACK_RS] += kb[2]
+                    tot[L.OP_COPYOUT_RS] += kb[3]
+        return tot
+
+    def kernel_launches(self):
+        """Launches per step of each data kernel (buckets whose table is non-empty)."""
+        n = {L.OP_PACK_AG: 0, L.OP_UNPACK: 0, L.OP_PACK_RS: 0, L.OP_COPYOUT_RS: 0}
+        for phase, bs in ((0, self.fwd), (1, self.bwd)):
+            for b in bs:
+                kb = b.query()["kernel_bytes"]
+                n[L.OP_PACK_AG] += kb[0] > 0
+                n[L.OP_UNPACK] += kb[1] > 0
+                if phase == 1:
+                    n[L.OP_PACK_RS] += kb[2] > 0
+                    n[L.OP_COPYOUT_RS] += kb[3] > 0
+        return n
+
+    def zero_copy(self):
+        q = [b.query() for b in self.fwd + self.bwd]
+        return {"ag_buckets": sum(x["ag_zero_copy"] for x in q), "rs_buckets": sum(x["rs_zero_copy"] for x in q[len(self.fwd):]),
+                "buckets": len(q)}
 
 
 def plans_for(specs, world, mode, t_fwd=None, t_bwd=None, ag=(0, 0), rs=(0, 0), mem_max=0,

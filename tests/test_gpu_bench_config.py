@@ -1,0 +1,69 @@
+"""-m gpu: parity of the bench configuration itself (BASELINE configs[1] at
+the launch configuration bench.py times): the full Llama-3-8B rank state at
+layout world 8, one reordered step through fsdp_run_schedule, then checks on
+sampled outputs the oracle computes one element at a time, and on properties
+that hold at any size.
+
+With a layout-only ctx (rank 0, no peers) the step's observable results are:
+  * every gradient shard = this rank's own chunk, widened and times fl32(1/8)
+    (the reduce-scatter has no other contributor), element-exact;
+  * the full-parameter slots of the last two backward buckets hold this rank's
+    shard in rows [0, c) and the (never written, zero-initialised) peer
+    segments in rows [c, d).
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2411_00284_b200 as F
+from paper_2411_00284_b200 import _lib as L
+from paper_2411_00284_b200 import harness as H
+from oracle import bf16
+from oracle.collectives import inv_world_f32
+from workloads import llama
+
+pytestmark = pytest.mark.gpu
+
+
+def test_llama8b_bench_step_sampled_parity():
+    world = 8
+    specs = llama("8b")
+    ctx = F.Ctx(world, 0)
+    fplan, bplan = H.plans_for(specs, world, L.PLAN_MANUAL)
+    st = H.RankState(specs, world, 0, fplan, bplan, ctx, seed=77)
+    st.gshard_buf.fill_(0xAB)
+    cs, ms = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+    flags = L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT
+    rep = st.step(flags, cs.cuda_stream, ms.cuda_stream, want_log=True)
+    torch.cuda.synchronize()
+    # 35 buckets per phase; shards live in segment layout, so no pack (K1):
+    # forward unpack, backward unpack + grad pack + copy-out (no peers: K6 runs)
+    assert st.zero_copy()["ag_buckets"] == 70
+    assert rep["kernel_launches"] == 4 * 35, rep["kernel_launches"]
+    assert rep["log_len"] == 5 * 35 + 9 * 35, rep["log_len"]
+
+    inv = inv_world_f32(world)
+    rng = np.random.Generator(np.random.Philox(5))
+    gs_u8 = st.gshard_buf
+    for b, bk in enumerate(st.bwd):
+        slot = st.grad_slots[b % 2]
+        offs, _ = H._carve([st.full_numel[j] * 2 for j in bk.members])
+        for j, goff in zip(bk.members, offs):
+            n = st.shard_numel[j]               # rank 0 owns rows [0, c): the first n elements
+            idx = rng.integers(0, n, size=64)
+            g = slot[goff:goff + 2 * st.full_numel[j]].view(torch.int16)[torch.from_numpy(idx).cuda()]
+            want = bf16.widen(g.cpu().numpy().view(np.uint16)) * inv
+            got = gs_u8[st.gs_offs[j]:st.gs_offs[j] + 4 * n].view(torch.float32)[torch.from_numpy(idx).cuda()]
+            assert np.array_equal(got.cpu().numpy().view(np.uint32), want.astype(np.float32).view(np.uint32)), \
+                specs[j].name
+
+    for b in (len(st.bwd) - 1, len(st.bwd) - 2):
+        bk = st.bwd[b]
+        offs, _ = H._carve([st.full_numel[j] * 2 for j in bk.members])
+        slot = st.full_slots[b % 2]
+        for j, o in zip(bk.members, offs):
+            full = slot[o:o + 2 * st.full_numel[j]]
+            n = st.shard_numel[j]
+            sh = st.shard_buf[st.shard_offs[j]:st.shard_offs[j] + 2 * n]
+            assert torch.equal(full[:2 * n], sh), specs[j].name
+            assert int(torch.count_nonzero(full[2 * n:])) == 0, specs[j].name

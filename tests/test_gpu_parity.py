@@ -261,6 +261,89 @@ def test_405b_layer_allgather_64bit_offsets():
         assert int(st16[pos]) == want
 
 
+# ------------------------------------------------- segment-layout storage
+def _segment_storage(params, world, rank, dt, align, elem):
+    """One buffer holding this rank's shards at the library's segment offsets
+    (garbage in the gaps, which fsdp_bucket_create must zero)."""
+    descs = [(p.shape[0], p.shape[1], 0) for p in params]
+    offs, seg = F.layout(descs, world, elem, align)
+    buf = np.full(seg, 0xEE, dtype=np.uint8)
+    for p, o in zip(params, offs):
+        b = shard(p, world, rank).reshape(-1).view(np.uint8)
+        buf[o:o + b.size] = b
+    return DevArray(buf), offs, seg
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("dt", [L.FP32, L.BF16])
+def test_zero_copy_allgather_simulated(world, dt):
+    specs = toy_mlp()
+    params = [param_tensor(p, "f32" if dt == L.FP32 else "bf16", 300 + i) for i, p in enumerate(specs)]
+    descs = [(p.shape[0], p.shape[1], 0) for p in params]
+    stor, buckets, ctxs, outs = [], [], [], []
+    for r in range(world):
+        sbuf, offs, seg = _segment_storage(params, world, r, dt, 16, _esize(dt))
+        ctx = F.Ctx(world, r)
+        out = [DevArray(nbytes=p.nbytes, fill=0x5A, dtype=p.dtype, shape=p.shape) for p in params]
+        b = F.Bucket(ctx, descs, shards=[sbuf.ptr + o for o in offs], fulls=[o.ptr for o in out],
+                     param_dtype=dt, grad_dtype=dt, flags=L.BUCKET_SEGMENT_SHARDS)
+        assert b.query()["ag_zero_copy"] and b.query()["kernel_bytes"][0] == 0
+        stor.append(sbuf)
+        buckets.append(b)
+        ctxs.append(ctx)
+        outs.append(out)
+    g_ref, _ = OC.bucketed_all_gather(params, world, 16)
+    staging = DevArray(nbytes=world * seg, fill=0xCD)
+    for r in range(world):
+        F.allgather_bucket(ctxs[r], buckets[r], staging.ptr, flags=L.ISSUE)   # no pack: nothing written
+        seg_r = stor[r].get()
+        assert np.array_equal(seg_r, g_ref[r * seg:(r + 1) * seg])           # storage == packed segment, gaps zeroed
+    # the all-gather (NCCL on real GPUs): every rank's storage segment into the staging
+    host = staging.get()
+    for r in range(world):
+        host[r * seg:(r + 1) * seg] = stor[r].get()
+    staging.t[staging.off:staging.off + staging.nbytes].copy_(torch.from_numpy(host))
+    for r in range(world):
+        F.allgather_bucket(ctxs[r], buckets[r], staging.ptr, flags=L.WAIT)
+        for o, p in zip(outs[r], params):
+            assert np.array_equal(bits(o.get()), bits(p))
+
+
+def test_zero_copy_with_nccl_world1():
+    # out-of-place AG from the storage and RS straight into gradient-shard storage
+    specs = toy_mlp()
+    params = [param_tensor(p, "bf16", 400 + i) for i, p in enumerate(specs)]
+    grads = [grad_tensor(p, "bf16", 401, 0) for p in specs]
+    descs = [(p.shape[0], p.shape[1], 0) for p in params]
+    ctx = F.Ctx(1, 0, 0, nccl_uid=F.nccl_get_unique_id())
+    sbuf, offs, seg = _segment_storage(params, 1, 0, L.BF16, 16, 2)
+    roffs, rseg = F.layout(descs, 1, 4, 16)
+    gstor = DevArray(nbytes=rseg, fill=0x33, dtype=np.float32)
+    out = [DevArray(nbytes=p.nbytes, fill=0x5A, dtype=p.dtype, shape=p.shape) for p in params]
+    gd = [DevArray(g) for g in grads]
+    b = F.Bucket(ctx, descs, shards=[sbuf.ptr + o for o in offs], fulls=[o.ptr for o in out],
+                 full_grads=[g.ptr for g in gd], grad_shards=[gstor.ptr + o for o in roffs],
+                 flags=L.BUCKET_SEGMENT_SHARDS | L.BUCKET_SEGMENT_GRAD_SHARDS)
+    q = b.query()
+    assert q["ag_zero_copy"] and q["rs_zero_copy"] and q["kernel_bytes"][0] == 0 and q["kernel_bytes"][3] == 0
+    ag = DevArray(nbytes=seg, fill=0xCD)
+    rs = DevArray(nbytes=rseg, fill=0xCD)
+    cs, ms = torch.cuda.Stream(), torch.cuda.Stream()
+    F.allgather_bucket(ctx, b, ag.ptr, cs.cuda_stream, ms.cuda_stream)
+    F.reduce_scatter_bucket(ctx, b, rs.ptr, cs.cuda_stream, ms.cuda_stream)
+    torch.cuda.synchronize()
+    g_ref, _ = OC.bucketed_all_gather(params, 1, 16)
+    assert np.array_equal(ag.get(), g_ref)            # NCCL copied the storage segment
+    for o, p in zip(out, params):
+        assert np.array_equal(o.get(), p)
+    _, _, shards_ref = OC.bucketed_reduce_scatter([grads], 1, 16)
+    got = gstor.get()
+    for j, o in enumerate(roffs):
+        n = shards_ref[0][j].size
+        assert np.array_equal(got[o // 4:o // 4 + n].view(np.uint32), shards_ref[0][j].reshape(-1).view(np.uint32))
+    ctx.close()
+
+
 # ------------------------------------------------------------------ schedule
 def _schedule_case(world_comm):
     specs = toy_mlp()
@@ -321,6 +404,17 @@ def test_proxy_calibration_scales():
     t1 = F.proxy_calibrate(ctx, 20000)
     t2 = F.proxy_calibrate(ctx, 40000)
     assert t1 > 0 and 1.6 < t2 / t1 < 2.4
+
+
+def test_segment_flag_validated():
+    ctx = F.Ctx(2, 0)
+    p = DevArray(np.zeros((64, 4), np.uint16))
+    with pytest.raises(F.FsdpError):   # second member not at its segment offset
+        F.Bucket(ctx, [(8, 4, 0), (8, 4, 0)], shards=[p.ptr, p.ptr + 1024], fulls=[p.ptr, p.ptr],
+                 flags=L.BUCKET_SEGMENT_SHARDS)
+    b = F.Bucket(ctx, [(8, 4, 0), (8, 4, 0)], shards=[p.ptr, p.ptr + 32], fulls=[p.ptr, p.ptr],
+                 flags=L.BUCKET_SEGMENT_SHARDS)
+    assert b.query()["ag_zero_copy"]
 
 
 def test_abi_rejects_misaligned_staging_and_foreign_bucket():
