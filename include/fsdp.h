@@ -344,6 +344,52 @@ typedef struct {
 
 fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, fsdp_step_report* out);
 
+/* ------------------------------------- peer-memory (fused) collectives
+ * The same two collectives as one kernel each over peer memory (NVLink P2P on
+ * a multi-GPU node, CUDA IPC mappings; on one GPU, buffers of simulated ranks):
+ * every rank pulls what it needs straight from its peers' buffers into its own
+ * destination layout -- no staging buffer, no pack, no copy-out, no NCCL.
+ *
+ *   fsdp_p2p_allgather_bucket: K8 copies the valid rows of every
+ *     rank q's shards from peer_segs[q] (rank q's segment-layout shard storage
+ *     of this bucket, FSDP_BUCKET_SEGMENT_SHARDS) into this rank's full
+ *     parameters.  Wire bytes: (N-1)/N of the gathered bucket, as the AG.
+ *   fsdp_p2p_reduce_scatter_bucket: K9 computes this rank's
+ *     gradient shards directly: g_shard[t] = sum over q = 0..N-1, in rank order,
+ *     of fl32(fp32(grad_q[row r*c + t]) * fl32(1/N)), reading the bf16 (or fp32)
+ *     full gradients of every peer: peer_grads[q] is rank q's address of what
+ *     this rank binds as full_grads[0]; the members' full_grads must keep the
+ *     same offsets from full_grads[0] on every rank (symmetric layout).  Wire
+ *     bytes: (N-1)/N of the bucket in the *gradient* dtype (half the fp32 RS for
+ *     bf16 gradients); the rank-order fp32 sum is bit-exact against the oracle at
+ *     any N.
+ * Both are stream-ordered on `stream` and read peer memory without further
+ * synchronisation: the caller orders them after the peers' producers (for
+ * example with fsdp_p2p_signal / fsdp_p2p_wait, or a host barrier).  world <= 16.
+ * Arrays hold `world` device pointers valid in this process. */
+fsdp_status fsdp_p2p_allgather_bucket(fsdp_ctx* ctx, fsdp_bucket* b, const void* const* peer_segs,
+                                      fsdp_stream_t stream);
+fsdp_status fsdp_p2p_reduce_scatter_bucket(fsdp_ctx* ctx, fsdp_bucket* b, const void* const* peer_grads,
+                                           fsdp_stream_t stream);
+
+/* Cross-rank signalling for the peer-memory path (monotonic 64-bit epochs).
+ * fsdp_p2p_signal: one thread stores `value` with release semantics at the
+ *   system scope into each slots[q] (q < world; NULL entries skipped): slot of
+ *   this rank in rank q's flag array, mapped in this process.
+ * fsdp_p2p_wait: one warp spins (acquire loads) until flags[q] >= value for
+ *   every q < world (flags: this rank's own array), or `timeout_ns` elapses, in
+ *   which case it sets *error_flag (device int, nullable) to 1 and returns. */
+fsdp_status fsdp_p2p_signal(fsdp_ctx* ctx, void* const* slots, uint64_t value, fsdp_stream_t stream);
+fsdp_status fsdp_p2p_wait(fsdp_ctx* ctx, const void* flags, uint64_t value, int64_t timeout_ns,
+                          int32_t* error_flag, fsdp_stream_t stream);
+
+/* IPC plumbing for the peer-memory path: a cudaMalloc'd buffer and its
+ * 64-byte cudaIpcMemHandle (host memory), to be opened by peer processes. */
+fsdp_status fsdp_ipc_alloc(int64_t bytes, void** dev_ptr, void* handle64);
+fsdp_status fsdp_ipc_open(const void* handle64, void** dev_ptr);
+fsdp_status fsdp_ipc_close(void* dev_ptr);
+fsdp_status fsdp_ipc_free(void* dev_ptr);
+
 /* ----------------------------------------------- compute proxy (K7)
  * A measurement device, not a method step: stands in for the layer compute
  * that the paper's reordering overlaps communication with, so that

@@ -36,6 +36,8 @@ EXPORTED = [
     "fsdp_ctx_destroy", "fsdp_shard", "fsdp_plan_buckets", "fsdp_layout", "fsdp_bucket_create",
     "fsdp_bucket_destroy", "fsdp_bucket_query", "fsdp_allgather_bucket", "fsdp_reduce_scatter_bucket",
     "fsdp_run_schedule", "fsdp_proxy_launch", "fsdp_proxy_calibrate",
+    "fsdp_p2p_allgather_bucket", "fsdp_p2p_reduce_scatter_bucket", "fsdp_p2p_signal", "fsdp_p2p_wait",
+    "fsdp_ipc_alloc", "fsdp_ipc_open", "fsdp_ipc_close", "fsdp_ipc_free",
 ]
 
 
@@ -124,6 +126,14 @@ _sigs = {
     "fsdp_proxy_launch": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, _P]),
     "fsdp_proxy_calibrate": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _P,
                                        C.POINTER(C.c_int64)]),
+    "fsdp_p2p_allgather_bucket": (C.c_int, [_P, _P, C.POINTER(_P), _P]),
+    "fsdp_p2p_reduce_scatter_bucket": (C.c_int, [_P, _P, C.POINTER(_P), _P]),
+    "fsdp_p2p_signal": (C.c_int, [_P, C.POINTER(_P), C.c_uint64, _P]),
+    "fsdp_p2p_wait": (C.c_int, [_P, _P, C.c_uint64, C.c_int64, _P, _P]),
+    "fsdp_ipc_alloc": (C.c_int, [C.c_int64, C.POINTER(_P), _P]),
+    "fsdp_ipc_open": (C.c_int, [_P, C.POINTER(_P)]),
+    "fsdp_ipc_close": (C.c_int, [_P]),
+    "fsdp_ipc_free": (C.c_int, [_P]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(lib, _name)

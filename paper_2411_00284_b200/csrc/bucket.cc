@@ -26,6 +26,8 @@ void destroy_bucket(fsdp_bucket* b) {
   release(&b->ag_unpack);
   release(&b->rs_pack);
   release(&b->rs_copyout);
+  release(&b->p2p_ag);
+  release(&b->p2p_rs);
   for (cudaEvent_t* e : {&b->ev_ag_packed, &b->ev_ag_done, &b->ev_rs_packed, &b->ev_rs_done})
     if (*e) cudaEventDestroy(*e);
   delete b;
@@ -86,7 +88,7 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
                   "FSDP_BUCKET_SEGMENT_GRAD_SHARDS: grad shards do not follow the segment offsets");
   }
 
-  TableBuilder pack, unpack, rpack, rcopy, gaps;
+  TableBuilder pack, unpack, rpack, rcopy, gaps, p2p_ag, p2p_rs;
   for (int32_t j = 0; j < k; ++j) {
     const fsdp_param_desc& p = d->params[j];
     const ShardRows own = shard_rows(p.dim0, N, r);
@@ -129,6 +131,25 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
         rpack.zero(dst + s.v * R * 4, rs_end - rs_off[j] - s.v * R * 4);
       }
     }
+    if (ag_zc && d->fulls) {
+      // K8 (peer-memory AG): valid rows of rank q's shard, read at offset off_j of
+      // rank q's segment storage, into rows [q c, q c + v) of the full param.
+      for (int32_t q = 0; q < N; ++q) {
+        const ShardRows s = shard_rows(p.dim0, N, q);
+        if (s.v > 0)
+          p2p_ag.copy(static_cast<uint64_t>(ag_off[j]),
+                      reinterpret_cast<uint64_t>(d->fulls[j]) + static_cast<uint64_t>(s.begin * R * ep),
+                      s.v * R * ep, static_cast<uint32_t>(q) << kPeerShift);
+      }
+    }
+    if (d->full_grads && d->grad_shards) {
+      // K9 (peer-memory RS): rows of chunk r at the same offset from full_grads[0]
+      // on every rank, summed in rank order into the fp32 shard; pad rows +0.0.
+      const uint64_t rel = reinterpret_cast<uint64_t>(d->full_grads[j]) - reinterpret_cast<uint64_t>(d->full_grads[0]);
+      const uint64_t dst = reinterpret_cast<uint64_t>(d->grad_shards[j]);
+      p2p_rs.peer_reduce(rel + static_cast<uint64_t>(own.begin * R * eg), dst, own.v * R, eg, N);
+      p2p_rs.zero(dst + static_cast<uint64_t>(own.v * R * 4), (own.c - own.v) * R * 4);
+    }
     if (d->grad_shards) {
       // K6: own segment r -> fp32 gradient shard [c, R].
       rcopy.copy(static_cast<uint64_t>(r * rs_seg + rs_off[j]),
@@ -168,6 +189,8 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   if (st == FSDP_OK) st = upload(unpack, &b->ag_unpack);
   if (st == FSDP_OK) st = upload(rpack, &b->rs_pack);
   if (st == FSDP_OK) st = upload(rcopy, &b->rs_copyout);
+  if (st == FSDP_OK && N <= kMaxPeers) st = upload(p2p_ag, &b->p2p_ag);
+  if (st == FSDP_OK && N <= kMaxPeers) st = upload(p2p_rs, &b->p2p_rs);
   for (cudaEvent_t* e : {&b->ev_ag_packed, &b->ev_ag_done, &b->ev_rs_packed, &b->ev_rs_done}) {
     if (st != FSDP_OK) break;
     cudaError_t err = cudaEventCreateWithFlags(e, cudaEventDisableTiming);

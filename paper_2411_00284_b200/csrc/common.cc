@@ -116,6 +116,23 @@ void TableBuilder::scale(uint64_t src, uint64_t dst, int64_t elems) {
   }
 }
 
+void TableBuilder::peer_reduce(uint64_t src, uint64_t dst, int64_t elems, int eb, int world) {
+  if (elems <= 0) return;
+  bytes_moved += elems * (static_cast<int64_t>(eb) * world + 4);  // every peer's elements + fp32 write
+  const uint32_t op = eb == 2 ? OP_PEER_REDUCE_BF16 : OP_PEER_REDUCE_F32;
+  const int64_t g = eb == 2 ? 8 : 4;  // elements per 16-B load
+  const int64_t body = (src % 16 == 0 && dst % 16 == 0) ? elems / g * g : 0;
+  const int64_t per_chunk = kChunkBytes / 4;  // fp32 outputs per chunk
+  for (int64_t e = 0; e < body; e += per_chunk) {
+    const int64_t ne = std::min<int64_t>(per_chunk, body - e);
+    push(chunks, src + eb * e, dst + 4 * e, static_cast<uint32_t>(ne / g), op, 16);
+  }
+  for (int64_t e = body; e < elems; e += per_chunk) {
+    const int64_t ne = std::min<int64_t>(per_chunk, elems - e);
+    push(chunks, src + eb * e, dst + 4 * e, static_cast<uint32_t>(ne), op, static_cast<uint32_t>(eb));
+  }
+}
+
 fsdp_status upload(const TableBuilder& tb, DevTable* out) {
   out->n = static_cast<int32_t>(tb.chunks.size());
   out->bytes_moved = tb.bytes_moved;

@@ -70,6 +70,17 @@ enum ChunkOp : uint32_t {
   OP_ZERO = 1,   // n units of `unit` bytes at dst
   OP_WIDEN = 2,  // bf16 -> fp32 * scale; unit 16: n groups of 8 elems, unit 2: n elems
   OP_SCALE = 3,  // fp32 * scale;        unit 16: n groups of 4 elems, unit 4: n elems
+  // peer-memory reduce (K9): src = offset into every peer's gradient region;
+  // unit 16: n groups of 8 bf16 / 4 fp32 elements, unit 2 / 4: n elements
+  OP_PEER_REDUCE_BF16 = 4,
+  OP_PEER_REDUCE_F32 = 5,
+};
+// Peer-memory copy (K8): OP_COPY chunks whose src is an offset into peer q's
+// segment, q in op_unit bits 24..31.
+constexpr uint32_t kPeerShift = 24;
+constexpr int kMaxPeers = 16;
+struct PeerTable {
+  const char* p[kMaxPeers];
 };
 
 struct Chunk {
@@ -92,6 +103,9 @@ struct TableBuilder {
   void zero(uint64_t dst, int64_t bytes);
   void widen(uint64_t src, uint64_t dst, int64_t elems);  // bf16 -> f32 * s
   void scale(uint64_t src, uint64_t dst, int64_t elems);  // f32 -> f32 * s
+  // K9: rank-order sum over peers of `elems` gradient elements of elem_bytes
+  // (2 = bf16, 4 = fp32) at offset src of every peer region -> fp32 at dst
+  void peer_reduce(uint64_t src, uint64_t dst, int64_t elems, int elem_bytes, int world);
 };
 
 struct DevTable {
@@ -108,6 +122,12 @@ enum KernelKind { KK_SHARD = 0, KK_AG_PACK, KK_AG_UNPACK, KK_RS_PACK, KK_RS_COPY
 cudaError_t launch_table(KernelKind kind, const DevTable& t, char* base, float scale, cudaStream_t s,
                          int max_ctas);
 cudaError_t launch_proxy(int64_t iters, int grid, int smem, float* sink, cudaStream_t s);
+cudaError_t launch_p2p_allgather(const DevTable& t, const PeerTable& pt, cudaStream_t s, int max_ctas);
+cudaError_t launch_p2p_reduce_scatter(const DevTable& t, const PeerTable& pt, int world, float scale,
+                                      cudaStream_t s, int max_ctas);
+cudaError_t launch_p2p_signal(const PeerTable& slots, int world, uint64_t value, cudaStream_t s);
+cudaError_t launch_p2p_wait(const void* flags, int world, uint64_t value, int64_t timeout_ns, int* err,
+                            cudaStream_t s);
 int device_sm_count(int device);
 
 // Per-bucket steps shared by the public calls and the schedule executor
@@ -152,6 +172,7 @@ struct fsdp_bucket {
   char* shard_seg = nullptr;   // this rank's AG segment in shard storage
   char* gshard_seg = nullptr;  // this rank's RS segment in grad-shard storage
   fsdp::DevTable ag_pack, ag_unpack, rs_pack, rs_copyout;
+  fsdp::DevTable p2p_ag, p2p_rs;  // K8 / K9 tables (peer-memory path)
   cudaEvent_t ev_ag_packed = nullptr, ev_ag_done = nullptr;
   cudaEvent_t ev_rs_packed = nullptr, ev_rs_done = nullptr;
 };

@@ -407,6 +407,155 @@ __global__ void __launch_bounds__(32) fsdp_rs_copyout_bulk_kernel(const Chunk* t
   run_table_bulk<true, false>(tab, n, base, s);
 }
 
+// ------------------------------------------------ peer-memory collectives
+namespace {
+
+// K8 body: chunk src is an offset into peer q's segment (q in op_unit bits 24..31).
+__device__ __forceinline__ void run_peer_copy(const Chunk* __restrict__ tab, int n, const PeerTable& pt) {
+  for (int c = blockIdx.x; c < n; c += gridDim.x) {
+    const Chunk ch = tab[c];
+    const char* src = pt.p[ch.op_unit >> 24] + ch.src;
+    process_chunk<kThreads>(ch, src, reinterpret_cast<char*>(ch.dst), 1.0f);
+  }
+}
+
+// fp32 accumulate of one 16-B gradient vector from one peer, rank order kept
+// by the caller: acc = acc + fl32(x * scale) (first peer: acc = fl32(x * scale)).
+template <bool kBf16>
+__device__ __forceinline__ void acc_vec(float (&acc)[8], const uint4& v, float scale, bool first) {
+  float x[8];
+  if (kBf16) {
+    x[0] = bf16_lo(v.x); x[1] = bf16_hi(v.x); x[2] = bf16_lo(v.y); x[3] = bf16_hi(v.y);
+    x[4] = bf16_lo(v.z); x[5] = bf16_hi(v.z); x[6] = bf16_lo(v.w); x[7] = bf16_hi(v.w);
+  } else {
+    x[0] = __uint_as_float(v.x); x[1] = __uint_as_float(v.y); x[2] = __uint_as_float(v.z);
+    x[3] = __uint_as_float(v.w);
+  }
+  constexpr int K = kBf16 ? 8 : 4;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const float t = __fmul_rn(x[k], scale);
+    acc[k] = first ? t : __fadd_rn(acc[k], t);
+  }
+}
+
+// K9 body: this rank's gradient shard = rank-order fp32 sum over every peer.
+// Vector chunks: n groups of 8 bf16 (or 4 fp32) elements; 4 peers' loads in
+// flight per thread, added strictly in rank order.
+template <bool kBf16>
+__device__ __forceinline__ void peer_reduce16(const PeerTable& pt, int world, uint64_t off, char* dst,
+                                              uint32_t n, float scale) {
+  constexpr int K = kBf16 ? 8 : 4;
+  for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
+    float acc[8];
+    const uint64_t o = off + 16ull * i;
+    for (int q0 = 0; q0 < world; q0 += 4) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q0 + u < world) v[u] = ld_stream(reinterpret_cast<const uint4*>(pt.p[q0 + u] + o));
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q0 + u < world) acc_vec<kBf16>(acc, v[u], scale, q0 + u == 0);
+    }
+    uint4 a, b;
+    a.x = __float_as_uint(acc[0]); a.y = __float_as_uint(acc[1]); a.z = __float_as_uint(acc[2]);
+    a.w = __float_as_uint(acc[3]);
+    if (kBf16) {
+      b.x = __float_as_uint(acc[4]); b.y = __float_as_uint(acc[5]); b.z = __float_as_uint(acc[6]);
+      b.w = __float_as_uint(acc[7]);
+      uint4* d = reinterpret_cast<uint4*>(dst) + 2 * i;
+      st_v4(d, a);
+      st_v4(d + 1, b);
+    } else {
+      st_v4(reinterpret_cast<uint4*>(dst) + i, a);
+    }
+    (void)K;
+  }
+}
+
+template <bool kBf16>
+__device__ __forceinline__ void peer_reduce1(const PeerTable& pt, int world, uint64_t off, char* dst, uint32_t n,
+                                             float scale) {
+  float* d = reinterpret_cast<float*>(dst);
+  for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
+    float acc = 0.f;
+    for (int q = 0; q < world; ++q) {
+      float x;
+      if (kBf16) {
+        x = __uint_as_float(static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(pt.p[q] + off + 2ull * i)) << 16);
+      } else {
+        x = *reinterpret_cast<const float*>(pt.p[q] + off + 4ull * i);
+      }
+      const float t = __fmul_rn(x, scale);
+      acc = q == 0 ? t : __fadd_rn(acc, t);
+    }
+    d[i] = acc;
+  }
+}
+
+__device__ __forceinline__ void run_peer_reduce(const Chunk* __restrict__ tab, int n, const PeerTable& pt, int world,
+                                                float scale) {
+  for (int c = blockIdx.x; c < n; c += gridDim.x) {
+    const Chunk ch = tab[c];
+    const uint32_t op = ch.op_unit & 0xFFu, unit = (ch.op_unit >> 8) & 0xFFu;
+    char* dst = reinterpret_cast<char*>(ch.dst);
+    if (op == OP_ZERO) {
+      process_chunk<kThreads>(ch, nullptr, dst, 1.0f);
+    } else if (op == OP_PEER_REDUCE_BF16) {
+      if (unit == 16) peer_reduce16<true>(pt, world, ch.src, dst, ch.n, scale);
+      else peer_reduce1<true>(pt, world, ch.src, dst, ch.n, scale);
+    } else {
+      if (unit == 16) peer_reduce16<false>(pt, world, ch.src, dst, ch.n, scale);
+      else peer_reduce1<false>(pt, world, ch.src, dst, ch.n, scale);
+    }
+  }
+}
+
+}  // namespace
+
+// K8: fused all-gather + copy-out over peer memory.
+__global__ void FSDP_LSU_BOUNDS fsdp_p2p_allgather_kernel(const Chunk* tab, int n, const __grid_constant__ PeerTable pt) {
+  run_peer_copy(tab, n, pt);
+}
+// K9: fused gradient widen + 1/N + reduce-scatter + copy-out over peer memory.
+__global__ void FSDP_LSU_BOUNDS fsdp_p2p_reduce_scatter_kernel(const Chunk* tab, int n, const __grid_constant__ PeerTable pt, int world,
+                                                               float scale) {
+  run_peer_reduce(tab, n, pt, world, scale);
+}
+
+__global__ void fsdp_p2p_signal_kernel(const __grid_constant__ PeerTable slots, int world, unsigned long long value) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int q = 0; q < world; ++q) {
+    unsigned long long* p = reinterpret_cast<unsigned long long*>(const_cast<char*>(slots.p[q]));
+    if (p) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(value) : "memory");
+  }
+}
+
+__global__ void fsdp_p2p_wait_kernel(const unsigned long long* flags, int world, unsigned long long value,
+                                     long long timeout_ns, int* err) {
+  const int q = threadIdx.x;
+  bool timed_out = false;
+  if (q < world) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + q) : "memory");
+      if (v >= value) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (timeout_ns > 0 && static_cast<long long>(t - t0) > timeout_ns) {
+        timed_out = true;
+        break;
+      }
+      __nanosleep(200);
+    }
+  }
+  if (__any_sync(0xFFFFFFFFu, timed_out) && q == 0 && err) *err = 1;
+  __threadfence_system();
+}
+
 // K7: persistent compute proxy.  Four independent FMA chains per thread; the
 // result is consumed behind an impossible branch so the loop survives.
 __global__ void __launch_bounds__(256) fsdp_compute_proxy_kernel(long long iters, float* sink) {
@@ -478,6 +627,36 @@ cudaError_t launch_table(KernelKind kind, const DevTable& t, char* base, float s
     case KK_RS_PACK: fsdp_rs_pack_kernel<<<grid, kThreads, 0, s>>>(t.d, t.n, base, scale); break;
     case KK_RS_COPYOUT: fsdp_rs_copyout_kernel<<<grid, kThreads, 0, s>>>(t.d, t.n, base, scale); break;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_allgather(const DevTable& t, const PeerTable& pt, cudaStream_t s, int max_ctas) {
+  if (t.n == 0) return cudaSuccess;
+  (void)cudaGetLastError();
+  fsdp_p2p_allgather_kernel<<<t.n < max_ctas ? t.n : max_ctas, kThreads, 0, s>>>(t.d, t.n, pt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_reduce_scatter(const DevTable& t, const PeerTable& pt, int world, float scale,
+                                      cudaStream_t s, int max_ctas) {
+  if (t.n == 0) return cudaSuccess;
+  (void)cudaGetLastError();
+  fsdp_p2p_reduce_scatter_kernel<<<t.n < max_ctas ? t.n : max_ctas, kThreads, 0, s>>>(t.d, t.n, pt, world, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_signal(const PeerTable& slots, int world, uint64_t value, cudaStream_t s) {
+  (void)cudaGetLastError();
+  fsdp_p2p_signal_kernel<<<1, 32, 0, s>>>(slots, world, static_cast<unsigned long long>(value));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_wait(const void* flags, int world, uint64_t value, int64_t timeout_ns, int* err,
+                            cudaStream_t s) {
+  (void)cudaGetLastError();
+  fsdp_p2p_wait_kernel<<<1, 32, 0, s>>>(static_cast<const unsigned long long*>(flags), world,
+                                        static_cast<unsigned long long>(value), static_cast<long long>(timeout_ns),
+                                        err);
   return cudaGetLastError();
 }
 

@@ -183,3 +183,45 @@ def proxy_calibrate(ctx, iters, ctas_per_sm=1, smem_bytes=0, reps=5, stream=0):
     check(L.lib.fsdp_proxy_calibrate(ctx.h, int(iters), ctas_per_sm, smem_bytes, reps, stream or None,
                                      C.byref(ns)))
     return ns.value
+
+
+# ------------------------------------------------ peer-memory (fused) path
+def p2p_allgather_bucket(ctx, bucket, peer_segs, stream=0):
+    """fsdp_p2p_allgather_bucket: peer_segs[q] = rank q's segment-layout shard storage."""
+    check(L.lib.fsdp_p2p_allgather_bucket(ctx.h, bucket.h, L.ptr_array(peer_segs), stream or None))
+
+
+def p2p_reduce_scatter_bucket(ctx, bucket, peer_grads, stream=0):
+    """fsdp_p2p_reduce_scatter_bucket: peer_grads[q] = rank q's full_grads[0]."""
+    check(L.lib.fsdp_p2p_reduce_scatter_bucket(ctx.h, bucket.h, L.ptr_array(peer_grads), stream or None))
+
+
+def p2p_signal(ctx, slots, value, stream=0):
+    check(L.lib.fsdp_p2p_signal(ctx.h, L.ptr_array([s or 0 for s in slots]), int(value), stream or None))
+
+
+def p2p_wait(ctx, flags_ptr, value, timeout_ns=10**9, error_flag_ptr=0, stream=0):
+    check(L.lib.fsdp_p2p_wait(ctx.h, flags_ptr, int(value), int(timeout_ns), error_flag_ptr or None, stream or None))
+
+
+def ipc_alloc(nbytes):
+    """Returns (device pointer, 64-byte IPC handle)."""
+    p = C.c_void_p()
+    h = (C.c_uint8 * 64)()
+    check(L.lib.fsdp_ipc_alloc(int(nbytes), C.byref(p), C.cast(h, C.c_void_p)))
+    return p.value, bytes(h)
+
+
+def ipc_open(handle):
+    p = C.c_void_p()
+    h = (C.c_uint8 * 64).from_buffer_copy(handle)
+    check(L.lib.fsdp_ipc_open(C.cast(h, C.c_void_p), C.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr):
+    check(L.lib.fsdp_ipc_close(ptr))
+
+
+def ipc_free(ptr):
+    check(L.lib.fsdp_ipc_free(ptr))

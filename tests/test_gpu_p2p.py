@@ -1,0 +1,151 @@
+"""-m gpu parity of the peer-memory ("fused") collectives K8 / K9.
+
+One process, N simulated ranks on one GPU: every rank's segment-layout shard
+storage and full-gradient region is a real device buffer, and rank r's kernel
+reads the others' buffers exactly as it would read NVLink-mapped peer memory.
+K8 must reproduce all_gather(shard(p)) == p bit-exactly; K9 sums in rank order
+in fp32 like the oracle, so it is bit-exact at EVERY world size (the NCCL path
+is bit-exact only where the summation order cannot matter).
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2411_00284_b200 as F
+from paper_2411_00284_b200 import _lib as L
+from oracle import collectives as OC
+from oracle.shard import shard
+from workloads import llama, toy_mlp
+from workloads.data import grad_tensor, param_tensor
+from workloads.shapes import ParamSpec
+
+from .gpu_util import DevArray, bits
+
+pytestmark = pytest.mark.gpu
+
+
+def _esize(dt):
+    return 2 if dt == L.BF16 else 4
+
+
+def _storage(params, world, rank, elem):
+    descs = [(p.shape[0], p.shape[1], 0) for p in params]
+    offs, seg = F.layout(descs, world, elem, 16)
+    buf = np.full(seg, 0xEE, dtype=np.uint8)
+    for p, o in zip(params, offs):
+        b = shard(p, world, rank).reshape(-1).view(np.uint8)
+        buf[o:o + b.size] = b
+    return DevArray(buf), offs
+
+
+def _grad_region(grads):
+    """One rank's full gradients back to back at 256-B aligned offsets (the
+    same offsets on every rank: a symmetric layout)."""
+    offs, cur = [], 0
+    for g in grads:
+        offs.append(cur)
+        cur += -(-g.nbytes // 256) * 256
+    buf = np.zeros(cur, dtype=np.uint8)
+    for g, o in zip(grads, offs):
+        buf[o:o + g.nbytes] = g.reshape(-1).view(np.uint8)
+    return DevArray(buf), offs
+
+
+def run_p2p(params, grads_per_rank, world, dt, gdt):
+    descs = [(p.shape[0], p.shape[1], 0) for p in params]
+    stor = [_storage(params, world, r, _esize(dt)) for r in range(world)]
+    regions = [_grad_region(grads_per_rank[r]) for r in range(world)]
+    _, _, shards_ref = OC.bucketed_reduce_scatter(grads_per_rank, world, 16)
+    for r in range(world):
+        ctx = F.Ctx(world, r)
+        out = [DevArray(nbytes=p.nbytes, fill=0x5A, dtype=p.dtype, shape=p.shape) for p in params]
+        gs = [DevArray(nbytes=-(-d // world) * R * 4, fill=0x77, dtype=np.float32, shape=(-(-d // world), R))
+              for d, R, _ in descs]
+        sbuf, soffs = stor[r]
+        gbuf, goffs = regions[r]
+        b = F.Bucket(ctx, descs, shards=[sbuf.ptr + o for o in soffs], fulls=[o.ptr for o in out],
+                     full_grads=[gbuf.ptr + o for o in goffs], grad_shards=[g.ptr for g in gs],
+                     param_dtype=dt, grad_dtype=gdt, flags=L.BUCKET_SEGMENT_SHARDS)
+        F.p2p_allgather_bucket(ctx, b, [stor[q][0].ptr for q in range(world)])
+        F.p2p_reduce_scatter_bucket(ctx, b, [regions[q][0].ptr for q in range(world)])
+        torch.cuda.synchronize()
+        for o, p in zip(out, params):
+            assert np.array_equal(bits(o.get()), bits(p))
+        for j, g in enumerate(gs):
+            assert np.array_equal(bits(g.get()), bits(shards_ref[r][j])), (r, j)
+    return True
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 5, 7, 8])
+@pytest.mark.parametrize("dt", [L.FP32, L.BF16])
+def test_toy_p2p_bit_exact_any_world(world, dt):
+    specs = toy_mlp()
+    s = "f32" if dt == L.FP32 else "bf16"
+    params = [param_tensor(p, s, 500 + i) for i, p in enumerate(specs)]
+    grads = [[grad_tensor(p, s, 501, r) for p in specs] for r in range(world)]
+    assert run_p2p(params, grads, world, dt, dt)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_shapes_p2p(seed):
+    rng = np.random.Generator(np.random.Philox(2000 + seed))
+    world = int(rng.integers(2, 9))
+    dims = [(int(rng.integers(1, 200)), int(rng.integers(1, 40))) for _ in range(int(rng.integers(1, 9)))]
+    specs = [ParamSpec("p%d" % i, d, r, 0) for i, (d, r) in enumerate(dims)]
+    params = [param_tensor(p, "bf16", seed * 7 + i) for i, p in enumerate(specs)]
+    grads = [[grad_tensor(p, "bf16", seed, r) for p in specs] for r in range(world)]
+    assert run_p2p(params, grads, world, L.BF16, L.BF16)
+
+
+def test_llama8b_block_p2p_full_size():
+    # BASELINE configs[1] bucket at N = 8: two of the eight ranks checked
+    specs = llama("8b", n_layers=1, with_embeddings=False)
+    world = 8
+    params = [param_tensor(p, "bf16", 600 + i) for i, p in enumerate(specs)]
+    grads = [[grad_tensor(p, "bf16", 601, r) for p in specs] for r in range(world)]
+    descs = [(p.dim0, p.row_numel, 0) for p in specs]
+    stor = [_storage(params, world, r, 2) for r in range(world)]
+    regions = [_grad_region(grads[r]) for r in range(world)]
+    _, _, shards_ref = OC.bucketed_reduce_scatter(grads, world, 16)
+    for r in (0, 5):
+        ctx = F.Ctx(world, r)
+        out = [torch.empty(p.size, dtype=torch.int16, device="cuda") for p in params]
+        gs = [torch.empty(-(-d // world) * R, dtype=torch.float32, device="cuda") for d, R, _ in descs]
+        b = F.Bucket(ctx, descs, shards=[stor[r][0].ptr + o for o in stor[r][1]], fulls=[o.data_ptr() for o in out],
+                     full_grads=[regions[r][0].ptr + o for o in regions[r][1]], grad_shards=[g.data_ptr() for g in gs],
+                     flags=L.BUCKET_SEGMENT_SHARDS)
+        F.p2p_allgather_bucket(ctx, b, [s[0].ptr for s in stor])
+        F.p2p_reduce_scatter_bucket(ctx, b, [g[0].ptr for g in regions])
+        torch.cuda.synchronize()
+        for o, p in zip(out, params):
+            assert np.array_equal(o.cpu().numpy().view(np.uint16), p.reshape(-1))
+        for j, g in enumerate(gs):
+            assert np.array_equal(g.cpu().numpy().view(np.uint32), shards_ref[r][j].reshape(-1).view(np.uint32))
+
+
+def test_signal_wait_and_timeout():
+    world = 4
+    ctxs = [F.Ctx(world, r) for r in range(world)]
+    flags = [torch.zeros(world, dtype=torch.int64, device="cuda") for _ in range(world)]
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    # every rank q writes epoch 3 into slot q of every rank's flag array
+    for q in range(world):
+        F.p2p_signal(ctxs[q], [flags[r].data_ptr() + 8 * q for r in range(world)], 3, s.cuda_stream)
+    for r in range(world):
+        F.p2p_wait(ctxs[r], flags[r].data_ptr(), 3, 10**9, err.data_ptr(), s.cuda_stream)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    assert all(torch.equal(f, torch.full((world,), 3, dtype=torch.int64, device="cuda")) for f in flags)
+    # an epoch nobody signals: the wait gives up after the timeout and flags the error
+    F.p2p_wait(ctxs[0], flags[0].data_ptr(), 4, 2 * 10**6, err.data_ptr(), s.cuda_stream)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 1
+
+
+def test_p2p_rejects_plain_storage():
+    ctx = F.Ctx(2, 0)
+    p = DevArray(np.zeros((64, 4), np.uint16))
+    b = F.Bucket(ctx, [(8, 4, 0)], shards=[p.ptr], fulls=[p.ptr])
+    with pytest.raises(F.FsdpError):
+        F.p2p_allgather_bucket(ctx, b, [p.ptr, p.ptr])
