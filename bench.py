@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--proxy-ctas", type=int, default=1)
     ap.add_argument("--proxy-smem", type=int, default=0)
+    ap.add_argument("--collective", default="nccl", choices=["nccl", "p2p"],
+                    help="nccl: pack + NCCL + copy-out (the paper's bucketing); p2p: fused peer-memory "
+                         "kernels K8/K9 (1 GPU: the 7 peers are simulated as separate buffers)")
     return ap.parse_args()
 
 
@@ -230,7 +233,14 @@ def main():
         nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
         pf = H.proxy_iters(H.bucket_times(fplan, t_fwd), nspi)
         pb = H.proxy_iters(H.bucket_times(bplan, t_bwd), nspi)
+    p2p = args.collective == "p2p"
+    if p2p:
+        if multi:
+            raise SystemExit("--collective p2p is wired for the 1-GPU simulated world only this round")
+        st.setup_p2p_simulated(seed=99)
     flags = 0 if args.no_reorder else L.SCHED_REORDER
+    if p2p:
+        flags |= L.SCHED_P2P
     if args.fwd_placement == "before":
         flags |= L.SCHED_FWD_AG_BEFORE_WAIT
     if args.bwd_placement == "before":
@@ -282,9 +292,15 @@ def main():
     # per-op device time from the timed steps' events -> dominant data kernel
     op_ns = [sum(r["op_ns"][i] for r in reports) for i in range(L.N_OPS)]
     op_cnt = [sum(r["op_count"][i] for r in reports) for i in range(L.N_OPS)]
-    kbytes, klaunch = st.kernel_bytes(), st.kernel_launches()
-    names = {L.OP_PACK_AG: "fsdp_ag_pack_kernel", L.OP_UNPACK: "fsdp_ag_unpack_kernel",
-             L.OP_PACK_RS: "fsdp_rs_pack_kernel", L.OP_COPYOUT_RS: "fsdp_rs_copyout_kernel"}
+    if p2p:
+        k8, k9 = st.p2p_bytes()
+        kbytes = {L.OP_AG: k8, L.OP_RS: k9}
+        klaunch = {L.OP_AG: len(st.fwd) + len(st.bwd), L.OP_RS: len(st.bwd)}
+        names = {L.OP_AG: "fsdp_p2p_allgather_kernel", L.OP_RS: "fsdp_p2p_reduce_scatter_kernel"}
+    else:
+        kbytes, klaunch = st.kernel_bytes(), st.kernel_launches()
+        names = {L.OP_PACK_AG: "fsdp_ag_pack_kernel", L.OP_UNPACK: "fsdp_ag_unpack_kernel",
+                 L.OP_PACK_RS: "fsdp_rs_pack_kernel", L.OP_COPYOUT_RS: "fsdp_rs_copyout_kernel"}
     live = [op for op in kbytes if kbytes[op] > 0 and op_ns[op] > 0]
     dom = max(live, key=lambda op: op_ns[op])
     peak, peak_src = measured_peak_hbm()
@@ -345,9 +361,13 @@ def main():
             "config": {
                 "workload": ("llama3-8b FSDP rank step, %s plan, %s" % (args.plan, "reorder fwd-%s/bwd-%s" % (
                     args.fwd_placement, args.bwd_placement) if not args.no_reorder else "vanilla order")) +
-                (", 1 GPU = rank 0 of a simulated %d-way job (pack/unpack only, no peers)" % world if not multi
+                ((", 1 GPU = rank 0 of a simulated %d-way job (pack/unpack only, no peers)" % world if not p2p else
+                  ", 1 GPU = rank 0 of a simulated %d-way job (peers' buffers simulated in local HBM)" % world)
+                 if not multi
                  else ", %d ranks over NCCL" % world),
                 "model": "llama3-8b shapes (Table 2; vocab 128256, 8 KV heads)", "layout_world": world,
+                "collective": ("NCCL all-gather / reduce-scatter with pack + copy-out kernels" if not p2p else
+                               "fused peer-memory kernels K8/K9 (peers simulated as separate HBM buffers)"),
                 "buckets_fwd": len(fplan), "buckets_bwd": len(bplan), "param_dtype": "bf16",
                 "reduce_dtype": "fp32", "proxy_tokens_per_gpu": tokens,
                 "value_def": "sum over ranks of full AG(fwd)+AG(bwd)+RS bucket bytes per second of step time",

@@ -238,6 +238,8 @@ typedef struct {
   int32_t kernel_chunks[4];
   int32_t ag_zero_copy;
   int32_t rs_zero_copy;
+  int64_t p2p_bytes[2];    /* algorithmic bytes per launch of K8 (peer AG) and K9 (peer RS):
+                              bytes read from all ranks (local + peers) + bytes written */
 } fsdp_bucket_info;
 fsdp_status fsdp_bucket_query(const fsdp_bucket* b, fsdp_bucket_info* out);
 
@@ -291,7 +293,23 @@ fsdp_status fsdp_reduce_scatter_bucket(fsdp_ctx* ctx, fsdp_bucket* b, void* rs_s
  *   FSDP_SCHED_DRY_RUN            write the log only, enqueue nothing (ctx may be NULL)
  *   FSDP_SCHED_TIMING             CUDA events around every op; synchronises at
  *                                 the end and fills step_ns, op_ns/op_count and
- *                                 log[i].ns */
+ *                                 log[i].ns
+ *   FSDP_SCHED_P2P                collectives over peer memory (K8 / K9, see
+ *                                 fsdp_p2p_*) instead of NCCL, with `p2p` below:
+ *     step start : signal + wait epoch E0 = epoch_base + 1 on the ready flags
+ *                  (every rank's shards are final);
+ *     PACK_AG    : no kernel (buckets need FSDP_BUCKET_SEGMENT_SHARDS); event;
+ *     AG b       : comm stream waits the event, K8 writes the full parameters
+ *                  (UNPACK is then empty);
+ *     COMPUTE_B b: (b >= 2) first waits the consumed flags >= E(b-2): peers have
+ *                  read the gradient slot this bucket's backward overwrites;
+ *     PACK_RS b  : signal "gradients of b ready" E(b) = epoch_base + 2 + b;
+ *     RS b       : comm stream waits ready flags >= E(b), K9 writes this rank's
+ *                  gradient shards, then signals "consumed" E(b);
+ *     COPYOUT_RS : no kernel;
+ *     step end   : wait consumed >= E(n_bwd - 1), signal + wait epoch_base +
+ *                  n_bwd + 2 on the ready flags.
+ *   The next step must use epoch_base + n_bwd + 2. */
 enum {
   FSDP_OP_PACK_AG = 0, FSDP_OP_AG = 1, FSDP_OP_WAIT_AG = 2, FSDP_OP_UNPACK = 3,
   FSDP_OP_COMPUTE_F = 4, FSDP_OP_COMPUTE_B = 5, FSDP_OP_PACK_RS = 6, FSDP_OP_RS = 7,
@@ -303,8 +321,25 @@ enum {
   FSDP_SCHED_BWD_AG_BEFORE_WAIT = 4u,
   FSDP_SCHED_NO_COMM = 8u,
   FSDP_SCHED_DRY_RUN = 16u,
-  FSDP_SCHED_TIMING = 32u
+  FSDP_SCHED_TIMING = 32u,
+  FSDP_SCHED_P2P = 64u
 };
+
+/* Peer tables of one rank for FSDP_SCHED_P2P (device pointers valid in this
+ * process; `world` entries per row). */
+typedef struct {
+  const void* const* ag_peers;  /* (n_fwd + n_bwd) rows: forward buckets then backward
+                                   buckets; [q] = rank q's segment storage of that bucket */
+  const void* const* rs_peers;  /* n_bwd rows: [q] = rank q's full_grads[0] of that bucket */
+  void* const* ready_slots;     /* [q] = this rank's slot in rank q's ready-flag array */
+  void* const* done_slots;      /* [q] = this rank's slot in rank q's consumed-flag array */
+  const void* ready_flags;      /* this rank's ready-flag array (world uint64) */
+  const void* done_flags;       /* this rank's consumed-flag array (world uint64) */
+  uint64_t epoch_base;
+  int64_t timeout_ns;           /* per wait; 0 = forever */
+  int32_t* error_flag;          /* device int set to 1 by a timed-out wait (nullable) */
+  int32_t reserved[2];
+} fsdp_p2p_schedule;
 
 typedef struct {
   fsdp_bucket* const* fwd;      /* n_fwd handles, forward execution order */
@@ -321,6 +356,7 @@ typedef struct {
   int32_t proxy_ctas_per_sm; /* K7 footprint: CTAs per SM (>= 1) */
   int32_t proxy_smem_bytes;  /* K7 footprint: dynamic shared memory per CTA */
   int32_t reserved;
+  const fsdp_p2p_schedule* p2p; /* FSDP_SCHED_P2P only, else NULL */
 } fsdp_schedule;
 
 typedef struct {

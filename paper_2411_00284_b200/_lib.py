@@ -28,7 +28,7 @@ ISSUE, WAIT = 1, 2
  OP_WAIT_RS, OP_COPYOUT_RS) = range(10)
 N_OPS = 10
 SCHED_REORDER, SCHED_FWD_AG_BEFORE_WAIT, SCHED_BWD_AG_BEFORE_WAIT = 1, 2, 4
-SCHED_NO_COMM, SCHED_DRY_RUN, SCHED_TIMING = 8, 16, 32
+SCHED_NO_COMM, SCHED_DRY_RUN, SCHED_TIMING, SCHED_P2P = 8, 16, 32, 64
 BUCKET_SEGMENT_SHARDS, BUCKET_SEGMENT_GRAD_SHARDS = 1, 2
 
 EXPORTED = [
@@ -79,7 +79,15 @@ class BucketDesc(C.Structure):
 
 class BucketInfo(C.Structure):
     _fields_ = [("ag_seg_bytes", C.c_int64), ("rs_seg_bytes", C.c_int64), ("kernel_bytes", C.c_int64 * 4),
-                ("kernel_chunks", C.c_int32 * 4), ("ag_zero_copy", C.c_int32), ("rs_zero_copy", C.c_int32)]
+                ("kernel_chunks", C.c_int32 * 4), ("ag_zero_copy", C.c_int32), ("rs_zero_copy", C.c_int32),
+                ("p2p_bytes", C.c_int64 * 2)]
+
+
+class P2PSchedule(C.Structure):
+    _fields_ = [("ag_peers", C.POINTER(C.c_void_p)), ("rs_peers", C.POINTER(C.c_void_p)),
+                ("ready_slots", C.POINTER(C.c_void_p)), ("done_slots", C.POINTER(C.c_void_p)),
+                ("ready_flags", C.c_void_p), ("done_flags", C.c_void_p), ("epoch_base", C.c_uint64),
+                ("timeout_ns", C.c_int64), ("error_flag", C.c_void_p), ("reserved", C.c_int32 * 2)]
 
 
 class Schedule(C.Structure):
@@ -88,7 +96,7 @@ class Schedule(C.Structure):
                 ("ag_staging", C.c_void_p * 2), ("rs_staging", C.c_void_p * 2),
                 ("compute", C.c_void_p), ("comm", C.c_void_p), ("n_fwd", C.c_int32),
                 ("n_bwd", C.c_int32), ("flags", C.c_uint32), ("proxy_ctas_per_sm", C.c_int32),
-                ("proxy_smem_bytes", C.c_int32), ("reserved", C.c_int32)]
+                ("proxy_smem_bytes", C.c_int32), ("reserved", C.c_int32), ("p2p", C.POINTER(P2PSchedule))]
 
 
 class LogEntry(C.Structure):

@@ -219,6 +219,8 @@ extern "C" fsdp_status fsdp_bucket_query(const fsdp_bucket* b, fsdp_bucket_info*
   if (b->rs_zero_copy && b->ctx && b->ctx->comm) out->kernel_bytes[3] = 0;
   out->ag_zero_copy = b->ag_zero_copy ? 1 : 0;
   out->rs_zero_copy = b->rs_zero_copy ? 1 : 0;
+  out->p2p_bytes[0] = b->p2p_ag.n ? b->p2p_ag.bytes_moved : 0;
+  out->p2p_bytes[1] = b->p2p_rs.n ? b->p2p_rs.bytes_moved : 0;
   return FSDP_OK;
 }
 

@@ -53,6 +53,12 @@
 #ifndef FSDP_WIDEN_V8
 #define FSDP_WIDEN_V8 1  // K4: one 256-bit store per 8 widened elements
 #endif
+#ifndef FSDP_K9_TEMPLATED
+#define FSDP_K9_TEMPLATED 0  // K9: compile-time world (all peers' loads in flight) vs batches of 4
+#endif
+#ifndef FSDP_K9_MIN_BLOCKS
+#define FSDP_K9_MIN_BLOCKS FSDP_MIN_BLOCKS
+#endif
 #ifndef FSDP_BULK
 #define FSDP_BULK 0  // bulk engine for: 0 none, 1 K3, 2 all pure-copy kernels (K0, K1, K3, K6)
 #endif
@@ -442,9 +448,52 @@ __device__ __forceinline__ void acc_vec(float (&acc)[8], const uint4& v, float s
 // K9 body: this rank's gradient shard = rank-order fp32 sum over every peer.
 // Vector chunks: n groups of 8 bf16 (or 4 fp32) elements; 4 peers' loads in
 // flight per thread, added strictly in rank order.
+// Compile-time world: all W peers' 16-B loads are issued before the first add
+// (W loads in flight per thread), then added strictly in rank order.
+template <bool kBf16, int W>
+__device__ __forceinline__ void peer_reduce16_w(const PeerTable& pt, uint64_t off, char* dst, uint32_t n,
+                                                float scale) {
+  for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
+    const uint64_t o = off + 16ull * i;
+    uint4 v[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) v[q] = ld_stream(reinterpret_cast<const uint4*>(pt.p[q] + o));
+    float acc[8];
+#pragma unroll
+    for (int q = 0; q < W; ++q) acc_vec<kBf16>(acc, v[q], scale, q == 0);
+    uint4 a, b;
+    a.x = __float_as_uint(acc[0]); a.y = __float_as_uint(acc[1]); a.z = __float_as_uint(acc[2]);
+    a.w = __float_as_uint(acc[3]);
+    if (kBf16) {
+      b.x = __float_as_uint(acc[4]); b.y = __float_as_uint(acc[5]); b.z = __float_as_uint(acc[6]);
+      b.w = __float_as_uint(acc[7]);
+      if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(reinterpret_cast<uint4*>(dst) + 2 * i),
+                     "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                     : "memory");
+      } else {
+        uint4* d = reinterpret_cast<uint4*>(dst) + 2 * i;
+        st_v4(d, a);
+        st_v4(d + 1, b);
+      }
+    } else {
+      st_v4(reinterpret_cast<uint4*>(dst) + i, a);
+    }
+  }
+}
+
 template <bool kBf16>
 __device__ __forceinline__ void peer_reduce16(const PeerTable& pt, int world, uint64_t off, char* dst,
                                               uint32_t n, float scale) {
+  if (FSDP_K9_TEMPLATED) {
+    switch (world) {
+      case 1: return peer_reduce16_w<kBf16, 1>(pt, off, dst, n, scale);
+      case 2: return peer_reduce16_w<kBf16, 2>(pt, off, dst, n, scale);
+      case 4: return peer_reduce16_w<kBf16, 4>(pt, off, dst, n, scale);
+      case 8: return peer_reduce16_w<kBf16, 8>(pt, off, dst, n, scale);
+      default: break;
+    }
+  }
   constexpr int K = kBf16 ? 8 : 4;
   for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
     float acc[8];
@@ -465,8 +514,14 @@ __device__ __forceinline__ void peer_reduce16(const PeerTable& pt, int world, ui
       b.x = __float_as_uint(acc[4]); b.y = __float_as_uint(acc[5]); b.z = __float_as_uint(acc[6]);
       b.w = __float_as_uint(acc[7]);
       uint4* d = reinterpret_cast<uint4*>(dst) + 2 * i;
-      st_v4(d, a);
-      st_v4(d + 1, b);
+      if (FSDP_WIDEN_V8 && (reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(d), "r"(a.x), "r"(a.y),
+                     "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                     : "memory");
+      } else {
+        st_v4(d, a);
+        st_v4(d + 1, b);
+      }
     } else {
       st_v4(reinterpret_cast<uint4*>(dst) + i, a);
     }
@@ -519,7 +574,7 @@ __global__ void FSDP_LSU_BOUNDS fsdp_p2p_allgather_kernel(const Chunk* tab, int 
   run_peer_copy(tab, n, pt);
 }
 // K9: fused gradient widen + 1/N + reduce-scatter + copy-out over peer memory.
-__global__ void FSDP_LSU_BOUNDS fsdp_p2p_reduce_scatter_kernel(const Chunk* tab, int n, const __grid_constant__ PeerTable pt, int world,
+__global__ void __launch_bounds__(kThreads, FSDP_K9_MIN_BLOCKS) fsdp_p2p_reduce_scatter_kernel(const Chunk* tab, int n, const __grid_constant__ PeerTable pt, int world,
                                                                float scale) {
   run_peer_reduce(tab, n, pt, world, scale);
 }

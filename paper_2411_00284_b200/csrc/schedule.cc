@@ -103,9 +103,10 @@ fsdp_status grow_events(fsdp_ctx* c, size_t n) {
 extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, fsdp_step_report* out) {
   if (!s) return fail(FSDP_ERR_INVALID_ARG, "NULL schedule");
   const uint32_t known = FSDP_SCHED_REORDER | FSDP_SCHED_FWD_AG_BEFORE_WAIT | FSDP_SCHED_BWD_AG_BEFORE_WAIT |
-                         FSDP_SCHED_NO_COMM | FSDP_SCHED_DRY_RUN | FSDP_SCHED_TIMING;
+                         FSDP_SCHED_NO_COMM | FSDP_SCHED_DRY_RUN | FSDP_SCHED_TIMING | FSDP_SCHED_P2P;
   if (s->flags & ~known) return fail(FSDP_ERR_INVALID_ARG, "unknown schedule flag");
   if (s->n_fwd < 0 || s->n_bwd < 0) return fail(FSDP_ERR_INVALID_ARG, "negative bucket count");
+  const bool p2p = s->flags & FSDP_SCHED_P2P;
   const bool dry = s->flags & FSDP_SCHED_DRY_RUN;
   const bool timing = (s->flags & FSDP_SCHED_TIMING) && !dry;
   const bool with_comm = !(s->flags & FSDP_SCHED_NO_COMM);
@@ -151,10 +152,34 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     if (!s->bwd[i] || s->bwd[i]->ctx != ctx || !s->bwd[i]->has_shards || !s->bwd[i]->has_fulls ||
         !s->bwd[i]->has_grads || !s->bwd[i]->has_gshards)
       return fail(FSDP_ERR_INVALID_ARG, "backward bucket missing, foreign or without AG/RS pointers");
-  if ((s->n_fwd || s->n_bwd) && (!s->ag_staging[0] || !s->ag_staging[1]))
-    return fail(FSDP_ERR_INVALID_ARG, "NULL AG staging slot");
-  if (s->n_bwd && (!s->rs_staging[0] || !s->rs_staging[1]))
-    return fail(FSDP_ERR_INVALID_ARG, "NULL RS staging slot");
+  if (p2p) {
+    const fsdp_p2p_schedule* pp = s->p2p;
+    if (!pp || !pp->ag_peers || (s->n_bwd && !pp->rs_peers) || !pp->ready_slots || !pp->done_slots ||
+        !pp->ready_flags || !pp->done_flags)
+      return fail(FSDP_ERR_INVALID_ARG, "FSDP_SCHED_P2P needs a complete fsdp_p2p_schedule");
+    if (ctx->world > kMaxPeers) return fail(FSDP_ERR_UNSUPPORTED, "peer-memory path supports world <= 16");
+    for (int32_t i = 0; i < s->n_fwd + s->n_bwd; ++i) {
+      fsdp_bucket* b = i < s->n_fwd ? s->fwd[i] : s->bwd[i - s->n_fwd];
+      if (!b->ag_zero_copy) return fail(FSDP_ERR_INVALID_ARG, "FSDP_SCHED_P2P needs FSDP_BUCKET_SEGMENT_SHARDS buckets");
+      for (int32_t q = 0; q < ctx->world; ++q) {
+        const void* p = pp->ag_peers[static_cast<int64_t>(i) * ctx->world + q];
+        if (!p || reinterpret_cast<uintptr_t>(p) % 16) return fail(FSDP_ERR_INVALID_ARG, "bad ag_peers entry");
+      }
+    }
+    for (int32_t i = 0; i < s->n_bwd; ++i)
+      for (int32_t q = 0; q < ctx->world; ++q) {
+        const void* p = pp->rs_peers[static_cast<int64_t>(i) * ctx->world + q];
+        if (!p || reinterpret_cast<uintptr_t>(p) % 16) return fail(FSDP_ERR_INVALID_ARG, "bad rs_peers entry");
+      }
+    for (int32_t q = 0; q < ctx->world; ++q)
+      if (reinterpret_cast<uintptr_t>(pp->ready_slots[q]) % 8 || reinterpret_cast<uintptr_t>(pp->done_slots[q]) % 8)
+        return fail(FSDP_ERR_INVALID_ARG, "flag slot not 8-B aligned");
+  } else {
+    if ((s->n_fwd || s->n_bwd) && (!s->ag_staging[0] || !s->ag_staging[1]))
+      return fail(FSDP_ERR_INVALID_ARG, "NULL AG staging slot");
+    if (s->n_bwd && (!s->rs_staging[0] || !s->rs_staging[1]))
+      return fail(FSDP_ERR_INVALID_ARG, "NULL RS staging slot");
+  }
   for (int i = 0; i < 2; ++i)
     if (reinterpret_cast<uintptr_t>(s->ag_staging[i]) % 16 || reinterpret_cast<uintptr_t>(s->rs_staging[i]) % 16)
       return fail(FSDP_ERR_INVALID_ARG, "staging slot not 16-B aligned");
@@ -171,9 +196,102 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   if (timing) FSDP_CUDA_TRY(cudaEventRecord(ev[0], cs));
 
   int launches = 0, colls = 0;
+  // ---- peer-memory mode: epoch protocol of include/fsdp.h (FSDP_SCHED_P2P)
+  const fsdp_p2p_schedule* pp = p2p ? s->p2p : nullptr;
+  PeerTable ready_slots{}, done_slots{};
+  auto epoch = [&](int64_t b) { return pp->epoch_base + 2 + static_cast<uint64_t>(b); };
+  auto p2p_wait = [&](const void* flags, uint64_t v, cudaStream_t st) -> fsdp_status {
+    FSDP_CUDA_TRY(launch_p2p_wait(flags, ctx->world, v, pp->timeout_ns, pp->error_flag, st));
+    ++launches;
+    return FSDP_OK;
+  };
+  auto p2p_signal = [&](const PeerTable& slots, uint64_t v, cudaStream_t st) -> fsdp_status {
+    FSDP_CUDA_TRY(launch_p2p_signal(slots, ctx->world, v, st));
+    ++launches;
+    return FSDP_OK;
+  };
+  auto peer_row = [&](const void* const* rows, int64_t row) {
+    PeerTable t{};
+    for (int32_t q = 0; q < ctx->world; ++q) t.p[q] = static_cast<const char*>(rows[row * ctx->world + q]);
+    return t;
+  };
+  if (pp && with_comm) {
+    for (int32_t q = 0; q < ctx->world; ++q) {
+      ready_slots.p[q] = static_cast<const char*>(pp->ready_slots[q]);
+      done_slots.p[q] = static_cast<const char*>(pp->done_slots[q]);
+    }
+    FSDP_TRY(p2p_signal(ready_slots, pp->epoch_base + 1, cs));  // my shards are final
+    FSDP_TRY(p2p_wait(pp->ready_flags, pp->epoch_base + 1, cs));
+  }
   for (size_t i = 0; i < seq.size(); ++i) {
     const Op& o = seq[i];
     fsdp_bucket* b = (o.phase == 0 ? s->fwd : s->bwd)[o.bucket];
+    if (pp) {
+      // the peer-memory path: same sequence, different work per op
+      const bool comm_op = is_comm(o.op);
+      const bool skipped = !with_comm && (comm_op || o.op == FSDP_OP_WAIT_AG || o.op == FSDP_OP_WAIT_RS);
+      cudaStream_t on = comm_op ? ms : cs;
+      if (timing && !skipped) {
+        if (comm_op) FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, o.op == FSDP_OP_AG ? b->ev_ag_packed : b->ev_rs_packed, 0));
+        FSDP_CUDA_TRY(cudaEventRecord(ev[2 + 2 * i], on));
+      }
+      switch (o.op) {
+        case FSDP_OP_PACK_AG:
+          if (with_comm) FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_packed, cs));
+          break;
+        case FSDP_OP_AG:
+          if (with_comm) {
+            FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_ag_packed, 0));
+            const int64_t row = o.phase == 0 ? o.bucket : s->n_fwd + o.bucket;
+            FSDP_CUDA_TRY(launch_p2p_allgather(b->p2p_ag, peer_row(pp->ag_peers, row), ms, ctx->max_ctas));
+            FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_done, ms));
+            ++launches;
+            ++colls;
+          }
+          break;
+        case FSDP_OP_WAIT_AG:
+          if (with_comm) FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, b->ev_ag_done, 0));
+          break;
+        case FSDP_OP_COMPUTE_F:
+        case FSDP_OP_COMPUTE_B: {
+          // the backward of bucket b overwrites gradient slot b % 2: peers must be done with b - 2
+          if (o.op == FSDP_OP_COMPUTE_B && with_comm && o.bucket >= 2)
+            FSDP_TRY(p2p_wait(pp->done_flags, epoch(o.bucket - 2), cs));
+          const int64_t* it = o.op == FSDP_OP_COMPUTE_F ? s->proxy_iters_fwd : s->proxy_iters_bwd;
+          if (it && it[o.bucket] > 0) {
+            FSDP_CUDA_TRY(launch_proxy(it[o.bucket], proxy_grid, s->proxy_smem_bytes, ctx->sink, cs));
+            ++launches;
+          }
+          break;
+        }
+        case FSDP_OP_PACK_RS:
+          if (with_comm) {
+            FSDP_TRY(p2p_signal(ready_slots, epoch(o.bucket), cs));  // my gradients of b are final
+            FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_packed, cs));
+          }
+          break;
+        case FSDP_OP_RS:
+          if (with_comm) {
+            FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_rs_packed, 0));
+            FSDP_TRY(p2p_wait(pp->ready_flags, epoch(o.bucket), ms));
+            const float inv = 1.0f / static_cast<float>(ctx->world);
+            FSDP_CUDA_TRY(launch_p2p_reduce_scatter(b->p2p_rs, peer_row(pp->rs_peers, o.bucket), ctx->world, inv, ms,
+                                                    ctx->max_ctas));
+            ++launches;
+            FSDP_TRY(p2p_signal(done_slots, epoch(o.bucket), ms));  // done reading peers' b
+            FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_done, ms));
+            ++colls;
+          }
+          break;
+        case FSDP_OP_WAIT_RS:
+          if (with_comm) FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, b->ev_rs_done, 0));
+          break;
+        default:  // UNPACK, COPYOUT_RS: the peer kernels wrote the destinations
+          break;
+      }
+      if (timing && !skipped) FSDP_CUDA_TRY(cudaEventRecord(ev[3 + 2 * i], on));
+      continue;
+    }
     char* ag_st = static_cast<char*>(s->ag_staging[o.bucket & 1]);
     char* rs_st = static_cast<char*>(s->rs_staging[o.bucket & 1]);
     const bool comm_op = is_comm(o.op);
@@ -206,6 +324,12 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
       case FSDP_OP_COPYOUT_RS: FSDP_TRY(rs_copyout(ctx, b, rs_st, cs, with_comm, &launches)); break;
     }
     if (timing && !skipped) FSDP_CUDA_TRY(cudaEventRecord(ev[3 + 2 * i], on));
+  }
+  if (pp && with_comm) {
+    // step end: peers are done with every gradient slot and every shard of mine
+    if (s->n_bwd > 0) FSDP_TRY(p2p_wait(pp->done_flags, epoch(s->n_bwd - 1), cs));
+    FSDP_TRY(p2p_signal(ready_slots, epoch(s->n_bwd), cs));
+    FSDP_TRY(p2p_wait(pp->ready_flags, epoch(s->n_bwd), cs));
   }
   if (timing) FSDP_CUDA_TRY(cudaEventRecord(ev[1], cs));
 

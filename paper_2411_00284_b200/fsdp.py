@@ -121,7 +121,7 @@ class Bucket:
         check(L.lib.fsdp_bucket_query(self.h, C.byref(i)))
         return dict(ag_seg=i.ag_seg_bytes, rs_seg=i.rs_seg_bytes, kernel_bytes=list(i.kernel_bytes),
                     kernel_chunks=list(i.kernel_chunks), ag_zero_copy=bool(i.ag_zero_copy),
-                    rs_zero_copy=bool(i.rs_zero_copy))
+                    rs_zero_copy=bool(i.rs_zero_copy), p2p_bytes=list(i.p2p_bytes))
 
     def close(self):
         if self.h:
@@ -145,10 +145,13 @@ def reduce_scatter_bucket(ctx, bucket, staging_ptr, compute=0, comm=0, flags=L.I
 
 def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0, comm=0, flags=0,
                  proxy_iters_fwd=None, proxy_iters_bwd=None, proxy_ctas_per_sm=1, proxy_smem_bytes=0,
-                 n_fwd=None, n_bwd=None, want_log=True):
+                 n_fwd=None, n_bwd=None, want_log=True, p2p=None):
     """fsdp_run_schedule.  fwd / bwd: Bucket lists in execution order (or
     counts via n_fwd / n_bwd with FSDP_SCHED_DRY_RUN and ctx=None).  Returns the
-    step report as a dict (log as a list of (phase, op, bucket, stream, ns))."""
+    step report as a dict (log as a list of (phase, op, bucket, stream, ns)).
+    p2p (with FSDP_SCHED_P2P): dict with ag_peers (rows of world pointers),
+    rs_peers, ready_slots, done_slots, ready_flags, done_flags, epoch_base,
+    timeout_ns, error_flag."""
     nf = len(fwd) if fwd is not None else (n_fwd or 0)
     nb = len(bwd) if bwd is not None else (n_bwd or 0)
     s = L.Schedule()
@@ -162,6 +165,19 @@ def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0,
     s.compute, s.comm = compute or None, comm or None
     s.n_fwd, s.n_bwd, s.flags = nf, nb, flags
     s.proxy_ctas_per_sm, s.proxy_smem_bytes, s.reserved = proxy_ctas_per_sm, proxy_smem_bytes, 0
+    keep = []
+    if p2p is not None:
+        ps = L.P2PSchedule()
+        arrs = [L.ptr_array([x for row in p2p["ag_peers"] for x in row]),
+                L.ptr_array([x for row in p2p.get("rs_peers", []) for x in row]),
+                L.ptr_array(p2p["ready_slots"]), L.ptr_array(p2p["done_slots"])]
+        keep += arrs
+        ps.ag_peers, ps.rs_peers, ps.ready_slots, ps.done_slots = arrs
+        ps.ready_flags, ps.done_flags = p2p["ready_flags"], p2p["done_flags"]
+        ps.epoch_base, ps.timeout_ns = int(p2p["epoch_base"]), int(p2p.get("timeout_ns", 10**10))
+        ps.error_flag = p2p.get("error_flag") or None
+        keep.append(ps)
+        s.p2p = C.pointer(ps)
     cap = 5 * nf + 9 * nb + 4
     log = (L.LogEntry * cap)() if want_log else None
     rep = L.StepReport()

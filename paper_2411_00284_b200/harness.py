@@ -129,14 +129,74 @@ class RankState:
             v = buf[: buf.numel() // 4 * 4].view(torch.float32)
         v.normal_(0.0, std, generator=gen)
 
+    # ------------------------------------------------------ peer-memory path
+    def setup_p2p_simulated(self, seed=1, fill=True):
+        """Peer-memory (FSDP_SCHED_P2P) state for this rank with the other
+        world - 1 ranks SIMULATED on the same GPU: their shard storage and
+        gradient slots are separate device buffers (same layout as ours, as on
+        real peers), read by K8 / K9 exactly as NVLink-mapped peer memory would
+        be; their flag slots are pre-set far ahead so the epoch waits only
+        track this rank's own signals."""
+        W, r = self.world, self.rank
+        g = torch.Generator(device=self.shard_buf.device).manual_seed(seed)
+        self.peer_shards, self.peer_grads = [], []
+        for q in range(W):
+            if q == r:
+                self.peer_shards.append(self.shard_buf)
+                self.peer_grads.append(self.grad_slots)
+                continue
+            sb = torch.zeros_like(self.shard_buf)
+            gs = [torch.empty_like(t) for t in self.grad_slots]
+            if fill:
+                self._fill_normal(sb, 0.02, g, self.param_dtype)
+                for t in gs:
+                    self._fill_normal(t, 1e-3, g, L.BF16)
+            self.peer_shards.append(sb)
+            self.peer_grads.append(gs)
+        dev = self.shard_buf.device
+        self.ready = torch.full((W,), 2 ** 62, dtype=torch.int64, device=dev)
+        self.done = torch.full((W,), 2 ** 62, dtype=torch.int64, device=dev)
+        self.ready[r] = 0
+        self.done[r] = 0
+        self.sink = torch.zeros(2 * W, dtype=torch.int64, device=dev)   # simulated peers' slots
+        self.p2p_err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.ready_slots = [self.ready.data_ptr() + 8 * r if q == r else self.sink.data_ptr() + 8 * q
+                            for q in range(W)]
+        self.done_slots = [self.done.data_ptr() + 8 * r if q == r else self.sink.data_ptr() + 8 * (W + q)
+                           for q in range(W)]
+        self._p2p_tables()
+
+    def _p2p_tables(self):
+        W = self.world
+        self.ag_peers = [[self.peer_shards[q].data_ptr() + self.shard_offs[b.members[0]] for q in range(W)]
+                         for b in self.fwd + self.bwd]
+        self.rs_peers = [[self.peer_grads[q][i % 2].data_ptr() for q in range(W)] for i, b in enumerate(self.bwd)]
+        self.epoch = 0
+
+    def p2p_schedule(self, timeout_ns=10 ** 10):
+        return dict(ag_peers=self.ag_peers, rs_peers=self.rs_peers, ready_slots=self.ready_slots,
+                    done_slots=self.done_slots, ready_flags=self.ready.data_ptr(), done_flags=self.done.data_ptr(),
+                    epoch_base=self.epoch, timeout_ns=timeout_ns, error_flag=self.p2p_err.data_ptr())
+
+    def p2p_bytes(self):
+        """Algorithmic bytes per step of K8 (peer AG, both phases) and K9 (peer RS)."""
+        k8 = sum(b.query()["p2p_bytes"][0] for b in self.fwd + self.bwd)
+        k9 = sum(b.query()["p2p_bytes"][1] for b in self.bwd)
+        return k8, k9
+
     def step(self, flags, compute, comm, proxy_fwd=None, proxy_bwd=None, ctas_per_sm=1, smem=0,
              want_log=False):
+        p2p = None
+        if flags & L.SCHED_P2P:
+            p2p = self.p2p_schedule()
+            if not flags & L.SCHED_NO_COMM:
+                self.epoch += len(self.bwd) + 2
         return F.run_schedule(self.ctx, self.fwd, self.bwd,
                               ag_staging=(self.ag_st[0].data_ptr(), self.ag_st[1].data_ptr()),
                               rs_staging=(self.rs_st[0].data_ptr(), self.rs_st[1].data_ptr()),
                               compute=compute, comm=comm, flags=flags, proxy_iters_fwd=proxy_fwd,
                               proxy_iters_bwd=proxy_bwd, proxy_ctas_per_sm=ctas_per_sm,
-                              proxy_smem_bytes=smem, want_log=want_log)
+                              proxy_smem_bytes=smem, want_log=want_log, p2p=p2p)
 
     # -------------------------------------------------------------- accounting
     def step_bytes(self):

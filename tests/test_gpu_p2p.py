@@ -143,6 +143,80 @@ def test_signal_wait_and_timeout():
     assert int(err.item()) == 1
 
 
+@pytest.mark.parametrize("flags", [L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT, 0,
+                                   L.SCHED_REORDER | L.SCHED_BWD_AG_BEFORE_WAIT])
+def test_p2p_schedule_step_bit_exact(flags):
+    """A whole step through fsdp_run_schedule with FSDP_SCHED_P2P for rank 1 of
+    4 simulated ranks (peers' buffers hold the peers' real data): every full
+    parameter gathered, every gradient shard equal to the oracle's RS."""
+    world, rank = 4, 1
+    specs = toy_mlp()
+    descs = [(p.dim0, p.row_numel, p.module_id) for p in specs]
+    params = [param_tensor(p, "bf16", 800 + i) for i, p in enumerate(specs)]
+    grads = [[grad_tensor(p, "bf16", 801, q) for p in specs] for q in range(world)]
+    fplan, _ = F.plan_buckets(descs, world, [0] * 8, (0, 0), (0, 0), 0, L.PLAN_MANUAL, L.PHASE_FWD)
+    bplan, _ = F.plan_buckets(descs, world, [0] * 8, (0, 0), (0, 0), 0, L.PLAN_MANUAL, L.PHASE_BWD)
+    ctx = F.Ctx(world, rank)
+    # segment storage of every rank for every (forward) bucket; backward buckets have the same members
+    seg_of = {}
+    keep = []
+    for members in fplan:
+        m = tuple(sorted(members))
+        bufs = []
+        for q in range(world):
+            sbuf, offs = _storage([params[j] for j in m], world, q, 2)
+            bufs.append((sbuf, offs))
+            keep.append(sbuf)
+        seg_of[m] = bufs
+    fulls = {}
+
+    def bucket(members, phase, i):
+        m = tuple(sorted(members))
+        sbuf, offs = seg_of[m][rank]
+        out = [DevArray(nbytes=params[j].nbytes, fill=0x5A, dtype=np.uint16, shape=params[j].shape) for j in m]
+        fulls[(phase, i)] = (m, out)
+        kw = {}
+        if phase == 1:
+            regions = [_grad_region([grads[q][j] for j in m]) for q in range(world)]
+            gs = [DevArray(nbytes=-(-params[j].shape[0] // world) * params[j].shape[1] * 4, fill=0x77,
+                           dtype=np.float32) for j in m]
+            keep.extend(r[0] for r in regions)
+            kw = dict(full_grads=[regions[rank][0].ptr + o for o in regions[rank][1]], grad_shards=[g.ptr for g in gs])
+            fulls[(phase, i)] = (m, out, gs, [r[0].ptr for r in regions])
+        return F.Bucket(ctx, [descs[j] for j in m], shards=[sbuf.ptr + o for o in offs], fulls=[o.ptr for o in out],
+                        flags=L.BUCKET_SEGMENT_SHARDS, **kw)
+    fwd = [bucket(m, 0, i) for i, m in enumerate(fplan)]
+    bwd = [bucket(m, 1, i) for i, m in enumerate(bplan)]
+    ag_peers = [[seg_of[tuple(sorted(m))][q][0].ptr for q in range(world)] for m in list(fplan) + list(bplan)]
+    rs_peers = [fulls[(1, i)][3] for i in range(len(bplan))]
+    ready = torch.full((world,), 2 ** 62, dtype=torch.int64, device="cuda")
+    done = torch.full((world,), 2 ** 62, dtype=torch.int64, device="cuda")
+    ready[rank] = 0
+    done[rank] = 0
+    sink = torch.zeros(2 * world, dtype=torch.int64, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    p2p = dict(ag_peers=ag_peers, rs_peers=rs_peers,
+               ready_slots=[ready.data_ptr() + 8 * rank if q == rank else sink.data_ptr() + 8 * q for q in range(world)],
+               done_slots=[done.data_ptr() + 8 * rank if q == rank else sink.data_ptr() + 8 * (world + q)
+                           for q in range(world)],
+               ready_flags=ready.data_ptr(), done_flags=done.data_ptr(), epoch_base=0, timeout_ns=5 * 10**9,
+               error_flag=err.data_ptr())
+    cs, ms = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+    rep = F.run_schedule(ctx, fwd, bwd, compute=cs.cuda_stream, comm=ms.cuda_stream,
+                         flags=flags | L.SCHED_P2P | L.SCHED_TIMING, p2p=p2p)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    assert rep["collectives"] == len(fwd) + 2 * len(bwd)
+    assert int(ready[rank].item()) == len(bwd) + 2 and int(done[rank].item()) == len(bwd) + 1
+    _, _, shards_ref = OC.bucketed_reduce_scatter(grads, world, 16)
+    for (phase, i), v in fulls.items():
+        for j, o in zip(v[0], v[1]):
+            assert np.array_equal(o.get(), params[j]), (phase, i, j)
+        if phase == 1:
+            for j, g in zip(v[0], v[2]):
+                assert np.array_equal(g.get().view(np.uint32), shards_ref[rank][j].reshape(-1).view(np.uint32))
+
+
 def test_p2p_rejects_plain_storage():
     ctx = F.Ctx(2, 0)
     p = DevArray(np.zeros((64, 4), np.uint16))

@@ -48,7 +48,16 @@ SWEEP3 = {
     "d8_c1k_t128_u4": ["FSDP_CTAS_PER_SM=1024", "FSDP_THREADS=128", "FSDP_UNROLL=4", "FSDP_MIN_BLOCKS=16"],
 }
 
+SWEEP4 = {
+    "e0_default": [],
+    "e1_k9tpl": ["FSDP_K9_TEMPLATED=1"],
+    "e2_k9tpl_mb2": ["FSDP_K9_TEMPLATED=1", "FSDP_K9_MIN_BLOCKS=2"],
+    "e3_k9_mb2": ["FSDP_K9_MIN_BLOCKS=2"],
+    "e4_k9tpl_k16": ["FSDP_K9_TEMPLATED=1", "FSDP_CHUNK_KB=16"],
+}
+
 VARIANTS = {
+    **SWEEP4,
     **SWEEP3,
     **SWEEP2,
     "base": [],
@@ -111,7 +120,46 @@ def measure(reps=5, nblocks=4):
         "K6_rs_copyout": (lambda b: F.reduce_scatter_bucket(ctx, b[0], b[2].data_ptr(), s.cuda_stream, 0, L.WAIT),
                           8 * sum(shard)),
     }
+    # peer-memory kernels: rank 0 of 8, the 7 peers' buffers simulated in local HBM
+    goffs, gtot = [], 0
+    for n in full:
+        goffs.append(gtot)
+        gtot += -(-2 * n // 256) * 256
+    soffs, sseg = F.layout(descs, world, 2, 16)
+    pblocks = []
+    for b in range(nblocks):
+        stor = [torch.randn(sseg // 2, device="cuda").to(torch.bfloat16) for _ in range(world)]
+        greg = [torch.randn(gtot // 2, device="cuda").to(torch.bfloat16) for _ in range(world)]
+        fu = [torch.empty(n, dtype=torch.bfloat16, device="cuda") for n in full]
+        gs = [torch.empty(n, dtype=torch.float32, device="cuda") for n in shard]
+        bk = F.Bucket(ctx, descs, shards=[stor[0].data_ptr() + o for o in soffs], fulls=[x.data_ptr() for x in fu],
+                      full_grads=[greg[0].data_ptr() + o for o in goffs], grad_shards=[x.data_ptr() for x in gs],
+                      flags=L.BUCKET_SEGMENT_SHARDS)
+        pblocks.append((bk, [x.data_ptr() for x in stor], [x.data_ptr() for x in greg], stor, greg, fu, gs))
+    q0 = pblocks[0][0].query()["p2p_bytes"]
+    pops = {
+        "K8_p2p_ag": (lambda b: F.p2p_allgather_bucket(ctx, b[0], b[1], s.cuda_stream), q0[0]),
+        "K9_p2p_rs": (lambda b: F.p2p_reduce_scatter_bucket(ctx, b[0], b[2], s.cuda_stream), q0[1]),
+    }
     out = {}
+    for name, (fn, nbytes) in pops.items():
+        for b in pblocks:
+            fn(b)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(reps):
+            for b in pblocks:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                fn(b)
+                e1.record(s)
+                times.append((e0, e1))
+        torch.cuda.synchronize()
+        ms = sorted(a.elapsed_time(b) for a, b in times)
+        med = ms[len(ms) // 2]
+        out[name] = {"GB/s": round(nbytes / (med * 1e-3) / 1e9, 1), "ms": round(med, 4), "bytes": nbytes}
+    del pblocks
+    torch.cuda.empty_cache()
     for name, (fn, nbytes) in ops.items():
         for b in blocks:       # warm-up
             fn(b)
