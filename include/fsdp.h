@@ -240,7 +240,16 @@ typedef struct {
   int32_t rs_zero_copy;
   int64_t p2p_bytes[2];    /* algorithmic bytes per launch of K8 (peer AG) and K9 (peer RS):
                               bytes read from all ranks (local + peers) + bytes written */
+  int32_t ag_direct;       /* 1: direct gather (below) */
+  int32_t reserved;
 } fsdp_bucket_info;
+/* Direct gather: a one-parameter bucket whose dim 0 divides evenly over the
+ * world and whose segment has no alignment gap has a gathered buffer that is
+ * byte-identical to the full parameter.  Such a bucket never uses ag_staging:
+ * the all-gather writes the full parameter itself (ISSUE packs this rank's
+ * rows into it unless the collective sends from segment storage; WAIT has no
+ * copy-out).  A layout-only ctx's ISSUE therefore writes this rank's rows of
+ * the full parameter only.  Detected automatically. */
 fsdp_status fsdp_bucket_query(const fsdp_bucket* b, fsdp_bucket_info* out);
 
 /* ------------------------------------------ 3. fsdp_allgather_bucket

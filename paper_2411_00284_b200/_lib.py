@@ -80,7 +80,7 @@ class BucketDesc(C.Structure):
 class BucketInfo(C.Structure):
     _fields_ = [("ag_seg_bytes", C.c_int64), ("rs_seg_bytes", C.c_int64), ("kernel_bytes", C.c_int64 * 4),
                 ("kernel_chunks", C.c_int32 * 4), ("ag_zero_copy", C.c_int32), ("rs_zero_copy", C.c_int32),
-                ("p2p_bytes", C.c_int64 * 2)]
+                ("p2p_bytes", C.c_int64 * 2), ("ag_direct", C.c_int32), ("reserved", C.c_int32)]
 
 
 class P2PSchedule(C.Structure):

@@ -88,6 +88,13 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
                   "FSDP_BUCKET_SEGMENT_GRAD_SHARDS: grad shards do not follow the segment offsets");
   }
 
+  // Direct gather: a one-parameter bucket without padding (N | d and no
+  // alignment gap) has a gathered buffer byte-identical to the full parameter,
+  // so the all-gather writes the full parameter itself -- no staging, no
+  // copy-out (the per-parameter collective of the paper's unbucketed graph).
+  const bool direct = k == 1 && d->fulls && d->params[0].dim0 % N == 0 &&
+                      ag_seg == (d->params[0].dim0 / N) * d->params[0].row_numel * ep;
+
   TableBuilder pack, unpack, rpack, rcopy, gaps, p2p_ag, p2p_rs;
   for (int32_t j = 0; j < k; ++j) {
     const fsdp_param_desc& p = d->params[j];
@@ -95,7 +102,12 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
     const int64_t R = p.row_numel;
     const int64_t ag_end = (j + 1 < k) ? ag_off[j + 1] : ag_seg;
     const int64_t rs_end = (j + 1 < k) ? rs_off[j + 1] : rs_seg;
-    if (d->shards) {
+    if (d->shards && direct) {
+      // own rows straight into the full parameter (used unless the collective
+      // sends from segment storage itself)
+      pack.copy(reinterpret_cast<uint64_t>(d->shards[0]),
+                reinterpret_cast<uint64_t>(d->fulls[0]) + static_cast<uint64_t>(r * ag_seg), ag_seg, kAbsDst);
+    } else if (d->shards) {
       const int64_t nb = own.c * R * ep;
       if (ag_zc) {
         gaps.zero(reinterpret_cast<uint64_t>(d->shards[0]) + ag_off[j] + nb, ag_end - ag_off[j] - nb);
@@ -112,7 +124,7 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
     }
     for (int32_t q = 0; q < N; ++q) {
       const ShardRows s = shard_rows(p.dim0, N, q);
-      if (d->fulls && s.v > 0) {
+      if (d->fulls && s.v > 0 && !direct) {
         // K3: valid rows of rank q's chunk -> rows [q c, q c + v) of the full param
         // (this rank's rows from its segment-layout storage when zero-copy).
         const uint64_t dst = reinterpret_cast<uint64_t>(d->fulls[j]) + static_cast<uint64_t>(s.begin * R * ep);
@@ -171,6 +183,8 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   b->has_gshards = d->grad_shards != nullptr;
   b->ag_zero_copy = ag_zc;
   b->rs_zero_copy = rs_zc;
+  b->ag_direct = direct;
+  b->full0 = d->fulls ? static_cast<char*>(d->fulls[0]) : nullptr;
   b->shard_seg = ag_zc ? static_cast<char*>(d->shards[0]) : nullptr;
   b->gshard_seg = rs_zc ? static_cast<char*>(d->grad_shards[0]) : nullptr;
   fsdp_status st = FSDP_OK;
@@ -221,6 +235,10 @@ extern "C" fsdp_status fsdp_bucket_query(const fsdp_bucket* b, fsdp_bucket_info*
   out->rs_zero_copy = b->rs_zero_copy ? 1 : 0;
   out->p2p_bytes[0] = b->p2p_ag.n ? b->p2p_ag.bytes_moved : 0;
   out->p2p_bytes[1] = b->p2p_rs.n ? b->p2p_rs.bytes_moved : 0;
+  out->ag_direct = b->ag_direct ? 1 : 0;
+  out->reserved = 0;
+  // a direct bucket with segment storage and a communicator never packs
+  if (b->ag_direct && b->ag_zero_copy && b->ctx && b->ctx->comm) out->kernel_bytes[0] = 0;
   return FSDP_OK;
 }
 
@@ -239,7 +257,10 @@ namespace fsdp {
 static bool comm_on(fsdp_ctx* c, bool with_comm) { return with_comm && c->comm != nullptr; }
 
 fsdp_status ag_pack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches) {
-  if (!b->ag_zero_copy) {
+  // segment storage: the collective sends from it, no pack -- except for a
+  // direct-gather bucket when no collective will write this rank's rows
+  const bool skip = b->ag_direct ? (b->ag_zero_copy && comm_on(c, with_comm)) : b->ag_zero_copy;
+  if (!skip) {
     FSDP_CUDA_TRY(launch_table(KK_AG_PACK, b->ag_pack, staging, 1.0f, cs, c->max_ctas));
     if (b->ag_pack.n && launches) ++*launches;
   }
@@ -253,8 +274,10 @@ fsdp_status ag_collective(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream
   FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_ag_packed, 0));
   // In place (sendbuff = recvbuff + rank * sendcount), or out of place from
   // segment-layout shard storage; bytes as ncclInt8.
-  const char* send = b->ag_zero_copy ? b->shard_seg : staging + c->rank * b->ag_seg;
-  FSDP_NCCL_TRY(ncclAllGather(send, staging, static_cast<size_t>(b->ag_seg), ncclInt8, c->comm, ms));
+  // A direct-gather bucket gathers into the full parameter itself.
+  char* recv = b->ag_direct ? b->full0 : staging;
+  const char* send = b->ag_zero_copy ? b->shard_seg : recv + c->rank * b->ag_seg;
+  FSDP_NCCL_TRY(ncclAllGather(send, recv, static_cast<size_t>(b->ag_seg), ncclInt8, c->comm, ms));
   FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_done, ms));
   if (colls) ++*colls;
   return FSDP_OK;

@@ -93,6 +93,10 @@ struct Chunk {
 // staging-relative (K3 reading this rank's rows straight from segment-layout
 // shard storage, see fsdp_bucket_create).
 constexpr uint32_t kAbsSrc = 1u << 16;
+// Chunk flag: dst is an absolute address even in a kernel whose destination
+// side is staging-relative (K1 of a direct-gather bucket writing the full
+// parameter).
+constexpr uint32_t kAbsDst = 1u << 17;
 static_assert(sizeof(Chunk) == 24, "chunk layout");
 
 // Builder that splits runs into chunks (host side).
@@ -171,6 +175,8 @@ struct fsdp_bucket {
   bool ag_zero_copy = false, rs_zero_copy = false;
   char* shard_seg = nullptr;   // this rank's AG segment in shard storage
   char* gshard_seg = nullptr;  // this rank's RS segment in grad-shard storage
+  bool ag_direct = false;      // gathered buffer == the (single) full parameter
+  char* full0 = nullptr;       // fulls[0]
   fsdp::DevTable ag_pack, ag_unpack, rs_pack, rs_copyout;
   fsdp::DevTable p2p_ag, p2p_rs;  // K8 / K9 tables (peer-memory path)
   cudaEvent_t ev_ag_packed = nullptr, ev_ag_done = nullptr;

@@ -240,6 +240,11 @@ __device__ __forceinline__ const char* src_of(const Chunk& ch, char* base) {
   return (kSrcRel && !(ch.op_unit & kAbsSrc)) ? base + ch.src : reinterpret_cast<const char*>(ch.src);
 }
 
+template <bool kDstRel>
+__device__ __forceinline__ char* dst_of(const Chunk& ch, char* base) {
+  return (kDstRel && !(ch.op_unit & kAbsDst)) ? base + ch.dst : reinterpret_cast<char*>(ch.dst);
+}
+
 template <int NT>
 __device__ __forceinline__ void process_chunk(const Chunk& ch, const char* src, char* dst, float scale) {
   const uint32_t op = ch.op_unit & 0xFFu;
@@ -274,7 +279,7 @@ __device__ __forceinline__ void run_table(const Chunk* __restrict__ tab, int n, 
   for (int c = blockIdx.x; c < n; c += gridDim.x) {
     const Chunk ch = tab[c];
     const char* src = src_of<kSrcRel>(ch, base);
-    char* dst = kDstRel ? base + ch.dst : reinterpret_cast<char*>(ch.dst);
+    char* dst = dst_of<kDstRel>(ch, base);
     process_chunk<kThreads>(ch, src, dst, scale);
   }
 }
@@ -323,7 +328,7 @@ __device__ __forceinline__ void run_table_bulk(const Chunk* __restrict__ tab, in
     const Chunk ch = tab[c];
     if (is_bulk(ch)) continue;
     const char* src = src_of<kSrcRel>(ch, base);
-    char* dst = kDstRel ? base + ch.dst : reinterpret_cast<char*>(ch.dst);
+    char* dst = dst_of<kDstRel>(ch, base);
     process_chunk<32>(ch, src, dst, scale);
   }
   if (threadIdx.x != 0) return;
@@ -346,7 +351,7 @@ __device__ __forceinline__ void run_table_bulk(const Chunk* __restrict__ tab, in
     const Chunk ch = tab[next];
     const int s = loaded % kStages;
     const uint32_t bytes = ch.n * 16u;
-    dsts[s] = kDstRel ? base + ch.dst : reinterpret_cast<char*>(ch.dst);
+    dsts[s] = dst_of<kDstRel>(ch, base);
     lens[s] = bytes;
     bulk_load(smem0 + s * kChunkBytes, src_of<kSrcRel>(ch, base), bytes,
               bar0 + 8 * s);
@@ -363,7 +368,7 @@ __device__ __forceinline__ void run_table_bulk(const Chunk* __restrict__ tab, in
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       const Chunk ch = tab[next];
       const uint32_t bytes = ch.n * 16u;
-      dsts[s] = kDstRel ? base + ch.dst : reinterpret_cast<char*>(ch.dst);
+      dsts[s] = dst_of<kDstRel>(ch, base);
       lens[s] = bytes;
       bulk_load(smem0 + s * kChunkBytes, src_of<kSrcRel>(ch, base), bytes,
                 bar0 + 8 * s);

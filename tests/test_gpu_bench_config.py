@@ -66,4 +66,8 @@ def test_llama8b_bench_step_sampled_parity():
             n = st.shard_numel[j]
             sh = st.shard_buf[st.shard_offs[j]:st.shard_offs[j] + 2 * n]
             assert torch.equal(full[:2 * n], sh), specs[j].name
-            assert int(torch.count_nonzero(full[2 * n:])) == 0, specs[j].name
+            if not bk.query()["ag_direct"]:
+                # peer rows come from the never-written (zero) staging segments; a
+                # direct-gather bucket (emb / output / final norm) has no staging:
+                # without a collective its peer rows are simply not written
+                assert int(torch.count_nonzero(full[2 * n:])) == 0, specs[j].name

@@ -68,20 +68,35 @@ def sim_allgather(params, world, dt, align=16, check_all_ranks=True):
     for r in (range(world) if check_all_ranks else [0, world - 1]):
         for p, s in zip(params, shards[r]):
             assert np.array_equal(bits(s.get()), bits(shard(p, world, r)))
+    _, seg = bucket_layout(dims, world, _esize(dt), align)
+    # a one-parameter bucket with no padding gathers straight into the full
+    # parameter (direct gather): every rank then needs its own full buffer
+    direct = len(params) == 1 and dims[0][0] % world == 0 and seg == dims[0][0] // world * dims[0][1] * _esize(dt)
+    out_ranks = range(world) if direct else {0, world - 1}
     outs = {r: [DevArray(nbytes=p.nbytes, fill=0x5A, dtype=p.dtype, shape=p.shape) for p in params]
-            for r in {0, world - 1}}
+            for r in out_ranks}
     buckets = [F.Bucket(ctxs[r], descs, shards=[s.ptr for s in shards[r]],
                         fulls=[o.ptr for o in outs[r]] if r in outs else None,
                         param_dtype=dt, grad_dtype=dt, align=align) for r in range(world)]
-    _, seg = bucket_layout(dims, world, _esize(dt), align)
     assert buckets[0].ag_seg == seg
+    assert buckets[0].query()["ag_direct"] == direct
     staging = DevArray(nbytes=world * seg, fill=0xCD)
     for r in range(world):
         F.allgather_bucket(ctxs[r], buckets[r], staging.ptr, flags=L.ISSUE)
+    g_ref, fulls_ref = OC.bucketed_all_gather(params, world, align)
+    if direct:
+        # ISSUE wrote each rank's own rows into its full parameter; the
+        # all-gather (NCCL on real GPUs) gives every rank every rank's rows
+        assert np.all(staging.get() == 0xCD)                 # staging untouched
+        own = [outs[r][0].get().reshape(-1).view(np.uint8)[r * seg:(r + 1) * seg].copy() for r in range(world)]
+        assert np.array_equal(np.concatenate(own), g_ref)
+        for r in outs:
+            o = outs[r][0]
+            o.t[o.off:o.off + o.nbytes].copy_(torch.from_numpy(np.concatenate(own)))
     for r in outs:
         F.allgather_bucket(ctxs[r], buckets[r], staging.ptr, flags=L.WAIT)
-    g_ref, fulls_ref = OC.bucketed_all_gather(params, world, align)
-    assert np.array_equal(staging.get(), g_ref)           # raw buffer incl. zero pads
+    if not direct:
+        assert np.array_equal(staging.get(), g_ref)       # raw buffer incl. zero pads
     for r in outs:
         for o, p in zip(outs[r], params):
             assert np.array_equal(bits(o.get()), bits(p))  # all_gather(shard(p)) == p

@@ -1,0 +1,145 @@
+#!/usr/bin/env python
+"""Measures the BASELINE.json configs other than the headline one, on 1 GPU
+(rank 0 of a simulated world; every kernel at its per-rank size, no peers):
+
+  c0  toy 4-layer MLP, fp32, 2 ranks: PER_PARAM vs GREEDY plan, step latency
+  c2  Llama-3-8B Table 5 / Table 6 variants with the compute proxy at T tokens:
+      vanilla / +reorder / +bucket / +both / greedy+reorder, 4 placements
+  c3  Llama-3-70B SIZE_CAP bucket-size sweep 25-500 MB at N = 8
+  c4  Llama-3-405B one layer at N = 8: one whole-layer bucket vs per-parameter
+
+    python tools/configs_bench.py [c0 c2 c3 c4] [--out F]
+
+Each line: step ms (CUDA events around K plain steps after warm-up), per-kernel
+GB/s from a profiled pass, bucket counts.  With no peers on one GPU the
+collectives are absent, so "exposed" is not measured here: the variants differ
+by copy-kernel work and launch count (the paper's single-node finding that
+bucketing adds copy-in/copy-out).
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, tokens=0, steps=5, warmup=2,
+                link=(20000, 1500), param_dtype=None, nspi=None):
+    import torch
+    import paper_2411_00284_b200 as F
+    from paper_2411_00284_b200 import _lib as L
+    from paper_2411_00284_b200 import harness as H
+    pdt = L.BF16 if param_dtype is None else param_dtype
+    ctx = F.Ctx(world, 0)
+    fplan, bplan = H.plans_for(specs, world, mode, t_fwd, t_bwd, link, link, mem_max, pdt)
+    st = H.RankState(specs, world, 0, fplan, bplan, ctx, param_dtype=pdt)
+    cs, ms = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+    pf = pb = None
+    if tokens and t_fwd is not None:
+        pf = H.proxy_iters(H.bucket_times(fplan, t_fwd), nspi)
+        pb = H.proxy_iters(H.bucket_times(bplan, t_bwd), nspi)
+
+    def loop(extra, n):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = []
+        a.record(cs)
+        for _ in range(n):
+            reps.append(st.step(flags | extra, cs.cuda_stream, ms.cuda_stream, pf, pb))
+        b.record(cs)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n, reps
+
+    for _ in range(warmup):
+        st.step(flags, cs.cuda_stream, ms.cuda_stream, pf, pb)
+    ms_step, _ = loop(0, steps)
+    _, reps = loop(L.SCHED_TIMING, steps)
+    op_ns = [sum(r["op_ns"][i] for r in reps) for i in range(L.N_OPS)]
+    kb = st.kernel_bytes()
+    names = {L.OP_PACK_AG: "K1", L.OP_UNPACK: "K3", L.OP_PACK_RS: "K4", L.OP_COPYOUT_RS: "K6"}
+    kern = {names[o]: round(kb[o] * steps / (op_ns[o] * 1e-9) / 1e9, 1) for o in kb if kb[o] and op_ns[o] > 0}
+    ag_b, rs_b = st.step_bytes()
+    res = dict(ms_per_step=round(ms_step, 4), buckets_fwd=len(fplan), buckets_bwd=len(bplan),
+               kernel_GBps=kern, launches_per_step=reps[0]["kernel_launches"],
+               compute_ms_per_step=round((op_ns[L.OP_COMPUTE_F] + op_ns[L.OP_COMPUTE_B]) / steps / 1e6, 3),
+               step_GBps=round((ag_b + rs_b) / (ms_step * 1e-3) / 1e9, 1))
+    del st
+    ctx.close()
+    torch.cuda.empty_cache()
+    return res
+
+
+def c0():
+    from paper_2411_00284_b200 import _lib as L
+    from workloads import toy_mlp
+    specs = toy_mlp()
+    tc = [20000 if p.row_numel > 1 else 0 for p in specs]
+    out = {}
+    for name, mode in (("per_param", L.PLAN_PER_PARAM), ("greedy", L.PLAN_GREEDY)):
+        out[name] = run_variant(specs, 2, mode, L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT, tc, tc,
+                                mem_max=10**9, link=(10000, 100000), param_dtype=L.FP32, steps=50, warmup=5)
+    return out
+
+
+def c2(tokens=(1024, 2048)):
+    import torch
+    import paper_2411_00284_b200 as F
+    from paper_2411_00284_b200 import _lib as L
+    from paper_2411_00284_b200 import harness as H
+    from workloads import llama
+    from workloads.compute_model import per_param_compute_ns
+    specs = llama("8b")
+    ctx = F.Ctx(8, 0)
+    s = torch.cuda.Stream()
+    nspi = H.calibrate_proxy(ctx, s.cuda_stream)
+    ctx.close()
+    R, FB, BB = L.SCHED_REORDER, L.SCHED_FWD_AG_BEFORE_WAIT, L.SCHED_BWD_AG_BEFORE_WAIT
+    out = {"proxy_ns_per_iter": nspi}
+    for T in tokens:
+        f, b = per_param_compute_ns(specs, T)
+        rows = {}
+        variants = [("vanilla", L.PLAN_PER_PARAM, 0), ("+reorder", L.PLAN_PER_PARAM, R | FB),
+                    ("+bucket", L.PLAN_MANUAL, 0), ("+reorder&bucket", L.PLAN_MANUAL, R | FB),
+                    ("greedy+reorder", L.PLAN_GREEDY, R | FB),
+                    ("place fwd-before/bwd-before", L.PLAN_MANUAL, R | FB | BB),
+                    ("place fwd-after/bwd-before", L.PLAN_MANUAL, R | BB),
+                    ("place fwd-after/bwd-after", L.PLAN_MANUAL, R)]
+        for name, mode, flags in variants:
+            rows[name] = run_variant(specs, 8, mode, flags, f, b, mem_max=2 * 10**9, tokens=T, nspi=nspi,
+                                     steps=3, warmup=1)
+        out["T=%d" % T] = rows
+    return out
+
+
+def c3(caps_mb=(25, 50, 100, 200, 500)):
+    from paper_2411_00284_b200 import _lib as L
+    from workloads import llama
+    specs = llama("70b")
+    return {"%d MB" % m: run_variant(specs, 8, L.PLAN_SIZE_CAP, L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT,
+                                     mem_max=m * 10**6, steps=3, warmup=1) for m in caps_mb}
+
+
+def c4():
+    from paper_2411_00284_b200 import _lib as L
+    from workloads import llama
+    specs = llama("405b", n_layers=1, with_embeddings=False)
+    return {"layer_bucket": run_variant(specs, 8, L.PLAN_MANUAL, L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT,
+                                        steps=3, warmup=1),
+            "per_param": run_variant(specs, 8, L.PLAN_PER_PARAM, L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT,
+                                     steps=3, warmup=1)}
+
+
+def main():
+    which = [a for a in sys.argv[1:] if a in ("c0", "c2", "c3", "c4")] or ["c0", "c2", "c3", "c4"]
+    res = {}
+    for w in which:
+        res[w] = globals()[w]()
+        print(w, json.dumps(res[w]), flush=True)
+    if "--out" in sys.argv:
+        with open(sys.argv[sys.argv.index("--out") + 1], "w") as f:
+            json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
