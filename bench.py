@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--proxy-ctas", type=int, default=1)
     ap.add_argument("--proxy-smem", type=int, default=0)
+    ap.add_argument("--predict-tokens", type=int, default=1024,
+                    help="N=1: tokens/GPU of the compute proxy for the predicted N-rank exposure (0 = off)")
     ap.add_argument("--collective", default="nccl", choices=["nccl", "p2p"],
                     help="nccl: pack + NCCL + copy-out (the paper's bucketing); p2p: fused peer-memory "
                          "kernels K8/K9 (1 GPU: the 7 peers are simulated as separate buffers)")
@@ -289,6 +291,35 @@ def main():
     ranks = world_env if multi else 1
     value = ranks * (ag_b + rs_b) / (ms_step * 1e-3) / 1e9
 
+    # N = 1 has no peers, so exposure cannot be measured; report the library's
+    # two-stream PREDICTION for the N-rank job instead (fsdp_simulate_schedule):
+    # every compute-stream op at its duration measured here (copy kernels and
+    # the compute proxy at --predict-tokens), every collective at alpha + beta n
+    # of modelled NVLink 5 (720 GB/s bus, 20 us); no contention modelled.
+    predicted = None
+    if not multi and not p2p and args.predict_tokens:
+        ptf, ptb = per_param_compute_ns(specs, args.predict_tokens)
+        nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
+        ppf = H.proxy_iters(H.bucket_times(fplan, ptf), nspi)
+        ppb = H.proxy_iters(H.bucket_times(bplan, ptb), nspi)
+        rep = st.step(flags | L.SCHED_TIMING, cs, ms, ppf, ppb, args.proxy_ctas, args.proxy_smem, want_log=True)
+        beta = round((world - 1) / world / 720e9 * 1e15)
+        link = (20000, beta)
+        durs = []
+        for ph, op, b, _s, ns in rep["log"]:
+            bk = (st.fwd if ph == 0 else st.bwd)[b]
+            if op == L.OP_AG:
+                durs.append(F.comm_time_ns(world * bk.ag_seg, link))
+            elif op == L.OP_RS:
+                durs.append(F.comm_time_ns(world * bk.rs_seg, link))
+            else:
+                durs.append(max(ns, 0))
+        tot, exp, _, _ = F.simulate_schedule(rep["log"], durs)
+        predicted = {"world": world, "tokens_per_gpu": args.predict_tokens, "link_alpha_ns": link[0],
+                     "link_beta_fs_per_byte": link[1], "total_ms": round(tot / 1e6, 3),
+                     "exposed_comm_ms": round(exp / 1e6, 3),
+                     "model": "measured compute-stream ops + alpha/beta NVLink collectives, no contention"}
+
     # per-op device time from the timed steps' events -> dominant data kernel
     op_ns = [sum(r["op_ns"][i] for r in reports) for i in range(L.N_OPS)]
     op_cnt = [sum(r["op_count"][i] for r in reports) for i in range(L.N_OPS)]
@@ -375,6 +406,7 @@ def main():
                 "parallelism": "fsdp%d" % world if multi else "fsdp1 (simulated %d)" % world},
             "exposed_comm_ms": round(ms_step - ms_compute, 3), "compute_stream_ms": round(ms_compute, 3),
             "profiled_ms_per_step": round(ms_prof, 3),
+            "predicted": predicted,
             "collectives": coll_ms, "busbw_GBps": busbw, "kernels": per_kernel,
             "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),

@@ -389,6 +389,23 @@ typedef struct {
 
 fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, fsdp_step_report* out);
 
+/* ------------------------------------------- cost model and prediction
+ * fsdp_comm_time_ns: T(n) = alpha_ns + ceil(n * beta_fs_per_byte / 1e6), the
+ *   communication model of P:222 in integer units (what Algorithm 1 uses).
+ * fsdp_simulate_schedule: the two-stream timeline of an op sequence (e.g. the
+ *   log of fsdp_run_schedule, FSDP_SCHED_DRY_RUN) given per-entry durations
+ *   (ns): compute-stream ops run back to back in order; the comm stream is
+ *   FIFO and a collective starts when it is at its head and its pack
+ *   (PACK_AG / PACK_RS of the same phase and bucket) has finished; a WAIT
+ *   blocks the compute stream until its collective has finished (its own
+ *   duration is ignored).  Writes the finish time of the compute stream and the
+ *   exposed (blocked) time; start/end (nullable, n entries) get each entry's
+ *   interval.  Integer ns, deterministic; FSDP_ERR_INVALID_ARG if a collective
+ *   or WAIT precedes what it depends on.  Host-only. */
+fsdp_status fsdp_comm_time_ns(int64_t nbytes, const fsdp_link* link, int64_t* ns);
+fsdp_status fsdp_simulate_schedule(const fsdp_log_entry* seq, int32_t n, const int64_t* dur_ns, int64_t* total_ns,
+                                   int64_t* exposed_ns, int64_t* start_ns, int64_t* end_ns);
+
 /* ------------------------------------- peer-memory (fused) collectives
  * The same two collectives as one kernel each over peer memory (NVLink P2P on
  * a multi-GPU node, CUDA IPC mappings; on one GPU, buffers of simulated ranks):

@@ -38,6 +38,7 @@ EXPORTED = [
     "fsdp_run_schedule", "fsdp_proxy_launch", "fsdp_proxy_calibrate",
     "fsdp_p2p_allgather_bucket", "fsdp_p2p_reduce_scatter_bucket", "fsdp_p2p_signal", "fsdp_p2p_wait",
     "fsdp_ipc_alloc", "fsdp_ipc_open", "fsdp_ipc_close", "fsdp_ipc_free",
+    "fsdp_comm_time_ns", "fsdp_simulate_schedule",
 ]
 
 
@@ -142,6 +143,10 @@ _sigs = {
     "fsdp_ipc_open": (C.c_int, [_P, C.POINTER(_P)]),
     "fsdp_ipc_close": (C.c_int, [_P]),
     "fsdp_ipc_free": (C.c_int, [_P]),
+    "fsdp_comm_time_ns": (C.c_int, [C.c_int64, C.POINTER(Link), C.POINTER(C.c_int64)]),
+    "fsdp_simulate_schedule": (C.c_int, [C.POINTER(LogEntry), C.c_int32, C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_int64)]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(lib, _name)

@@ -241,3 +241,25 @@ def ipc_close(ptr):
 
 def ipc_free(ptr):
     check(L.lib.fsdp_ipc_free(ptr))
+
+
+# ------------------------------------------------------ cost model / prediction
+def comm_time_ns(nbytes, link):
+    """fsdp_comm_time_ns: alpha + ceil(n * beta_fs / 1e6) (P:222)."""
+    ns = C.c_int64()
+    check(L.lib.fsdp_comm_time_ns(int(nbytes), C.byref(L.Link(int(link[0]), int(link[1]))), C.byref(ns)))
+    return ns.value
+
+
+def simulate_schedule(seq, durations):
+    """fsdp_simulate_schedule.  seq: (phase, op, bucket, stream[, ...]) tuples,
+    durations: ns per entry.  Returns (total_ns, exposed_ns, starts, ends)."""
+    n = len(seq)
+    arr = (L.LogEntry * max(n, 1))()
+    for i, e in enumerate(seq):
+        arr[i].ns, arr[i].phase, arr[i].op, arr[i].bucket, arr[i].stream = -1, e[0], e[1], e[2], e[3]
+    d = (C.c_int64 * max(n, 1))(*[int(x) for x in durations])
+    tot, exp = C.c_int64(), C.c_int64()
+    st, en = (C.c_int64 * max(n, 1))(), (C.c_int64 * max(n, 1))()
+    check(L.lib.fsdp_simulate_schedule(arr, n, d, C.byref(tot), C.byref(exp), st, en))
+    return tot.value, exp.value, list(st[:n]), list(en[:n])

@@ -137,6 +137,42 @@ def test_dry_run_schedule_log_equals_oracle(kf, kb, reorder, fb, bb):
     assert all(e[4] == -1 for e in rep["log"])
 
 
+@given(n=st.integers(0, 10**12), alpha=st.integers(0, 10**7), beta=st.integers(0, 10**8))
+@settings(max_examples=300, deadline=None)
+def test_comm_time_matches_oracle(n, alpha, beta):
+    from oracle.cost import comm_time
+    assert F.comm_time_ns(n, (alpha, beta)) == comm_time(n, alpha, beta)
+
+
+@given(kf=st.integers(0, 12), kb=st.integers(0, 12), reorder=st.booleans(), fb=st.booleans(), bb=st.booleans(),
+       seed=st.integers(0, 2**31))
+@settings(max_examples=300, deadline=None)
+def test_simulator_matches_oracle(kf, kb, reorder, fb, bb, seed):
+    from oracle.sim import simulate
+    seq = OS.step_sequence(kf, kb, reorder, OS.BEFORE if fb else OS.AFTER, OS.BEFORE if bb else OS.AFTER)
+    rng = np.random.Generator(np.random.Philox(seed))
+    dur = [int(x) for x in rng.integers(0, 50000, size=len(seq))]
+    table = {e[:3]: d for e, d in zip(seq, dur)}
+    ref = simulate(seq, lambda ph, op, b: table[(ph, op, b)], lambda ph, op, b: table[(ph, op, b)])
+    tot, exp, starts, ends = F.simulate_schedule(seq, dur)
+    assert (tot, exp) == (ref["total"], ref["exposed"])
+    ev = {(e[0], e[1], e[2]): (e[4], e[5]) for e in ref["events"]}
+    for e, s, f in zip(seq, starts, ends):
+        if e[:3] in ev and e[1] not in (OS.WAIT_AG, OS.WAIT_RS):
+            assert (s, f) == ev[e[:3]]
+
+
+def test_simulator_spec_traces(golden):
+    for ex in golden("spec_examples.json")["sim_traces"]:
+        if ex["case"] == "compute_only":
+            continue
+        seq = OS.forward_sequence(len(ex["ag_ns"]), ex["reorder"], OS.BEFORE)
+        dur = [ex["compute_ns"][e[2]] if e[1] == OS.COMPUTE_F else ex["ag_ns"][e[2]] if e[1] == OS.AG else 0
+               for e in seq]
+        tot, exp, _, _ = F.simulate_schedule(seq, dur)
+        assert (tot, exp) == (ex["total_ns"], ex["exposed_ns"]), ex["cite"]
+
+
 def test_toy_plan_parity():
     ps = toy_mlp()
     params = [(p.dim0, p.row_numel, p.module_id) for p in ps]

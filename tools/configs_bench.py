@@ -25,7 +25,7 @@ sys.path.insert(0, ROOT)
 
 
 def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, tokens=0, steps=5, warmup=2,
-                link=(20000, 1500), param_dtype=None, nspi=None):
+                link=(20000, 1500), param_dtype=None, nspi=None, predict_link=None):
     import torch
     import paper_2411_00284_b200 as F
     from paper_2411_00284_b200 import _lib as L
@@ -55,6 +55,24 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
         st.step(flags, cs.cuda_stream, ms.cuda_stream, pf, pb)
     ms_step, _ = loop(0, steps)
     _, reps = loop(L.SCHED_TIMING, steps)
+    predicted = None
+    if predict_link is not None:
+        # the N-rank step predicted by the library's two-stream model: every
+        # compute-stream op at its MEASURED duration on this B200 (copies,
+        # proxy compute), every collective at alpha + beta n of its bucket
+        # (modelled NVLink; no SM / HBM contention)
+        rep = st.step(flags | L.SCHED_TIMING, cs.cuda_stream, ms.cuda_stream, pf, pb, want_log=True)
+        durs = []
+        for ph, op, b, stream, ns in rep["log"]:
+            bk = (st.fwd if ph == 0 else st.bwd)[b]
+            if op == L.OP_AG:
+                durs.append(F.comm_time_ns(world * bk.ag_seg, predict_link[0]))
+            elif op == L.OP_RS:
+                durs.append(F.comm_time_ns(world * bk.rs_seg, predict_link[1]))
+            else:
+                durs.append(max(ns, 0))
+        tot, exp, _, _ = F.simulate_schedule(rep["log"], durs)
+        predicted = dict(total_ms=round(tot / 1e6, 3), exposed_ms=round(exp / 1e6, 3))
     op_ns = [sum(r["op_ns"][i] for r in reps) for i in range(L.N_OPS)]
     kb = st.kernel_bytes()
     names = {L.OP_PACK_AG: "K1", L.OP_UNPACK: "K3", L.OP_PACK_RS: "K4", L.OP_COPYOUT_RS: "K6"}
@@ -64,6 +82,8 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
                kernel_GBps=kern, launches_per_step=reps[0]["kernel_launches"],
                compute_ms_per_step=round((op_ns[L.OP_COMPUTE_F] + op_ns[L.OP_COMPUTE_B]) / steps / 1e6, 3),
                step_GBps=round((ag_b + rs_b) / (ms_step * 1e-3) / 1e9, 1))
+    if predicted:
+        res["predicted_N%d" % world] = predicted
     del st
     ctx.close()
     torch.cuda.empty_cache()
@@ -105,9 +125,12 @@ def c2(tokens=(1024, 2048)):
                     ("place fwd-before/bwd-before", L.PLAN_MANUAL, R | FB | BB),
                     ("place fwd-after/bwd-before", L.PLAN_MANUAL, R | BB),
                     ("place fwd-after/bwd-after", L.PLAN_MANUAL, R)]
+        # modelled NVLink 5 at N = 8: 720 GB/s bus bandwidth (80 % of 900) and
+        # 20 us base latency -> beta = (7/8) / 720e9 s per full byte = 1215 fs/B
+        nvl = (20000, 1215)
         for name, mode, flags in variants:
             rows[name] = run_variant(specs, 8, mode, flags, f, b, mem_max=2 * 10**9, tokens=T, nspi=nspi,
-                                     steps=3, warmup=1)
+                                     steps=3, warmup=1, link=nvl, predict_link=(nvl, nvl))
         out["T=%d" % T] = rows
     return out
 
