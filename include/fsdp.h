@@ -366,7 +366,28 @@ typedef struct {
   int32_t proxy_smem_bytes;  /* K7 footprint: dynamic shared memory per CTA */
   int32_t reserved;
   const fsdp_p2p_schedule* p2p; /* FSDP_SCHED_P2P only, else NULL */
+  const struct fsdp_host_io* io; /* host-resident shards / gradient shards, else NULL */
 } fsdp_schedule;
+
+/* Host-resident parameters and gradients (offload): with `io` set, the step
+ * streams this rank's shards in from pinned host memory and its averaged
+ * gradient shards back out, overlapped bucket by bucket with the device path:
+ *   - forward bucket k: on the h2d stream, its segment (ag_seg bytes) is copied
+ *     from fwd_host_shards[k] into the bucket's segment-layout shard storage;
+ *     PACK_AG k (compute stream) waits for that copy;
+ *   - backward bucket j: after its gradient shards are final (COPYOUT_RS j, or
+ *     WAIT_RS j with a communicator), the d2h stream copies its gradient-shard
+ *     segment (rs_seg bytes) to bwd_host_grads[j]; the step's last
+ *     compute-stream work waits for every such copy.
+ * Forward buckets need FSDP_BUCKET_SEGMENT_SHARDS and backward buckets
+ * FSDP_BUCKET_SEGMENT_GRAD_SHARDS; host memory should be pinned; NULL entries
+ * are skipped; h2d / d2h NULL = library-owned streams. */
+typedef struct fsdp_host_io {
+  const void* const* fwd_host_shards; /* n_fwd */
+  void* const* bwd_host_grads;        /* n_bwd */
+  fsdp_stream_t h2d;
+  fsdp_stream_t d2h;
+} fsdp_host_io;
 
 typedef struct {
   int64_t ns;     /* TIMING: event-measured duration of this op, else -1 */

@@ -91,13 +91,19 @@ class P2PSchedule(C.Structure):
                 ("timeout_ns", C.c_int64), ("error_flag", C.c_void_p), ("reserved", C.c_int32 * 2)]
 
 
+class HostIO(C.Structure):
+    _fields_ = [("fwd_host_shards", C.POINTER(C.c_void_p)), ("bwd_host_grads", C.POINTER(C.c_void_p)),
+                ("h2d", C.c_void_p), ("d2h", C.c_void_p)]
+
+
 class Schedule(C.Structure):
     _fields_ = [("fwd", C.POINTER(C.c_void_p)), ("bwd", C.POINTER(C.c_void_p)),
                 ("proxy_iters_fwd", C.POINTER(C.c_int64)), ("proxy_iters_bwd", C.POINTER(C.c_int64)),
                 ("ag_staging", C.c_void_p * 2), ("rs_staging", C.c_void_p * 2),
                 ("compute", C.c_void_p), ("comm", C.c_void_p), ("n_fwd", C.c_int32),
                 ("n_bwd", C.c_int32), ("flags", C.c_uint32), ("proxy_ctas_per_sm", C.c_int32),
-                ("proxy_smem_bytes", C.c_int32), ("reserved", C.c_int32), ("p2p", C.POINTER(P2PSchedule))]
+                ("proxy_smem_bytes", C.c_int32), ("reserved", C.c_int32), ("p2p", C.POINTER(P2PSchedule)),
+                ("io", C.POINTER(HostIO))]
 
 
 class LogEntry(C.Structure):

@@ -219,7 +219,10 @@ fsdp_status fsdp_ctx_destroy(fsdp_ctx* c) {
   if (!c) return FSDP_OK;
   cudaSetDevice(c->device);
   for (cudaEvent_t ev : c->timing_events) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : c->io_events) cudaEventDestroy(ev);
   if (c->own_comm_stream) cudaStreamDestroy(c->own_comm_stream);
+  if (c->own_h2d) cudaStreamDestroy(c->own_h2d);
+  if (c->own_d2h) cudaStreamDestroy(c->own_d2h);
   if (c->sink) cudaFree(c->sink);
   fsdp_status st = FSDP_OK;
   if (c->owns_comm && c->comm) {

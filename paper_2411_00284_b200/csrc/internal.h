@@ -161,6 +161,8 @@ struct fsdp_ctx {
   int max_ctas = 148 * 8;
   float* sink = nullptr;
   std::vector<cudaEvent_t> timing_events;  // pool for FSDP_SCHED_TIMING
+  std::vector<cudaEvent_t> io_events;      // pool for host I/O ordering (fsdp_host_io)
+  cudaStream_t own_h2d = nullptr, own_d2h = nullptr;
 };
 
 struct fsdp_bucket {

@@ -186,6 +186,14 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   if (s->proxy_ctas_per_sm < 0 || s->proxy_smem_bytes < 0)
     return fail(FSDP_ERR_INVALID_ARG, "bad proxy footprint");
   (void)max_seg;  // slot sizes are the caller's contract (>= world * largest segment)
+  if (s->io) {
+    for (int32_t k = 0; k < s->n_fwd; ++k)
+      if (s->io->fwd_host_shards && s->io->fwd_host_shards[k] && !s->fwd[k]->ag_zero_copy)
+        return fail(FSDP_ERR_INVALID_ARG, "host I/O: forward buckets need FSDP_BUCKET_SEGMENT_SHARDS");
+    for (int32_t j = 0; j < s->n_bwd; ++j)
+      if (s->io->bwd_host_grads && s->io->bwd_host_grads[j] && !s->bwd[j]->rs_zero_copy)
+        return fail(FSDP_ERR_INVALID_ARG, "host I/O: backward buckets need FSDP_BUCKET_SEGMENT_GRAD_SHARDS");
+  }
 
   FSDP_CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t cs = static_cast<cudaStream_t>(s->compute);
@@ -215,6 +223,55 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     for (int32_t q = 0; q < ctx->world; ++q) t.p[q] = static_cast<const char*>(rows[row * ctx->world + q]);
     return t;
   };
+  // ---- host I/O (fsdp_host_io): per-bucket H2D of shards, D2H of gradient shards
+  const fsdp_host_io* io = s->io;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t* iev = nullptr;  // [0] step start, [1 + k] forward bucket k loaded, [1 + n_fwd + j] grads of j final, [last] d2h done
+  if (io) {
+    h2d = io->h2d ? static_cast<cudaStream_t>(io->h2d) : ctx->own_h2d;
+    d2h = io->d2h ? static_cast<cudaStream_t>(io->d2h) : ctx->own_d2h;
+    if (!h2d) {
+      FSDP_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->own_h2d, cudaStreamNonBlocking));
+      h2d = ctx->own_h2d;
+    }
+    if (!d2h) {
+      FSDP_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->own_d2h, cudaStreamNonBlocking));
+      d2h = ctx->own_d2h;
+    }
+    const size_t need = 2 + static_cast<size_t>(s->n_fwd + s->n_bwd);
+    while (ctx->io_events.size() < need) {
+      cudaEvent_t e;
+      FSDP_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ctx->io_events.push_back(e);
+    }
+    iev = ctx->io_events.data();
+    // the previous step's readers of the shard storage are ordered before this point
+    FSDP_CUDA_TRY(cudaEventRecord(iev[0], cs));
+    FSDP_CUDA_TRY(cudaStreamWaitEvent(h2d, iev[0], 0));
+    for (int32_t k = 0; k < s->n_fwd; ++k) {
+      if (!io->fwd_host_shards || !io->fwd_host_shards[k]) continue;
+      FSDP_CUDA_TRY(cudaMemcpyAsync(s->fwd[k]->shard_seg, io->fwd_host_shards[k], static_cast<size_t>(s->fwd[k]->ag_seg),
+                                    cudaMemcpyHostToDevice, h2d));
+      FSDP_CUDA_TRY(cudaEventRecord(iev[1 + k], h2d));
+    }
+  }
+  auto io_before = [&](const Op& o) -> fsdp_status {
+    if (io && o.op == FSDP_OP_PACK_AG && o.phase == 0 && io->fwd_host_shards && io->fwd_host_shards[o.bucket])
+      FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, iev[1 + o.bucket], 0));
+    return FSDP_OK;
+  };
+  auto io_after = [&](const Op& o) -> fsdp_status {
+    if (io && o.op == FSDP_OP_COPYOUT_RS && io->bwd_host_grads && io->bwd_host_grads[o.bucket]) {
+      fsdp_bucket* bb = s->bwd[o.bucket];
+      cudaEvent_t e = iev[1 + s->n_fwd + o.bucket];
+      FSDP_CUDA_TRY(cudaEventRecord(e, cs));
+      FSDP_CUDA_TRY(cudaStreamWaitEvent(d2h, e, 0));
+      FSDP_CUDA_TRY(cudaMemcpyAsync(io->bwd_host_grads[o.bucket], bb->gshard_seg, static_cast<size_t>(bb->rs_seg),
+                                    cudaMemcpyDeviceToHost, d2h));
+    }
+    return FSDP_OK;
+  };
+
   if (pp && with_comm) {
     for (int32_t q = 0; q < ctx->world; ++q) {
       ready_slots.p[q] = static_cast<const char*>(pp->ready_slots[q]);
@@ -226,6 +283,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   for (size_t i = 0; i < seq.size(); ++i) {
     const Op& o = seq[i];
     fsdp_bucket* b = (o.phase == 0 ? s->fwd : s->bwd)[o.bucket];
+    FSDP_TRY(io_before(o));
     if (pp) {
       // the peer-memory path: same sequence, different work per op
       const bool comm_op = is_comm(o.op);
@@ -290,6 +348,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
           break;
       }
       if (timing && !skipped) FSDP_CUDA_TRY(cudaEventRecord(ev[3 + 2 * i], on));
+      FSDP_TRY(io_after(o));
       continue;
     }
     char* ag_st = static_cast<char*>(s->ag_staging[o.bucket & 1]);
@@ -324,6 +383,13 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
       case FSDP_OP_COPYOUT_RS: FSDP_TRY(rs_copyout(ctx, b, rs_st, cs, with_comm, &launches)); break;
     }
     if (timing && !skipped) FSDP_CUDA_TRY(cudaEventRecord(ev[3 + 2 * i], on));
+    FSDP_TRY(io_after(o));
+  }
+  if (io && s->n_bwd > 0) {
+    // the step ends when its gradient shards are on the host
+    cudaEvent_t e = iev[1 + s->n_fwd + s->n_bwd];
+    FSDP_CUDA_TRY(cudaEventRecord(e, d2h));
+    FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, e, 0));
   }
   if (pp && with_comm) {
     // step end: peers are done with every gradient slot and every shard of mine

@@ -145,7 +145,7 @@ def reduce_scatter_bucket(ctx, bucket, staging_ptr, compute=0, comm=0, flags=L.I
 
 def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0, comm=0, flags=0,
                  proxy_iters_fwd=None, proxy_iters_bwd=None, proxy_ctas_per_sm=1, proxy_smem_bytes=0,
-                 n_fwd=None, n_bwd=None, want_log=True, p2p=None):
+                 n_fwd=None, n_bwd=None, want_log=True, p2p=None, io=None):
     """fsdp_run_schedule.  fwd / bwd: Bucket lists in execution order (or
     counts via n_fwd / n_bwd with FSDP_SCHED_DRY_RUN and ctx=None).  Returns the
     step report as a dict (log as a list of (phase, op, bucket, stream, ns)).
@@ -178,6 +178,15 @@ def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0,
         ps.error_flag = p2p.get("error_flag") or None
         keep.append(ps)
         s.p2p = C.pointer(ps)
+    if io is not None:
+        # io: dict(fwd_host_shards=[ptr or 0 per forward bucket], bwd_host_grads=[...], h2d=stream, d2h=stream)
+        hio = L.HostIO()
+        a = L.ptr_array(io.get("fwd_host_shards"))
+        g = L.ptr_array(io.get("bwd_host_grads"))
+        keep += [a, g, hio]
+        hio.fwd_host_shards, hio.bwd_host_grads = a, g
+        hio.h2d, hio.d2h = io.get("h2d") or None, io.get("d2h") or None
+        s.io = C.pointer(hio)
     cap = 5 * nf + 9 * nb + 4
     log = (L.LogEntry * cap)() if want_log else None
     rep = L.StepReport()

@@ -184,8 +184,17 @@ class RankState:
         k9 = sum(b.query()["p2p_bytes"][1] for b in self.bwd)
         return k8, k9
 
+    def host_io(self, host_shards, host_gshards, h2d=0, d2h=0):
+        """fsdp_host_io for pinned host mirrors laid out like shard_buf /
+        gshard_buf: forward bucket k streams in from host_shards at its segment
+        offset, backward bucket j streams its gradient shards out to host_gshards."""
+        hs, hg = host_shards.data_ptr(), host_gshards.data_ptr()
+        fwd = [hs + self.shard_offs[b.members[0]] if b.query()["ag_zero_copy"] else 0 for b in self.fwd]
+        bwd = [hg + self.gs_offs[b.members[0]] if b.query()["rs_zero_copy"] else 0 for b in self.bwd]
+        return dict(fwd_host_shards=fwd, bwd_host_grads=bwd, h2d=h2d, d2h=d2h)
+
     def step(self, flags, compute, comm, proxy_fwd=None, proxy_bwd=None, ctas_per_sm=1, smem=0,
-             want_log=False):
+             want_log=False, io=None):
         p2p = None
         if flags & L.SCHED_P2P:
             p2p = self.p2p_schedule()
@@ -196,7 +205,7 @@ class RankState:
                               rs_staging=(self.rs_st[0].data_ptr(), self.rs_st[1].data_ptr()),
                               compute=compute, comm=comm, flags=flags, proxy_iters_fwd=proxy_fwd,
                               proxy_iters_bwd=proxy_bwd, proxy_ctas_per_sm=ctas_per_sm,
-                              proxy_smem_bytes=smem, want_log=want_log, p2p=p2p)
+                              proxy_smem_bytes=smem, want_log=want_log, p2p=p2p, io=io)
 
     # -------------------------------------------------------------- accounting
     def step_bytes(self):

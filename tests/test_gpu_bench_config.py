@@ -25,6 +25,40 @@ from workloads import llama
 pytestmark = pytest.mark.gpu
 
 
+def test_host_io_step():
+    """fsdp_host_io: the step loads every forward bucket's shards from pinned
+    host memory before its all-gather and stores every backward bucket's
+    gradient shards to host memory before the step ends."""
+    from workloads import toy_mlp
+    world = 2
+    specs = llama("8b", n_layers=2)
+    ctx = F.Ctx(world, 0)
+    fplan, bplan = H.plans_for(specs, world, L.PLAN_MANUAL)
+    st = H.RankState(specs, world, 0, fplan, bplan, ctx, seed=5)
+    h_sh = torch.empty(st.shard_buf.numel(), dtype=torch.uint8, pin_memory=True)
+    g = torch.Generator().manual_seed(3)
+    h_sh.copy_(torch.randint(0, 256, (h_sh.numel(),), dtype=torch.uint8, generator=g))
+    # the gap bytes of the segment storage are zero by contract
+    dev_before = st.shard_buf.cpu()
+    gaps = torch.ones(st.shard_buf.numel(), dtype=torch.bool)
+    for j, o in enumerate(st.shard_offs):
+        gaps[o:o + st.shard_numel[j] * 2] = False
+    h_sh[gaps] = dev_before[gaps]
+    h_gs = torch.full((st.gshard_buf.numel(),), 0xAB, dtype=torch.uint8).pin_memory()
+    cs, ms = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+    io = st.host_io(h_sh, h_gs)
+    assert all(io["fwd_host_shards"]) and all(io["bwd_host_grads"])
+    st.step(L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT, cs.cuda_stream, ms.cuda_stream, io=io)
+    cs.synchronize()   # the step's compute stream waits for the D2H copies
+    assert torch.equal(st.shard_buf.cpu(), h_sh)
+    seg_bytes = torch.zeros(st.gshard_buf.numel(), dtype=torch.bool)
+    for b in st.bwd:
+        base = st.gs_offs[b.members[0]]
+        seg_bytes[base:base + b.rs_seg] = True
+    assert torch.equal(h_gs[seg_bytes], st.gshard_buf.cpu()[seg_bytes])
+    del toy_mlp
+
+
 def test_llama8b_bench_step_sampled_parity():
     world = 8
     specs = llama("8b")
