@@ -186,6 +186,7 @@ fsdp_status fsdp_ctx_create(fsdp_ctx** out, int32_t world, int32_t rank, int32_t
   FSDP_CUDA_TRY(cudaGetDeviceCount(&ndev));
   if (cuda_device < 0 || cuda_device >= ndev) return fail(FSDP_ERR_INVALID_ARG, "bad cuda_device");
   FSDP_CUDA_TRY(cudaSetDevice(cuda_device));
+  FSDP_CUDA_TRY(preload_kernels());
   fsdp_ctx* c = new fsdp_ctx();
   c->world = world;
   c->rank = rank;

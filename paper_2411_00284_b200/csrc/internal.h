@@ -133,6 +133,7 @@ cudaError_t launch_p2p_signal(const PeerTable& slots, int world, uint64_t value,
 cudaError_t launch_p2p_wait(const void* flags, int world, uint64_t value, int64_t timeout_ns, int* err,
                             cudaStream_t s);
 int device_sm_count(int device);
+cudaError_t preload_kernels();  // defeat lazy loading (see kernels.cu)
 
 // Per-bucket steps shared by the public calls and the schedule executor
 // (bucket.cc).  `launches` / `colls` (nullable) count enqueued kernels and

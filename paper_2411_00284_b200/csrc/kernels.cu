@@ -731,6 +731,27 @@ cudaError_t launch_proxy(int64_t iters, int grid, int smem, float* sink, cudaStr
   return cudaGetLastError();
 }
 
+// CUDA loads kernels lazily by default (CUDA_MODULE_LOADING=LAZY): the first
+// launch of a kernel loads it, and loading waits for the device, so a first
+// launch enqueued while an epoch wait kernel spins (peer-memory path) would
+// only start once the wait times out.  Load every kernel up front.
+cudaError_t preload_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {
+      reinterpret_cast<const void*>(fsdp_shard_kernel), reinterpret_cast<const void*>(fsdp_ag_pack_kernel),
+      reinterpret_cast<const void*>(fsdp_ag_unpack_kernel), reinterpret_cast<const void*>(fsdp_rs_pack_kernel),
+      reinterpret_cast<const void*>(fsdp_rs_copyout_kernel), reinterpret_cast<const void*>(fsdp_shard_bulk_kernel),
+      reinterpret_cast<const void*>(fsdp_ag_pack_bulk_kernel), reinterpret_cast<const void*>(fsdp_ag_unpack_bulk_kernel),
+      reinterpret_cast<const void*>(fsdp_rs_copyout_bulk_kernel), reinterpret_cast<const void*>(fsdp_p2p_allgather_kernel),
+      reinterpret_cast<const void*>(fsdp_p2p_reduce_scatter_kernel), reinterpret_cast<const void*>(fsdp_p2p_signal_kernel),
+      reinterpret_cast<const void*>(fsdp_p2p_wait_kernel), reinterpret_cast<const void*>(fsdp_compute_proxy_kernel)};
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 int device_sm_count(int device) {
   int n = 0;
   if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;

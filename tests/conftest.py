@@ -3,6 +3,11 @@ import sys
 
 import pytest
 
+# The all-ranks-concurrently peer-memory test runs 2 x world streams whose
+# spin-waits depend on each other: give every stream its own hardware queue
+# (must be set before CUDA initialises).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -217,6 +217,84 @@ def test_p2p_schedule_step_bit_exact(flags):
                 assert np.array_equal(g.get().view(np.uint32), shards_ref[rank][j].reshape(-1).view(np.uint32))
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_p2p_schedule_all_ranks_concurrently(world):
+    """Every rank of a `world`-way job runs its whole FSDP_SCHED_P2P step at the
+    same time on one GPU (own streams per rank), reading the other ranks' real
+    buffers and synchronising through the real epoch flags (no pre-set slots):
+    two consecutive steps, every rank's full parameters and gradient shards
+    bit-exact against the oracle, no wait times out."""
+    specs = toy_mlp()
+    descs = [(p.dim0, p.row_numel, p.module_id) for p in specs]
+    params = [param_tensor(p, "bf16", 900 + i) for i, p in enumerate(specs)]
+    grads = [[grad_tensor(p, "bf16", 901, q) for p in specs] for q in range(world)]
+    fplan, _ = F.plan_buckets(descs, world, [0] * 8, (0, 0), (0, 0), 0, L.PLAN_MANUAL, L.PHASE_FWD)
+    bplan, _ = F.plan_buckets(descs, world, [0] * 8, (0, 0), (0, 0), 0, L.PLAN_MANUAL, L.PHASE_BWD)
+    keep = []
+    stor = {}      # (bucket members, rank) -> (DevArray, offsets)
+    for members in fplan:
+        m = tuple(sorted(members))
+        for q in range(world):
+            stor[(m, q)] = _storage([params[j] for j in m], world, q, 2)
+    gregion = {}   # (bucket members, rank) -> (DevArray, offsets)  own region per backward bucket
+    for members in bplan:
+        m = tuple(sorted(members))
+        for q in range(world):
+            gregion[(m, q)] = _grad_region([grads[q][j] for j in m])
+    ready = [torch.zeros(world, dtype=torch.int64, device="cuda") for _ in range(world)]
+    done = [torch.zeros(world, dtype=torch.int64, device="cuda") for _ in range(world)]
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ranks = []
+    for r in range(world):
+        ctx = F.Ctx(world, r)
+        outs, gss = {}, {}
+
+        def bucket(members, phase, i):
+            m = tuple(sorted(members))
+            sbuf, offs = stor[(m, r)]
+            out = [DevArray(nbytes=params[j].nbytes, fill=0x5A, dtype=np.uint16) for j in m]
+            outs[(phase, i)] = (m, out)
+            kw = {}
+            if phase == 1:
+                gbuf, goffs = gregion[(m, r)]
+                gs = [DevArray(nbytes=-(-params[j].shape[0] // world) * params[j].shape[1] * 4, fill=0x77,
+                               dtype=np.float32) for j in m]
+                gss[i] = (m, gs)
+                kw = dict(full_grads=[gbuf.ptr + o for o in goffs], grad_shards=[g.ptr for g in gs])
+            return F.Bucket(ctx, [descs[j] for j in m], shards=[sbuf.ptr + o for o in offs],
+                            fulls=[o.ptr for o in out], flags=L.BUCKET_SEGMENT_SHARDS, **kw)
+        fwd = [bucket(m, 0, i) for i, m in enumerate(fplan)]
+        bwd = [bucket(m, 1, i) for i, m in enumerate(bplan)]
+        p2p = dict(ag_peers=[[stor[(tuple(sorted(m)), q)][0].ptr for q in range(world)] for m in list(fplan) + list(bplan)],
+                   rs_peers=[[gregion[(tuple(sorted(m)), q)][0].ptr for q in range(world)] for m in bplan],
+                   ready_slots=[ready[q].data_ptr() + 8 * r for q in range(world)],
+                   done_slots=[done[q].data_ptr() + 8 * r for q in range(world)],
+                   ready_flags=ready[r].data_ptr(), done_flags=done[r].data_ptr(), timeout_ns=20 * 10**9,
+                   error_flag=err.data_ptr())
+        ranks.append(dict(ctx=ctx, fwd=fwd, bwd=bwd, p2p=p2p, outs=outs, gss=gss,
+                          cs=torch.cuda.Stream(), ms=torch.cuda.Stream(priority=-1)))
+    torch.cuda.synchronize()
+    epoch = 0
+    for _ in range(2):                       # two steps: epochs keep increasing
+        for rk in ranks:                     # enqueue every rank; they run concurrently
+            p = dict(rk["p2p"], epoch_base=epoch)
+            F.run_schedule(rk["ctx"], rk["fwd"], rk["bwd"], compute=rk["cs"].cuda_stream, comm=rk["ms"].cuda_stream,
+                           flags=L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT | L.SCHED_P2P, p2p=p, want_log=False)
+        epoch += len(bplan) + 2
+        torch.cuda.synchronize()
+        assert int(err.item()) == 0, "an epoch wait timed out"
+    _, _, shards_ref = OC.bucketed_reduce_scatter(grads, world, 16)
+    for r, rk in enumerate(ranks):
+        for (phase, i), (m, out) in rk["outs"].items():
+            for j, o in zip(m, out):
+                assert np.array_equal(o.get().reshape(-1), params[j].reshape(-1)), (r, phase, i, j)
+        for i, (m, gs) in rk["gss"].items():
+            for j, g in zip(m, gs):
+                assert np.array_equal(g.get().view(np.uint32), shards_ref[r][j].reshape(-1).view(np.uint32)), (r, j)
+    assert all(int(f[q].item()) == 2 * (len(bplan) + 2) for f in ready for q in range(world))
+    del keep
+
+
 def test_p2p_rejects_plain_storage():
     ctx = F.Ctx(2, 0)
     p = DevArray(np.zeros((64, 4), np.uint16))
