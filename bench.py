@@ -56,6 +56,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--proxy-ctas", type=int, default=1)
     ap.add_argument("--proxy-smem", type=int, default=0)
+    ap.add_argument("--pg", default="auto", choices=["auto", "nccl", "gloo"],
+                    help="torch.distributed backend for host plumbing (auto: nccl, gloo for p2p)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="TEST ONLY: put every rank on cuda:0 (exercises the multi-process p2p path on one GPU; "
+                         "timings are meaningless)")
     ap.add_argument("--predict-tokens", type=int, default=1024,
                     help="N=1: tokens/GPU of the compute proxy for the predicted N-rank exposure (0 = off)")
     ap.add_argument("--collective", default="nccl", choices=["nccl", "p2p"],
@@ -205,15 +210,25 @@ def main():
     from workloads.compute_model import per_param_compute_ns
 
     assert torch.cuda.is_available(), "bench.py needs a B200"
+    if args.same_device:
+        local = 0    # test only: every rank on cuda:0 (exercises the multi-process path on one GPU)
     torch.cuda.set_device(local)
     multi = args.gpus > 1
+    p2p = args.collective == "p2p"
+    pg = args.pg if args.pg != "auto" else ("gloo" if (p2p or args.same_device) else "nccl")
     if multi:
         assert world_env == args.gpus, "launch with torchrun --nproc-per-node %d" % args.gpus
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        uid = [F.nccl_get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
+        if pg == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
         world = args.gpus
-        ctx = F.Ctx(world, rank, local, nccl_uid=uid[0])
+        if p2p:
+            ctx = F.Ctx(world, rank, local)   # peer-memory collectives need no NCCL communicator
+        else:
+            uid = [F.nccl_get_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            ctx = F.Ctx(world, rank, local, nccl_uid=uid[0])
     else:
         world = args.sim_world
         ctx = F.Ctx(world, 0, local)   # layout-only: rank 0 of a simulated `world`-way job
@@ -225,7 +240,8 @@ def main():
             "size_cap": L.PLAN_SIZE_CAP}[args.plan]
     link = (args.alpha_ns, args.beta_fs)
     fplan, bplan = H.plans_for(specs, world, mode, t_fwd, t_bwd, link, link, int(args.mem_limit))
-    st = H.RankState(specs, world, rank if multi else 0, fplan, bplan, ctx, seed=1234 + rank)
+    st = H.RankState(specs, world, rank if multi else 0, fplan, bplan, ctx, seed=1234 + rank,
+                     ipc=multi and p2p)
     compute = torch.cuda.Stream()
     comm = torch.cuda.Stream(priority=-1)
     cs, ms = compute.cuda_stream, comm.cuda_stream
@@ -235,11 +251,15 @@ def main():
         nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
         pf = H.proxy_iters(H.bucket_times(fplan, t_fwd), nspi)
         pb = H.proxy_iters(H.bucket_times(bplan, t_bwd), nspi)
-    p2p = args.collective == "p2p"
     if p2p:
         if multi:
-            raise SystemExit("--collective p2p is wired for the 1-GPU simulated world only this round")
-        st.setup_p2p_simulated(seed=99)
+            def exchange(obj):
+                out = [None] * world
+                dist.all_gather_object(out, obj)
+                return out
+            st.setup_p2p_ipc(exchange)
+        else:
+            st.setup_p2p_simulated(seed=99)
     flags = 0 if args.no_reorder else L.SCHED_REORDER
     if p2p:
         flags |= L.SCHED_P2P
@@ -259,7 +279,7 @@ def main():
     def max_over_ranks(x):
         if not multi:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if pg == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -402,9 +422,11 @@ def main():
                 ((", 1 GPU = rank 0 of a simulated %d-way job (pack/unpack only, no peers)" % world if not p2p else
                   ", 1 GPU = rank 0 of a simulated %d-way job (peers' buffers simulated in local HBM)" % world)
                  if not multi
-                 else ", %d ranks over NCCL" % world),
+                 else ", %d ranks over %s%s" % (world, "peer memory (CUDA IPC)" if p2p else "NCCL",
+                                               " [TEST: all ranks on one GPU]" if args.same_device else "")),
                 "model": "llama3-8b shapes (Table 2; vocab 128256, 8 KV heads)", "layout_world": world,
                 "collective": ("NCCL all-gather / reduce-scatter with pack + copy-out kernels" if not p2p else
+                               "fused peer-memory kernels K8/K9 over CUDA IPC mappings of the peers" if multi else
                                "fused peer-memory kernels K8/K9 (peers simulated as separate HBM buffers)"),
                 "buckets_fwd": len(fplan), "buckets_bwd": len(bplan), "param_dtype": "bf16",
                 "reduce_dtype": "fp32", "proxy_tokens_per_gpu": tokens,
@@ -421,6 +443,7 @@ def main():
                          "traffic_launch_algorithmic_bytes": ncu_traffic(names[dom] + "_algorithmic"),
                          "algorithmic_bytes_per_launch": kbytes[dom] // max(1, klaunch[dom])},
             "zero_copy": st.zero_copy(),
+            "p2p_wait_timeouts": int(st.p2p_err.item()) if p2p else None,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
         }

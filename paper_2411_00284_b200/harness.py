@@ -34,7 +34,25 @@ def _carve(sizes, align=ALIGN):
 
 class RankState:
     def __init__(self, specs, world, rank, fwd_plan, bwd_plan, ctx, param_dtype=L.BF16,
-                 device="cuda", seed=0, fill=True, segment_storage=True):
+                 device="cuda", seed=0, fill=True, segment_storage=True, ipc=False):
+        # ipc=True: the buffers peers read in the peer-memory path (shard
+        # storage, gradient slots) come from fsdp_ipc_alloc so that other
+        # processes can map them (setup_p2p_ipc)
+        self.ipc_handles = {}
+        self._ipc_ptrs = []
+
+        def alloc(name, nbytes, zero=False):
+            if not ipc:
+                return (torch.zeros if zero else torch.empty)(nbytes, dtype=torch.uint8, device=device)
+            from .dlpack_view import uint8_view
+            ptr, handle = F.ipc_alloc(nbytes)
+            self._ipc_ptrs.append(ptr)
+            self.ipc_handles[name] = handle
+            t = uint8_view(ptr, nbytes, torch.device(device).index or torch.cuda.current_device())
+            if zero:
+                t.zero_()
+            return t
+        self._alloc = alloc
         self.specs, self.world, self.rank, self.ctx = specs, world, rank, ctx
         self.descs = [(p.dim0, p.row_numel, p.module_id) for p in specs]
         self.param_dtype = param_dtype
@@ -54,14 +72,14 @@ class RankState:
         else:
             self.shard_offs, tot = _carve([n * ep for n in self.shard_numel])
             self.gs_offs, tot_g = _carve([n * 4 for n in self.shard_numel])
-        self.shard_buf = torch.zeros(tot, dtype=torch.uint8, device=device)
+        self.shard_buf = alloc("shards", tot, zero=True)
         self.gshard_buf = torch.zeros(tot_g, dtype=torch.uint8, device=device)
         # slots sized to the largest bucket of either phase
         buckets = list(fwd_plan) + list(bwd_plan)
         self.slot_bytes = max(_carve([self.full_numel[j] * ep for j in sorted(b)])[1] for b in buckets)
         self.gslot_bytes = max(_carve([self.full_numel[j] * 2 for j in sorted(b)])[1] for b in buckets)
         self.full_slots = [torch.empty(self.slot_bytes, dtype=torch.uint8, device=device) for _ in range(2)]
-        self.grad_slots = [torch.empty(self.gslot_bytes, dtype=torch.uint8, device=device) for _ in range(2)]
+        self.grad_slots = [alloc("grads%d" % i, self.gslot_bytes) for i in range(2)]
         if fill:
             g = torch.Generator(device=device).manual_seed(seed)
             # N(0, 0.02) bf16 parameters and N(0, 1e-3) bf16 gradients (DESIGN.md input recipe)
@@ -164,13 +182,53 @@ class RankState:
                             for q in range(W)]
         self.done_slots = [self.done.data_ptr() + 8 * r if q == r else self.sink.data_ptr() + 8 * (W + q)
                            for q in range(W)]
-        self._p2p_tables()
+        self._p2p_tables([t.data_ptr() for t in self.peer_shards],
+                         [[t.data_ptr() for t in gs] for gs in self.peer_grads])
 
-    def _p2p_tables(self):
+    def setup_p2p_ipc(self, exchange):
+        """Peer-memory state across processes: ``exchange(obj)`` returns the
+        list of every rank's obj (e.g. torch.distributed.all_gather_object).
+        Requires RankState(..., ipc=True).  Shards, gradient slots and the flag
+        arrays of every peer are mapped with fsdp_ipc_open."""
+        W, r = self.world, self.rank
+        flags_ptr, flags_h = F.ipc_alloc(16 * W)
+        self._ipc_ptrs.append(flags_ptr)
+        from .dlpack_view import uint8_view
+        fl = uint8_view(flags_ptr, 16 * W, torch.cuda.current_device())
+        fl.zero_()
+        torch.cuda.synchronize()
+        self.ready = fl[:8 * W].view(torch.int64)
+        self.done = fl[8 * W:].view(torch.int64)
+        self.p2p_err = torch.zeros(1, dtype=torch.int32, device=self.shard_buf.device)
+        mine = dict(rank=r, shards=self.ipc_handles["shards"], g0=self.ipc_handles["grads0"],
+                    g1=self.ipc_handles["grads1"], flags=flags_h)
+        allh = sorted(exchange(mine), key=lambda d: d["rank"])
+        self._opened = []
+        shard_base, grad_base, flag_base = [], [], []
+        for q, h in enumerate(allh):
+            if q == r:
+                shard_base.append(self.shard_buf.data_ptr())
+                grad_base.append([t.data_ptr() for t in self.grad_slots])
+                flag_base.append(flags_ptr)
+                continue
+            ptrs = [F.ipc_open(h[k]) for k in ("shards", "g0", "g1", "flags")]
+            self._opened += ptrs
+            shard_base.append(ptrs[0])
+            grad_base.append([ptrs[1], ptrs[2]])
+            flag_base.append(ptrs[3])
+        self.ready_slots = [flag_base[q] + 8 * r for q in range(W)]
+        self.done_slots = [flag_base[q] + 8 * W + 8 * r for q in range(W)]
+        self._p2p_tables(shard_base, grad_base)
+
+    def close_ipc(self):
+        for p in getattr(self, "_opened", []):
+            F.ipc_close(p)
+        self._opened = []
+
+    def _p2p_tables(self, shard_base, grad_base):
         W = self.world
-        self.ag_peers = [[self.peer_shards[q].data_ptr() + self.shard_offs[b.members[0]] for q in range(W)]
-                         for b in self.fwd + self.bwd]
-        self.rs_peers = [[self.peer_grads[q][i % 2].data_ptr() for q in range(W)] for i, b in enumerate(self.bwd)]
+        self.ag_peers = [[shard_base[q] + self.shard_offs[b.members[0]] for q in range(W)] for b in self.fwd + self.bwd]
+        self.rs_peers = [[grad_base[q][i % 2] for q in range(W)] for i, b in enumerate(self.bwd)]
         self.epoch = 0
 
     def p2p_schedule(self, timeout_ns=10 ** 10):

@@ -25,6 +25,31 @@ from workloads import llama
 pytestmark = pytest.mark.gpu
 
 
+def test_bench_p2p_two_processes_one_gpu():
+    """bench.py's multi-rank peer-memory path (IPC handle exchange over
+    torch.distributed, epoch flags across processes) end to end with 2 ranks
+    on one GPU (--same-device, time-sliced: the timings mean nothing)."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"),
+           "--gpus", "2", "--collective", "p2p", "--same-device", "--steps", "2", "--warmup", "1",
+           "--layers", "1", "--tokens", "0", "--no-e2e"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["p2p_wait_timeouts"] == 0
+    assert line["kernels"]["fsdp_p2p_allgather_kernel"]["launches_per_step"] == 2 * line["config"]["buckets_fwd"]
+
+
 def test_host_io_step():
     """fsdp_host_io: the step loads every forward bucket's shards from pinned
     host memory before its all-gather and stores every backward bucket's
