@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--proxy-ctas", type=int, default=1)
     ap.add_argument("--proxy-smem", type=int, default=0)
+    ap.add_argument("--trace", default=None, help="write a Chrome trace of one profiled step to this path")
     ap.add_argument("--pg", default="auto", choices=["auto", "nccl", "gloo"],
                     help="torch.distributed backend for host plumbing (auto: nccl, gloo for p2p)")
     ap.add_argument("--same-device", action="store_true",
@@ -303,6 +304,9 @@ def main():
     # (2) the same K steps with a CUDA event pair around every op (per-kernel
     #     device time on the launching stream; synchronises once per step)
     ms_prof, reports = timed_loop(L.SCHED_TIMING, args.steps)
+    if args.trace and rank == 0:
+        rep_t = st.step(flags | L.SCHED_TIMING, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, want_log=True)
+        H.chrome_trace(rep_t["log"], args.trace)
     # (3) compute-stream-only baseline: same ops, no collective, no wait
     step(L.SCHED_NO_COMM)
     ms_compute, _ = timed_loop(L.SCHED_NO_COMM, args.steps)
@@ -326,7 +330,7 @@ def main():
         beta = round((world - 1) / world / 720e9 * 1e15)
         link = (20000, beta)
         durs = []
-        for ph, op, b, _s, ns in rep["log"]:
+        for ph, op, b, _s, ns, _t in rep["log"]:
             bk = (st.fwd if ph == 0 else st.bwd)[b]
             if op == L.OP_AG:
                 durs.append(F.comm_time_ns(world * bk.ag_seg, link))

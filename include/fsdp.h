@@ -390,11 +390,13 @@ typedef struct fsdp_host_io {
 } fsdp_host_io;
 
 typedef struct {
-  int64_t ns;     /* TIMING: event-measured duration of this op, else -1 */
-  int32_t phase;  /* 0 forward, 1 backward */
-  int32_t op;     /* FSDP_OP_* */
-  int32_t bucket; /* index in the phase's execution order */
-  int32_t stream; /* 0 compute, 1 comm */
+  int64_t ns;       /* TIMING: event-measured duration of this op, else -1 */
+  int32_t phase;    /* 0 forward, 1 backward */
+  int32_t op;       /* FSDP_OP_* */
+  int32_t bucket;   /* index in the phase's execution order */
+  int32_t stream;   /* 0 compute, 1 comm */
+  int64_t start_ns; /* TIMING: start relative to the step's first event (a timeline /
+                       Chrome trace), else -1 */
 } fsdp_log_entry;
 
 typedef struct {

@@ -108,7 +108,7 @@ class Schedule(C.Structure):
 
 class LogEntry(C.Structure):
     _fields_ = [("ns", C.c_int64), ("phase", C.c_int32), ("op", C.c_int32), ("bucket", C.c_int32),
-                ("stream", C.c_int32)]
+                ("stream", C.c_int32), ("start_ns", C.c_int64)]
 
 
 class StepReport(C.Structure):

@@ -283,8 +283,22 @@ fsdp_status ag_collective(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream
   return FSDP_OK;
 }
 
+// Asynchronous NCCL failures (a peer died, a network error) surface here, at
+// every WAIT and at the end of each scheduled step.
+fsdp_status check_async_error(fsdp_ctx* c) {
+  if (!c->comm) return FSDP_OK;
+  ncclResult_t ae = ncclSuccess;
+  FSDP_NCCL_TRY(ncclCommGetAsyncError(c->comm, &ae));
+  if (ae != ncclSuccess && ae != ncclInProgress)
+    return fail(FSDP_ERR_NCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(ae));
+  return FSDP_OK;
+}
+
 fsdp_status ag_wait(fsdp_ctx* c, fsdp_bucket* b, cudaStream_t cs, bool with_comm) {
-  if (comm_on(c, with_comm)) FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, b->ev_ag_done, 0));
+  if (comm_on(c, with_comm)) {
+    FSDP_TRY(check_async_error(c));
+    FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, b->ev_ag_done, 0));
+  }
   return FSDP_OK;
 }
 
@@ -316,7 +330,10 @@ fsdp_status rs_collective(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream
 }
 
 fsdp_status rs_wait(fsdp_ctx* c, fsdp_bucket* b, cudaStream_t cs, bool with_comm) {
-  if (comm_on(c, with_comm)) FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, b->ev_rs_done, 0));
+  if (comm_on(c, with_comm)) {
+    FSDP_TRY(check_async_error(c));
+    FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, b->ev_rs_done, 0));
+  }
   return FSDP_OK;
 }
 

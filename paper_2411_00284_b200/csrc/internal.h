@@ -151,6 +151,7 @@ fsdp_status rs_collective(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream
 fsdp_status rs_wait(fsdp_ctx* c, fsdp_bucket* b, cudaStream_t cs, bool with_comm);
 fsdp_status rs_copyout(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches);
 cudaStream_t resolve_comm(fsdp_ctx* c, fsdp_stream_t s);
+fsdp_status check_async_error(fsdp_ctx* c);  // ncclCommGetAsyncError, if the ctx has a comm
 }  // namespace fsdp
 
 struct fsdp_ctx {

@@ -1,6 +1,8 @@
 // fsdp_run_schedule: the reordered (Table 6) or vanilla op
 // sequence of one training step, executed on a compute and a comm stream.
 // Also the compute proxy (K7) launch and calibration.
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <vector>
 
@@ -15,6 +17,16 @@ struct Op {
 };
 
 bool is_comm(int32_t op) { return op == FSDP_OP_AG || op == FSDP_OP_RS; }
+
+// NVTX range names (host-side enqueue ranges; visible in nsys / ncu --nvtx).
+const char* const kOpNames[FSDP_N_OPS] = {"fsdp:PACK_AG", "fsdp:AG",        "fsdp:WAIT_AG", "fsdp:UNPACK",
+                                          "fsdp:COMPUTE_F", "fsdp:COMPUTE_B", "fsdp:PACK_RS", "fsdp:RS",
+                                          "fsdp:WAIT_RS", "fsdp:COPYOUT_RS"};
+
+struct NvtxRange {
+  explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // Forward: prefetch depth 1; AG(k+1) before Wa(k) or after Wa(k) and its
 // copy-out.  Vanilla: AG(k) right before Wa(k).
@@ -133,6 +145,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
       if (out->log) {
         fsdp_log_entry& e = out->log[i];
         e.ns = -1;
+        e.start_ns = -1;
         e.phase = seq[i].phase;
         e.op = seq[i].op;
         e.bucket = seq[i].bucket;
@@ -280,9 +293,11 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     FSDP_TRY(p2p_signal(ready_slots, pp->epoch_base + 1, cs));  // my shards are final
     FSDP_TRY(p2p_wait(pp->ready_flags, pp->epoch_base + 1, cs));
   }
+  NvtxRange step_range("fsdp:step");
   for (size_t i = 0; i < seq.size(); ++i) {
     const Op& o = seq[i];
     fsdp_bucket* b = (o.phase == 0 ? s->fwd : s->bwd)[o.bucket];
+    NvtxRange op_range(kOpNames[o.op]);
     FSDP_TRY(io_before(o));
     if (pp) {
       // the peer-memory path: same sequence, different work per op
@@ -398,6 +413,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     FSDP_TRY(p2p_wait(pp->ready_flags, epoch(s->n_bwd), cs));
   }
   if (timing) FSDP_CUDA_TRY(cudaEventRecord(ev[1], cs));
+  FSDP_TRY(check_async_error(ctx));
 
   if (out) {
     out->kernel_launches = launches;
@@ -417,7 +433,12 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
         FSDP_CUDA_TRY(cudaEventElapsedTime(&t, ev[2 + 2 * i], ev[3 + 2 * i]));
         const int64_t ns = static_cast<int64_t>(t * 1e6);
         out->op_ns[o.op] += ns;
-        if (out->log) out->log[i].ns = ns;
+        if (out->log) {
+          out->log[i].ns = ns;
+          float t0 = 0.f;
+          FSDP_CUDA_TRY(cudaEventElapsedTime(&t0, ev[0], ev[2 + 2 * i]));
+          out->log[i].start_ns = static_cast<int64_t>(t0 * 1e6);
+        }
       }
     }
   }

@@ -195,7 +195,7 @@ def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0,
     out = dict(step_ns=rep.step_ns, op_ns=list(rep.op_ns), op_count=list(rep.op_count),
                kernel_launches=rep.kernel_launches, collectives=rep.collectives, log_len=rep.log_len)
     if want_log:
-        out["log"] = [(e.phase, e.op, e.bucket, e.stream, e.ns) for e in log[:rep.log_len]]
+        out["log"] = [(e.phase, e.op, e.bucket, e.stream, e.ns, e.start_ns) for e in log[:rep.log_len]]
     return out
 
 

@@ -309,6 +309,27 @@ class RankState:
                 "buckets": len(q)}
 
 
+OP_NAMES = ["PACK_AG", "AG", "WAIT_AG", "UNPACK", "COMPUTE_F", "COMPUTE_B", "PACK_RS", "RS", "WAIT_RS",
+            "COPYOUT_RS"]
+
+
+def chrome_trace(log, path, pid=0):
+    """Chrome-trace JSON of a FSDP_SCHED_TIMING step log (entries with
+    start_ns / ns >= 0): one complete ("X") event per op, tid 0 compute /
+    1 comm, microseconds."""
+    import json
+    ev = []
+    for ph, op, b, stream, ns, start in log:
+        if ns is None or ns < 0 or start is None or start < 0:
+            continue
+        ev.append({"name": "%s %s[%d]" % (OP_NAMES[op], "fwd" if ph == 0 else "bwd", b), "ph": "X",
+                   "ts": start / 1e3, "dur": ns / 1e3, "pid": pid, "tid": stream,
+                   "args": {"phase": ph, "op": OP_NAMES[op], "bucket": b}})
+    with open(path, "w") as f:
+        json.dump({"traceEvents": ev, "displayTimeUnit": "ms"}, f)
+    return len(ev)
+
+
 def plans_for(specs, world, mode, t_fwd=None, t_bwd=None, ag=(0, 0), rs=(0, 0), mem_max=0,
               param_dtype=L.BF16):
     descs = [(p.dim0, p.row_numel, p.module_id) for p in specs]

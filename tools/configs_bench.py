@@ -63,7 +63,7 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
         # (modelled NVLink; no SM / HBM contention)
         rep = st.step(flags | L.SCHED_TIMING, cs.cuda_stream, ms.cuda_stream, pf, pb, want_log=True)
         durs = []
-        for ph, op, b, stream, ns in rep["log"]:
+        for ph, op, b, stream, ns, _t in rep["log"]:
             bk = (st.fwd if ph == 0 else st.bwd)[b]
             if op == L.OP_AG:
                 durs.append(F.comm_time_ns(world * bk.ag_seg, predict_link[0]))
