@@ -65,6 +65,11 @@
 #ifndef FSDP_BULK_STAGES
 #define FSDP_BULK_STAGES 6
 #endif
+#ifndef FSDP_BULK_LAG
+#define FSDP_BULK_LAG 0  // bulk engine: stores kept in flight before a stage is reloaded
+#endif
+#define FSDP_STR2(x) #x
+#define FSDP_STR(x) FSDP_STR2(x)
 #ifndef FSDP_BULK_CTAS_PER_SM
 #define FSDP_BULK_CTAS_PER_SM 1  // resident bulk CTAs per SM the smem ring is sized for
 #endif
@@ -358,20 +363,25 @@ __device__ __forceinline__ void run_table_bulk(const Chunk* __restrict__ tab, in
     ++loaded;
     next = advance(next + gridDim.x);
   }
+  // Stage of chunk c is reloaded (with chunk c + kStages) right after store
+  // c + kLag is issued, once all but the kLag most recent stores have read
+  // shared memory: kLag stores and kStages - 1 - kLag loads stay in flight.
+  constexpr int kLag = FSDP_BULK_LAG;
+  static_assert(kLag >= 0 && kLag < kStages, "bulk lag");
   while (stored < loaded) {
     const int s = stored % kStages;
     mbar_wait(bar0 + 8 * s, (stored / kStages) & 1);
     bulk_store(dsts[s], smem0 + s * kChunkBytes, lens[s]);
     ++stored;
-    if (next < n) {
-      // the stage is reused: its store must have finished reading shared memory
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    const int c = stored - 1 - kLag;
+    if (c >= 0 && next < n && loaded == c + kStages) {
+      asm volatile("cp.async.bulk.wait_group.read " FSDP_STR(FSDP_BULK_LAG) ";" ::: "memory");
+      const int rs = c % kStages;
       const Chunk ch = tab[next];
       const uint32_t bytes = ch.n * 16u;
-      dsts[s] = dst_of<kDstRel>(ch, base);
-      lens[s] = bytes;
-      bulk_load(smem0 + s * kChunkBytes, src_of<kSrcRel>(ch, base), bytes,
-                bar0 + 8 * s);
+      dsts[rs] = dst_of<kDstRel>(ch, base);
+      lens[rs] = bytes;
+      bulk_load(smem0 + rs * kChunkBytes, src_of<kSrcRel>(ch, base), bytes, bar0 + 8 * rs);
       ++loaded;
       next = advance(next + gridDim.x);
     }

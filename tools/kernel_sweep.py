@@ -56,7 +56,21 @@ SWEEP4 = {
     "e4_k9tpl_k16": ["FSDP_K9_TEMPLATED=1", "FSDP_CHUNK_KB=16"],
 }
 
+SWEEP5 = {
+    "f1_bulk_s8_l2_k16_c1": ["FSDP_BULK=2", "FSDP_BULK_STAGES=8", "FSDP_BULK_LAG=2", "FSDP_CHUNK_KB=16",
+                             "FSDP_BULK_CTAS_PER_SM=1", "FSDP_BULK_GRID_PER_SM=1"],
+    "f2_bulk_s6_l2_k32_c1": ["FSDP_BULK=2", "FSDP_BULK_STAGES=6", "FSDP_BULK_LAG=2",
+                             "FSDP_BULK_CTAS_PER_SM=1", "FSDP_BULK_GRID_PER_SM=1"],
+    "f3_bulk_s4_l1_k16_c2": ["FSDP_BULK=2", "FSDP_BULK_STAGES=6", "FSDP_BULK_LAG=1", "FSDP_CHUNK_KB=16",
+                             "FSDP_BULK_CTAS_PER_SM=2", "FSDP_BULK_GRID_PER_SM=2"],
+    "f4_bulk_s8_l3_k16_c1": ["FSDP_BULK=2", "FSDP_BULK_STAGES=12", "FSDP_BULK_LAG=3", "FSDP_CHUNK_KB=16",
+                             "FSDP_BULK_CTAS_PER_SM=1", "FSDP_BULK_GRID_PER_SM=1"],
+    "f5_bulk_s4_l1_k16_c3": ["FSDP_BULK=2", "FSDP_BULK_STAGES=4", "FSDP_BULK_LAG=1", "FSDP_CHUNK_KB=16",
+                             "FSDP_BULK_CTAS_PER_SM=3", "FSDP_BULK_GRID_PER_SM=3"],
+}
+
 VARIANTS = {
+    **SWEEP5,
     **SWEEP4,
     **SWEEP3,
     **SWEEP2,
