@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--proxy-ctas", type=int, default=1)
     ap.add_argument("--proxy-smem", type=int, default=0)
     ap.add_argument("--trace", default=None, help="write a Chrome trace of one profiled step to this path")
+    ap.add_argument("--compute", default="proxy", choices=["proxy", "gemm"],
+                    help="bucket compute: calibrated proxy kernel (--tokens) or cuBLASLt linear layers on the "
+                         "gathered parameters (tokens = --tokens or 1024)")
     ap.add_argument("--pg", default="auto", choices=["auto", "nccl", "gloo"],
                     help="torch.distributed backend for host plumbing (auto: nccl, gloo for p2p)")
     ap.add_argument("--same-device", action="store_true",
@@ -120,6 +123,16 @@ def measured_peak_hbm():
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except (OSError, KeyError, ValueError):
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def measured_peak_bf16():
+    """Sustained dense bf16 TFLOP/s (MEASURED_PEAKS.json; for a kernel timed
+    inside a long step), else the guide's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops_sustained"])
+    except (OSError, KeyError, ValueError):
+        return 1400.0
 
 
 def ncu_traffic(op_name):
@@ -269,8 +282,15 @@ def main():
     if args.bwd_placement == "before":
         flags |= L.SCHED_BWD_AG_BEFORE_WAIT
 
+    gemm = None
+    if args.compute == "gemm":
+        # linear-layer compute: cuBLASLt bf16 GEMMs on the gathered parameters,
+        # the backward writing the gradients the reduce-scatter averages
+        gemm = st.setup_gemm(tokens or 1024)
+        pf = pb = None
+
     def step(extra=0):
-        return st.step(flags | extra, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem)
+        return st.step(flags | extra, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, gemm=gemm)
 
     def barrier():
         if multi:
@@ -321,12 +341,16 @@ def main():
     # the compute proxy at --predict-tokens), every collective at alpha + beta n
     # of modelled NVLink 5 (720 GB/s bus, 20 us); no contention modelled.
     predicted = None
-    if not multi and not p2p and args.predict_tokens:
-        ptf, ptb = per_param_compute_ns(specs, args.predict_tokens)
-        nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
-        ppf = H.proxy_iters(H.bucket_times(fplan, ptf), nspi)
-        ppb = H.proxy_iters(H.bucket_times(bplan, ptb), nspi)
-        rep = st.step(flags | L.SCHED_TIMING, cs, ms, ppf, ppb, args.proxy_ctas, args.proxy_smem, want_log=True)
+    if not multi and not p2p and (args.predict_tokens or gemm):
+        if gemm:   # the measured GEMMs of this run are the compute
+            rep = st.step(flags | L.SCHED_TIMING, cs, ms, None, None, want_log=True, gemm=gemm)
+        else:
+            ptf, ptb = per_param_compute_ns(specs, args.predict_tokens)
+            nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
+            ppf = H.proxy_iters(H.bucket_times(fplan, ptf), nspi)
+            ppb = H.proxy_iters(H.bucket_times(bplan, ptb), nspi)
+            rep = st.step(flags | L.SCHED_TIMING, cs, ms, ppf, ppb, args.proxy_ctas, args.proxy_smem,
+                          want_log=True)
         beta = round((world - 1) / world / 720e9 * 1e15)
         link = (20000, beta)
         durs = []
@@ -339,10 +363,22 @@ def main():
             else:
                 durs.append(max(ns, 0))
         tot, exp, _, _ = F.simulate_schedule(rep["log"], durs)
-        predicted = {"world": world, "tokens_per_gpu": args.predict_tokens, "link_alpha_ns": link[0],
-                     "link_beta_fs_per_byte": link[1], "total_ms": round(tot / 1e6, 3),
+        predicted = {"world": world, "tokens_per_gpu": gemm["tokens"] if gemm else args.predict_tokens,
+                     "compute": "cuBLASLt linear layers (measured)" if gemm else "calibrated proxy (per-op model)",
+                     "link_alpha_ns": link[0], "link_beta_fs_per_byte": link[1], "total_ms": round(tot / 1e6, 3),
                      "exposed_comm_ms": round(exp / 1e6, 3),
                      "model": "measured compute-stream ops + alpha/beta NVLink collectives, no contention"}
+
+    # linear-layer compute throughput (cuBLASLt, tensor cores) of the timed steps
+    gemm_report = None
+    if gemm:
+        ops_ns = sum(r["op_ns"][L.OP_COMPUTE_F] + r["op_ns"][L.OP_COMPUTE_B] for r in reports) / len(reports)
+        tf = st.gemm_flops / (ops_ns * 1e-9) / 1e12
+        peak_tf = measured_peak_bf16()
+        gemm_report = {"tokens": gemm["tokens"], "tflops_per_step": round(st.gemm_flops / 1e12, 2),
+                       "compute_ms_per_step": round(ops_ns / 1e6, 3), "achieved_TFLOPs": round(tf, 1),
+                       "peak_TFLOPs": peak_tf, "frac": round(tf / peak_tf, 3),
+                       "note": "library GEMMs (cuBLASLt), bf16 in/out, fp32 accumulate"}
 
     # per-op device time from the timed steps' events -> dominant data kernel
     op_ns = [sum(r["op_ns"][i] for r in reports) for i in range(L.N_OPS)]
@@ -440,6 +476,7 @@ def main():
             "exposed_comm_ms": round(ms_step - ms_compute, 3), "compute_stream_ms": round(ms_compute, 3),
             "profiled_ms_per_step": round(ms_prof, 3),
             "predicted": predicted,
+            "linear_compute": gemm_report,
             "collectives": coll_ms, "busbw_GBps": busbw, "kernels": per_kernel,
             "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),

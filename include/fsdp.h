@@ -367,7 +367,29 @@ typedef struct {
   int32_t reserved;
   const fsdp_p2p_schedule* p2p; /* FSDP_SCHED_P2P only, else NULL */
   const struct fsdp_host_io* io; /* host-resident shards / gradient shards, else NULL */
+  const struct fsdp_gemm_compute* gemm; /* real linear-layer compute instead of K7, else NULL */
 } fsdp_schedule;
+
+/* Linear-layer compute instead of the proxy: every
+ * member with row_numel > 1 is treated as a linear layer W [d, R] (out = d,
+ * in = R, row-major, the gathered full parameter) applied to T tokens with
+ * cuBLASLt bf16 GEMMs (fp32 accumulate) on the compute stream:
+ *   COMPUTE_F b : Y[T, out]  = X[T, in] . W^T
+ *   COMPUTE_B b : dX[T, in]  = dY[T, out] . W,   dW[out, in] = dY^T . X  -> written
+ *                 into the member's full_grads (bf16), i.e. the gradients the
+ *                 reduce-scatter then averages are real products of the step.
+ * 1-D members (norms) take no compute.  No attention / nonlinearity is
+ * modelled.  Buffers (device, caller-owned): x [T, max in] and dy [T, max out]
+ * bf16 activations, y bf16 scratch of T * max(in, out) elements, a cuBLASLt
+ * workspace.  Backward buckets need bf16 gradients. */
+typedef struct fsdp_gemm_compute {
+  int64_t tokens;
+  const void* x;
+  const void* dy;
+  void* y;
+  void* workspace;
+  int64_t workspace_bytes;
+} fsdp_gemm_compute;
 
 /* Host-resident parameters and gradients (offload): with `io` set, the step
  * streams this rank's shards in from pinned host memory and its averaged

@@ -96,6 +96,11 @@ class HostIO(C.Structure):
                 ("h2d", C.c_void_p), ("d2h", C.c_void_p)]
 
 
+class GemmCompute(C.Structure):
+    _fields_ = [("tokens", C.c_int64), ("x", C.c_void_p), ("dy", C.c_void_p), ("y", C.c_void_p),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64)]
+
+
 class Schedule(C.Structure):
     _fields_ = [("fwd", C.POINTER(C.c_void_p)), ("bwd", C.POINTER(C.c_void_p)),
                 ("proxy_iters_fwd", C.POINTER(C.c_int64)), ("proxy_iters_bwd", C.POINTER(C.c_int64)),
@@ -103,7 +108,7 @@ class Schedule(C.Structure):
                 ("compute", C.c_void_p), ("comm", C.c_void_p), ("n_fwd", C.c_int32),
                 ("n_bwd", C.c_int32), ("flags", C.c_uint32), ("proxy_ctas_per_sm", C.c_int32),
                 ("proxy_smem_bytes", C.c_int32), ("reserved", C.c_int32), ("p2p", C.POINTER(P2PSchedule)),
-                ("io", C.POINTER(HostIO))]
+                ("io", C.POINTER(HostIO)), ("gemm", C.POINTER(GemmCompute))]
 
 
 class LogEntry(C.Structure):

@@ -42,6 +42,15 @@ def nccl_dirs():
     return inc, lib
 
 
+def cublas_dirs():
+    import nvidia.cublas  # the wheel torch links against (plain library GEMMs only)
+    base = list(nvidia.cublas.__path__)[0]
+    inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+    if not os.path.exists(os.path.join(inc, "cublasLt.h")) or not os.path.exists(os.path.join(lib, "libcublasLt.so.12")):
+        raise RuntimeError("cuBLASLt headers/library not found under %s" % base)
+    return inc, lib
+
+
 def _run(cmd, verbose):
     if verbose:
         print(" ".join(cmd), flush=True)
@@ -67,12 +76,14 @@ def build(verbose=False, force=False, defines=None, variant=None):
     cuda = cuda_home()
     nvcc = os.path.join(cuda, "bin", "nvcc")
     inc_nccl, lib_nccl = nccl_dirs()
+    inc_blas, lib_blas = cublas_dirs()
     bdir = os.path.join(BUILD, "variants", variant) if variant else BUILD
     lib = os.path.join(bdir, "libfsdp_b200.so") if variant else LIB
     os.makedirs(bdir, exist_ok=True)
     dflags = ["-D" + d for d in (defines or [])]
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
-    incs = ["-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc_nccl, "-I", os.path.join(cuda, "include")]
+    incs = ["-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc_nccl, "-I", inc_blas,
+            "-I", os.path.join(cuda, "include")]
     objs = []
     ptxas_log = []
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
@@ -90,7 +101,8 @@ def build(verbose=False, force=False, defines=None, variant=None):
                   *incs, "-c", src, "-o", obj], verbose)
     if force or variant or _stale(lib, objs):
         _run([nvcc, "-shared", *ARCH, "-o", lib, *objs, "-L", lib_nccl, "-l:libnccl.so.2",
-              "-Xlinker", "-rpath," + lib_nccl, "-cudart", "static"], verbose)
+              "-Xlinker", "-rpath," + lib_nccl, "-L", lib_blas, "-l:libcublasLt.so.12",
+              "-Xlinker", "-rpath," + lib_blas, "-cudart", "static"], verbose)
     if ptxas_log:
         with open(os.path.join(bdir, "ptxas.log"), "w") as f:
             f.write("\n".join(ptxas_log))

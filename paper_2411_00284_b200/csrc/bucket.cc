@@ -185,6 +185,11 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   b->rs_zero_copy = rs_zc;
   b->ag_direct = direct;
   b->full0 = d->fulls ? static_cast<char*>(d->fulls[0]) : nullptr;
+  b->members.assign(d->params, d->params + k);
+  for (int32_t j = 0; j < k; ++j) {
+    b->fulls.push_back(d->fulls ? d->fulls[j] : nullptr);
+    b->grads.push_back(d->full_grads ? const_cast<void*>(d->full_grads[j]) : nullptr);
+  }
   b->shard_seg = ag_zc ? static_cast<char*>(d->shards[0]) : nullptr;
   b->gshard_seg = rs_zc ? static_cast<char*>(d->grad_shards[0]) : nullptr;
   fsdp_status st = FSDP_OK;

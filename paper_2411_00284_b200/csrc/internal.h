@@ -152,6 +152,10 @@ fsdp_status rs_wait(fsdp_ctx* c, fsdp_bucket* b, cudaStream_t cs, bool with_comm
 fsdp_status rs_copyout(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches);
 cudaStream_t resolve_comm(fsdp_ctx* c, fsdp_stream_t s);
 fsdp_status check_async_error(fsdp_ctx* c);  // ncclCommGetAsyncError, if the ctx has a comm
+// gemm.cc
+fsdp_status bucket_compute(fsdp_ctx* c, fsdp_bucket* b, const fsdp_gemm_compute* g, bool backward, cudaStream_t s,
+                           int* launches);
+void gemm_cache_destroy(void* p);
 }  // namespace fsdp
 
 struct fsdp_ctx {
@@ -165,6 +169,7 @@ struct fsdp_ctx {
   std::vector<cudaEvent_t> timing_events;  // pool for FSDP_SCHED_TIMING
   std::vector<cudaEvent_t> io_events;      // pool for host I/O ordering (fsdp_host_io)
   cudaStream_t own_h2d = nullptr, own_d2h = nullptr;
+  void* gemm_cache = nullptr;              // cuBLASLt handle + plans (gemm.cc)
 };
 
 struct fsdp_bucket {
@@ -181,6 +186,9 @@ struct fsdp_bucket {
   char* gshard_seg = nullptr;  // this rank's RS segment in grad-shard storage
   bool ag_direct = false;      // gathered buffer == the (single) full parameter
   char* full0 = nullptr;       // fulls[0]
+  // members and their full-parameter / full-gradient pointers (linear-layer compute)
+  std::vector<fsdp_param_desc> members;
+  std::vector<void*> fulls, grads;
   fsdp::DevTable ag_pack, ag_unpack, rs_pack, rs_copyout;
   fsdp::DevTable p2p_ag, p2p_rs;  // K8 / K9 tables (peer-memory path)
   cudaEvent_t ev_ag_packed = nullptr, ev_ag_done = nullptr;

@@ -199,6 +199,14 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   if (s->proxy_ctas_per_sm < 0 || s->proxy_smem_bytes < 0)
     return fail(FSDP_ERR_INVALID_ARG, "bad proxy footprint");
   (void)max_seg;  // slot sizes are the caller's contract (>= world * largest segment)
+  if (s->gemm) {
+    const fsdp_gemm_compute* g = s->gemm;
+    if (g->tokens < 1 || g->tokens > INT32_MAX || !g->x || !g->dy || !g->y || g->workspace_bytes < 0 ||
+        (g->workspace_bytes && !g->workspace))
+      return fail(FSDP_ERR_INVALID_ARG, "bad fsdp_gemm_compute");
+    for (int32_t j = 0; j < s->n_bwd; ++j)
+      if (s->bwd[j]->grad_bytes != 2) return fail(FSDP_ERR_INVALID_ARG, "linear-layer compute needs bf16 gradients");
+  }
   if (s->io) {
     for (int32_t k = 0; k < s->n_fwd; ++k)
       if (s->io->fwd_host_shards && s->io->fwd_host_shards[k] && !s->fwd[k]->ag_zero_copy)
@@ -293,6 +301,16 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     FSDP_TRY(p2p_signal(ready_slots, pp->epoch_base + 1, cs));  // my shards are final
     FSDP_TRY(p2p_wait(pp->ready_flags, pp->epoch_base + 1, cs));
   }
+  // the compute of a bucket: linear-layer GEMMs (fsdp_gemm_compute) or the K7 proxy
+  auto compute = [&](const Op& o, fsdp_bucket* b) -> fsdp_status {
+    if (s->gemm) return bucket_compute(ctx, b, s->gemm, o.op == FSDP_OP_COMPUTE_B, cs, &launches);
+    const int64_t* it = o.op == FSDP_OP_COMPUTE_F ? s->proxy_iters_fwd : s->proxy_iters_bwd;
+    if (it && it[o.bucket] > 0) {
+      FSDP_CUDA_TRY(launch_proxy(it[o.bucket], proxy_grid, s->proxy_smem_bytes, ctx->sink, cs));
+      ++launches;
+    }
+    return FSDP_OK;
+  };
   NvtxRange step_range("fsdp:step");
   for (size_t i = 0; i < seq.size(); ++i) {
     const Op& o = seq[i];
@@ -330,11 +348,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
           // the backward of bucket b overwrites gradient slot b % 2: peers must be done with b - 2
           if (o.op == FSDP_OP_COMPUTE_B && with_comm && o.bucket >= 2)
             FSDP_TRY(p2p_wait(pp->done_flags, epoch(o.bucket - 2), cs));
-          const int64_t* it = o.op == FSDP_OP_COMPUTE_F ? s->proxy_iters_fwd : s->proxy_iters_bwd;
-          if (it && it[o.bucket] > 0) {
-            FSDP_CUDA_TRY(launch_proxy(it[o.bucket], proxy_grid, s->proxy_smem_bytes, ctx->sink, cs));
-            ++launches;
-          }
+          FSDP_TRY(compute(o, b));
           break;
         }
         case FSDP_OP_PACK_RS:
@@ -385,11 +399,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
       case FSDP_OP_UNPACK: FSDP_TRY(ag_unpack(ctx, b, ag_st, cs, &launches)); break;
       case FSDP_OP_COMPUTE_F:
       case FSDP_OP_COMPUTE_B: {
-        const int64_t* it = o.op == FSDP_OP_COMPUTE_F ? s->proxy_iters_fwd : s->proxy_iters_bwd;
-        if (it && it[o.bucket] > 0) {
-          FSDP_CUDA_TRY(launch_proxy(it[o.bucket], proxy_grid, s->proxy_smem_bytes, ctx->sink, cs));
-          ++launches;
-        }
+        FSDP_TRY(compute(o, b));
         break;
       }
       case FSDP_OP_PACK_RS: FSDP_TRY(rs_pack(ctx, b, rs_st, cs, with_comm, &launches)); break;

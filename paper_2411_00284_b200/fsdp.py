@@ -145,7 +145,7 @@ def reduce_scatter_bucket(ctx, bucket, staging_ptr, compute=0, comm=0, flags=L.I
 
 def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0, comm=0, flags=0,
                  proxy_iters_fwd=None, proxy_iters_bwd=None, proxy_ctas_per_sm=1, proxy_smem_bytes=0,
-                 n_fwd=None, n_bwd=None, want_log=True, p2p=None, io=None):
+                 n_fwd=None, n_bwd=None, want_log=True, p2p=None, io=None, gemm=None):
     """fsdp_run_schedule.  fwd / bwd: Bucket lists in execution order (or
     counts via n_fwd / n_bwd with FSDP_SCHED_DRY_RUN and ctx=None).  Returns the
     step report as a dict (log as a list of (phase, op, bucket, stream, ns)).
@@ -187,6 +187,12 @@ def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0,
         hio.fwd_host_shards, hio.bwd_host_grads = a, g
         hio.h2d, hio.d2h = io.get("h2d") or None, io.get("d2h") or None
         s.io = C.pointer(hio)
+    if gemm is not None:
+        # gemm: dict(tokens, x, dy, y, workspace, workspace_bytes) -- fsdp_gemm_compute
+        gc = L.GemmCompute(int(gemm["tokens"]), gemm["x"], gemm["dy"], gemm["y"], gemm.get("workspace") or None,
+                           int(gemm.get("workspace_bytes", 0)))
+        keep.append(gc)
+        s.gemm = C.pointer(gc)
     cap = 5 * nf + 9 * nb + 4
     log = (L.LogEntry * cap)() if want_log else None
     rep = L.StepReport()

@@ -251,8 +251,30 @@ class RankState:
         bwd = [hg + self.gs_offs[b.members[0]] if b.query()["rs_zero_copy"] else 0 for b in self.bwd]
         return dict(fwd_host_shards=fwd, bwd_host_grads=bwd, h2d=h2d, d2h=d2h)
 
+    def setup_gemm(self, tokens, seed=7, workspace_bytes=64 << 20):
+        """Linear-layer compute (fsdp_gemm_compute) at `tokens` tokens: bf16
+        activations X [T, max in] ~ N(0, 1) and upstream gradients dY [T, max
+        out] ~ N(0, 1e-2), a [T, max(in, out)] scratch, a cuBLASLt workspace."""
+        lin = [p for p in self.specs if p.row_numel > 1]
+        max_in = max(p.row_numel for p in lin)
+        max_out = max(p.dim0 for p in lin)
+        dev = self.shard_buf.device
+        g = torch.Generator(device=dev).manual_seed(seed)
+        self.g_x = torch.empty(tokens * max_in, dtype=torch.bfloat16, device=dev).normal_(0, 1, generator=g)
+        self.g_dy = torch.empty(tokens * max_out, dtype=torch.bfloat16, device=dev).normal_(0, 1e-2, generator=g)
+        self.g_y = torch.empty(tokens * max(max_in, max_out), dtype=torch.bfloat16, device=dev)
+        self.g_ws = torch.empty(workspace_bytes, dtype=torch.uint8, device=dev)
+        self.gemm = dict(tokens=tokens, x=self.g_x.data_ptr(), dy=self.g_dy.data_ptr(), y=self.g_y.data_ptr(),
+                         workspace=self.g_ws.data_ptr(), workspace_bytes=workspace_bytes)
+        # FLOPs per step: 2 T out in forward, 4 T out in backward, per linear member of every bucket
+        self.gemm_flops = sum(2 * tokens * self.specs[j].dim0 * self.specs[j].row_numel
+                              for b in self.fwd for j in b.members if self.specs[j].row_numel > 1)
+        self.gemm_flops += sum(4 * tokens * self.specs[j].dim0 * self.specs[j].row_numel
+                               for b in self.bwd for j in b.members if self.specs[j].row_numel > 1)
+        return self.gemm
+
     def step(self, flags, compute, comm, proxy_fwd=None, proxy_bwd=None, ctas_per_sm=1, smem=0,
-             want_log=False, io=None):
+             want_log=False, io=None, gemm=None):
         p2p = None
         if flags & L.SCHED_P2P:
             p2p = self.p2p_schedule()
@@ -263,7 +285,7 @@ class RankState:
                               rs_staging=(self.rs_st[0].data_ptr(), self.rs_st[1].data_ptr()),
                               compute=compute, comm=comm, flags=flags, proxy_iters_fwd=proxy_fwd,
                               proxy_iters_bwd=proxy_bwd, proxy_ctas_per_sm=ctas_per_sm,
-                              proxy_smem_bytes=smem, want_log=want_log, p2p=p2p, io=io)
+                              proxy_smem_bytes=smem, want_log=want_log, p2p=p2p, io=io, gemm=gemm)
 
     # -------------------------------------------------------------- accounting
     def step_bytes(self):

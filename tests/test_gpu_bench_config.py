@@ -50,6 +50,40 @@ def test_bench_p2p_two_processes_one_gpu():
     assert line["kernels"]["fsdp_p2p_allgather_kernel"]["launches_per_step"] == 2 * line["config"]["buckets_fwd"]
 
 
+def test_gemm_compute_feeds_real_gradients():
+    """fsdp_gemm_compute: the backward GEMM dW = dY^T X of every linear member
+    writes the full gradient the reduce-scatter then averages; dW matches an
+    fp32 torch reference within bf16 output rounding, and the gradient shards
+    equal widen(dW rows of this rank) * fl32(1/N) bit-exactly."""
+    world, T = 2, 256
+    specs = llama("8b", n_layers=1, with_embeddings=False)
+    ctx = F.Ctx(world, 0)
+    fplan, bplan = H.plans_for(specs, world, L.PLAN_MANUAL)
+    st = H.RankState(specs, world, 0, fplan, bplan, ctx, seed=9)
+    gemm = st.setup_gemm(T)
+    cs, ms = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+    rep = st.step(L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT | L.SCHED_TIMING, cs.cuda_stream, ms.cuda_stream,
+                  gemm=gemm)
+    torch.cuda.synchronize()
+    assert rep["op_ns"][L.OP_COMPUTE_B] > 0
+    bk = st.bwd[0]
+    goffs, _ = H._carve([st.full_numel[j] * 2 for j in bk.members])
+    X = st.g_x.float().cpu()
+    dY = st.g_dy.float().cpu()
+    for j, go in zip(bk.members, goffs):
+        p = specs[j]
+        if p.row_numel == 1:
+            continue
+        out, inn = p.dim0, p.row_numel
+        dW = st.grad_slots[0][go:go + 2 * out * inn].view(torch.bfloat16).view(out, inn)
+        ref = dY[:T * out].view(T, out).t() @ X[:T * inn].view(T, inn)
+        assert torch.allclose(dW.float().cpu(), ref, rtol=2e-2, atol=2e-2 * float(ref.abs().max())), p.name
+        c = -(-out // world)
+        gs = st.gshard_buf[st.gs_offs[j]:st.gs_offs[j] + 4 * c * inn].view(torch.float32).view(c, inn)
+        want = (dW[:c].float() * 0.5).cpu()
+        assert torch.equal(gs.cpu().view(torch.int32), want.view(torch.int32)), p.name
+
+
 def test_host_io_step():
     """fsdp_host_io: the step loads every forward bucket's shards from pinned
     host memory before its all-gather and stores every backward bucket's
