@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--proxy-ctas", type=int, default=1)
     ap.add_argument("--proxy-smem", type=int, default=0)
     ap.add_argument("--trace", default=None, help="write a Chrome trace of one profiled step to this path")
+    ap.add_argument("--graph", action="store_true", help="also time the step captured into a CUDA graph")
     ap.add_argument("--compute", default="proxy", choices=["proxy", "gemm"],
                     help="bucket compute: calibrated proxy kernel (--tokens) or cuBLASLt linear layers on the "
                          "gathered parameters (tokens = --tokens or 1024)")
@@ -331,6 +332,27 @@ def main():
     step(L.SCHED_NO_COMM)
     ms_compute, _ = timed_loop(L.SCHED_NO_COMM, args.steps)
 
+    # (4) optional: the step captured once into a CUDA graph and replayed
+    #     (removes host enqueue cost; NCCL calls are capturable; not for p2p,
+    #     whose epochs change every step)
+    ms_graph = None
+    if args.graph and not p2p:
+        g = torch.cuda.CUDAGraph()
+        barrier()
+        with torch.cuda.graph(g, stream=compute):
+            step()
+        g.replay()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(compute)
+        for _ in range(args.steps):
+            with torch.cuda.stream(compute):
+                g.replay()
+        b.record(compute)
+        barrier()
+        ms_graph = max_over_ranks(a.elapsed_time(b) / args.steps)
+        del g
+
     ag_b, rs_b = st.step_bytes()
     ranks = world_env if multi else 1
     value = ranks * (ag_b + rs_b) / (ms_step * 1e-3) / 1e9
@@ -477,6 +499,7 @@ def main():
             "profiled_ms_per_step": round(ms_prof, 3),
             "predicted": predicted,
             "linear_compute": gemm_report,
+            "graph_ms_per_step": round(ms_graph, 3) if ms_graph else None,
             "collectives": coll_ms, "busbw_GBps": busbw, "kernels": per_kernel,
             "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
