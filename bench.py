@@ -500,6 +500,10 @@ def main():
             "predicted": predicted,
             "linear_compute": gemm_report,
             "graph_ms_per_step": round(ms_graph, 3) if ms_graph else None,
+            # the paper's other metric: peak device memory of this rank
+            # (torch-allocated buffers: shards, slots, staging; the library's
+            # own run tables are a few MB)
+            "peak_device_mem_GiB": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
             "collectives": coll_ms, "busbw_GBps": busbw, "kernels": per_kernel,
             "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
