@@ -212,7 +212,13 @@ typedef struct {
 /* Bucket flags: the caller's storage already is this rank's segment (see
  * "Segment-layout storage" below); validated, FSDP_ERR_INVALID_ARG if the
  * pointers do not follow fsdp_layout's offsets. */
-enum { FSDP_BUCKET_SEGMENT_SHARDS = 1u, FSDP_BUCKET_SEGMENT_GRAD_SHARDS = 2u };
+enum { FSDP_BUCKET_SEGMENT_SHARDS = 1u, FSDP_BUCKET_SEGMENT_GRAD_SHARDS = 2u, FSDP_BUCKET_FP32_MASTER = 4u };
+/* FSDP_BUCKET_FP32_MASTER (mixed precision, "parameters are cast to
+ * param_dtype"): the shards are fp32 master weights [c_j, R_j] while the
+ * all-gather carries param_dtype = FSDP_BF16; the pack (K1) rounds them to
+ * bf16 (round to nearest even, cvt.rn.bf16.f32; NaN -> a quiet NaN) while
+ * copying.  Needs param_dtype FSDP_BF16; excludes FSDP_BUCKET_SEGMENT_SHARDS
+ * (the storage is not the bf16 segment). */
 
 fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc* desc, fsdp_bucket** out,
                                int64_t* ag_seg_bytes, int64_t* rs_seg_bytes);

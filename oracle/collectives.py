@@ -88,6 +88,25 @@ def bucketed_all_gather(params, world, align=16):
     return g, ag_unpack(g, dims, world, params[0].dtype, align)
 
 
+def mixed_precision_all_gather(masters, world, align=16):
+    """All-gather of fp32 master weights in param_dtype = bf16 ("the
+    parameters are cast to param_dtype" before they are used).  Step order as
+    in the paper's fp32-sharded / bf16-communicated setting: each rank holds
+    shard(master) in fp32, casts its shard to bf16 (round to nearest even),
+    copies it in, and the bucket is gathered and copied out in bf16.
+
+    ``masters``: full fp32 [d_j, R_j] master parameters in forward order.
+    Returns (gathered_buffer, fulls) like ``bucketed_all_gather``.
+    """
+    segs = []
+    for q in range(world):
+        local = [bf16.narrow(shard(m, world, q)) for m in masters]
+        segs.append(ag_pack(local, world, q, align))
+    g = all_gather(segs)
+    dims = [m.shape for m in masters]
+    return g, ag_unpack(g, dims, world, np.uint16, align)
+
+
 def _to_f32(g):
     if g.dtype == np.uint16:
         return bf16.widen(g)

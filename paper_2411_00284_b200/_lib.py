@@ -29,7 +29,7 @@ ISSUE, WAIT = 1, 2
 N_OPS = 10
 SCHED_REORDER, SCHED_FWD_AG_BEFORE_WAIT, SCHED_BWD_AG_BEFORE_WAIT = 1, 2, 4
 SCHED_NO_COMM, SCHED_DRY_RUN, SCHED_TIMING, SCHED_P2P = 8, 16, 32, 64
-BUCKET_SEGMENT_SHARDS, BUCKET_SEGMENT_GRAD_SHARDS = 1, 2
+BUCKET_SEGMENT_SHARDS, BUCKET_SEGMENT_GRAD_SHARDS, BUCKET_FP32_MASTER = 1, 2, 4
 
 EXPORTED = [
     "fsdp_last_error", "fsdp_abi_version", "fsdp_nccl_get_unique_id", "fsdp_ctx_create",

@@ -42,10 +42,15 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   const int32_t k = d->k;
   if (k < 1 || !d->params) return fail(FSDP_ERR_INVALID_ARG, "bucket needs >= 1 member");
   if (d->align_bytes < 1) return fail(FSDP_ERR_INVALID_ARG, "align_bytes < 1");
-  if (d->reserved != 0 || (d->flags & ~(FSDP_BUCKET_SEGMENT_SHARDS | FSDP_BUCKET_SEGMENT_GRAD_SHARDS)))
+  if (d->reserved != 0 || (d->flags & ~(FSDP_BUCKET_SEGMENT_SHARDS | FSDP_BUCKET_SEGMENT_GRAD_SHARDS |
+                                        FSDP_BUCKET_FP32_MASTER)))
     return fail(FSDP_ERR_INVALID_ARG, "unknown bucket flags");
   const int32_t ep = dtype_bytes(d->param_dtype), eg = dtype_bytes(d->grad_dtype);
   if (!ep || !eg) return fail(FSDP_ERR_INVALID_ARG, "unsupported dtype");
+  // fp32 master shards, cast to bf16 by the pack
+  const bool master = d->flags & FSDP_BUCKET_FP32_MASTER;
+  if (master && (d->param_dtype != FSDP_BF16 || (d->flags & FSDP_BUCKET_SEGMENT_SHARDS)))
+    return fail(FSDP_ERR_INVALID_ARG, "FSDP_BUCKET_FP32_MASTER needs param_dtype BF16 and no SEGMENT_SHARDS");
   for (int32_t j = 0; j < k; ++j) {
     const fsdp_param_desc& p = d->params[j];
     if (p.dim0 < 1 || p.row_numel < 1 || p.reserved != 0)
@@ -105,16 +110,20 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
     if (d->shards && direct) {
       // own rows straight into the full parameter (used unless the collective
       // sends from segment storage itself)
-      pack.copy(reinterpret_cast<uint64_t>(d->shards[0]),
-                reinterpret_cast<uint64_t>(d->fulls[0]) + static_cast<uint64_t>(r * ag_seg), ag_seg, kAbsDst);
+      const uint64_t src = reinterpret_cast<uint64_t>(d->shards[0]);
+      const uint64_t dst = reinterpret_cast<uint64_t>(d->fulls[0]) + static_cast<uint64_t>(r * ag_seg);
+      if (master) pack.narrow(src, dst, ag_seg / 2, kAbsDst);
+      else pack.copy(src, dst, ag_seg, kAbsDst);
     } else if (d->shards) {
       const int64_t nb = own.c * R * ep;
       if (ag_zc) {
         gaps.zero(reinterpret_cast<uint64_t>(d->shards[0]) + ag_off[j] + nb, ag_end - ag_off[j] - nb);
       } else {
-        // K1: this rank's whole padded shard into segment r, alignment gap zeroed.
+        // K1: this rank's whole padded shard into segment r, alignment gap zeroed
+        // (fp32 master shards rounded to bf16 on the way).
         const uint64_t dst = static_cast<uint64_t>(r * ag_seg + ag_off[j]);
-        pack.copy(reinterpret_cast<uint64_t>(d->shards[j]), dst, nb);
+        if (master) pack.narrow(reinterpret_cast<uint64_t>(d->shards[j]), dst, own.c * R);
+        else pack.copy(reinterpret_cast<uint64_t>(d->shards[j]), dst, nb);
         pack.zero(dst + nb, ag_end - ag_off[j] - nb);
       }
     }

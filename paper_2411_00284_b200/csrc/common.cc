@@ -116,6 +116,25 @@ void TableBuilder::scale(uint64_t src, uint64_t dst, int64_t elems) {
   }
 }
 
+// fp32 src (4 B/elem) -> bf16 dst (2 B/elem), round to nearest even.  Vector
+// body: groups of 8 elements (32 B in, 16 B out) when both ends are 16-B
+// aligned; scalar tail.
+void TableBuilder::narrow(uint64_t src, uint64_t dst, int64_t elems, uint32_t flags) {
+  if (elems <= 0) return;
+  bytes_moved += 6 * elems;
+  int64_t body = 0;
+  if (src % 16 == 0 && dst % 16 == 0) body = elems / 8 * 8;
+  const int64_t per_chunk = kChunkBytes / 4;  // elems per chunk (32 KiB of fp32 in)
+  for (int64_t e = 0; e < body; e += per_chunk) {
+    int64_t ne = std::min<int64_t>(per_chunk, body - e);
+    push(chunks, src + 4 * e, dst + 2 * e, static_cast<uint32_t>(ne / 8), OP_NARROW | flags, 16);
+  }
+  for (int64_t e = body; e < elems; e += per_chunk) {
+    int64_t ne = std::min<int64_t>(per_chunk, elems - e);
+    push(chunks, src + 4 * e, dst + 2 * e, static_cast<uint32_t>(ne), OP_NARROW | flags, 4);
+  }
+}
+
 void TableBuilder::peer_reduce(uint64_t src, uint64_t dst, int64_t elems, int eb, int world) {
   if (elems <= 0) return;
   bytes_moved += elems * (static_cast<int64_t>(eb) * world + 4);  // every peer's elements + fp32 write

@@ -74,6 +74,7 @@ enum ChunkOp : uint32_t {
   // unit 16: n groups of 8 bf16 / 4 fp32 elements, unit 2 / 4: n elements
   OP_PEER_REDUCE_BF16 = 4,
   OP_PEER_REDUCE_F32 = 5,
+  OP_NARROW = 6,  // fp32 -> bf16 RNE; unit 16: n groups of 8 elems (32 B in, 16 B out), unit 4: n elems
 };
 // Peer-memory copy (K8): OP_COPY chunks whose src is an offset into peer q's
 // segment, q in op_unit bits 24..31.
@@ -107,6 +108,7 @@ struct TableBuilder {
   void zero(uint64_t dst, int64_t bytes);
   void widen(uint64_t src, uint64_t dst, int64_t elems);  // bf16 -> f32 * s
   void scale(uint64_t src, uint64_t dst, int64_t elems);  // f32 -> f32 * s
+  void narrow(uint64_t src, uint64_t dst, int64_t elems, uint32_t flags = 0);  // f32 -> bf16 RNE
   // K9: rank-order sum over peers of `elems` gradient elements of elem_bytes
   // (2 = bf16, 4 = fp32) at offset src of every peer region -> fp32 at dst
   void peer_reduce(uint64_t src, uint64_t dst, int64_t elems, int elem_bytes, int world);

@@ -240,6 +240,49 @@ __device__ __forceinline__ void scale1(const char* src, char* dst, uint32_t n, f
   for (uint32_t i = threadIdx.x; i < n; i += NT) d[i] = __fmul_rn(s[i], scale);
 }
 
+// Two fp32 -> one bf16x2 word, round to nearest even (cvt.rn.bf16x2.f32 puts
+// its first source in the upper half): `lo` lands at the lower address.
+__device__ __forceinline__ uint32_t narrow2(uint32_t lo, uint32_t hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(hi)), "f"(__uint_as_float(lo)));
+  return r;
+}
+
+// fp32 master shard -> bf16 (mixed precision): n groups of 8 elements,
+// 32 B in (two 16-B loads), 16 B out.
+template <int NT>
+__device__ __forceinline__ void narrow16(const char* src, char* dst, uint32_t n) {
+  const uint4* s = reinterpret_cast<const uint4*>(src) + 2 * threadIdx.x;
+  uint4* d = reinterpret_cast<uint4*>(dst) + threadIdx.x;
+  constexpr int U = kUnroll / 2 > 0 ? kUnroll / 2 : 1;
+  auto pack = [](const uint4& a, const uint4& b) {
+    return make_uint4(narrow2(a.x, a.y), narrow2(a.z, a.w), narrow2(b.x, b.y), narrow2(b.z, b.w));
+  };
+  uint32_t base = 0;
+  for (; base + NT * U <= n; base += NT * U) {
+    uint4 a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a[u] = ld_stream(s + 2 * (base + u * NT));
+      b[u] = ld_stream(s + 2 * (base + u * NT) + 1);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) st_v4(d + base + u * NT, pack(a[u], b[u]));
+  }
+  for (uint32_t i = base + threadIdx.x; i < n; i += NT) {
+    const uint4* si = s - 2 * threadIdx.x + 2 * i;
+    st_v4(d - threadIdx.x + i, pack(ld_stream(si), ld_stream(si + 1)));
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ void narrow1(const char* src, char* dst, uint32_t n) {
+  const float* s = reinterpret_cast<const float*>(src);
+  uint16_t* d = reinterpret_cast<uint16_t*>(dst);
+  for (uint32_t i = threadIdx.x; i < n; i += NT)
+    d[i] = static_cast<uint16_t>(narrow2(__float_as_uint(s[i]), 0u) & 0xFFFFu);
+}
+
 template <bool kSrcRel>
 __device__ __forceinline__ const char* src_of(const Chunk& ch, char* base) {
   return (kSrcRel && !(ch.op_unit & kAbsSrc)) ? base + ch.src : reinterpret_cast<const char*>(ch.src);
@@ -273,6 +316,9 @@ __device__ __forceinline__ void process_chunk(const Chunk& ch, const char* src, 
   } else if (op == OP_WIDEN) {
     if (unit == 16) widen16<NT>(src, dst, ch.n, scale);
     else widen1<NT>(src, dst, ch.n, scale);
+  } else if (op == OP_NARROW) {
+    if (unit == 16) narrow16<NT>(src, dst, ch.n);
+    else narrow1<NT>(src, dst, ch.n);
   } else {
     if (unit == 16) scale16<NT>(src, dst, ch.n, scale);
     else scale1<NT>(src, dst, ch.n, scale);

@@ -72,6 +72,41 @@ def test_bucketing_changes_no_bits(dims, world, seed):
         assert np.array_equal(single[0], f)
 
 
+@given(dims=dims_st, world=st.integers(1, 8), a=st.sampled_from([1, 16]), seed=st.integers(0, 2**31))
+@settings(max_examples=100, deadline=None)
+def test_mixed_precision_allgather_is_rne_cast(dims, world, a, seed):
+    """P:302 master weights: gathered full params == the fp32 masters rounded
+    to bf16, the rounding taken by torch's CPU cast (an independent library
+    routine); zero bytes outside shard data as for bf16 params."""
+    import torch
+    from oracle.collectives import mixed_precision_all_gather
+    masters = _rand_params(dims, np.float32, seed)
+    g, fulls = mixed_precision_all_gather(masters, world, a)
+    for m, f in zip(masters, fulls):
+        ref = torch.from_numpy(m).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+        assert f.dtype == np.uint16 and np.array_equal(f, ref)
+    offs, seg = bucket_layout(dims, world, 2, a)
+    assert g.size == world * seg
+
+
+def test_mixed_precision_allgather_of_bf16_values_is_identity():
+    # a master that holds bf16-representable values gathers to those bf16 bits
+    dims = [(13, 7), (5, 16), (1, 3)]
+    rng = np.random.Generator(np.random.Philox(5))
+    bits16 = [rng.integers(0, 65536, size=d).astype(np.uint16) for d in dims]
+    bits16 = [np.where((b & 0x7F80) == 0x7F80, b & 0x807F, b) for b in bits16]  # drop inf/NaN
+    masters = [bf16.widen(b) for b in bits16]
+    for w in (1, 2, 3, 8):
+        _, fulls = mixed_precision_all_gather_ref(masters, w)
+        for b, f in zip(bits16, fulls):
+            assert np.array_equal(f, b)
+
+
+def mixed_precision_all_gather_ref(masters, world):
+    from oracle.collectives import mixed_precision_all_gather
+    return mixed_precision_all_gather(masters, world, 16)
+
+
 def test_pack_writes_own_segment_only():
     ps = toy_mlp()
     params = [param_tensor(p, "f32", 11 + i) for i, p in enumerate(ps)]
