@@ -286,6 +286,19 @@ fsdp_status fsdp_allgather_bucket(fsdp_ctx* ctx, fsdp_bucket* b, void* ag_stagin
 fsdp_status fsdp_reduce_scatter_bucket(fsdp_ctx* ctx, fsdp_bucket* b, void* rs_staging,
                                        fsdp_stream_t compute, fsdp_stream_t comm, uint32_t flags);
 
+/* Gradient accumulation over micro-batches (the
+ * read-out of P:179 adds instead of overwriting): with on = 1, every later
+ * reduce-scatter of `b` -- fsdp_reduce_scatter_bucket, fsdp_p2p_reduce_scatter_bucket
+ * and the RS of fsdp_run_schedule -- leaves grad_shards[j] = grad_shards[j] +
+ * (this reduce-scatter's averaged shard), one fp32 addition per element;
+ * on = 0 (the default) overwrites.  The mode is latched when the RS is issued
+ * (ISSUE / PACK_RS), so toggle it between reduce-scatters, not between an
+ * ISSUE and its WAIT.  With FSDP_BUCKET_SEGMENT_GRAD_SHARDS and a
+ * communicator an accumulating RS lands in rs_staging and K6 adds it to the
+ * storage (the overwrite mode needs no copy-out there).  Host-only; errors:
+ * NULL bucket, on not 0/1. */
+fsdp_status fsdp_bucket_set_grad_accumulation(fsdp_bucket* b, int32_t on);
+
 /* ------------------------------------------------ 5. fsdp_run_schedule
  * One training step's communication path (Table 6):
  *   reorder on : forward prefetch depth 1 -- AG(k+1) before (default) or after

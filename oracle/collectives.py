@@ -167,6 +167,13 @@ def rs_copyout(rs_out, dims, world, align=16):
     return res
 
 
+def accumulate_grad_shards(existing, new):
+    """Gradient accumulation over micro-batches: the
+    gradient shards read out of this reduce-scatter are added to the shards
+    already held, one fp32 addition per element: existing + new."""
+    return [(e + n).astype(np.float32) for e, n in zip(existing, new)]
+
+
 def bucketed_reduce_scatter(grads_per_rank, world, align=16):
     """Full pipeline for one bucket.  ``grads_per_rank[r]`` is rank r's list
     of full gradients.  Returns (packed inputs, RS outputs, grad shards per

@@ -34,7 +34,8 @@ BUCKET_SEGMENT_SHARDS, BUCKET_SEGMENT_GRAD_SHARDS, BUCKET_FP32_MASTER = 1, 2, 4
 EXPORTED = [
     "fsdp_last_error", "fsdp_abi_version", "fsdp_nccl_get_unique_id", "fsdp_ctx_create",
     "fsdp_ctx_destroy", "fsdp_shard", "fsdp_plan_buckets", "fsdp_layout", "fsdp_bucket_create",
-    "fsdp_bucket_destroy", "fsdp_bucket_query", "fsdp_allgather_bucket", "fsdp_reduce_scatter_bucket",
+    "fsdp_bucket_destroy", "fsdp_bucket_query", "fsdp_bucket_set_grad_accumulation",
+    "fsdp_allgather_bucket", "fsdp_reduce_scatter_bucket",
     "fsdp_run_schedule", "fsdp_proxy_launch", "fsdp_proxy_calibrate",
     "fsdp_p2p_allgather_bucket", "fsdp_p2p_reduce_scatter_bucket", "fsdp_p2p_signal", "fsdp_p2p_wait",
     "fsdp_ipc_alloc", "fsdp_ipc_open", "fsdp_ipc_close", "fsdp_ipc_free",
@@ -140,6 +141,7 @@ _sigs = {
                                      C.POINTER(C.c_int64)]),
     "fsdp_bucket_destroy": (C.c_int, [_P]),
     "fsdp_bucket_query": (C.c_int, [_P, C.POINTER(BucketInfo)]),
+    "fsdp_bucket_set_grad_accumulation": (C.c_int, [_P, C.c_int32]),
     "fsdp_allgather_bucket": (C.c_int, [_P, _P, _P, _P, _P, C.c_uint32]),
     "fsdp_reduce_scatter_bucket": (C.c_int, [_P, _P, _P, _P, _P, C.c_uint32]),
     "fsdp_run_schedule": (C.c_int, [_P, C.POINTER(Schedule), C.POINTER(StepReport)]),

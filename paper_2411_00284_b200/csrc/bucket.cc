@@ -23,6 +23,7 @@ cudaStream_t comm_stream(fsdp_ctx* c, fsdp_stream_t s) {
 
 void destroy_bucket(fsdp_bucket* b) {
   release(&b->ag_pack);
+  release(&b->rs_accum);
   release(&b->ag_unpack);
   release(&b->rs_pack);
   release(&b->rs_copyout);
@@ -100,7 +101,7 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   const bool direct = k == 1 && d->fulls && d->params[0].dim0 % N == 0 &&
                       ag_seg == (d->params[0].dim0 / N) * d->params[0].row_numel * ep;
 
-  TableBuilder pack, unpack, rpack, rcopy, gaps, p2p_ag, p2p_rs;
+  TableBuilder pack, unpack, rpack, rcopy, raccum, gaps, p2p_ag, p2p_rs;
   for (int32_t j = 0; j < k; ++j) {
     const fsdp_param_desc& p = d->params[j];
     const ShardRows own = shard_rows(p.dim0, N, r);
@@ -175,6 +176,9 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
       // K6: own segment r -> fp32 gradient shard [c, R].
       rcopy.copy(static_cast<uint64_t>(r * rs_seg + rs_off[j]),
                  reinterpret_cast<uint64_t>(d->grad_shards[j]), own.c * R * 4);
+      // K6 in accumulation mode: grad shard += own segment (pad rows add +0.0)
+      raccum.accum(static_cast<uint64_t>(r * rs_seg + rs_off[j]),
+                   reinterpret_cast<uint64_t>(d->grad_shards[j]), own.c * R);
     }
   }
   FSDP_CUDA_TRY(cudaSetDevice(ctx->device));
@@ -217,6 +221,7 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   if (st == FSDP_OK) st = upload(unpack, &b->ag_unpack);
   if (st == FSDP_OK) st = upload(rpack, &b->rs_pack);
   if (st == FSDP_OK) st = upload(rcopy, &b->rs_copyout);
+  if (st == FSDP_OK) st = upload(raccum, &b->rs_accum);
   if (st == FSDP_OK && N <= kMaxPeers) st = upload(p2p_ag, &b->p2p_ag);
   if (st == FSDP_OK && N <= kMaxPeers) st = upload(p2p_rs, &b->p2p_rs);
   for (cudaEvent_t* e : {&b->ev_ag_packed, &b->ev_ag_done, &b->ev_rs_packed, &b->ev_rs_done}) {
@@ -324,6 +329,7 @@ fsdp_status ag_unpack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t c
 
 fsdp_status rs_pack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches) {
   const float inv = 1.0f / static_cast<float>(c->world);  // fl32(1/N), correctly rounded
+  b->rs_accum_issued = b->grad_accumulate;  // latched for the matching collective / copy-out
   FSDP_CUDA_TRY(launch_table(KK_RS_PACK, b->rs_pack, staging, inv, cs, c->max_ctas));
   if (b->rs_pack.n && launches) ++*launches;
   if (comm_on(c, with_comm)) FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_packed, cs));
@@ -335,7 +341,8 @@ fsdp_status rs_collective(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream
   FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_rs_packed, 0));
   // fp32 sum of pre-scaled chunks; in place (recvbuff = sendbuff + rank *
   // recvcount) or straight into segment-layout gradient-shard storage.
-  char* recv = b->rs_zero_copy ? b->gshard_seg : staging + c->rank * b->rs_seg;
+  // (accumulation needs the result beside the shards, so it goes to staging)
+  char* recv = (b->rs_zero_copy && !b->rs_accum_issued) ? b->gshard_seg : staging + c->rank * b->rs_seg;
   FSDP_NCCL_TRY(ncclReduceScatter(staging, recv, static_cast<size_t>(b->rs_seg / 4), ncclFloat32, ncclSum,
                                   c->comm, ms));
   FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_done, ms));
@@ -354,6 +361,11 @@ fsdp_status rs_wait(fsdp_ctx* c, fsdp_bucket* b, cudaStream_t cs, bool with_comm
 fsdp_status rs_copyout(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches) {
   // with a communicator and segment-layout storage the collective already
   // wrote the result in place: nothing to copy
+  if (b->rs_accum_issued) {
+    FSDP_CUDA_TRY(launch_table(KK_RS_COPYOUT, b->rs_accum, staging, 1.0f, cs, c->max_ctas));
+    if (b->rs_accum.n && launches) ++*launches;
+    return FSDP_OK;
+  }
   if (b->rs_zero_copy && comm_on(c, with_comm)) return FSDP_OK;
   FSDP_CUDA_TRY(launch_table(KK_RS_COPYOUT, b->rs_copyout, staging, 1.0f, cs, c->max_ctas));
   if (b->rs_copyout.n && launches) ++*launches;
@@ -410,5 +422,12 @@ extern "C" fsdp_status fsdp_reduce_scatter_bucket(fsdp_ctx* c, fsdp_bucket* b, v
     FSDP_TRY(rs_wait(c, b, cs, true));
     FSDP_TRY(rs_copyout(c, b, st, cs, true, nullptr));
   }
+  return FSDP_OK;
+}
+
+extern "C" fsdp_status fsdp_bucket_set_grad_accumulation(fsdp_bucket* b, int32_t on) {
+  if (!b) return fail(FSDP_ERR_INVALID_ARG, "NULL bucket");
+  if (on != 0 && on != 1) return fail(FSDP_ERR_INVALID_ARG, "on must be 0 or 1");
+  b->grad_accumulate = on != 0;
   return FSDP_OK;
 }

@@ -135,6 +135,23 @@ void TableBuilder::narrow(uint64_t src, uint64_t dst, int64_t elems, uint32_t fl
   }
 }
 
+// fp32 dst = dst + src (gradient accumulation): 12 B per element.
+void TableBuilder::accum(uint64_t src, uint64_t dst, int64_t elems) {
+  if (elems <= 0) return;
+  bytes_moved += 12 * elems;
+  int64_t body = 0;
+  if (src % 16 == 0 && dst % 16 == 0) body = elems / 4 * 4;
+  const int64_t per_chunk = kChunkBytes / 4;
+  for (int64_t e = 0; e < body; e += per_chunk) {
+    int64_t ne = std::min<int64_t>(per_chunk, body - e);
+    push(chunks, src + 4 * e, dst + 4 * e, static_cast<uint32_t>(ne / 4), OP_ACCUM, 16);
+  }
+  for (int64_t e = body; e < elems; e += per_chunk) {
+    int64_t ne = std::min<int64_t>(per_chunk, elems - e);
+    push(chunks, src + 4 * e, dst + 4 * e, static_cast<uint32_t>(ne), OP_ACCUM, 4);
+  }
+}
+
 void TableBuilder::peer_reduce(uint64_t src, uint64_t dst, int64_t elems, int eb, int world) {
   if (elems <= 0) return;
   bytes_moved += elems * (static_cast<int64_t>(eb) * world + 4);  // every peer's elements + fp32 write

@@ -75,6 +75,7 @@ enum ChunkOp : uint32_t {
   OP_PEER_REDUCE_BF16 = 4,
   OP_PEER_REDUCE_F32 = 5,
   OP_NARROW = 6,  // fp32 -> bf16 RNE; unit 16: n groups of 8 elems (32 B in, 16 B out), unit 4: n elems
+  OP_ACCUM = 7,   // fp32 dst = dst + src;  unit 16: n groups of 4 elems, unit 4: n elems
 };
 // Peer-memory copy (K8): OP_COPY chunks whose src is an offset into peer q's
 // segment, q in op_unit bits 24..31.
@@ -109,6 +110,7 @@ struct TableBuilder {
   void widen(uint64_t src, uint64_t dst, int64_t elems);  // bf16 -> f32 * s
   void scale(uint64_t src, uint64_t dst, int64_t elems);  // f32 -> f32 * s
   void narrow(uint64_t src, uint64_t dst, int64_t elems, uint32_t flags = 0);  // f32 -> bf16 RNE
+  void accum(uint64_t src, uint64_t dst, int64_t elems);  // f32 dst += src
   // K9: rank-order sum over peers of `elems` gradient elements of elem_bytes
   // (2 = bf16, 4 = fp32) at offset src of every peer region -> fp32 at dst
   void peer_reduce(uint64_t src, uint64_t dst, int64_t elems, int elem_bytes, int world);
@@ -130,7 +132,7 @@ cudaError_t launch_table(KernelKind kind, const DevTable& t, char* base, float s
 cudaError_t launch_proxy(int64_t iters, int grid, int smem, float* sink, cudaStream_t s);
 cudaError_t launch_p2p_allgather(const DevTable& t, const PeerTable& pt, cudaStream_t s, int max_ctas);
 cudaError_t launch_p2p_reduce_scatter(const DevTable& t, const PeerTable& pt, int world, float scale,
-                                      cudaStream_t s, int max_ctas);
+                                      bool accumulate, cudaStream_t s, int max_ctas);
 cudaError_t launch_p2p_signal(const PeerTable& slots, int world, uint64_t value, cudaStream_t s);
 cudaError_t launch_p2p_wait(const void* flags, int world, uint64_t value, int64_t timeout_ns, int* err,
                             cudaStream_t s);
@@ -149,6 +151,8 @@ fsdp_status ag_collective(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream
 fsdp_status ag_wait(fsdp_ctx* c, fsdp_bucket* b, cudaStream_t cs, bool with_comm);
 fsdp_status ag_unpack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, int* launches);
 fsdp_status rs_pack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches);
+// The gradient-accumulation mode (fsdp_bucket_set_grad_accumulation) is
+// latched by rs_pack and used by the matching rs_collective / rs_copyout.
 fsdp_status rs_collective(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t ms, bool with_comm, int* colls);
 fsdp_status rs_wait(fsdp_ctx* c, fsdp_bucket* b, cudaStream_t cs, bool with_comm);
 fsdp_status rs_copyout(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches);
@@ -192,6 +196,9 @@ struct fsdp_bucket {
   std::vector<fsdp_param_desc> members;
   std::vector<void*> fulls, grads;
   fsdp::DevTable ag_pack, ag_unpack, rs_pack, rs_copyout;
+  fsdp::DevTable rs_accum;           // K6 variant: grad_shards += own segment (accumulation)
+  bool grad_accumulate = false;      // fsdp_bucket_set_grad_accumulation
+  bool rs_accum_issued = false;      // mode latched by the last rs_pack
   fsdp::DevTable p2p_ag, p2p_rs;  // K8 / K9 tables (peer-memory path)
   cudaEvent_t ev_ag_packed = nullptr, ev_ag_done = nullptr;
   cudaEvent_t ev_rs_packed = nullptr, ev_rs_done = nullptr;

@@ -2,10 +2,12 @@
 // path has no dense contraction).
 //
 //   K0 fsdp_shard_kernel       full param -> padded dim-0 shard
-//   K1 fsdp_ag_pack_kernel     shards -> rank segment of the AG bucket  ("flattens and concatenates")
+//   K1 fsdp_ag_pack_kernel     shards -> rank segment of the AG bucket  ("flattens and concatenates";
+//                              fp32 master shards rounded to bf16 on the way)
 //   K3 fsdp_ag_unpack_kernel   gathered bucket -> full params           ("copy out ... original tensor size")
 //   K4 fsdp_rs_pack_kernel     full grads -> rank-major fp32 chunks x 1/N ("splits ... into chunks", P:302/311 fp32 avg)
-//   K6 fsdp_rs_copyout_kernel  own RS segment -> grad shards            ("read out from RS12")
+//   K6 fsdp_rs_copyout_kernel  own RS segment -> grad shards            ("read out from RS12";
+//                              or added to them: gradient accumulation)
 //   K7 fsdp_compute_proxy_kernel  calibrated stand-in for layer compute (measurement device)
 //
 // Every data kernel walks a host-built table of <= kChunkBytes chunks; one CTA
@@ -283,6 +285,41 @@ __device__ __forceinline__ void narrow1(const char* src, char* dst, uint32_t n) 
     d[i] = static_cast<uint16_t>(narrow2(__float_as_uint(s[i]), 0u) & 0xFFFFu);
 }
 
+// Gradient accumulation: fp32 dst = dst + src, one rounding per element.
+__device__ __forceinline__ uint4 add4(const uint4& a, const uint4& b) {
+  return make_uint4(__float_as_uint(__fadd_rn(__uint_as_float(a.x), __uint_as_float(b.x))),
+                    __float_as_uint(__fadd_rn(__uint_as_float(a.y), __uint_as_float(b.y))),
+                    __float_as_uint(__fadd_rn(__uint_as_float(a.z), __uint_as_float(b.z))),
+                    __float_as_uint(__fadd_rn(__uint_as_float(a.w), __uint_as_float(b.w))));
+}
+
+template <int NT>
+__device__ __forceinline__ void accum16(const char* src, char* dst, uint32_t n) {
+  const uint4* s = reinterpret_cast<const uint4*>(src) + threadIdx.x;
+  uint4* d = reinterpret_cast<uint4*>(dst) + threadIdx.x;
+  constexpr int U = kUnroll / 2 > 0 ? kUnroll / 2 : 1;
+  uint32_t base = 0;
+  for (; base + NT * U <= n; base += NT * U) {
+    uint4 a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a[u] = *(d + base + u * NT);  // existing shard: plain (cached) load, it is rewritten next
+      b[u] = ld_stream(s + base + u * NT);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) st_v4(d + base + u * NT, add4(a[u], b[u]));
+  }
+  for (uint32_t i = base + threadIdx.x; i < n; i += NT)
+    st_v4(d - threadIdx.x + i, add4(*(d - threadIdx.x + i), ld_stream(s - threadIdx.x + i)));
+}
+
+template <int NT>
+__device__ __forceinline__ void accum1(const char* src, char* dst, uint32_t n) {
+  const float* s = reinterpret_cast<const float*>(src);
+  float* d = reinterpret_cast<float*>(dst);
+  for (uint32_t i = threadIdx.x; i < n; i += NT) d[i] = __fadd_rn(d[i], s[i]);
+}
+
 template <bool kSrcRel>
 __device__ __forceinline__ const char* src_of(const Chunk& ch, char* base) {
   return (kSrcRel && !(ch.op_unit & kAbsSrc)) ? base + ch.src : reinterpret_cast<const char*>(ch.src);
@@ -319,6 +356,9 @@ __device__ __forceinline__ void process_chunk(const Chunk& ch, const char* src, 
   } else if (op == OP_NARROW) {
     if (unit == 16) narrow16<NT>(src, dst, ch.n);
     else narrow1<NT>(src, dst, ch.n);
+  } else if (op == OP_ACCUM) {
+    if (unit == 16) accum16<NT>(src, dst, ch.n);
+    else accum1<NT>(src, dst, ch.n);
   } else {
     if (unit == 16) scale16<NT>(src, dst, ch.n, scale);
     else scale1<NT>(src, dst, ch.n, scale);
@@ -506,14 +546,30 @@ __device__ __forceinline__ void acc_vec(float (&acc)[8], const uint4& v, float s
   }
 }
 
-// K9 body: this rank's gradient shard = rank-order fp32 sum over every peer.
-// Vector chunks: n groups of 8 bf16 (or 4 fp32) elements; 4 peers' loads in
-// flight per thread, added strictly in rank order.
-// Compile-time world: all W peers' 16-B loads are issued before the first add
-// (W loads in flight per thread), then added strictly in rank order.
+// K9 body: this rank's gradient shard = rank-order fp32 sum over every peer
+// (with `accum`: the existing shard + that sum, gradient accumulation).
+// Vector chunks: n groups of 8 bf16 (or 4 fp32) elements.  Compile-time world:
+// all W peers' 16-B loads are issued before the first add (W loads in flight
+// per thread), then added strictly in rank order.
+__device__ __forceinline__ void add_existing(float (&acc)[8], const char* dst, uint32_t i, bool bf16) {
+  const uint4* d = reinterpret_cast<const uint4*>(dst) + (bf16 ? 2 * i : i);
+  const uint4 a = d[0];
+  acc[0] = __fadd_rn(__uint_as_float(a.x), acc[0]);
+  acc[1] = __fadd_rn(__uint_as_float(a.y), acc[1]);
+  acc[2] = __fadd_rn(__uint_as_float(a.z), acc[2]);
+  acc[3] = __fadd_rn(__uint_as_float(a.w), acc[3]);
+  if (bf16) {
+    const uint4 b = d[1];
+    acc[4] = __fadd_rn(__uint_as_float(b.x), acc[4]);
+    acc[5] = __fadd_rn(__uint_as_float(b.y), acc[5]);
+    acc[6] = __fadd_rn(__uint_as_float(b.z), acc[6]);
+    acc[7] = __fadd_rn(__uint_as_float(b.w), acc[7]);
+  }
+}
+
 template <bool kBf16, int W>
 __device__ __forceinline__ void peer_reduce16_w(const PeerTable& pt, uint64_t off, char* dst, uint32_t n,
-                                                float scale) {
+                                                float scale, bool accum) {
   for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
     const uint64_t o = off + 16ull * i;
     uint4 v[W];
@@ -522,6 +578,7 @@ __device__ __forceinline__ void peer_reduce16_w(const PeerTable& pt, uint64_t of
     float acc[8];
 #pragma unroll
     for (int q = 0; q < W; ++q) acc_vec<kBf16>(acc, v[q], scale, q == 0);
+    if (accum) add_existing(acc, dst, i, kBf16);
     uint4 a, b;
     a.x = __float_as_uint(acc[0]); a.y = __float_as_uint(acc[1]); a.z = __float_as_uint(acc[2]);
     a.w = __float_as_uint(acc[3]);
@@ -545,13 +602,13 @@ __device__ __forceinline__ void peer_reduce16_w(const PeerTable& pt, uint64_t of
 
 template <bool kBf16>
 __device__ __forceinline__ void peer_reduce16(const PeerTable& pt, int world, uint64_t off, char* dst,
-                                              uint32_t n, float scale) {
+                                              uint32_t n, float scale, bool accum) {
   if (FSDP_K9_TEMPLATED) {
     switch (world) {
-      case 1: return peer_reduce16_w<kBf16, 1>(pt, off, dst, n, scale);
-      case 2: return peer_reduce16_w<kBf16, 2>(pt, off, dst, n, scale);
-      case 4: return peer_reduce16_w<kBf16, 4>(pt, off, dst, n, scale);
-      case 8: return peer_reduce16_w<kBf16, 8>(pt, off, dst, n, scale);
+      case 1: return peer_reduce16_w<kBf16, 1>(pt, off, dst, n, scale, accum);
+      case 2: return peer_reduce16_w<kBf16, 2>(pt, off, dst, n, scale, accum);
+      case 4: return peer_reduce16_w<kBf16, 4>(pt, off, dst, n, scale, accum);
+      case 8: return peer_reduce16_w<kBf16, 8>(pt, off, dst, n, scale, accum);
       default: break;
     }
   }
@@ -568,6 +625,7 @@ __device__ __forceinline__ void peer_reduce16(const PeerTable& pt, int world, ui
       for (int u = 0; u < 4; ++u)
         if (q0 + u < world) acc_vec<kBf16>(acc, v[u], scale, q0 + u == 0);
     }
+    if (accum) add_existing(acc, dst, i, kBf16);
     uint4 a, b;
     a.x = __float_as_uint(acc[0]); a.y = __float_as_uint(acc[1]); a.z = __float_as_uint(acc[2]);
     a.w = __float_as_uint(acc[3]);
@@ -592,7 +650,7 @@ __device__ __forceinline__ void peer_reduce16(const PeerTable& pt, int world, ui
 
 template <bool kBf16>
 __device__ __forceinline__ void peer_reduce1(const PeerTable& pt, int world, uint64_t off, char* dst, uint32_t n,
-                                             float scale) {
+                                             float scale, bool accum) {
   float* d = reinterpret_cast<float*>(dst);
   for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
     float acc = 0.f;
@@ -606,24 +664,29 @@ __device__ __forceinline__ void peer_reduce1(const PeerTable& pt, int world, uin
       const float t = __fmul_rn(x, scale);
       acc = q == 0 ? t : __fadd_rn(acc, t);
     }
-    d[i] = acc;
+    d[i] = accum ? __fadd_rn(d[i], acc) : acc;
   }
 }
 
 __device__ __forceinline__ void run_peer_reduce(const Chunk* __restrict__ tab, int n, const PeerTable& pt, int world,
-                                                float scale) {
+                                                float scale, bool accum) {
   for (int c = blockIdx.x; c < n; c += gridDim.x) {
     const Chunk ch = tab[c];
     const uint32_t op = ch.op_unit & 0xFFu, unit = (ch.op_unit >> 8) & 0xFFu;
     char* dst = reinterpret_cast<char*>(ch.dst);
-    if (op == OP_ZERO) {
+    if (op == OP_ZERO && accum) {
+      // pad rows while accumulating: dst + (+0.0), like every other element
+      float* d = reinterpret_cast<float*>(dst);
+      const uint32_t nf = ch.n * unit / 4;
+      for (uint32_t i = threadIdx.x; i < nf; i += kThreads) d[i] = __fadd_rn(d[i], 0.0f);
+    } else if (op == OP_ZERO) {
       process_chunk<kThreads>(ch, nullptr, dst, 1.0f);
     } else if (op == OP_PEER_REDUCE_BF16) {
-      if (unit == 16) peer_reduce16<true>(pt, world, ch.src, dst, ch.n, scale);
-      else peer_reduce1<true>(pt, world, ch.src, dst, ch.n, scale);
+      if (unit == 16) peer_reduce16<true>(pt, world, ch.src, dst, ch.n, scale, accum);
+      else peer_reduce1<true>(pt, world, ch.src, dst, ch.n, scale, accum);
     } else {
-      if (unit == 16) peer_reduce16<false>(pt, world, ch.src, dst, ch.n, scale);
-      else peer_reduce1<false>(pt, world, ch.src, dst, ch.n, scale);
+      if (unit == 16) peer_reduce16<false>(pt, world, ch.src, dst, ch.n, scale, accum);
+      else peer_reduce1<false>(pt, world, ch.src, dst, ch.n, scale, accum);
     }
   }
 }
@@ -636,8 +699,8 @@ __global__ void FSDP_LSU_BOUNDS fsdp_p2p_allgather_kernel(const Chunk* tab, int 
 }
 // K9: fused gradient widen + 1/N + reduce-scatter + copy-out over peer memory.
 __global__ void __launch_bounds__(kThreads, FSDP_K9_MIN_BLOCKS) fsdp_p2p_reduce_scatter_kernel(const Chunk* tab, int n, const __grid_constant__ PeerTable pt, int world,
-                                                               float scale) {
-  run_peer_reduce(tab, n, pt, world, scale);
+                                                               float scale, int accum) {
+  run_peer_reduce(tab, n, pt, world, scale, accum != 0);
 }
 
 __global__ void fsdp_p2p_signal_kernel(const __grid_constant__ PeerTable slots, int world, unsigned long long value) {
@@ -754,10 +817,11 @@ cudaError_t launch_p2p_allgather(const DevTable& t, const PeerTable& pt, cudaStr
 }
 
 cudaError_t launch_p2p_reduce_scatter(const DevTable& t, const PeerTable& pt, int world, float scale,
-                                      cudaStream_t s, int max_ctas) {
+                                      bool accumulate, cudaStream_t s, int max_ctas) {
   if (t.n == 0) return cudaSuccess;
   (void)cudaGetLastError();
-  fsdp_p2p_reduce_scatter_kernel<<<t.n < max_ctas ? t.n : max_ctas, kThreads, 0, s>>>(t.d, t.n, pt, world, scale);
+  fsdp_p2p_reduce_scatter_kernel<<<t.n < max_ctas ? t.n : max_ctas, kThreads, 0, s>>>(t.d, t.n, pt, world, scale,
+                                                                                     accumulate ? 1 : 0);
   return cudaGetLastError();
 }
 

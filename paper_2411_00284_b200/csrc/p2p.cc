@@ -47,8 +47,8 @@ extern "C" fsdp_status fsdp_p2p_reduce_scatter_bucket(fsdp_ctx* c, fsdp_bucket* 
   FSDP_TRY(peer_table(c, peer_grads, &pt, false));
   FSDP_CUDA_TRY(cudaSetDevice(c->device));
   const float inv = 1.0f / static_cast<float>(c->world);  // fl32(1/N)
-  FSDP_CUDA_TRY(launch_p2p_reduce_scatter(b->p2p_rs, pt, c->world, inv, static_cast<cudaStream_t>(stream),
-                                          c->max_ctas));
+  FSDP_CUDA_TRY(launch_p2p_reduce_scatter(b->p2p_rs, pt, c->world, inv, b->grad_accumulate,
+                                          static_cast<cudaStream_t>(stream), c->max_ctas));
   return FSDP_OK;
 }
 

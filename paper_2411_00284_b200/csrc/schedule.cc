@@ -362,8 +362,8 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
             FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_rs_packed, 0));
             FSDP_TRY(p2p_wait(pp->ready_flags, epoch(o.bucket), ms));
             const float inv = 1.0f / static_cast<float>(ctx->world);
-            FSDP_CUDA_TRY(launch_p2p_reduce_scatter(b->p2p_rs, peer_row(pp->rs_peers, o.bucket), ctx->world, inv, ms,
-                                                    ctx->max_ctas));
+            FSDP_CUDA_TRY(launch_p2p_reduce_scatter(b->p2p_rs, peer_row(pp->rs_peers, o.bucket), ctx->world, inv,
+                                                    b->grad_accumulate, ms, ctx->max_ctas));
             ++launches;
             FSDP_TRY(p2p_signal(done_slots, epoch(o.bucket), ms));  // done reading peers' b
             FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_done, ms));

@@ -114,6 +114,11 @@ class Bucket:
         self.h = h
         self.ag_seg, self.rs_seg = ag.value, rs.value
 
+    def set_grad_accumulation(self, on):
+        """fsdp_bucket_set_grad_accumulation: later reduce-scatters add into
+        the gradient shards (on) or overwrite them (off, the default)."""
+        check(L.lib.fsdp_bucket_set_grad_accumulation(self.h, 1 if on else 0))
+
     def query(self):
         """fsdp_bucket_query: segment sizes, zero-copy flags, per-kernel
         algorithmic bytes per launch (K1, K3, K4, K6; 0 = not launched)."""

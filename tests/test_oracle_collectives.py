@@ -194,3 +194,39 @@ def test_llama_block_rs_sample():
     small = [type(p)(p.name, p.dim0, min(p.row_numel, 8), p.module_id) for p in ps]
     g = [[grad_tensor(p, "bf16", 5, r) for p in small] for r in range(8)]
     _check_rs(g, 8, 16, exact=False)
+
+
+@given(dims=dims_st, seed=st.integers(0, 2**31))
+@settings(max_examples=100, deadline=None)
+def test_accumulate_is_correctly_rounded_sum(dims, seed):
+    # fp32 a + b, against the exact sum rounded once: the float64 sum of two
+    # fp32 values rounded to fp32 (53 >= 2*24 + 2 bits: double rounding is
+    # innocuous for addition)
+    from oracle.collectives import accumulate_grad_shards
+    rng = np.random.Generator(np.random.Philox(seed))
+    a = [(rng.standard_normal((d, r)) * 10.0 ** rng.integers(-30, 30)).astype(np.float32) for d, r in dims]
+    b = [rng.standard_normal((d, r), dtype=np.float32) for d, r in dims]
+    for x, y, z in zip(a, b, accumulate_grad_shards(a, b)):
+        want = (x.astype(np.float64) + y.astype(np.float64)).astype(np.float32)
+        assert np.array_equal(z.view(np.uint32), want.view(np.uint32))
+
+
+def test_accumulated_micro_batches_equal_exact_mean_sum():
+    # k micro-batches of exactly representable gradients at N = 4: the
+    # accumulated shards equal sum_m mean_r g_{m,r}, computed in float64
+    from oracle.collectives import accumulate_grad_shards
+    dims, world = [(37, 5), (8, 16), (3, 1)], 4
+    rng = np.random.Generator(np.random.Philox(11))
+    acc = None
+    total = [np.zeros(d) for d in dims]
+    for m in range(5):
+        g = [[(rng.integers(-256, 257, size=d).astype(np.float32) * np.float32(2 ** -8)) for d in dims]
+             for _ in range(world)]
+        _, _, shards = bucketed_reduce_scatter(g, world)
+        acc = shards if acc is None else [accumulate_grad_shards(a, s) for a, s in zip(acc, shards)]
+        for j in range(len(dims)):
+            total[j] += sum(g[r][j].astype(np.float64) for r in range(world)) / world
+    for q in range(world):
+        for j, (d, r) in enumerate(dims):
+            want = shard(total[j].astype(np.float32), world, q)
+            assert np.array_equal(acc[q][j].view(np.uint32), want.view(np.uint32))
