@@ -71,6 +71,9 @@ def parse():
     ap.add_argument("--collective", default="nccl", choices=["nccl", "p2p"],
                     help="nccl: pack + NCCL + copy-out (the paper's bucketing); p2p: fused peer-memory "
                          "kernels K8/K9 (1 GPU: the 7 peers are simulated as separate buffers)")
+    ap.add_argument("--no-fused-leg", action="store_true",
+                    help="N=1 with --collective nccl: skip the extra run of the fused peer-memory mode whose "
+                         "summary is reported under 'fused_p2p'")
     return ap.parse_args()
 
 
@@ -207,6 +210,22 @@ def run_reference(args, rank):
 
 
 # -------------------------------------------------------------------- ours
+def fused_leg(args):
+    """bench.py --collective p2p at N = 1 on the same workload (child process)."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--collective", "p2p", "--steps", str(args.steps),
+           "--warmup", str(args.warmup), "--no-e2e", "--no-cpu-baseline", "--no-fused-leg",
+           "--predict-tokens", "0", "--plan", args.plan, "--model", args.model, "--sim-world", str(args.sim_world)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        d = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    except Exception as e:  # reported, never fatal to the headline
+        return {"error": "%s: %s" % (type(e).__name__, str(e)[:200])}
+    return {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"],
+            "collective": d["config"]["collective"], "kernels": d["kernels"], "roofline": d["roofline"],
+            "gpu_launches": d["gpu_launches"], "p2p_wait_timeouts": d["p2p_wait_timeouts"],
+            "how": "bench.py --collective p2p (same workload, same K/W, own process)"}
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -472,6 +491,13 @@ def main():
         cpu = {"value": round(v, 3), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc,
                "seconds": round(dt, 2), "host_cpus": os.cpu_count()}
 
+    # the fused peer-memory path (K8/K9) on the same
+    # workload, in a child process of its own (separate allocations and
+    # timings), summarised beside the headline
+    fused = None
+    if rank == 0 and not multi and not p2p and not args.no_fused_leg:
+        fused = fused_leg(args)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": args.gpus,
@@ -512,6 +538,7 @@ def main():
                          "algorithmic_bytes_per_launch": kbytes[dom] // max(1, klaunch[dom])},
             "zero_copy": st.zero_copy(),
             "p2p_wait_timeouts": int(st.p2p_err.item()) if p2p else None,
+            "fused_p2p": fused,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
         }
