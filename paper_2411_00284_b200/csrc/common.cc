@@ -230,8 +230,14 @@ fsdp_status fsdp_ctx_create(fsdp_ctx** out, int32_t world, int32_t rank, int32_t
   c->sm_count = device_sm_count(cuda_device);
   if (c->sm_count <= 0) c->sm_count = 148;
   c->max_ctas = c->sm_count * FSDP_CTAS_PER_SM;
-  cudaError_t e = cudaMalloc(&c->sink, 4096 * sizeof(float));
+  // proxy sink (4096 floats) followed by the fused-K9 grid counter (zeroed)
+  cudaError_t e = cudaMalloc(&c->sink, 4096 * sizeof(float) + 256);
+  if (e == cudaSuccess) {
+    c->p2p_counter = reinterpret_cast<unsigned int*>(c->sink + 4096);
+    e = cudaMemset(c->p2p_counter, 0, 256);
+  }
   if (e != cudaSuccess) {
+    if (c->sink) cudaFree(c->sink);
     delete c;
     return fail(FSDP_ERR_CUDA, std::string("cudaMalloc sink: ") + cudaGetErrorString(e));
   }

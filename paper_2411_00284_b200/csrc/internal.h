@@ -64,6 +64,14 @@ void layout(const fsdp_param_desc* m, int32_t k, int32_t world, int64_t elem_byt
 #define FSDP_CTAS_PER_SM 1024
 #endif
 constexpr uint32_t kChunkBytes = FSDP_CHUNK_KB * 1024;
+#ifndef FSDP_P2P_FUSED_SYNC
+// Scheduled peer-memory RS: epoch wait + signal fused into K9 (1) or separate
+// 1-warp launches around it (0, default).  Measured equal step time on one
+// B200 (13.57 vs 13.52 ms, profiles/r01_summary.md); the separate wait is kept
+// because a fused K9 waiting for a late peer would hold every SM spinning and
+// starve this rank's compute stream, while a 1-warp wait kernel does not.
+#define FSDP_P2P_FUSED_SYNC 0
+#endif
 
 enum ChunkOp : uint32_t {
   OP_COPY = 0,   // n units of `unit` bytes
@@ -131,8 +139,20 @@ cudaError_t launch_table(KernelKind kind, const DevTable& t, char* base, float s
                          int max_ctas);
 cudaError_t launch_proxy(int64_t iters, int grid, int smem, float* sink, cudaStream_t s);
 cudaError_t launch_p2p_allgather(const DevTable& t, const PeerTable& pt, cudaStream_t s, int max_ctas);
+// Epoch handshake fused into K9 (scheduled step): wait for wait_flags[q] >=
+// wait_value before reading, store signal_value into every signal_slots[q]
+// once the whole grid is done; counter: a zeroed device word per stream.
+struct P2PSync {
+  const unsigned long long* wait_flags;
+  unsigned long long wait_value;
+  long long timeout_ns;
+  int* err;
+  PeerTable signal_slots;
+  unsigned long long signal_value;
+  unsigned int* counter;  // NULL = no fused handshake
+};
 cudaError_t launch_p2p_reduce_scatter(const DevTable& t, const PeerTable& pt, int world, float scale,
-                                      bool accumulate, cudaStream_t s, int max_ctas);
+                                      bool accumulate, cudaStream_t s, int max_ctas, const P2PSync* sync = nullptr);
 cudaError_t launch_p2p_signal(const PeerTable& slots, int world, uint64_t value, cudaStream_t s);
 cudaError_t launch_p2p_wait(const void* flags, int world, uint64_t value, int64_t timeout_ns, int* err,
                             cudaStream_t s);
@@ -172,6 +192,7 @@ struct fsdp_ctx {
   int sm_count = 148;
   int max_ctas = 148 * 8;
   float* sink = nullptr;
+  unsigned int* p2p_counter = nullptr;  // fused K9 handshake (zeroed; comm stream only)
   std::vector<cudaEvent_t> timing_events;  // pool for FSDP_SCHED_TIMING
   std::vector<cudaEvent_t> io_events;      // pool for host I/O ordering (fsdp_host_io)
   cudaStream_t own_h2d = nullptr, own_d2h = nullptr;

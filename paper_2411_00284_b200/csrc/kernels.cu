@@ -697,24 +697,13 @@ __device__ __forceinline__ void run_peer_reduce(const Chunk* __restrict__ tab, i
 __global__ void FSDP_LSU_BOUNDS fsdp_p2p_allgather_kernel(const Chunk* tab, int n, const __grid_constant__ PeerTable pt) {
   run_peer_copy(tab, n, pt);
 }
-// K9: fused gradient widen + 1/N + reduce-scatter + copy-out over peer memory.
-__global__ void __launch_bounds__(kThreads, FSDP_K9_MIN_BLOCKS) fsdp_p2p_reduce_scatter_kernel(const Chunk* tab, int n, const __grid_constant__ PeerTable pt, int world,
-                                                               float scale, int accum) {
-  run_peer_reduce(tab, n, pt, world, scale, accum != 0);
-}
-
-__global__ void fsdp_p2p_signal_kernel(const __grid_constant__ PeerTable slots, int world, unsigned long long value) {
-  if (threadIdx.x != 0) return;
-  __threadfence_system();
-  for (int q = 0; q < world; ++q) {
-    unsigned long long* p = reinterpret_cast<unsigned long long*>(const_cast<char*>(slots.p[q]));
-    if (p) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(value) : "memory");
-  }
-}
-
-__global__ void fsdp_p2p_wait_kernel(const unsigned long long* flags, int world, unsigned long long value,
-                                     long long timeout_ns, int* err) {
-  const int q = threadIdx.x;
+namespace {
+// Spin (lanes q < world of the calling warp) until flags[q] >= value at system
+// scope, or timeout_ns elapses (then *err = 1 and return: the caller proceeds
+// rather than hang).
+__device__ __forceinline__ void wait_flags(const unsigned long long* flags, int world, unsigned long long value,
+                                           long long timeout_ns, int* err) {
+  const int q = threadIdx.x & 31;
   bool timed_out = false;
   if (q < world) {
     unsigned long long t0, t;
@@ -732,6 +721,52 @@ __global__ void fsdp_p2p_wait_kernel(const unsigned long long* flags, int world,
     }
   }
   if (__any_sync(0xFFFFFFFFu, timed_out) && q == 0 && err) *err = 1;
+}
+
+__device__ __forceinline__ void store_flags(const PeerTable& slots, int world, unsigned long long value) {
+  for (int q = 0; q < world; ++q) {
+    unsigned long long* p = reinterpret_cast<unsigned long long*>(const_cast<char*>(slots.p[q]));
+    if (p) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(value) : "memory");
+  }
+}
+}  // namespace
+
+// K9: fused gradient widen + 1/N + reduce-scatter + copy-out over peer memory.
+// With sync.counter set (the scheduled step) the epoch handshake is fused in
+// too: every CTA first waits for the peers' "gradients ready" flags, and the
+// last CTA to finish publishes "done reading" to every peer -- no separate
+// wait / signal launches around the reduction.
+__global__ void __launch_bounds__(kThreads, FSDP_K9_MIN_BLOCKS) fsdp_p2p_reduce_scatter_kernel(
+    const Chunk* tab, int n, const __grid_constant__ PeerTable pt, int world, float scale, int accum,
+    const __grid_constant__ P2PSync sync) {
+  if (sync.counter) {
+    if (threadIdx.x < 32) wait_flags(sync.wait_flags, world, sync.wait_value, sync.timeout_ns, sync.err);
+    __syncthreads();
+  }
+  run_peer_reduce(tab, n, pt, world, scale, accum != 0);
+  if (sync.counter) {
+    __syncthreads();  // every thread of this CTA is done reading peer memory
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned int prev = atomicAdd(sync.counter, 1u);
+      if (prev == gridDim.x - 1) {  // last CTA: all reads of the grid are done
+        __threadfence_system();
+        store_flags(sync.signal_slots, world, sync.signal_value);
+        *sync.counter = 0u;  // ready for the next launch (stream-ordered)
+      }
+    }
+  }
+}
+
+__global__ void fsdp_p2p_signal_kernel(const __grid_constant__ PeerTable slots, int world, unsigned long long value) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  store_flags(slots, world, value);
+}
+
+__global__ void fsdp_p2p_wait_kernel(const unsigned long long* flags, int world, unsigned long long value,
+                                     long long timeout_ns, int* err) {
+  wait_flags(flags, world, value, timeout_ns, err);
   __threadfence_system();
 }
 
@@ -817,11 +852,14 @@ cudaError_t launch_p2p_allgather(const DevTable& t, const PeerTable& pt, cudaStr
 }
 
 cudaError_t launch_p2p_reduce_scatter(const DevTable& t, const PeerTable& pt, int world, float scale,
-                                      bool accumulate, cudaStream_t s, int max_ctas) {
-  if (t.n == 0) return cudaSuccess;
+                                      bool accumulate, cudaStream_t s, int max_ctas, const P2PSync* sync) {
+  P2PSync none{};
+  if (t.n == 0 && !sync) return cudaSuccess;
   (void)cudaGetLastError();
-  fsdp_p2p_reduce_scatter_kernel<<<t.n < max_ctas ? t.n : max_ctas, kThreads, 0, s>>>(t.d, t.n, pt, world, scale,
-                                                                                     accumulate ? 1 : 0);
+  // a fused handshake needs >= 1 CTA even for an empty table
+  const int grid = t.n == 0 ? 1 : (t.n < max_ctas ? t.n : max_ctas);
+  fsdp_p2p_reduce_scatter_kernel<<<grid, kThreads, 0, s>>>(t.d, t.n, pt, world, scale, accumulate ? 1 : 0,
+                                                           sync ? *sync : none);
   return cudaGetLastError();
 }
 

@@ -360,12 +360,22 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
         case FSDP_OP_RS:
           if (with_comm) {
             FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_rs_packed, 0));
-            FSDP_TRY(p2p_wait(pp->ready_flags, epoch(o.bucket), ms));
             const float inv = 1.0f / static_cast<float>(ctx->world);
+#if FSDP_P2P_FUSED_SYNC
+            // one launch: wait "ready" >= E(b), reduce, last CTA signals "consumed" E(b)
+            P2PSync sync{static_cast<const unsigned long long*>(pp->ready_flags), epoch(o.bucket),
+                         static_cast<long long>(pp->timeout_ns), pp->error_flag, done_slots, epoch(o.bucket),
+                         ctx->p2p_counter};
+            FSDP_CUDA_TRY(launch_p2p_reduce_scatter(b->p2p_rs, peer_row(pp->rs_peers, o.bucket), ctx->world, inv,
+                                                    b->grad_accumulate, ms, ctx->max_ctas, &sync));
+            ++launches;
+#else
+            FSDP_TRY(p2p_wait(pp->ready_flags, epoch(o.bucket), ms));
             FSDP_CUDA_TRY(launch_p2p_reduce_scatter(b->p2p_rs, peer_row(pp->rs_peers, o.bucket), ctx->world, inv,
                                                     b->grad_accumulate, ms, ctx->max_ctas));
             ++launches;
             FSDP_TRY(p2p_signal(done_slots, epoch(o.bucket), ms));  // done reading peers' b
+#endif
             FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_done, ms));
             ++colls;
           }

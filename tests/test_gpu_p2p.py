@@ -301,3 +301,21 @@ def test_p2p_rejects_plain_storage():
     b = F.Bucket(ctx, [(8, 4, 0)], shards=[p.ptr], fulls=[p.ptr])
     with pytest.raises(F.FsdpError):
         F.p2p_allgather_bucket(ctx, b, [p.ptr, p.ptr])
+
+
+def test_fused_sync_variant_schedule():
+    """The FSDP_P2P_FUSED_SYNC=1 build (epoch wait + signal inside K9) runs the
+    scheduled p2p steps bit-exactly too, including all ranks concurrently."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    from paper_2411_00284_b200 import build as B
+    lib = os.path.join(B.BUILD, "variants", "fusedsync", "libfsdp_b200.so")
+    if not os.path.exists(lib):
+        lib = B.build(defines=["FSDP_P2P_FUSED_SYNC=1"], variant="fusedsync")
+    env = dict(os.environ, FSDP_B200_LIB=lib)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "p2p_schedule",
+                        os.path.join(root, "tests", "test_gpu_p2p.py")], env=env, cwd=root,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
