@@ -152,3 +152,45 @@ def test_fuzz_peer_memory(seed):
             assert np.array_equal(bits(o.get()), bits(p))
         for j, g in enumerate(gs):
             assert np.array_equal(bits(g.get()), bits(shards_ref[r][j].reshape(-1)))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_master_weights_and_accumulation(seed):
+    """fp32 master shards (K1 rounds to bf16) and gradient accumulation over
+    two micro-batches, random shapes / alignments / world sizes."""
+    from .test_gpu_mixed_precision import sim_master_allgather
+    world, dims, align, dt = _case(300 + seed)
+    rng = np.random.Generator(np.random.Philox(77 + seed))
+    masters = [rng.standard_normal(d, dtype=np.float32) for d in dims]
+    assert sim_master_allgather(masters, world, align)
+    s = "bf16" if dt == L.BF16 else "f32"
+    specs = [ParamSpec("p%d" % i, d, r, 0) for i, (d, r) in enumerate(dims)]
+    descs = [(d, r, 0) for d, r in dims]
+    _, rseg = bucket_layout(dims, world, 4, align)
+    held = [[rng.standard_normal((-(-d // world), r), dtype=np.float32) for d, r in dims] for _ in range(world)]
+    want = [list(h) for h in held]
+    ctxs = [F.Ctx(world, r) for r in range(world)]
+    gds = [[DevArray(nbytes=d * r * (2 if dt == L.BF16 else 4), fill=0) for d, r in dims] for _ in range(world)]
+    gss = [[DevArray(h) for h in held[q]] for q in range(world)]
+    bks = [F.Bucket(ctxs[q], descs, full_grads=[g.ptr for g in gds[q]], grad_shards=[g.ptr for g in gss[q]],
+                    param_dtype=dt, grad_dtype=dt, align=align) for q in range(world)]
+    rst = [DevArray(nbytes=world * rseg, fill=0xEF, dtype=np.float32) for _ in range(world)]
+    for m in range(2):
+        grads = [[grad_tensor(p, s, 400 + 10 * seed + m, q) for p in specs] for q in range(world)]
+        for q in range(world):
+            bks[q].set_grad_accumulation(True)
+            for dv, g in zip(gds[q], grads[q]):
+                dv.t[dv.off:dv.off + dv.nbytes].copy_(torch.from_numpy(g.reshape(-1).view(np.uint8)))
+            F.reduce_scatter_bucket(ctxs[q], bks[q], rst[q].ptr, flags=L.ISSUE)
+        packed = [x.get() for x in rst]
+        outs = OC.reduce_scatter(packed, world)
+        _, _, ref = OC.bucketed_reduce_scatter(grads, world, align)
+        for q in range(world):
+            h = packed[q].copy()
+            h[q * rseg // 4:(q + 1) * rseg // 4] = outs[q]
+            rst[q].t[rst[q].off:rst[q].off + rst[q].nbytes].copy_(torch.from_numpy(h.view(np.uint8)))
+            F.reduce_scatter_bucket(ctxs[q], bks[q], rst[q].ptr, flags=L.WAIT)
+            want[q] = OC.accumulate_grad_shards(want[q], ref[q])
+    for q in range(world):
+        for j, g in enumerate(gss[q]):
+            assert np.array_equal(bits(g.get()), bits(want[q][j])), (q, j)
