@@ -16,6 +16,7 @@ collectives are absent, so "exposed" is not measured here: the variants differ
 by copy-kernel work and launch count (the paper's single-node finding that
 bucketing adds copy-in/copy-out).
 """
+import gc
 import json
 import os
 import sys
@@ -84,9 +85,11 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
                step_GBps=round((ag_b + rs_b) / (ms_step * 1e-3) / 1e9, 1))
     if predicted:
         res["predicted_N%d" % world] = predicted
-    del st
+    del st, loop
     ctx.close()
+    gc.collect()
     torch.cuda.empty_cache()
+    print("  [mem after variant: %.1f GiB allocated]" % (torch.cuda.memory_allocated() / 2**30), file=sys.stderr)
     return res
 
 
