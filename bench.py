@@ -71,6 +71,9 @@ def parse():
     ap.add_argument("--collective", default="nccl", choices=["nccl", "p2p"],
                     help="nccl: pack + NCCL + copy-out (the paper's bucketing); p2p: fused peer-memory "
                          "kernels K8/K9 (1 GPU: the 7 peers are simulated as separate buffers)")
+    ap.add_argument("--dist", action="store_true",
+                    help="run the torch.distributed / NCCL-communicator path even at --gpus 1 (world 1 with a "
+                         "real communicator: checks the N > 1 plumbing on one GPU)")
     ap.add_argument("--no-fused-leg", action="store_true",
                     help="N=1 with --collective nccl: skip the extra run of the fused peer-memory mode whose "
                          "summary is reported under 'fused_p2p'")
@@ -247,7 +250,7 @@ def main():
     if args.same_device:
         local = 0    # test only: every rank on cuda:0 (exercises the multi-process path on one GPU)
     torch.cuda.set_device(local)
-    multi = args.gpus > 1
+    multi = args.gpus > 1 or args.dist
     p2p = args.collective == "p2p"
     pg = args.pg if args.pg != "auto" else ("gloo" if (p2p or args.same_device) else "nccl")
     if multi:

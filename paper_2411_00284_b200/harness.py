@@ -52,7 +52,6 @@ class RankState:
             if zero:
                 t.zero_()
             return t
-        self._alloc = alloc
         self.specs, self.world, self.rank, self.ctx = specs, world, rank, ctx
         self.descs = [(p.dim0, p.row_numel, p.module_id) for p in specs]
         self.param_dtype = param_dtype

@@ -50,6 +50,35 @@ def test_bench_p2p_two_processes_one_gpu():
     assert line["kernels"]["fsdp_p2p_allgather_kernel"]["launches_per_step"] == 2 * line["config"]["buckets_fwd"]
 
 
+@pytest.mark.parametrize("collective", ["nccl", "p2p"])
+def test_bench_distributed_path_world1(collective):
+    """The N > 1 code path of bench.py (torchrun, process group, NCCL unique-id
+    broadcast / IPC exchange, barriers, max over ranks, real collectives) at
+    world 1 with a real communicator: what the driver's --gpus 2/4/8 runs use."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"),
+           "--gpus", "1", "--dist", "--collective", collective, "--steps", "3", "--warmup", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 1 and line["config"]["layout_world"] == 1 and line["value"] > 0
+    assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+    if collective == "nccl":
+        assert line["collectives"]["ag_ms_per_step"] > 0 and line["busbw_GBps"] is not None
+    else:
+        assert line["p2p_wait_timeouts"] == 0
+
+
 def test_gemm_compute_feeds_real_gradients():
     """fsdp_gemm_compute: the backward GEMM dW = dY^T X of every linear member
     writes the full gradient the reduce-scatter then averages; dW matches an
