@@ -71,6 +71,10 @@ def parse():
     ap.add_argument("--collective", default="nccl", choices=["nccl", "p2p"],
                     help="nccl: pack + NCCL + copy-out (the paper's bucketing); p2p: fused peer-memory "
                          "kernels K8/K9 (1 GPU: the 7 peers are simulated as separate buffers)")
+    ap.add_argument("--nccl-register", default="none", choices=["none", "local", "symmetric"],
+                    help="N > 1 NCCL path: allocate the collective buffers with ncclMemAlloc and register them "
+                         "(ncclCommRegister / symmetric ncclCommWindowRegister) for zero-copy NVLS / symmetric "
+                         "kernels")
     ap.add_argument("--dist", action="store_true",
                     help="run the torch.distributed / NCCL-communicator path even at --gpus 1 (world 1 with a "
                          "real communicator: checks the N > 1 plumbing on one GPU)")
@@ -277,8 +281,9 @@ def main():
             "size_cap": L.PLAN_SIZE_CAP}[args.plan]
     link = (args.alpha_ns, args.beta_fs)
     fplan, bplan = H.plans_for(specs, world, mode, t_fwd, t_bwd, link, link, int(args.mem_limit))
+    reg = args.nccl_register if (multi and not p2p and args.nccl_register != "none") else None
     st = H.RankState(specs, world, rank if multi else 0, fplan, bplan, ctx, seed=1234 + rank,
-                     ipc=multi and p2p)
+                     ipc=multi and p2p, nccl_register=reg)
     compute = torch.cuda.Stream()
     comm = torch.cuda.Stream(priority=-1)
     cs, ms = compute.cuda_stream, comm.cuda_stream
@@ -523,7 +528,8 @@ def main():
                 "reduce_dtype": "fp32", "proxy_tokens_per_gpu": tokens,
                 "value_def": "sum over ranks of full AG(fwd)+AG(bwd)+RS bucket bytes per second of step time",
                 "bytes_per_rank_step": ag_b + rs_b, "l2": "inputs > L2 (126 MB): 64 GB of bucket traffic per step",
-                "parallelism": "fsdp%d" % world if multi else "fsdp1 (simulated %d)" % world},
+                "parallelism": "fsdp%d" % world if multi else "fsdp1 (simulated %d)" % world,
+                "nccl_register": reg or "none"},
             "exposed_comm_ms": round(ms_step - ms_compute, 3), "compute_stream_ms": round(ms_compute, 3),
             "profiled_ms_per_step": round(ms_prof, 3),
             "predicted": predicted,
@@ -547,6 +553,7 @@ def main():
         }
         print(json.dumps(line), flush=True)
     ctx_close = getattr(ctx, "close", None)
+    st.close_nccl_mem()
     del st
     if ctx_close:
         ctx_close()

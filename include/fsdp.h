@@ -516,6 +516,33 @@ fsdp_status fsdp_ipc_open(const void* handle64, void** dev_ptr);
 fsdp_status fsdp_ipc_close(void* dev_ptr);
 fsdp_status fsdp_ipc_free(void* dev_ptr);
 
+/* ------------------------------------------ NCCL buffer registration
+ * So that the NCCL collectives of the path (8(e)) can run zero-copy on
+ * NVSwitch (NVLink SHARP multicast, NCCL's symmetric-memory kernels) instead
+ * of staging through NCCL's internal buffers:
+ *   fsdp_mem_alloc : ncclMemAlloc -- cuMem-backed device memory NCCL can map
+ *                    for multicast; *dev_ptr is at least 4096-B aligned.
+ *   fsdp_mem_free  : releases every registration of the ctx that starts at
+ *                    dev_ptr, then ncclMemFree.
+ *   fsdp_register_buffer: registers [dev_ptr, dev_ptr + bytes) with the ctx's
+ *                    communicator:
+ *     FSDP_REG_LOCAL     ncclCommRegister (a local call);
+ *     FSDP_REG_SYMMETRIC ncclCommWindowRegister(..., NCCL_WIN_COLL_SYMMETRIC):
+ *                        a COLLECTIVE call -- every rank registers a buffer of
+ *                        the same size, in the same order; dev_ptr from
+ *                        fsdp_mem_alloc, 4096-B aligned; collectives on it must
+ *                        use the same offsets on every rank (the plan's layout
+ *                        guarantees that).
+ * Registrations live until fsdp_mem_free of their base pointer or
+ * fsdp_ctx_destroy (released before the communicator).  Errors: a ctx with no
+ * communicator, NULL / unaligned pointers, bytes < 1 -> FSDP_ERR_INVALID_ARG;
+ * NCCL failures -> FSDP_ERR_NCCL (the caller may keep unregistered buffers:
+ * registration changes speed, never results). */
+enum { FSDP_REG_LOCAL = 0, FSDP_REG_SYMMETRIC = 1 };
+fsdp_status fsdp_mem_alloc(fsdp_ctx* ctx, int64_t bytes, void** dev_ptr);
+fsdp_status fsdp_mem_free(fsdp_ctx* ctx, void* dev_ptr);
+fsdp_status fsdp_register_buffer(fsdp_ctx* ctx, void* dev_ptr, int64_t bytes, int32_t mode);
+
 /* ----------------------------------------------- compute proxy (K7)
  * A measurement device, not a method step: stands in for the layer compute
  * that the paper's reordering overlaps communication with, so that

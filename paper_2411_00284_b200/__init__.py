@@ -11,7 +11,8 @@ before the library exists.)
 _API = ("Bucket", "Ctx", "abi_version", "allgather_bucket", "layout", "nccl_get_unique_id",
         "plan_buckets", "proxy_calibrate", "proxy_launch", "reduce_scatter_bucket", "run_schedule",
         "shard", "p2p_allgather_bucket", "p2p_reduce_scatter_bucket", "p2p_signal", "p2p_wait",
-        "ipc_alloc", "ipc_open", "ipc_close", "ipc_free", "comm_time_ns", "simulate_schedule")
+        "ipc_alloc", "ipc_open", "ipc_close", "ipc_free", "comm_time_ns", "simulate_schedule",
+        "mem_alloc", "mem_free", "register_buffer")
 
 
 def __getattr__(name):

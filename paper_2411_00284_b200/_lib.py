@@ -30,6 +30,7 @@ N_OPS = 10
 SCHED_REORDER, SCHED_FWD_AG_BEFORE_WAIT, SCHED_BWD_AG_BEFORE_WAIT = 1, 2, 4
 SCHED_NO_COMM, SCHED_DRY_RUN, SCHED_TIMING, SCHED_P2P = 8, 16, 32, 64
 BUCKET_SEGMENT_SHARDS, BUCKET_SEGMENT_GRAD_SHARDS, BUCKET_FP32_MASTER = 1, 2, 4
+REG_LOCAL, REG_SYMMETRIC = 0, 1
 
 EXPORTED = [
     "fsdp_last_error", "fsdp_abi_version", "fsdp_nccl_get_unique_id", "fsdp_ctx_create",
@@ -39,6 +40,7 @@ EXPORTED = [
     "fsdp_run_schedule", "fsdp_proxy_launch", "fsdp_proxy_calibrate",
     "fsdp_p2p_allgather_bucket", "fsdp_p2p_reduce_scatter_bucket", "fsdp_p2p_signal", "fsdp_p2p_wait",
     "fsdp_ipc_alloc", "fsdp_ipc_open", "fsdp_ipc_close", "fsdp_ipc_free",
+    "fsdp_mem_alloc", "fsdp_mem_free", "fsdp_register_buffer",
     "fsdp_comm_time_ns", "fsdp_simulate_schedule",
 ]
 
@@ -156,6 +158,9 @@ _sigs = {
     "fsdp_ipc_open": (C.c_int, [_P, C.POINTER(_P)]),
     "fsdp_ipc_close": (C.c_int, [_P]),
     "fsdp_ipc_free": (C.c_int, [_P]),
+    "fsdp_mem_alloc": (C.c_int, [_P, C.c_int64, C.POINTER(_P)]),
+    "fsdp_mem_free": (C.c_int, [_P, _P]),
+    "fsdp_register_buffer": (C.c_int, [_P, _P, C.c_int64, C.c_int32]),
     "fsdp_comm_time_ns": (C.c_int, [C.c_int64, C.POINTER(Link), C.POINTER(C.c_int64)]),
     "fsdp_simulate_schedule": (C.c_int, [C.POINTER(LogEntry), C.c_int32, C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),

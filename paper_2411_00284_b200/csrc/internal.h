@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "fsdp.h"
@@ -197,7 +198,13 @@ struct fsdp_ctx {
   std::vector<cudaEvent_t> io_events;      // pool for host I/O ordering (fsdp_host_io)
   cudaStream_t own_h2d = nullptr, own_d2h = nullptr;
   void* gemm_cache = nullptr;              // cuBLASLt handle + plans (gemm.cc)
+  // NCCL registrations (ncclmem.cc): base pointer -> local handle / window
+  std::vector<std::pair<void*, void*>> nccl_regs;
+  std::vector<std::pair<void*, ncclWindow_t>> nccl_wins;
 };
+namespace fsdp {
+void release_registrations(fsdp_ctx* c, void* base);  // base NULL = all
+}
 
 struct fsdp_bucket {
   fsdp_ctx* ctx = nullptr;

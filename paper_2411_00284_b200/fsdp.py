@@ -263,6 +263,23 @@ def ipc_free(ptr):
     check(L.lib.fsdp_ipc_free(ptr))
 
 
+def mem_alloc(ctx, nbytes):
+    """fsdp_mem_alloc: ncclMemAlloc'd device memory (NVLS / symmetric-capable)."""
+    p = C.c_void_p()
+    check(L.lib.fsdp_mem_alloc(ctx.h, int(nbytes), C.byref(p)))
+    return p.value
+
+
+def mem_free(ctx, ptr):
+    check(L.lib.fsdp_mem_free(ctx.h, ptr))
+
+
+def register_buffer(ctx, ptr, nbytes, mode=L.REG_LOCAL):
+    """fsdp_register_buffer: REG_LOCAL (ncclCommRegister) or REG_SYMMETRIC
+    (collective ncclCommWindowRegister)."""
+    check(L.lib.fsdp_register_buffer(ctx.h, ptr, int(nbytes), int(mode)))
+
+
 # ------------------------------------------------------ cost model / prediction
 def comm_time_ns(nbytes, link):
     """fsdp_comm_time_ns: alpha + ceil(n * beta_fs / 1e6) (P:222)."""

@@ -34,15 +34,36 @@ def _carve(sizes, align=ALIGN):
 
 class RankState:
     def __init__(self, specs, world, rank, fwd_plan, bwd_plan, ctx, param_dtype=L.BF16,
-                 device="cuda", seed=0, fill=True, segment_storage=True, ipc=False):
+                 device="cuda", seed=0, fill=True, segment_storage=True, ipc=False, nccl_register=None):
         # ipc=True: the buffers peers read in the peer-memory path (shard
         # storage, gradient slots) come from fsdp_ipc_alloc so that other
-        # processes can map them (setup_p2p_ipc)
+        # processes can map them (setup_p2p_ipc).
+        # nccl_register="local" / "symmetric": every buffer an NCCL collective
+        # sends from or receives into (shard storage, full-parameter slots, AG /
+        # RS staging, gradient-shard storage) comes from fsdp_mem_alloc and is
+        # registered with the ctx's communicator (fsdp_register_buffer).
         self.ipc_handles = {}
         self._ipc_ptrs = []
+        self._nccl_ptrs = []
+        reg_mode = {None: None, "none": None, "local": L.REG_LOCAL, "symmetric": L.REG_SYMMETRIC}[nccl_register]
+        dev_index = torch.device(device).index or torch.cuda.current_device()
 
-        def alloc(name, nbytes, zero=False):
-            if not ipc:
+        def nccl_buf(nbytes, zero=False):
+            from .dlpack_view import uint8_view
+            nbytes = max(int(nbytes), 4096)
+            ptr = F.mem_alloc(ctx, nbytes)
+            self._nccl_ptrs.append(ptr)
+            F.register_buffer(ctx, ptr, nbytes, reg_mode)
+            t = uint8_view(ptr, nbytes, dev_index)
+            if zero:
+                t.zero_()
+            return t
+
+        def alloc(name, nbytes, zero=False, collective=False, peer=False):
+            # collective: an NCCL send / receive buffer; peer: read by peers (K8 / K9)
+            if collective and reg_mode is not None:
+                return nccl_buf(nbytes, zero)
+            if not (ipc and peer):
                 return (torch.zeros if zero else torch.empty)(nbytes, dtype=torch.uint8, device=device)
             from .dlpack_view import uint8_view
             ptr, handle = F.ipc_alloc(nbytes)
@@ -71,14 +92,14 @@ class RankState:
         else:
             self.shard_offs, tot = _carve([n * ep for n in self.shard_numel])
             self.gs_offs, tot_g = _carve([n * 4 for n in self.shard_numel])
-        self.shard_buf = alloc("shards", tot, zero=True)
-        self.gshard_buf = torch.zeros(tot_g, dtype=torch.uint8, device=device)
+        self.shard_buf = alloc("shards", tot, zero=True, collective=True, peer=True)
+        self.gshard_buf = alloc("gshards", tot_g, zero=True, collective=True)
         # slots sized to the largest bucket of either phase
         buckets = list(fwd_plan) + list(bwd_plan)
         self.slot_bytes = max(_carve([self.full_numel[j] * ep for j in sorted(b)])[1] for b in buckets)
         self.gslot_bytes = max(_carve([self.full_numel[j] * 2 for j in sorted(b)])[1] for b in buckets)
-        self.full_slots = [torch.empty(self.slot_bytes, dtype=torch.uint8, device=device) for _ in range(2)]
-        self.grad_slots = [alloc("grads%d" % i, self.gslot_bytes) for i in range(2)]
+        self.full_slots = [alloc("fulls%d" % i, self.slot_bytes, collective=True) for i in range(2)]
+        self.grad_slots = [alloc("grads%d" % i, self.gslot_bytes, peer=True) for i in range(2)]
         if fill:
             g = torch.Generator(device=device).manual_seed(seed)
             # N(0, 0.02) bf16 parameters and N(0, 1e-3) bf16 gradients (DESIGN.md input recipe)
@@ -117,9 +138,9 @@ class RankState:
                 out.append(bk)
                 max_ag = max(max_ag, bk.ag_seg)
                 max_rs = max(max_rs, bk.rs_seg)
-        self.ag_st = [torch.zeros(world * max_ag + ALIGN, dtype=torch.uint8, device=device) for _ in range(2)]
-        self.rs_st = [torch.zeros(world * max(max_rs, 16) + ALIGN, dtype=torch.uint8, device=device)
-                      for _ in range(2)]
+        self.ag_st = [alloc("ag_st%d" % i, world * max_ag + ALIGN, zero=True, collective=True) for i in range(2)]
+        self.rs_st = [alloc("rs_st%d" % i, world * max(max_rs, 16) + ALIGN, zero=True, collective=True)
+                      for i in range(2)]
 
     def _segment_offsets(self, plan, elem_bytes):
         """Per-parameter byte offsets placing each bucket's members at the
@@ -218,6 +239,13 @@ class RankState:
         self.ready_slots = [flag_base[q] + 8 * r for q in range(W)]
         self.done_slots = [flag_base[q] + 8 * W + 8 * r for q in range(W)]
         self._p2p_tables(shard_base, grad_base)
+
+    def close_nccl_mem(self):
+        """Releases the fsdp_mem_alloc buffers (and their registrations); call
+        before the ctx is destroyed.  The torch views must not be used after."""
+        for p in self._nccl_ptrs:
+            F.mem_free(self.ctx, p)
+        self._nccl_ptrs = []
 
     def close_ipc(self):
         for p in getattr(self, "_opened", []):
