@@ -109,5 +109,19 @@ def build(verbose=False, force=False, defines=None, variant=None):
     return lib
 
 
+def build_examples(verbose=False):
+    """Compiles examples/c_abi_demo.c -- the C ABI used from plain C (driver
+    API for memory) -- against the in-tree library; returns the binary path."""
+    src = os.path.join(ROOT, "examples", "c_abi_demo.c")
+    out = os.path.join(ROOT, "examples", "c_abi_demo")
+    cuda = cuda_home()
+    if not _stale(out, [src, LIB, os.path.join(ROOT, "include", "fsdp.h")]):
+        return out
+    _run(["gcc", "-O2", "-std=c11", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
+          "-I", os.path.join(cuda, "include"), src, "-o", out, "-L", PKG, "-l:libfsdp_b200.so",
+          "-Wl,-rpath," + PKG, "-L", os.path.join(cuda, "lib64", "stubs"), "-lcuda"], verbose)
+    return out
+
+
 if __name__ == "__main__":
     print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv))
