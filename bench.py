@@ -21,6 +21,7 @@ value = sum over ranks of the full bucket bytes the step's collectives carry
 (64.3 GB of bucket traffic per rank-step) are far larger than the 126 MB L2.
 """
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -75,6 +76,8 @@ def parse():
                     help="N > 1 NCCL path: allocate the collective buffers with ncclMemAlloc and register them "
                          "(ncclCommRegister / symmetric ncclCommWindowRegister) for zero-copy NVLS / symmetric "
                          "kernels")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="N=1: skip the predicted exposure of the vanilla and greedy plans")
     ap.add_argument("--dist", action="store_true",
                     help="run the torch.distributed / NCCL-communicator path even at --gpus 1 (world 1 with a "
                          "real communicator: checks the N > 1 plumbing on one GPU)")
@@ -391,32 +394,45 @@ def main():
     # of modelled NVLink 5 (720 GB/s bus, 20 us); no contention modelled.
     predicted = None
     if not multi and not p2p and (args.predict_tokens or gemm):
+        beta = round((world - 1) / world / 720e9 * 1e15)
+        link = (20000, beta)
         if gemm:   # the measured GEMMs of this run are the compute
-            rep = st.step(flags | L.SCHED_TIMING, cs, ms, None, None, want_log=True, gemm=gemm)
+            ppf = ppb = None
         else:
             ptf, ptb = per_param_compute_ns(specs, args.predict_tokens)
             nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
             ppf = H.proxy_iters(H.bucket_times(fplan, ptf), nspi)
             ppb = H.proxy_iters(H.bucket_times(bplan, ptb), nspi)
-            rep = st.step(flags | L.SCHED_TIMING, cs, ms, ppf, ppb, args.proxy_ctas, args.proxy_smem,
-                          want_log=True)
-        beta = round((world - 1) / world / 720e9 * 1e15)
-        link = (20000, beta)
-        durs = []
-        for ph, op, b, _s, ns, _t in rep["log"]:
-            bk = (st.fwd if ph == 0 else st.bwd)[b]
-            if op == L.OP_AG:
-                durs.append(F.comm_time_ns(world * bk.ag_seg, link))
-            elif op == L.OP_RS:
-                durs.append(F.comm_time_ns(world * bk.rs_seg, link))
-            else:
-                durs.append(max(ns, 0))
-        tot, exp, _, _ = F.simulate_schedule(rep["log"], durs)
+        tot, exp = H.predict_exposure(st, flags, cs, ms, ppf, ppb, link, link, args.proxy_ctas, args.proxy_smem,
+                                      gemm=gemm)
         predicted = {"world": world, "tokens_per_gpu": gemm["tokens"] if gemm else args.predict_tokens,
                      "compute": "cuBLASLt linear layers (measured)" if gemm else "calibrated proxy (per-op model)",
                      "link_alpha_ns": link[0], "link_beta_fs_per_byte": link[1], "total_ms": round(tot / 1e6, 3),
-                     "exposed_comm_ms": round(exp / 1e6, 3),
+                     "exposed_ms": round(exp / 1e6, 3), "exposed_comm_ms": round(exp / 1e6, 3),
                      "model": "measured compute-stream ops + alpha/beta NVLink collectives, no contention"}
+        if not gemm and not args.no_variants:
+            # the north star's comparison: exposure under the greedy plan (Alg. 1)
+            # vs the unbucketed, unreordered baseline, same model, same compute
+            variants = {}
+            for name, vmode, vflags in (("vanilla (per-param, no reorder)", L.PLAN_PER_PARAM, 0),
+                                        ("greedy + reorder", L.PLAN_GREEDY,
+                                         L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT)):
+                vf, vb = H.plans_for(specs, world, vmode, ptf, ptb, link, link, int(args.mem_limit))
+                vst = H.RankState(specs, world, 0, vf, vb, ctx, seed=99)
+                vpf = H.proxy_iters(H.bucket_times(vf, ptf), nspi)
+                vpb = H.proxy_iters(H.bucket_times(vb, ptb), nspi)
+                vst.step(vflags, cs, ms, vpf, vpb, args.proxy_ctas, args.proxy_smem)   # warm-up
+                vt, ve = H.predict_exposure(vst, vflags, cs, ms, vpf, vpb, link, link, args.proxy_ctas,
+                                            args.proxy_smem)
+                variants[name] = {"buckets_fwd": len(vf), "buckets_bwd": len(vb),
+                                  "total_ms": round(vt / 1e6, 3), "exposed_ms": round(ve / 1e6, 3)}
+                del vst
+                gc.collect()
+                torch.cuda.empty_cache()
+            variants["manual (per-block) + reorder [this run]"] = {
+                "buckets_fwd": len(fplan), "buckets_bwd": len(bplan),
+                "total_ms": predicted["total_ms"], "exposed_ms": predicted["exposed_ms"]}
+            predicted["variants"] = variants
 
     # linear-layer compute throughput (cuBLASLt, tensor cores) of the timed steps
     gemm_report = None

@@ -404,3 +404,25 @@ def bucket_times(plan, t_per_param):
 
 def np_dtype(dt):
     return np.uint16 if dt == L.BF16 else np.float32
+
+
+def predict_exposure(st, flags, compute, comm, proxy_fwd, proxy_bwd, link_ag, link_rs, ctas_per_sm=1, smem=0,
+                     gemm=None):
+    """Two-stream prediction of the N-rank step (fsdp_simulate_schedule): one
+    timed step of this rank gives every compute-stream op its MEASURED
+    duration; every collective takes alpha + beta n of its full bucket bytes
+    (fsdp_comm_time_ns).  Returns (total_ns, exposed_ns).  A model: no SM /
+    HBM contention between the copies and the collectives."""
+    rep = st.step(flags | L.SCHED_TIMING, compute, comm, proxy_fwd, proxy_bwd, ctas_per_sm, smem, want_log=True,
+                  gemm=gemm)
+    durs = []
+    for ph, op, b, _s, ns, _t in rep["log"]:
+        bk = (st.fwd if ph == 0 else st.bwd)[b]
+        if op == L.OP_AG:
+            durs.append(F.comm_time_ns(st.world * bk.ag_seg, link_ag))
+        elif op == L.OP_RS:
+            durs.append(F.comm_time_ns(st.world * bk.rs_seg, link_rs))
+        else:
+            durs.append(max(ns, 0))
+    tot, exp, _, _ = F.simulate_schedule(rep["log"], durs)
+    return tot, exp
