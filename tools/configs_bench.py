@@ -5,6 +5,7 @@
   c0  toy 4-layer MLP, fp32, 2 ranks: PER_PARAM vs GREEDY plan, step latency
   c2  Llama-3-8B Table 5 / Table 6 variants with the compute proxy at T tokens:
       vanilla / +reorder / +bucket / +both / greedy+reorder, 4 placements
+  c2w the same at world sizes 2 / 4 / 8 (vanilla, manual+reorder, greedy+reorder)
   c3  Llama-3-70B SIZE_CAP bucket-size sweep 25-500 MB at N = 8
   c4  Llama-3-405B one layer at N = 8: one whole-layer bucket vs per-parameter
 
@@ -138,6 +139,34 @@ def c2(tokens=(1024, 2048)):
     return out
 
 
+def c2w(worlds=(2, 4, 8), T=1024):
+    """configs[2] across world sizes: vanilla vs manual+reorder vs greedy+reorder,
+    predicted N-rank exposure at each N (link beta scaled by (N-1)/N)."""
+    import torch
+    import paper_2411_00284_b200 as F
+    from paper_2411_00284_b200 import _lib as L
+    from paper_2411_00284_b200 import harness as H
+    from workloads import llama
+    from workloads.compute_model import per_param_compute_ns
+    specs = llama("8b")
+    ctx = F.Ctx(8, 0)
+    s = torch.cuda.Stream()
+    nspi = H.calibrate_proxy(ctx, s.cuda_stream)
+    ctx.close()
+    R, FB = L.SCHED_REORDER, L.SCHED_FWD_AG_BEFORE_WAIT
+    f, b = per_param_compute_ns(specs, T)
+    out = {"tokens_per_gpu": T, "proxy_ns_per_iter": nspi}
+    for w in worlds:
+        nvl = (20000, round((w - 1) / w / 720e9 * 1e15))
+        rows = {}
+        for name, mode, flags in (("vanilla", L.PLAN_PER_PARAM, 0), ("manual+reorder", L.PLAN_MANUAL, R | FB),
+                                  ("greedy+reorder", L.PLAN_GREEDY, R | FB)):
+            rows[name] = run_variant(specs, w, mode, flags, f, b, mem_max=2 * 10**9, tokens=T, nspi=nspi,
+                                     steps=3, warmup=1, link=nvl, predict_link=(nvl, nvl))
+        out["N=%d" % w] = rows
+    return out
+
+
 def c3(caps_mb=(25, 50, 100, 200, 500)):
     from paper_2411_00284_b200 import _lib as L
     from workloads import llama
@@ -157,7 +186,7 @@ def c4():
 
 
 def main():
-    which = [a for a in sys.argv[1:] if a in ("c0", "c2", "c3", "c4")] or ["c0", "c2", "c3", "c4"]
+    which = [a for a in sys.argv[1:] if a in ("c0", "c2", "c2w", "c3", "c4")] or ["c0", "c2", "c2w", "c3", "c4"]
     res = {}
     for w in which:
         res[w] = globals()[w]()
