@@ -312,7 +312,7 @@ def test_fused_sync_variant_schedule():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     from paper_2411_00284_b200 import build as B
     lib = os.path.join(B.BUILD, "variants", "fusedsync", "libfsdp_b200.so")
-    if not os.path.exists(lib):
+    if not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(B.LIB):   # stale vs the main build
         lib = B.build(defines=["FSDP_P2P_FUSED_SYNC=1"], variant="fusedsync")
     env = dict(os.environ, FSDP_B200_LIB=lib)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "p2p_schedule",
