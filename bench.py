@@ -466,8 +466,12 @@ def main():
                               "launches_per_step": klaunch[op],
                               "bytes_per_step": kbytes[op]} for op in live}
     launches = sum(r["kernel_launches"] for r in reports)
-    coll_ms = {"ag_ms_per_step": round(op_ns[L.OP_AG] / args.steps / 1e6, 3),
-               "rs_ms_per_step": round(op_ns[L.OP_RS] / args.steps / 1e6, 3)}
+    # device time of the collective ops (event pairs on the comm stream); at
+    # N = 1 with the NCCL design no collective exists (no peers): null
+    coll_ms = None
+    if multi or p2p:
+        coll_ms = {"ag_ms_per_step": round(op_ns[L.OP_AG] / args.steps / 1e6, 3),
+                   "rs_ms_per_step": round(op_ns[L.OP_RS] / args.steps / 1e6, 3)}
     busbw = None
     if multi and op_ns[L.OP_AG] > 0:
         busbw = {"ag": round((world - 1) / world * ag_b * args.steps / (op_ns[L.OP_AG] * 1e-9) / 1e9, 1),
