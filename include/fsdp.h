@@ -101,6 +101,20 @@ fsdp_status fsdp_ctx_create(fsdp_ctx** out, int32_t world, int32_t rank, int32_t
                             const void* nccl_uid, void* borrowed_comm);
 fsdp_status fsdp_ctx_destroy(fsdp_ctx* ctx);
 
+/* 2-D meshes (Tensor Parallel: a parameter "doubly sharded on both
+ * Data Parallel (DP) and Tensor Parallel (TP) dimensions ... is first
+ * redistributed (via an all-gather) on the DP sub-mesh"): the FSDP path runs
+ * unchanged on the DP sub-mesh over the TP-local tensors.  fsdp_ctx_split
+ * creates that sub-mesh ctx from a ctx with a communicator by ncclCommSplit
+ * (a collective call over the parent): ranks with equal `color` form one
+ * sub-communicator, ordered by `key`; e.g. TP innermost (rank = dp * TP + tp):
+ * color = tp, key = dp.  The new ctx owns its communicator (world / rank =
+ * the sub-mesh's); color = -1 (NCCL_SPLIT_NOCOLOR) leaves *out NULL.
+ * Errors: parent without communicator, color < -1 -> FSDP_ERR_INVALID_ARG. */
+fsdp_status fsdp_ctx_split(fsdp_ctx* parent, int32_t color, int32_t key, fsdp_ctx** out);
+/* World size and rank of a ctx (host-only; NULL outputs skipped). */
+fsdp_status fsdp_ctx_info(const fsdp_ctx* ctx, int32_t* world, int32_t* rank);
+
 /* ------------------------------------------------------------ 1. fsdp_shard
  * P:69 "partitioned per the number of devices ... Each device only holds one of
  * the partitions"; P:133 Shard(0) DTensors.  Always fills *info.  If both

@@ -18,12 +18,14 @@ Modules
 bf16        O1  bf16 codec (widen / round-to-nearest-even narrow)
 shard       O2  per-parameter dim-0 sharding
 layout      O3  flat bucket layout
-collectives O4/O5 bucketed all-gather and reduce-scatter(avg) over N simulated ranks
+collectives O4/O5 bucketed all-gather and reduce-scatter(avg) over N simulated ranks;
+            mixed-precision (fp32 master) all-gather, gradient accumulation
 cost        O6  alpha + beta*n communication model
 planner     O8  Algorithm 1 greedy auto-wrap + manual / per-param / size-cap plans
 schedule    O9  reordered / vanilla op sequences (Table 6)
 sim         O10 two-stream discrete-event simulator
 brute       O8(iv) exhaustive contiguous-partition search
+mesh        O11 2-D DP x TP composition: TP blocks, FSDP on the DP sub-mesh
 
 Parity status: every function is pinned by a ``-m "not gpu"`` test in
 ``tests/test_oracle_*.py`` against values or properties the paper or the

@@ -34,7 +34,7 @@ REG_LOCAL, REG_SYMMETRIC = 0, 1
 
 EXPORTED = [
     "fsdp_last_error", "fsdp_abi_version", "fsdp_nccl_get_unique_id", "fsdp_ctx_create",
-    "fsdp_ctx_destroy", "fsdp_shard", "fsdp_plan_buckets", "fsdp_layout", "fsdp_bucket_create",
+    "fsdp_ctx_destroy", "fsdp_ctx_split", "fsdp_ctx_info", "fsdp_shard", "fsdp_plan_buckets", "fsdp_layout", "fsdp_bucket_create",
     "fsdp_bucket_destroy", "fsdp_bucket_query", "fsdp_bucket_set_grad_accumulation",
     "fsdp_allgather_bucket", "fsdp_reduce_scatter_bucket",
     "fsdp_run_schedule", "fsdp_proxy_launch", "fsdp_proxy_calibrate",
@@ -133,6 +133,8 @@ _sigs = {
     "fsdp_nccl_get_unique_id": (C.c_int, [_P]),
     "fsdp_ctx_create": (C.c_int, [C.POINTER(_P), C.c_int32, C.c_int32, C.c_int32, _P, _P]),
     "fsdp_ctx_destroy": (C.c_int, [_P]),
+    "fsdp_ctx_split": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "fsdp_ctx_info": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "fsdp_shard": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(ParamDesc), C.c_int, _P, _P,
                              C.POINTER(ShardInfo), _P]),
     "fsdp_plan_buckets": (C.c_int, [C.POINTER(PlanIn), C.POINTER(C.c_int32), C.POINTER(C.c_int32),

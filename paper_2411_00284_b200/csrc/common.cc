@@ -258,6 +258,38 @@ fsdp_status fsdp_ctx_create(fsdp_ctx** out, int32_t world, int32_t rank, int32_t
   return FSDP_OK;
 }
 
+fsdp_status fsdp_ctx_info(const fsdp_ctx* c, int32_t* world, int32_t* rank) {
+  if (!c) return fail(FSDP_ERR_INVALID_ARG, "NULL ctx");
+  if (world) *world = c->world;
+  if (rank) *rank = c->rank;
+  return FSDP_OK;
+}
+
+fsdp_status fsdp_ctx_split(fsdp_ctx* parent, int32_t color, int32_t key, fsdp_ctx** out) {
+  if (!parent || !out) return fail(FSDP_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  if (!parent->comm) return fail(FSDP_ERR_INVALID_ARG, "fsdp_ctx_split needs a ctx with a communicator");
+  if (color < 0 && color != NCCL_SPLIT_NOCOLOR) return fail(FSDP_ERR_INVALID_ARG, "color < 0");
+  FSDP_CUDA_TRY(cudaSetDevice(parent->device));
+  ncclComm_t sub = nullptr;
+  FSDP_NCCL_TRY(ncclCommSplit(parent->comm, color, key, &sub, nullptr));
+  if (!sub) return FSDP_OK;  // NCCL_SPLIT_NOCOLOR: this rank is in no sub-mesh
+  int n = 0, r = 0;
+  ncclResult_t nr = ncclCommCount(sub, &n);
+  if (nr == ncclSuccess) nr = ncclCommUserRank(sub, &r);
+  if (nr != ncclSuccess) {
+    ncclCommDestroy(sub);
+    return fail(FSDP_ERR_NCCL, std::string("sub-communicator query: ") + ncclGetErrorString(nr));
+  }
+  fsdp_status st = fsdp_ctx_create(out, n, r, parent->device, nullptr, sub);
+  if (st != FSDP_OK) {
+    ncclCommDestroy(sub);
+    return st;
+  }
+  (*out)->owns_comm = true;
+  return FSDP_OK;
+}
+
 fsdp_status fsdp_ctx_destroy(fsdp_ctx* c) {
   if (!c) return FSDP_OK;
   cudaSetDevice(c->device);

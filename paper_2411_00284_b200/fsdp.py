@@ -84,6 +84,20 @@ class Ctx:
                                     borrowed_comm))
         self.h = h
 
+    def split(self, color, key):
+        """fsdp_ctx_split: the sub-mesh ctx (a collective over this ctx's
+        communicator); None for color -1."""
+        h = C.c_void_p()
+        check(L.lib.fsdp_ctx_split(self.h, int(color), int(key), C.byref(h)))
+        if not h.value:
+            return None
+        sub = Ctx.__new__(Ctx)
+        sub.device, sub.h = self.device, h
+        n, r = C.c_int32(), C.c_int32()
+        check(L.lib.fsdp_ctx_info(h, C.byref(n), C.byref(r)))
+        sub.world, sub.rank = n.value, r.value
+        return sub
+
     def close(self):
         if self.h:
             check(L.lib.fsdp_ctx_destroy(self.h))

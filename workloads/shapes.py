@@ -65,3 +65,37 @@ def toy_mlp():
 
 def numel(ps):
     return sum(p.dim0 * p.row_numel for p in ps)
+
+
+# Tensor-parallel plan for the 2-D DP x TP mesh, TorchTitan-style:
+# column-parallel weights are split on dim 0 (output features), row-parallel
+# ones on dim 1 (input features), the embedding on dim 0 (vocabulary), norms
+# replicated.  Only shapes live here; slicing values is the oracle's job.
+TP_AXIS = {"attention.wq.weight": 0, "attention.wk.weight": 0, "attention.wv.weight": 0,
+           "feed_forward.w1.weight": 0, "feed_forward.w3.weight": 0, "output.weight": 0,
+           "tok_embeddings.weight": 0, "attention.wo.weight": 1, "feed_forward.w2.weight": 1}
+
+
+def tp_axis(spec):
+    """0 / 1: the dim the TP plan splits; None: replicated over TP."""
+    for suffix, ax in TP_AXIS.items():
+        if spec.name.endswith(suffix):
+            return ax
+    return None
+
+
+def tp_local(specs, tp):
+    """The TP-local shapes of `specs` on a TP group of size `tp` (every split
+    dim divisible by tp for the Llama shapes at tp <= 8)."""
+    out = []
+    for p in specs:
+        ax = tp_axis(p)
+        if ax == 0:
+            assert p.dim0 % tp == 0
+            out.append(p._replace(dim0=p.dim0 // tp))
+        elif ax == 1:
+            assert p.row_numel % tp == 0
+            out.append(p._replace(row_numel=p.row_numel // tp))
+        else:
+            out.append(p)
+    return out
