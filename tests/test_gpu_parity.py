@@ -443,3 +443,29 @@ def test_abi_rejects_misaligned_staging_and_foreign_bucket():
         F.allgather_bucket(ctx2, b, st.ptr)
     with pytest.raises(F.FsdpError):
         F.reduce_scatter_bucket(ctx, b, st.ptr)  # created without gradient pointers
+
+
+def test_degenerate_steps_and_zero_row_ranks():
+    """Edge cases the method has: an empty step (no buckets), a forward-only
+    step, and ranks that own zero rows of every member (d < N)."""
+    ctx = F.Ctx(1, 0, 0, nccl_uid=F.nccl_get_unique_id())
+    rep = F.run_schedule(ctx, [], [], flags=L.SCHED_REORDER)
+    assert rep["log_len"] == 0 and rep["kernel_launches"] == 0 and rep["collectives"] == 0
+    ctx.close()
+    # world 8, members with d in {1, 3, 7}: ranks 1..7 own zero rows of d = 1, ranks 3..7 of d = 3
+    params = [param_tensor(s, "bf16", 90 + i) for i, s in enumerate(_specs_from_dims([(1, 24), (3, 8), (7, 1)]))]
+    assert sim_allgather(params, 8, L.BF16)
+    grads = [[grad_tensor(s, "bf16", 91, r) for s in _specs_from_dims([(1, 24), (3, 8), (7, 1)])] for r in range(8)]
+    assert sim_reduce_scatter(grads, 8, L.BF16)
+    # forward-only step on a layout-only ctx
+    lay = F.Ctx(2, 1)
+    p = param_tensor(ParamSpec("w", 10, 16, 0), "bf16", 5)
+    sh = DevArray(shard(p, 2, 1))
+    out = DevArray(nbytes=p.nbytes, fill=0, dtype=p.dtype, shape=p.shape)
+    b = F.Bucket(lay, [(10, 16, 0)], shards=[sh.ptr], fulls=[out.ptr])
+    ag = [DevArray(nbytes=2 * b.ag_seg, fill=0) for _ in range(2)]
+    rep = F.run_schedule(lay, [b], [], ag_staging=(ag[0].ptr, ag[1].ptr), flags=L.SCHED_REORDER)
+    torch.cuda.synchronize()
+    assert rep["op_count"][L.OP_PACK_AG] == 1 and rep["op_count"][L.OP_RS] == 0
+    # rank 1's own rows [5, 10) are in place; rank 0's rows come from a peer (none here)
+    assert np.array_equal(out.get()[5:], p[5:])
