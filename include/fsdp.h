@@ -283,7 +283,10 @@ fsdp_status fsdp_bucket_query(const fsdp_bucket* b, fsdp_bucket_info* out);
  * ag_staging: device, world * ag_seg_bytes, 16-B aligned.  The caller must not
  * re-ISSUE into the same staging before the previous WAIT was enqueued.
  * Layout-only ctx: ISSUE = pack only, WAIT = copy-out only. */
-enum { FSDP_ISSUE = 1, FSDP_WAIT = 2 };
+enum { FSDP_ISSUE = 1, FSDP_WAIT = 2, FSDP_NO_COLLECTIVE = 4 };
+/* FSDP_NO_COLLECTIVE (with FSDP_ISSUE alone, both bucket calls): run the pack
+ * only, no NCCL collective even with a communicator -- for callers that move
+ * the bytes themselves (e.g. fsdp_nvls_reduce_scatter_bucket below). */
 fsdp_status fsdp_allgather_bucket(fsdp_ctx* ctx, fsdp_bucket* b, void* ag_staging,
                                   fsdp_stream_t compute, fsdp_stream_t comm, uint32_t flags);
 
@@ -511,6 +514,36 @@ fsdp_status fsdp_p2p_allgather_bucket(fsdp_ctx* ctx, fsdp_bucket* b, const void*
                                       fsdp_stream_t stream);
 fsdp_status fsdp_p2p_reduce_scatter_bucket(fsdp_ctx* ctx, fsdp_bucket* b, const void* const* peer_grads,
                                            fsdp_stream_t stream);
+
+/* ------------------------------------------------ NVLS multicast (K10)
+ * NVLink SHARP: the NVSwitch reduces a load issued to a *multicast* address
+ * across every GPU of the team (multimem.ld_reduce), so a rank reads only its
+ * own reduced chunk -- 1/N of the RS bytes on its NVLink ingress instead of
+ * (N-1)/N.  Setup, one team per buffer (fabric handles, 64 B, exchanged by the
+ * caller, e.g. torch.distributed.all_gather_object):
+ *   rank 0   : fsdp_nvls_create(ctx, bytes, handle64, &m)  -- the multicast
+ *              object for ctx's world devices, its handle, this GPU added;
+ *   others   : fsdp_nvls_import(ctx, handle64, bytes, &m)  -- this GPU added;
+ *   (host barrier: every rank added)
+ *   every rank: fsdp_nvls_bind(m, &uc, &mc, &bytes)  -- this GPU's physical
+ *              memory bound, mapped at `uc` (unicast, this GPU only) and at
+ *              `mc` (multicast, the team); bytes rounded up to the granularity.
+ * Use as RS staging: fsdp_reduce_scatter_bucket(ISSUE | FSDP_NO_COLLECTIVE)
+ * packs (K4) into `uc`; after a cross-rank barrier (every rank packed),
+ * fsdp_nvls_reduce_scatter_bucket(ctx, b, mc, stream) runs K10: grad_shards =
+ * the switch's fp32 sum over ranks of segment `rank` (+ the held shards in
+ * accumulation mode); the next pack into the same staging needs another
+ * barrier (every rank done reading).  The switch's summation order is its
+ * own: results match the oracle within G7's fp32 bound (bit-exact at N <= 2).
+ * Errors: FSDP_ERR_UNSUPPORTED without multicast / fabric-handle support. */
+typedef struct fsdp_nvls fsdp_nvls;
+enum { FSDP_NVLS_HANDLE_BYTES = 64 };
+fsdp_status fsdp_nvls_create(fsdp_ctx* ctx, int64_t bytes, void* handle_out, fsdp_nvls** out);
+fsdp_status fsdp_nvls_import(fsdp_ctx* ctx, const void* handle, int64_t bytes, fsdp_nvls** out);
+fsdp_status fsdp_nvls_bind(fsdp_nvls* m, void** uc_ptr, void** mc_ptr, int64_t* bytes);
+fsdp_status fsdp_nvls_destroy(fsdp_nvls* m);
+fsdp_status fsdp_nvls_reduce_scatter_bucket(fsdp_ctx* ctx, fsdp_bucket* b, const void* mc_staging,
+                                            fsdp_stream_t stream);
 
 /* Cross-rank signalling for the peer-memory path (monotonic 64-bit epochs).
  * fsdp_p2p_signal: one thread stores `value` with release semantics at the

@@ -23,7 +23,8 @@ FSDP_OK, FSDP_ERR_INVALID_ARG, FSDP_ERR_CUDA, FSDP_ERR_NCCL, FSDP_ERR_OOM, FSDP_
 BF16, FP32 = 0, 1
 PLAN_PER_PARAM, PLAN_MANUAL, PLAN_SIZE_CAP, PLAN_GREEDY = range(4)
 PHASE_FWD, PHASE_BWD = 0, 1
-ISSUE, WAIT = 1, 2
+ISSUE, WAIT, NO_COLLECTIVE = 1, 2, 4
+NVLS_HANDLE_BYTES = 64
 (OP_PACK_AG, OP_AG, OP_WAIT_AG, OP_UNPACK, OP_COMPUTE_F, OP_COMPUTE_B, OP_PACK_RS, OP_RS,
  OP_WAIT_RS, OP_COPYOUT_RS) = range(10)
 N_OPS = 10
@@ -41,6 +42,8 @@ EXPORTED = [
     "fsdp_p2p_allgather_bucket", "fsdp_p2p_reduce_scatter_bucket", "fsdp_p2p_signal", "fsdp_p2p_wait",
     "fsdp_ipc_alloc", "fsdp_ipc_open", "fsdp_ipc_close", "fsdp_ipc_free",
     "fsdp_mem_alloc", "fsdp_mem_free", "fsdp_register_buffer",
+    "fsdp_nvls_create", "fsdp_nvls_import", "fsdp_nvls_bind", "fsdp_nvls_destroy",
+    "fsdp_nvls_reduce_scatter_bucket",
     "fsdp_comm_time_ns", "fsdp_simulate_schedule",
 ]
 
@@ -163,6 +166,11 @@ _sigs = {
     "fsdp_mem_alloc": (C.c_int, [_P, C.c_int64, C.POINTER(_P)]),
     "fsdp_mem_free": (C.c_int, [_P, _P]),
     "fsdp_register_buffer": (C.c_int, [_P, _P, C.c_int64, C.c_int32]),
+    "fsdp_nvls_create": (C.c_int, [_P, C.c_int64, _P, C.POINTER(_P)]),
+    "fsdp_nvls_import": (C.c_int, [_P, _P, C.c_int64, C.POINTER(_P)]),
+    "fsdp_nvls_bind": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(C.c_int64)]),
+    "fsdp_nvls_destroy": (C.c_int, [_P]),
+    "fsdp_nvls_reduce_scatter_bucket": (C.c_int, [_P, _P, _P, _P]),
     "fsdp_comm_time_ns": (C.c_int, [C.c_int64, C.POINTER(Link), C.POINTER(C.c_int64)]),
     "fsdp_simulate_schedule": (C.c_int, [C.POINTER(LogEntry), C.c_int32, C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),

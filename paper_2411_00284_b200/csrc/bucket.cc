@@ -24,6 +24,7 @@ cudaStream_t comm_stream(fsdp_ctx* c, fsdp_stream_t s) {
 void destroy_bucket(fsdp_bucket* b) {
   release(&b->ag_pack);
   release(&b->rs_accum);
+  release(&b->nvls_rs);
   release(&b->ag_unpack);
   release(&b->rs_pack);
   release(&b->rs_copyout);
@@ -101,7 +102,7 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   const bool direct = k == 1 && d->fulls && d->params[0].dim0 % N == 0 &&
                       ag_seg == (d->params[0].dim0 / N) * d->params[0].row_numel * ep;
 
-  TableBuilder pack, unpack, rpack, rcopy, raccum, gaps, p2p_ag, p2p_rs;
+  TableBuilder pack, unpack, rpack, rcopy, raccum, nvls, gaps, p2p_ag, p2p_rs;
   for (int32_t j = 0; j < k; ++j) {
     const fsdp_param_desc& p = d->params[j];
     const ShardRows own = shard_rows(p.dim0, N, r);
@@ -179,6 +180,9 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
       // K6 in accumulation mode: grad shard += own segment (pad rows add +0.0)
       raccum.accum(static_cast<uint64_t>(r * rs_seg + rs_off[j]),
                    reinterpret_cast<uint64_t>(d->grad_shards[j]), own.c * R);
+      // K10 (NVLS): own segment summed across GPUs by the switch -> grad shard
+      nvls.nvls(static_cast<uint64_t>(r * rs_seg + rs_off[j]), reinterpret_cast<uint64_t>(d->grad_shards[j]),
+                own.c * R);
     }
   }
   FSDP_CUDA_TRY(cudaSetDevice(ctx->device));
@@ -222,6 +226,7 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   if (st == FSDP_OK) st = upload(rpack, &b->rs_pack);
   if (st == FSDP_OK) st = upload(rcopy, &b->rs_copyout);
   if (st == FSDP_OK) st = upload(raccum, &b->rs_accum);
+  if (st == FSDP_OK) st = upload(nvls, &b->nvls_rs);
   if (st == FSDP_OK && N <= kMaxPeers) st = upload(p2p_ag, &b->p2p_ag);
   if (st == FSDP_OK && N <= kMaxPeers) st = upload(p2p_rs, &b->p2p_rs);
   for (cudaEvent_t* e : {&b->ev_ag_packed, &b->ev_ag_done, &b->ev_rs_packed, &b->ev_rs_done}) {
@@ -380,7 +385,8 @@ static fsdp_status check_call(fsdp_ctx* c, fsdp_bucket* b, void* staging, uint32
   if (!c || !b || !staging) return fail(FSDP_ERR_INVALID_ARG, "NULL argument");
   if (b->ctx != c) return fail(FSDP_ERR_INVALID_ARG, "bucket belongs to another ctx");
   if (reinterpret_cast<uintptr_t>(staging) % 16) return fail(FSDP_ERR_INVALID_ARG, "staging not 16-B aligned");
-  if (!flags || (flags & ~3u)) return fail(FSDP_ERR_INVALID_ARG, "flags must be ISSUE and/or WAIT");
+  if (!(flags & 3u) || (flags & ~7u) || ((flags & FSDP_NO_COLLECTIVE) && (flags & FSDP_WAIT)))
+    return fail(FSDP_ERR_INVALID_ARG, "flags must be ISSUE and/or WAIT (NO_COLLECTIVE only with ISSUE alone)");
   return FSDP_OK;
 }
 
@@ -394,8 +400,9 @@ extern "C" fsdp_status fsdp_allgather_bucket(fsdp_ctx* c, fsdp_bucket* b, void* 
   cudaStream_t ms = resolve_comm(c, comm);
   char* st = static_cast<char*>(staging);
   if (flags & FSDP_ISSUE) {
-    FSDP_TRY(ag_pack(c, b, st, cs, true, nullptr));
-    FSDP_TRY(ag_collective(c, b, st, ms, true, nullptr));
+    const bool coll = !(flags & FSDP_NO_COLLECTIVE);
+    FSDP_TRY(ag_pack(c, b, st, cs, coll, nullptr));
+    FSDP_TRY(ag_collective(c, b, st, ms, coll, nullptr));
   }
   if (flags & FSDP_WAIT) {
     FSDP_TRY(ag_wait(c, b, cs, true));
@@ -415,8 +422,9 @@ extern "C" fsdp_status fsdp_reduce_scatter_bucket(fsdp_ctx* c, fsdp_bucket* b, v
   cudaStream_t ms = resolve_comm(c, comm);
   char* st = static_cast<char*>(staging);
   if (flags & FSDP_ISSUE) {
-    FSDP_TRY(rs_pack(c, b, st, cs, true, nullptr));
-    FSDP_TRY(rs_collective(c, b, st, ms, true, nullptr));
+    const bool coll = !(flags & FSDP_NO_COLLECTIVE);
+    FSDP_TRY(rs_pack(c, b, st, cs, coll, nullptr));
+    FSDP_TRY(rs_collective(c, b, st, ms, coll, nullptr));
   }
   if (flags & FSDP_WAIT) {
     FSDP_TRY(rs_wait(c, b, cs, true));

@@ -152,6 +152,24 @@ void TableBuilder::accum(uint64_t src, uint64_t dst, int64_t elems) {
   }
 }
 
+// K10 (NVLS): fp32 elements reduced by the switch; 4 B read per rank
+// through the multicast address (counted once, the local copy) + 4 B written.
+void TableBuilder::nvls(uint64_t src, uint64_t dst, int64_t elems) {
+  if (elems <= 0) return;
+  bytes_moved += 8 * elems;
+  int64_t body = 0;
+  if (src % 16 == 0 && dst % 16 == 0) body = elems / 4 * 4;
+  const int64_t per_chunk = kChunkBytes / 4;
+  for (int64_t e = 0; e < body; e += per_chunk) {
+    int64_t ne = std::min<int64_t>(per_chunk, body - e);
+    push(chunks, src + 4 * e, dst + 4 * e, static_cast<uint32_t>(ne / 4), OP_NVLS, 16);
+  }
+  for (int64_t e = body; e < elems; e += per_chunk) {
+    int64_t ne = std::min<int64_t>(per_chunk, elems - e);
+    push(chunks, src + 4 * e, dst + 4 * e, static_cast<uint32_t>(ne), OP_NVLS, 4);
+  }
+}
+
 void TableBuilder::peer_reduce(uint64_t src, uint64_t dst, int64_t elems, int eb, int world) {
   if (elems <= 0) return;
   bytes_moved += elems * (static_cast<int64_t>(eb) * world + 4);  // every peer's elements + fp32 write

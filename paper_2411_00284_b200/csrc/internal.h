@@ -85,6 +85,7 @@ enum ChunkOp : uint32_t {
   OP_PEER_REDUCE_F32 = 5,
   OP_NARROW = 6,  // fp32 -> bf16 RNE; unit 16: n groups of 8 elems (32 B in, 16 B out), unit 4: n elems
   OP_ACCUM = 7,   // fp32 dst = dst + src;  unit 16: n groups of 4 elems, unit 4: n elems
+  OP_NVLS = 8,    // K10: fp32 dst (+)= multimem.ld_reduce.add(src); unit 16: n groups of 4, unit 4: n elems
 };
 // Peer-memory copy (K8): OP_COPY chunks whose src is an offset into peer q's
 // segment, q in op_unit bits 24..31.
@@ -120,6 +121,7 @@ struct TableBuilder {
   void scale(uint64_t src, uint64_t dst, int64_t elems);  // f32 -> f32 * s
   void narrow(uint64_t src, uint64_t dst, int64_t elems, uint32_t flags = 0);  // f32 -> bf16 RNE
   void accum(uint64_t src, uint64_t dst, int64_t elems);  // f32 dst += src
+  void nvls(uint64_t src, uint64_t dst, int64_t elems);   // f32 dst = switch-reduced src
   // K9: rank-order sum over peers of `elems` gradient elements of elem_bytes
   // (2 = bf16, 4 = fp32) at offset src of every peer region -> fp32 at dst
   void peer_reduce(uint64_t src, uint64_t dst, int64_t elems, int elem_bytes, int world);
@@ -154,6 +156,9 @@ struct P2PSync {
 };
 cudaError_t launch_p2p_reduce_scatter(const DevTable& t, const PeerTable& pt, int world, float scale,
                                       bool accumulate, cudaStream_t s, int max_ctas, const P2PSync* sync = nullptr);
+// K10: src offsets relative to the multicast mapping of the RS staging.
+cudaError_t launch_nvls_reduce(const DevTable& t, const char* mc_base, bool accumulate, cudaStream_t s,
+                               int max_ctas);
 cudaError_t launch_p2p_signal(const PeerTable& slots, int world, uint64_t value, cudaStream_t s);
 cudaError_t launch_p2p_wait(const void* flags, int world, uint64_t value, int64_t timeout_ns, int* err,
                             cudaStream_t s);
@@ -225,6 +230,7 @@ struct fsdp_bucket {
   std::vector<void*> fulls, grads;
   fsdp::DevTable ag_pack, ag_unpack, rs_pack, rs_copyout;
   fsdp::DevTable rs_accum;           // K6 variant: grad_shards += own segment (accumulation)
+  fsdp::DevTable nvls_rs;            // K10: own segment through the NVLS multicast mapping
   bool grad_accumulate = false;      // fsdp_bucket_set_grad_accumulation
   bool rs_accum_issued = false;      // mode latched by the last rs_pack
   fsdp::DevTable p2p_ag, p2p_rs;  // K8 / K9 tables (peer-memory path)

@@ -758,6 +758,42 @@ __global__ void __launch_bounds__(kThreads, FSDP_K9_MIN_BLOCKS) fsdp_p2p_reduce_
   }
 }
 
+// K10: NVLS reduce-scatter read-out.  Chunk src = offset of this rank's rows in
+// the RS staging, read through its multicast mapping: multimem.ld_reduce makes
+// the NVSwitch return the fp32 sum of that address over every GPU of the team;
+// dst = the gradient shard (absolute), accumulated into when accum.
+__global__ void FSDP_LSU_BOUNDS fsdp_nvls_reduce_scatter_kernel(const Chunk* tab, int n, const char* mc_base,
+                                                                 int accum) {
+  for (int c = blockIdx.x; c < n; c += gridDim.x) {
+    const Chunk ch = tab[c];
+    const char* src = mc_base + ch.src;
+    char* dst = reinterpret_cast<char*>(ch.dst);
+    const uint32_t unit = (ch.op_unit >> 8) & 0xFFu;
+    if (unit == 16) {
+      for (uint32_t i = threadIdx.x; i < ch.n; i += kThreads) {
+        uint4 v;
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(src + 16ull * i)
+                     : "memory");
+        uint4* d = reinterpret_cast<uint4*>(dst) + i;
+        if (accum) v = add4(*d, v);
+        st_v4(d, v);
+      }
+    } else {
+      float* d = reinterpret_cast<float*>(dst);
+      for (uint32_t i = threadIdx.x; i < ch.n; i += kThreads) {
+        uint32_t v;
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];"
+                     : "=r"(v)
+                     : "l"(src + 4ull * i)
+                     : "memory");
+        d[i] = accum ? __fadd_rn(d[i], __uint_as_float(v)) : __uint_as_float(v);
+      }
+    }
+  }
+}
+
 __global__ void fsdp_p2p_signal_kernel(const __grid_constant__ PeerTable slots, int world, unsigned long long value) {
   if (threadIdx.x != 0) return;
   __threadfence_system();
@@ -863,6 +899,15 @@ cudaError_t launch_p2p_reduce_scatter(const DevTable& t, const PeerTable& pt, in
   return cudaGetLastError();
 }
 
+cudaError_t launch_nvls_reduce(const DevTable& t, const char* mc_base, bool accumulate, cudaStream_t s,
+                               int max_ctas) {
+  if (t.n == 0) return cudaSuccess;
+  (void)cudaGetLastError();
+  fsdp_nvls_reduce_scatter_kernel<<<t.n < max_ctas ? t.n : max_ctas, kThreads, 0, s>>>(t.d, t.n, mc_base,
+                                                                                     accumulate ? 1 : 0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_p2p_signal(const PeerTable& slots, int world, uint64_t value, cudaStream_t s) {
   (void)cudaGetLastError();
   fsdp_p2p_signal_kernel<<<1, 32, 0, s>>>(slots, world, static_cast<unsigned long long>(value));
@@ -902,6 +947,7 @@ cudaError_t preload_kernels() {
       reinterpret_cast<const void*>(fsdp_ag_pack_bulk_kernel), reinterpret_cast<const void*>(fsdp_ag_unpack_bulk_kernel),
       reinterpret_cast<const void*>(fsdp_rs_copyout_bulk_kernel), reinterpret_cast<const void*>(fsdp_p2p_allgather_kernel),
       reinterpret_cast<const void*>(fsdp_p2p_reduce_scatter_kernel), reinterpret_cast<const void*>(fsdp_p2p_signal_kernel),
+      reinterpret_cast<const void*>(fsdp_nvls_reduce_scatter_kernel),
       reinterpret_cast<const void*>(fsdp_p2p_wait_kernel), reinterpret_cast<const void*>(fsdp_compute_proxy_kernel)};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);

@@ -294,6 +294,49 @@ def register_buffer(ctx, ptr, nbytes, mode=L.REG_LOCAL):
     check(L.lib.fsdp_register_buffer(ctx.h, ptr, int(nbytes), int(mode)))
 
 
+class Nvls:
+    """NVLS multicast team memory (fsdp_nvls_*).  Rank 0: Nvls(ctx, nbytes);
+    others: Nvls(ctx, nbytes, handle=<rank 0's .handle>); then, after every
+    rank constructed its object (a host barrier), .bind() -> (uc, mc, nbytes)."""
+
+    def __init__(self, ctx, nbytes, handle=None):
+        self.ctx = ctx
+        h = C.c_void_p()
+        if handle is None:
+            buf = (C.c_uint8 * L.NVLS_HANDLE_BYTES)()
+            check(L.lib.fsdp_nvls_create(ctx.h, int(nbytes), C.cast(buf, C.c_void_p), C.byref(h)))
+            self.handle = bytes(buf)
+        else:
+            buf = (C.c_uint8 * L.NVLS_HANDLE_BYTES).from_buffer_copy(handle)
+            check(L.lib.fsdp_nvls_import(ctx.h, C.cast(buf, C.c_void_p), int(nbytes), C.byref(h)))
+            self.handle = bytes(handle)
+        self.h = h
+        self.uc = self.mc = None
+        self.nbytes = int(nbytes)
+
+    def bind(self):
+        uc, mc, n = C.c_void_p(), C.c_void_p(), C.c_int64()
+        check(L.lib.fsdp_nvls_bind(self.h, C.byref(uc), C.byref(mc), C.byref(n)))
+        self.uc, self.mc, self.nbytes = uc.value, mc.value, n.value
+        return self.uc, self.mc, self.nbytes
+
+    def close(self):
+        if self.h:
+            check(L.lib.fsdp_nvls_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nvls_reduce_scatter_bucket(ctx, bucket, mc_staging, stream=0):
+    """K10: grad shards = the switch-reduced own segment of the staging."""
+    check(L.lib.fsdp_nvls_reduce_scatter_bucket(ctx.h, bucket.h, mc_staging, stream or None))
+
+
 # ------------------------------------------------------ cost model / prediction
 def comm_time_ns(nbytes, link):
     """fsdp_comm_time_ns: alpha + ceil(n * beta_fs / 1e6) (P:222)."""
