@@ -470,6 +470,22 @@ typedef struct {
 
 fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, fsdp_step_report* out);
 
+/* CUDA-graph capture of one step (CUDA graphs instead of a tracing
+ * compiler): fsdp_step_graph_create records everything fsdp_run_schedule
+ * would enqueue for `s` -- kernels, NCCL collectives, the events between the
+ * compute and comm streams -- by stream capture from s->compute (thread-local
+ * mode) and instantiates it; fsdp_step_graph_launch replays the whole step
+ * as one launch on `stream`.  Every pointer, proxy length and flag is baked
+ * in at capture: replay with the same buffers.  s->compute must be a
+ * non-default stream; FSDP_SCHED_P2P (its epochs change per step), TIMING,
+ * DRY_RUN and host I/O are rejected (FSDP_ERR_INVALID_ARG).
+ * fsdp_step_graph_info: library kernels / collectives in the captured step. */
+typedef struct fsdp_step_graph fsdp_step_graph;
+fsdp_status fsdp_step_graph_create(fsdp_ctx* ctx, const fsdp_schedule* s, fsdp_step_graph** out);
+fsdp_status fsdp_step_graph_launch(fsdp_step_graph* g, fsdp_stream_t stream);
+fsdp_status fsdp_step_graph_info(const fsdp_step_graph* g, int32_t* kernel_launches, int32_t* collectives);
+fsdp_status fsdp_step_graph_destroy(fsdp_step_graph* g);
+
 /* ------------------------------------------- cost model and prediction
  * fsdp_comm_time_ns: T(n) = alpha_ns + ceil(n * beta_fs_per_byte / 1e6), the
  *   communication model of P:222 in integer units (what Algorithm 1 uses).

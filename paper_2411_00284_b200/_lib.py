@@ -44,6 +44,7 @@ EXPORTED = [
     "fsdp_mem_alloc", "fsdp_mem_free", "fsdp_register_buffer",
     "fsdp_nvls_create", "fsdp_nvls_import", "fsdp_nvls_bind", "fsdp_nvls_destroy",
     "fsdp_nvls_reduce_scatter_bucket",
+    "fsdp_step_graph_create", "fsdp_step_graph_launch", "fsdp_step_graph_info", "fsdp_step_graph_destroy",
     "fsdp_comm_time_ns", "fsdp_simulate_schedule",
 ]
 
@@ -171,6 +172,10 @@ _sigs = {
     "fsdp_nvls_bind": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(C.c_int64)]),
     "fsdp_nvls_destroy": (C.c_int, [_P]),
     "fsdp_nvls_reduce_scatter_bucket": (C.c_int, [_P, _P, _P, _P]),
+    "fsdp_step_graph_create": (C.c_int, [_P, C.POINTER(Schedule), C.POINTER(_P)]),
+    "fsdp_step_graph_launch": (C.c_int, [_P, _P]),
+    "fsdp_step_graph_info": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "fsdp_step_graph_destroy": (C.c_int, [_P]),
     "fsdp_comm_time_ns": (C.c_int, [C.c_int64, C.POINTER(Link), C.POINTER(C.c_int64)]),
     "fsdp_simulate_schedule": (C.c_int, [C.POINTER(LogEntry), C.c_int32, C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),

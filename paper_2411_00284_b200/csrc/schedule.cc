@@ -465,6 +465,74 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   return FSDP_OK;
 }
 
+// ---------------------------------------------------------------- step graph
+struct fsdp_step_graph {
+  int32_t device = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int32_t kernel_launches = 0, collectives = 0;
+};
+
+extern "C" fsdp_status fsdp_step_graph_destroy(fsdp_step_graph* g) {
+  if (!g) return FSDP_OK;
+  cudaSetDevice(g->device);
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+  return FSDP_OK;
+}
+
+extern "C" fsdp_status fsdp_step_graph_create(fsdp_ctx* ctx, const fsdp_schedule* s, fsdp_step_graph** out) {
+  if (!ctx || !s || !out) return fail(FSDP_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  if (s->flags & (FSDP_SCHED_P2P | FSDP_SCHED_TIMING | FSDP_SCHED_DRY_RUN))
+    return fail(FSDP_ERR_INVALID_ARG, "step graph: no P2P (per-step epochs), TIMING or DRY_RUN");
+  if (s->io) return fail(FSDP_ERR_INVALID_ARG, "step graph: host I/O is not captured");
+  if (!s->compute) return fail(FSDP_ERR_INVALID_ARG, "step graph: needs a non-default compute stream");
+  FSDP_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t cs = static_cast<cudaStream_t>(s->compute);
+  (void)resolve_comm(ctx, s->comm);  // create a library-owned comm stream before capture
+  fsdp_step_report rep{};
+  // the whole step -- kernels, NCCL collectives, cross-stream events -- is
+  // recorded from `compute`; the comm stream joins through the event waits
+  FSDP_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  fsdp_status st = fsdp_run_schedule(ctx, s, &rep);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(cs, &graph);
+  if (st != FSDP_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (e != cudaSuccess) return fail(FSDP_ERR_CUDA, std::string("step graph capture: ") + cudaGetErrorString(e));
+  fsdp_step_graph* g = new fsdp_step_graph();
+  g->device = ctx->device;
+  g->graph = graph;
+  g->kernel_launches = rep.kernel_launches;
+  g->collectives = rep.collectives;
+  e = cudaGraphInstantiate(&g->exec, graph, 0);
+  if (e != cudaSuccess) {
+    fsdp_step_graph_destroy(g);
+    return fail(FSDP_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+  }
+  *out = g;
+  return FSDP_OK;
+}
+
+extern "C" fsdp_status fsdp_step_graph_launch(fsdp_step_graph* g, fsdp_stream_t stream) {
+  if (!g) return fail(FSDP_ERR_INVALID_ARG, "NULL graph");
+  FSDP_CUDA_TRY(cudaSetDevice(g->device));
+  FSDP_CUDA_TRY(cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream)));
+  return FSDP_OK;
+}
+
+extern "C" fsdp_status fsdp_step_graph_info(const fsdp_step_graph* g, int32_t* kernel_launches,
+                                            int32_t* collectives) {
+  if (!g) return fail(FSDP_ERR_INVALID_ARG, "NULL graph");
+  if (kernel_launches) *kernel_launches = g->kernel_launches;
+  if (collectives) *collectives = g->collectives;
+  return FSDP_OK;
+}
+
 extern "C" fsdp_status fsdp_proxy_launch(fsdp_ctx* ctx, int64_t iters, int32_t ctas_per_sm, int32_t smem_bytes,
                                          fsdp_stream_t stream) {
   if (!ctx || iters < 0 || ctas_per_sm < 1 || smem_bytes < 0)

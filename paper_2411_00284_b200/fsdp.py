@@ -164,7 +164,7 @@ def reduce_scatter_bucket(ctx, bucket, staging_ptr, compute=0, comm=0, flags=L.I
 
 def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0, comm=0, flags=0,
                  proxy_iters_fwd=None, proxy_iters_bwd=None, proxy_ctas_per_sm=1, proxy_smem_bytes=0,
-                 n_fwd=None, n_bwd=None, want_log=True, p2p=None, io=None, gemm=None):
+                 n_fwd=None, n_bwd=None, want_log=True, p2p=None, io=None, gemm=None, _capture=None):
     """fsdp_run_schedule.  fwd / bwd: Bucket lists in execution order (or
     counts via n_fwd / n_bwd with FSDP_SCHED_DRY_RUN and ctx=None).  Returns the
     step report as a dict (log as a list of (phase, op, bucket, stream, ns)).
@@ -212,6 +212,10 @@ def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0,
                            int(gemm.get("workspace_bytes", 0)))
         keep.append(gc)
         s.gemm = C.pointer(gc)
+    if _capture is not None:     # StepGraph: capture instead of run
+        h = C.c_void_p()
+        check(L.lib.fsdp_step_graph_create(ctx.h, C.byref(s), C.byref(h)))
+        return h
     cap = 5 * nf + 9 * nb + 4
     log = (L.LogEntry * cap)() if want_log else None
     rep = L.StepReport()
@@ -222,6 +226,31 @@ def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0,
     if want_log:
         out["log"] = [(e.phase, e.op, e.bucket, e.stream, e.ns, e.start_ns) for e in log[:rep.log_len]]
     return out
+
+
+class StepGraph:
+    """fsdp_step_graph_*: one step (same arguments as run_schedule) captured
+    into a CUDA graph; .launch(stream) replays it."""
+
+    def __init__(self, ctx, fwd, bwd, **kw):
+        self.h = run_schedule(ctx, fwd, bwd, want_log=False, _capture=True, **kw)
+        k, c = C.c_int32(), C.c_int32()
+        check(L.lib.fsdp_step_graph_info(self.h, C.byref(k), C.byref(c)))
+        self.kernel_launches, self.collectives = k.value, c.value
+
+    def launch(self, stream=0):
+        check(L.lib.fsdp_step_graph_launch(self.h, stream or None))
+
+    def close(self):
+        if self.h:
+            check(L.lib.fsdp_step_graph_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def proxy_launch(ctx, iters, ctas_per_sm=1, smem_bytes=0, stream=0):

@@ -314,6 +314,15 @@ class RankState:
                               proxy_iters_bwd=proxy_bwd, proxy_ctas_per_sm=ctas_per_sm,
                               proxy_smem_bytes=smem, want_log=want_log, p2p=p2p, io=io, gemm=gemm)
 
+    def capture(self, flags, compute, comm, proxy_fwd=None, proxy_bwd=None, ctas_per_sm=1, smem=0, gemm=None):
+        """The same step captured into a CUDA graph (fsdp_step_graph_create)."""
+        return F.StepGraph(self.ctx, self.fwd, self.bwd,
+                           ag_staging=(self.ag_st[0].data_ptr(), self.ag_st[1].data_ptr()),
+                           rs_staging=(self.rs_st[0].data_ptr(), self.rs_st[1].data_ptr()),
+                           compute=compute, comm=comm, flags=flags, proxy_iters_fwd=proxy_fwd,
+                           proxy_iters_bwd=proxy_bwd, proxy_ctas_per_sm=ctas_per_sm, proxy_smem_bytes=smem,
+                           gemm=gemm)
+
     # -------------------------------------------------------------- accounting
     def step_bytes(self):
         """Full (gathered / reduced) bucket bytes one step moves through its

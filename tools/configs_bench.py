@@ -27,7 +27,7 @@ sys.path.insert(0, ROOT)
 
 
 def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, tokens=0, steps=5, warmup=2,
-                link=(20000, 1500), param_dtype=None, nspi=None, predict_link=None):
+                link=(20000, 1500), param_dtype=None, nspi=None, predict_link=None, graph=False):
     import torch
     import paper_2411_00284_b200 as F
     from paper_2411_00284_b200 import _lib as L
@@ -75,6 +75,21 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
                 durs.append(max(ns, 0))
         tot, exp, _, _ = F.simulate_schedule(rep["log"], durs)
         predicted = dict(total_ms=round(tot / 1e6, 3), exposed_ms=round(exp / 1e6, 3))
+    graph_ms = None
+    if graph:
+        # the same step as one CUDA-graph launch (fsdp_step_graph): host enqueue cost removed
+        sg = st.capture(flags, cs.cuda_stream, ms.cuda_stream, pf, pb)
+        for _ in range(3):
+            sg.launch(cs.cuda_stream)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cs)
+        for _ in range(steps):
+            sg.launch(cs.cuda_stream)
+        b.record(cs)
+        torch.cuda.synchronize()
+        graph_ms = a.elapsed_time(b) / steps
+        sg.close()
     op_ns = [sum(r["op_ns"][i] for r in reps) for i in range(L.N_OPS)]
     kb = st.kernel_bytes()
     names = {L.OP_PACK_AG: "K1", L.OP_UNPACK: "K3", L.OP_PACK_RS: "K4", L.OP_COPYOUT_RS: "K6"}
@@ -86,6 +101,8 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
                step_GBps=round((ag_b + rs_b) / (ms_step * 1e-3) / 1e9, 1))
     if predicted:
         res["predicted_N%d" % world] = predicted
+    if graph_ms is not None:
+        res["graph_ms_per_step"] = round(graph_ms, 4)
     del st, loop
     ctx.close()
     gc.collect()
@@ -102,7 +119,8 @@ def c0():
     out = {}
     for name, mode in (("per_param", L.PLAN_PER_PARAM), ("greedy", L.PLAN_GREEDY)):
         out[name] = run_variant(specs, 2, mode, L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT, tc, tc,
-                                mem_max=10**9, link=(10000, 100000), param_dtype=L.FP32, steps=50, warmup=5)
+                                mem_max=10**9, link=(10000, 100000), param_dtype=L.FP32, steps=50, warmup=5,
+                                graph=True)
     return out
 
 
