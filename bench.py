@@ -353,10 +353,10 @@ def main():
     # (1) the headline: K plain steps, no instrumentation -- replayed as one
     #     CUDA graph per step (fsdp_step_graph: the library's whole step,
     #     kernels + NCCL collectives + cross-stream events, captured once) unless
-    #     --eager or the p2p path (its epochs change every step); the eager
-    #     enqueue of the same steps is timed beside it
+    #     --eager (the p2p path replays too: its epochs advance on the device);
+    #     the eager enqueue of the same steps is timed beside it
     sg = None
-    if not args.eager and not p2p:
+    if not args.eager:
         sg = st.capture(flags, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, gemm=gemm)
         for _ in range(args.warmup):
             sg.launch(cs)

@@ -383,7 +383,11 @@ typedef struct {
   uint64_t epoch_base;
   int64_t timeout_ns;           /* per wait; 0 = forever */
   int32_t* error_flag;          /* device int set to 1 by a timed-out wait (nullable) */
-  int32_t reserved[2];
+  uint64_t* epoch_counter;      /* nullable device uint64: if set, every epoch above is
+                                   epoch_base + *epoch_counter (read on the device) and the
+                                   step's last kernel adds n_bwd + 2 to it -- the step can
+                                   then be captured (fsdp_step_graph) and replayed; keep
+                                   epoch_base fixed.  Zero it once before the first step. */
 } fsdp_p2p_schedule;
 
 typedef struct {
@@ -477,8 +481,9 @@ fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, fsdp_step_r
  * mode) and instantiates it; fsdp_step_graph_launch replays the whole step
  * as one launch on `stream`.  Every pointer, proxy length and flag is baked
  * in at capture: replay with the same buffers.  s->compute must be a
- * non-default stream; FSDP_SCHED_P2P (its epochs change per step), TIMING,
- * DRY_RUN and host I/O are rejected (FSDP_ERR_INVALID_ARG).
+ * non-default stream; TIMING,
+ * DRY_RUN and host I/O are rejected, and FSDP_SCHED_P2P unless its
+ * fsdp_p2p_schedule has a device epoch_counter (FSDP_ERR_INVALID_ARG).
  * fsdp_step_graph_info: library kernels / collectives in the captured step. */
 typedef struct fsdp_step_graph fsdp_step_graph;
 fsdp_status fsdp_step_graph_create(fsdp_ctx* ctx, const fsdp_schedule* s, fsdp_step_graph** out);

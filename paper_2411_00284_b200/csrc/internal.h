@@ -159,9 +159,12 @@ cudaError_t launch_p2p_reduce_scatter(const DevTable& t, const PeerTable& pt, in
 // K10: src offsets relative to the multicast mapping of the RS staging.
 cudaError_t launch_nvls_reduce(const DevTable& t, const char* mc_base, bool accumulate, cudaStream_t s,
                                int max_ctas);
-cudaError_t launch_p2p_signal(const PeerTable& slots, int world, uint64_t value, cudaStream_t s);
+// base (nullable): device epoch counter added to `value` at run time
+cudaError_t launch_p2p_signal(const PeerTable& slots, int world, uint64_t value, cudaStream_t s,
+                              const uint64_t* base = nullptr);
 cudaError_t launch_p2p_wait(const void* flags, int world, uint64_t value, int64_t timeout_ns, int* err,
-                            cudaStream_t s);
+                            cudaStream_t s, const uint64_t* base = nullptr);
+cudaError_t launch_p2p_epoch_advance(uint64_t* base, uint64_t inc, cudaStream_t s);
 int device_sm_count(int device);
 cudaError_t preload_kernels();  // defeat lazy loading (see kernels.cu)
 

@@ -794,16 +794,26 @@ __global__ void FSDP_LSU_BOUNDS fsdp_nvls_reduce_scatter_kernel(const Chunk* tab
   }
 }
 
-__global__ void fsdp_p2p_signal_kernel(const __grid_constant__ PeerTable slots, int world, unsigned long long value) {
+// Epoch values are value + *base when `base` (a device-resident epoch
+// counter, see fsdp_p2p_schedule.epoch_counter) is set: a captured step then
+// replays with fresh epochs.
+__global__ void fsdp_p2p_signal_kernel(const __grid_constant__ PeerTable slots, int world, unsigned long long value,
+                                       const unsigned long long* base) {
   if (threadIdx.x != 0) return;
   __threadfence_system();
-  store_flags(slots, world, value);
+  store_flags(slots, world, value + (base ? *base : 0ull));
 }
 
 __global__ void fsdp_p2p_wait_kernel(const unsigned long long* flags, int world, unsigned long long value,
-                                     long long timeout_ns, int* err) {
-  wait_flags(flags, world, value, timeout_ns, err);
+                                     long long timeout_ns, int* err, const unsigned long long* base) {
+  wait_flags(flags, world, value + (base ? *base : 0ull), timeout_ns, err);
   __threadfence_system();
+}
+
+// The step's last p2p kernel: advance the device epoch counter by the epochs
+// one step uses, for the next step (replay).
+__global__ void fsdp_p2p_epoch_advance_kernel(unsigned long long* base, unsigned long long inc) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *base += inc;
 }
 
 // K7: persistent compute proxy.  Four independent FMA chains per thread; the
@@ -908,18 +918,27 @@ cudaError_t launch_nvls_reduce(const DevTable& t, const char* mc_base, bool accu
   return cudaGetLastError();
 }
 
-cudaError_t launch_p2p_signal(const PeerTable& slots, int world, uint64_t value, cudaStream_t s) {
+cudaError_t launch_p2p_signal(const PeerTable& slots, int world, uint64_t value, cudaStream_t s,
+                              const uint64_t* base) {
   (void)cudaGetLastError();
-  fsdp_p2p_signal_kernel<<<1, 32, 0, s>>>(slots, world, static_cast<unsigned long long>(value));
+  fsdp_p2p_signal_kernel<<<1, 32, 0, s>>>(slots, world, static_cast<unsigned long long>(value),
+                                          reinterpret_cast<const unsigned long long*>(base));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_epoch_advance(uint64_t* base, uint64_t inc, cudaStream_t s) {
+  (void)cudaGetLastError();
+  fsdp_p2p_epoch_advance_kernel<<<1, 32, 0, s>>>(reinterpret_cast<unsigned long long*>(base),
+                                                 static_cast<unsigned long long>(inc));
   return cudaGetLastError();
 }
 
 cudaError_t launch_p2p_wait(const void* flags, int world, uint64_t value, int64_t timeout_ns, int* err,
-                            cudaStream_t s) {
+                            cudaStream_t s, const uint64_t* base) {
   (void)cudaGetLastError();
   fsdp_p2p_wait_kernel<<<1, 32, 0, s>>>(static_cast<const unsigned long long*>(flags), world,
                                         static_cast<unsigned long long>(value), static_cast<long long>(timeout_ns),
-                                        err);
+                                        err, reinterpret_cast<const unsigned long long*>(base));
   return cudaGetLastError();
 }
 
@@ -948,6 +967,7 @@ cudaError_t preload_kernels() {
       reinterpret_cast<const void*>(fsdp_rs_copyout_bulk_kernel), reinterpret_cast<const void*>(fsdp_p2p_allgather_kernel),
       reinterpret_cast<const void*>(fsdp_p2p_reduce_scatter_kernel), reinterpret_cast<const void*>(fsdp_p2p_signal_kernel),
       reinterpret_cast<const void*>(fsdp_nvls_reduce_scatter_kernel),
+      reinterpret_cast<const void*>(fsdp_p2p_epoch_advance_kernel),
       reinterpret_cast<const void*>(fsdp_p2p_wait_kernel), reinterpret_cast<const void*>(fsdp_compute_proxy_kernel)};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);

@@ -229,13 +229,14 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   const fsdp_p2p_schedule* pp = p2p ? s->p2p : nullptr;
   PeerTable ready_slots{}, done_slots{};
   auto epoch = [&](int64_t b) { return pp->epoch_base + 2 + static_cast<uint64_t>(b); };
+  const uint64_t* ebase = pp ? pp->epoch_counter : nullptr;  // device epoch counter (nullable)
   auto p2p_wait = [&](const void* flags, uint64_t v, cudaStream_t st) -> fsdp_status {
-    FSDP_CUDA_TRY(launch_p2p_wait(flags, ctx->world, v, pp->timeout_ns, pp->error_flag, st));
+    FSDP_CUDA_TRY(launch_p2p_wait(flags, ctx->world, v, pp->timeout_ns, pp->error_flag, st, ebase));
     ++launches;
     return FSDP_OK;
   };
   auto p2p_signal = [&](const PeerTable& slots, uint64_t v, cudaStream_t st) -> fsdp_status {
-    FSDP_CUDA_TRY(launch_p2p_signal(slots, ctx->world, v, st));
+    FSDP_CUDA_TRY(launch_p2p_signal(slots, ctx->world, v, st, ebase));
     ++launches;
     return FSDP_OK;
   };
@@ -362,6 +363,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
             FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_rs_packed, 0));
             const float inv = 1.0f / static_cast<float>(ctx->world);
 #if FSDP_P2P_FUSED_SYNC
+            if (ebase) return fail(FSDP_ERR_UNSUPPORTED, "fused-sync build: no device epoch counter");
             // one launch: wait "ready" >= E(b), reduce, last CTA signals "consumed" E(b)
             P2PSync sync{static_cast<const unsigned long long*>(pp->ready_flags), epoch(o.bucket),
                          static_cast<long long>(pp->timeout_ns), pp->error_flag, done_slots, epoch(o.bucket),
@@ -431,6 +433,10 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     if (s->n_bwd > 0) FSDP_TRY(p2p_wait(pp->done_flags, epoch(s->n_bwd - 1), cs));
     FSDP_TRY(p2p_signal(ready_slots, epoch(s->n_bwd), cs));
     FSDP_TRY(p2p_wait(pp->ready_flags, epoch(s->n_bwd), cs));
+    if (pp->epoch_counter) {  // the next step (or replay) starts past this step's epochs
+      FSDP_CUDA_TRY(launch_p2p_epoch_advance(pp->epoch_counter, static_cast<uint64_t>(s->n_bwd) + 2, cs));
+      ++launches;
+    }
   }
   if (timing) FSDP_CUDA_TRY(cudaEventRecord(ev[1], cs));
   FSDP_TRY(check_async_error(ctx));
@@ -485,8 +491,10 @@ extern "C" fsdp_status fsdp_step_graph_destroy(fsdp_step_graph* g) {
 extern "C" fsdp_status fsdp_step_graph_create(fsdp_ctx* ctx, const fsdp_schedule* s, fsdp_step_graph** out) {
   if (!ctx || !s || !out) return fail(FSDP_ERR_INVALID_ARG, "NULL argument");
   *out = nullptr;
-  if (s->flags & (FSDP_SCHED_P2P | FSDP_SCHED_TIMING | FSDP_SCHED_DRY_RUN))
-    return fail(FSDP_ERR_INVALID_ARG, "step graph: no P2P (per-step epochs), TIMING or DRY_RUN");
+  if (s->flags & (FSDP_SCHED_TIMING | FSDP_SCHED_DRY_RUN))
+    return fail(FSDP_ERR_INVALID_ARG, "step graph: no TIMING or DRY_RUN");
+  if ((s->flags & FSDP_SCHED_P2P) && (!s->p2p || !s->p2p->epoch_counter))
+    return fail(FSDP_ERR_INVALID_ARG, "step graph with FSDP_SCHED_P2P needs a device epoch_counter");
   if (s->io) return fail(FSDP_ERR_INVALID_ARG, "step graph: host I/O is not captured");
   if (!s->compute) return fail(FSDP_ERR_INVALID_ARG, "step graph: needs a non-default compute stream");
   FSDP_CUDA_TRY(cudaSetDevice(ctx->device));

@@ -256,12 +256,14 @@ class RankState:
         W = self.world
         self.ag_peers = [[shard_base[q] + self.shard_offs[b.members[0]] for q in range(W)] for b in self.fwd + self.bwd]
         self.rs_peers = [[grad_base[q][i % 2] for q in range(W)] for i, b in enumerate(self.bwd)]
-        self.epoch = 0
+        self.epoch = 0   # fixed epoch_base: the epochs advance on the device (epoch_counter)
+        self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=self.shard_buf.device)
 
     def p2p_schedule(self, timeout_ns=10 ** 10):
         return dict(ag_peers=self.ag_peers, rs_peers=self.rs_peers, ready_slots=self.ready_slots,
                     done_slots=self.done_slots, ready_flags=self.ready.data_ptr(), done_flags=self.done.data_ptr(),
-                    epoch_base=self.epoch, timeout_ns=timeout_ns, error_flag=self.p2p_err.data_ptr())
+                    epoch_base=self.epoch, timeout_ns=timeout_ns, error_flag=self.p2p_err.data_ptr(),
+                    epoch_counter=self.epoch_ctr.data_ptr())
 
     def p2p_bytes(self):
         """Algorithmic bytes per step of K8 (peer AG, both phases) and K9 (peer RS)."""
@@ -304,9 +306,7 @@ class RankState:
              want_log=False, io=None, gemm=None):
         p2p = None
         if flags & L.SCHED_P2P:
-            p2p = self.p2p_schedule()
-            if not flags & L.SCHED_NO_COMM:
-                self.epoch += len(self.bwd) + 2
+            p2p = self.p2p_schedule()   # the device epoch counter advances inside the step
         return F.run_schedule(self.ctx, self.fwd, self.bwd,
                               ag_staging=(self.ag_st[0].data_ptr(), self.ag_st[1].data_ptr()),
                               rs_staging=(self.rs_st[0].data_ptr(), self.rs_st[1].data_ptr()),
@@ -316,7 +316,8 @@ class RankState:
 
     def capture(self, flags, compute, comm, proxy_fwd=None, proxy_bwd=None, ctas_per_sm=1, smem=0, gemm=None):
         """The same step captured into a CUDA graph (fsdp_step_graph_create)."""
-        return F.StepGraph(self.ctx, self.fwd, self.bwd,
+        p2p = self.p2p_schedule() if flags & L.SCHED_P2P else None
+        return F.StepGraph(self.ctx, self.fwd, self.bwd, p2p=p2p,
                            ag_staging=(self.ag_st[0].data_ptr(), self.ag_st[1].data_ptr()),
                            rs_staging=(self.rs_st[0].data_ptr(), self.rs_st[1].data_ptr()),
                            compute=compute, comm=comm, flags=flags, proxy_iters_fwd=proxy_fwd,

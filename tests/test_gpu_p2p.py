@@ -217,13 +217,16 @@ def test_p2p_schedule_step_bit_exact(flags):
                 assert np.array_equal(g.get().view(np.uint32), shards_ref[rank][j].reshape(-1).view(np.uint32))
 
 
+@pytest.mark.parametrize("mode", ["eager", "graph"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_p2p_schedule_all_ranks_concurrently(world):
+def test_p2p_schedule_all_ranks_concurrently(world, mode):
     """Every rank of a `world`-way job runs its whole FSDP_SCHED_P2P step at the
     same time on one GPU (own streams per rank), reading the other ranks' real
     buffers and synchronising through the real epoch flags (no pre-set slots):
     two consecutive steps, every rank's full parameters and gradient shards
-    bit-exact against the oracle, no wait times out."""
+    bit-exact against the oracle, no wait times out.  mode "graph": every rank's
+    step captured once (fsdp_step_graph) with a device epoch counter, and the
+    two steps are graph replays whose epochs advance on the device."""
     specs = toy_mlp()
     descs = [(p.dim0, p.row_numel, p.module_id) for p in specs]
     params = [param_tensor(p, "bf16", 900 + i) for i, p in enumerate(specs)]
@@ -274,15 +277,29 @@ def test_p2p_schedule_all_ranks_concurrently(world):
         ranks.append(dict(ctx=ctx, fwd=fwd, bwd=bwd, p2p=p2p, outs=outs, gss=gss,
                           cs=torch.cuda.Stream(), ms=torch.cuda.Stream(priority=-1)))
     torch.cuda.synchronize()
+    flags = L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT | L.SCHED_P2P
+    if mode == "graph":
+        for rk in ranks:
+            rk["ctr"] = torch.zeros(1, dtype=torch.int64, device="cuda")
+            p = dict(rk["p2p"], epoch_base=0, epoch_counter=rk["ctr"].data_ptr())
+            rk["graph"] = F.StepGraph(rk["ctx"], rk["fwd"], rk["bwd"], compute=rk["cs"].cuda_stream,
+                                      comm=rk["ms"].cuda_stream, flags=flags, p2p=p)
     epoch = 0
     for _ in range(2):                       # two steps: epochs keep increasing
         for rk in ranks:                     # enqueue every rank; they run concurrently
-            p = dict(rk["p2p"], epoch_base=epoch)
-            F.run_schedule(rk["ctx"], rk["fwd"], rk["bwd"], compute=rk["cs"].cuda_stream, comm=rk["ms"].cuda_stream,
-                           flags=L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT | L.SCHED_P2P, p2p=p, want_log=False)
+            if mode == "graph":
+                rk["graph"].launch(rk["cs"].cuda_stream)
+            else:
+                p = dict(rk["p2p"], epoch_base=epoch)
+                F.run_schedule(rk["ctx"], rk["fwd"], rk["bwd"], compute=rk["cs"].cuda_stream,
+                               comm=rk["ms"].cuda_stream, flags=flags, p2p=p, want_log=False)
         epoch += len(bplan) + 2
         torch.cuda.synchronize()
         assert int(err.item()) == 0, "an epoch wait timed out"
+    if mode == "graph":
+        assert all(int(rk["ctr"].item()) == 2 * (len(bplan) + 2) for rk in ranks)
+        for rk in ranks:
+            rk["graph"].close()
     _, _, shards_ref = OC.bucketed_reduce_scatter(grads, world, 16)
     for r, rk in enumerate(ranks):
         for (phase, i), (m, out) in rk["outs"].items():
@@ -315,7 +332,7 @@ def test_fused_sync_variant_schedule():
     if not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(B.LIB):   # stale vs the main build
         lib = B.build(defines=["FSDP_P2P_FUSED_SYNC=1"], variant="fusedsync")
     env = dict(os.environ, FSDP_B200_LIB=lib)
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "p2p_schedule",
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "p2p_schedule and not graph",
                         os.path.join(root, "tests", "test_gpu_p2p.py")], env=env, cwd=root,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

@@ -29,6 +29,7 @@ def test_graph_replay_matches_eager_toy(world_comm, flags):
     want_g = [g.get().copy() for g in gs]
     for x in fulls + gs:   # scrub the outputs, then replay
         x.t[x.off:x.off + x.nbytes].fill_(0x6B)
+    torch.cuda.synchronize()   # the scrub (default stream) before the replay (cs)
     g = F.StepGraph(ctx, fwd, bwd, **kw)
     assert g.kernel_launches == rep["kernel_launches"] and g.collectives == rep["collectives"]
     for _ in range(3):
@@ -54,6 +55,7 @@ def test_graph_replay_matches_eager_llama_block():
     want = st.gshard_buf.clone()
     wantf = [t.clone() for t in st.full_slots]
     st.gshard_buf.fill_(0x11)
+    torch.cuda.synchronize()   # the scrub (default stream) before the replay (cs)
     g = st.capture(flags, cs.cuda_stream, ms.cuda_stream)
     g.launch(cs.cuda_stream)
     torch.cuda.synchronize()
