@@ -79,6 +79,9 @@ def parse():
                          "kernels")
     ap.add_argument("--no-variants", action="store_true",
                     help="N=1: skip the predicted exposure of the vanilla and greedy plans")
+    ap.add_argument("--ag", default="flat", choices=["flat", "grouped"],
+                    help="flat: the paper's bucketing (copy-in, one AG of the flat buffer, copy-out); grouped: one "
+                         "NCCL group of per-member AGs straight into the full parameters (FSDP_BUCKET_GROUPED_AG)")
     ap.add_argument("--dist", action="store_true",
                     help="run the torch.distributed / NCCL-communicator path even at --gpus 1 (world 1 with a "
                          "real communicator: checks the N > 1 plumbing on one GPU)")
@@ -287,7 +290,7 @@ def main():
     fplan, bplan = H.plans_for(specs, world, mode, t_fwd, t_bwd, link, link, int(args.mem_limit))
     reg = args.nccl_register if (multi and not p2p and args.nccl_register != "none") else None
     st = H.RankState(specs, world, rank if multi else 0, fplan, bplan, ctx, seed=1234 + rank,
-                     ipc=multi and p2p, nccl_register=reg)
+                     ipc=multi and p2p, nccl_register=reg, ag_grouped=args.ag == "grouped")
     compute = torch.cuda.Stream()
     comm = torch.cuda.Stream(priority=-1)
     cs, ms = compute.cuda_stream, comm.cuda_stream
@@ -556,7 +559,7 @@ def main():
                 "value_def": "sum over ranks of full AG(fwd)+AG(bwd)+RS bucket bytes per second of step time",
                 "bytes_per_rank_step": ag_b + rs_b, "l2": "inputs > L2 (126 MB): 64 GB of bucket traffic per step",
                 "parallelism": "fsdp%d" % world if multi else "fsdp1 (simulated %d)" % world,
-                "nccl_register": reg or "none"},
+                "nccl_register": reg or "none", "ag": args.ag},
             # measured exposure: eager step - the same eager step without collectives / waits
             "exposed_comm_ms": round(ms_eager - ms_compute, 3), "compute_stream_ms": round(ms_compute, 3),
             "profiled_ms_per_step": round(ms_prof, 3),

@@ -226,7 +226,21 @@ typedef struct {
 /* Bucket flags: the caller's storage already is this rank's segment (see
  * "Segment-layout storage" below); validated, FSDP_ERR_INVALID_ARG if the
  * pointers do not follow fsdp_layout's offsets. */
-enum { FSDP_BUCKET_SEGMENT_SHARDS = 1u, FSDP_BUCKET_SEGMENT_GRAD_SHARDS = 2u, FSDP_BUCKET_FP32_MASTER = 4u };
+enum {
+  FSDP_BUCKET_SEGMENT_SHARDS = 1u,
+  FSDP_BUCKET_SEGMENT_GRAD_SHARDS = 2u,
+  FSDP_BUCKET_FP32_MASTER = 4u,
+  FSDP_BUCKET_GROUPED_AG = 8u
+};
+/* FSDP_BUCKET_GROUPED_AG (an alternative to copy-in / copy-out bucketing;
+ * every member's dim0 divisible by the world size, shards and fulls bound,
+ * no FP32_MASTER): the bucket's all-gather is ONE NCCL group of per-member
+ * out-of-place all-gathers, shards[j] (c_j rows) -> fulls[j], so NCCL writes
+ * every rank's rows straight into the full parameters: no staging, no K1
+ * pack, no K3 copy-out, one launch per bucket as with the flat buffer (P:177's
+ * goal), same bytes on the wire.  A layout-only ctx's ISSUE copies this rank's
+ * rows into the full parameters (K1).  The flat layout stays the default (the
+ * paper's design; the grouped form's NCCL efficiency at N > 1 is unmeasured). */
 /* FSDP_BUCKET_FP32_MASTER (mixed precision, "parameters are cast to
  * param_dtype"): the shards are fp32 master weights [c_j, R_j] while the
  * all-gather carries param_dtype = FSDP_BF16; the pack (K1) rounds them to
@@ -261,7 +275,7 @@ typedef struct {
   int64_t p2p_bytes[2];    /* algorithmic bytes per launch of K8 (peer AG) and K9 (peer RS):
                               bytes read from all ranks (local + peers) + bytes written */
   int32_t ag_direct;       /* 1: direct gather (below) */
-  int32_t reserved;
+  int32_t ag_grouped;      /* 1: FSDP_BUCKET_GROUPED_AG */
 } fsdp_bucket_info;
 /* Direct gather: a one-parameter bucket whose dim 0 divides evenly over the
  * world and whose segment has no alignment gap has a gathered buffer that is
@@ -614,9 +628,12 @@ fsdp_status fsdp_register_buffer(fsdp_ctx* ctx, void* dev_ptr, int64_t bytes, in
 /* ----------------------------------------------- compute proxy (K7)
  * A measurement device, not a method step: stands in for the layer compute
  * that the paper's reordering overlaps communication with, so that
- * exposed communication is measurable.  Persistent grid of ctas_per_sm CTAs
- * per SM x 256 threads running `iters` iterations of a dependent FMA chain,
- * each CTA holding smem_bytes of dynamic shared memory. */
+ * exposed communication is measurable.  `iters` iterations of four
+ * independent FMA chains per thread, cut into 16 waves of short CTAs: a grid
+ * of 16 x ctas_per_sm CTAs per SM x 256 threads, each CTA holding smem_bytes
+ * of dynamic shared memory and running ceil(iters / 16) iterations, so that,
+ * like the tiles of a real GEMM, the block scheduler balances it over the SM
+ * room a concurrent collective or copy leaves free. */
 fsdp_status fsdp_proxy_launch(fsdp_ctx* ctx, int64_t iters, int32_t ctas_per_sm, int32_t smem_bytes,
                               fsdp_stream_t stream);
 /* Times fsdp_proxy_launch(iters) on `stream` (median of `reps`) and writes the

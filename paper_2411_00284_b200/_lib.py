@@ -30,7 +30,7 @@ NVLS_HANDLE_BYTES = 64
 N_OPS = 10
 SCHED_REORDER, SCHED_FWD_AG_BEFORE_WAIT, SCHED_BWD_AG_BEFORE_WAIT = 1, 2, 4
 SCHED_NO_COMM, SCHED_DRY_RUN, SCHED_TIMING, SCHED_P2P = 8, 16, 32, 64
-BUCKET_SEGMENT_SHARDS, BUCKET_SEGMENT_GRAD_SHARDS, BUCKET_FP32_MASTER = 1, 2, 4
+BUCKET_SEGMENT_SHARDS, BUCKET_SEGMENT_GRAD_SHARDS, BUCKET_FP32_MASTER, BUCKET_GROUPED_AG = 1, 2, 4, 8
 REG_LOCAL, REG_SYMMETRIC = 0, 1
 
 EXPORTED = [
@@ -88,7 +88,7 @@ class BucketDesc(C.Structure):
 class BucketInfo(C.Structure):
     _fields_ = [("ag_seg_bytes", C.c_int64), ("rs_seg_bytes", C.c_int64), ("kernel_bytes", C.c_int64 * 4),
                 ("kernel_chunks", C.c_int32 * 4), ("ag_zero_copy", C.c_int32), ("rs_zero_copy", C.c_int32),
-                ("p2p_bytes", C.c_int64 * 2), ("ag_direct", C.c_int32), ("reserved", C.c_int32)]
+                ("p2p_bytes", C.c_int64 * 2), ("ag_direct", C.c_int32), ("ag_grouped", C.c_int32)]
 
 
 class P2PSchedule(C.Structure):

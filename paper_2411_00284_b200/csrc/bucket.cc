@@ -45,7 +45,7 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   if (k < 1 || !d->params) return fail(FSDP_ERR_INVALID_ARG, "bucket needs >= 1 member");
   if (d->align_bytes < 1) return fail(FSDP_ERR_INVALID_ARG, "align_bytes < 1");
   if (d->reserved != 0 || (d->flags & ~(FSDP_BUCKET_SEGMENT_SHARDS | FSDP_BUCKET_SEGMENT_GRAD_SHARDS |
-                                        FSDP_BUCKET_FP32_MASTER)))
+                                        FSDP_BUCKET_FP32_MASTER | FSDP_BUCKET_GROUPED_AG)))
     return fail(FSDP_ERR_INVALID_ARG, "unknown bucket flags");
   const int32_t ep = dtype_bytes(d->param_dtype), eg = dtype_bytes(d->grad_dtype);
   if (!ep || !eg) return fail(FSDP_ERR_INVALID_ARG, "unsupported dtype");
@@ -101,6 +101,16 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   // copy-out (the per-parameter collective of the paper's unbucketed graph).
   const bool direct = k == 1 && d->fulls && d->params[0].dim0 % N == 0 &&
                       ag_seg == (d->params[0].dim0 / N) * d->params[0].row_numel * ep;
+  // Grouped all-gather (FSDP_BUCKET_GROUPED_AG): one NCCL group of per-member
+  // out-of-place all-gathers, shard j -> full j; needs N | d_j for every member.
+  const bool grouped = d->flags & FSDP_BUCKET_GROUPED_AG;
+  if (grouped) {
+    if (!d->shards || !d->fulls || master)
+      return fail(FSDP_ERR_INVALID_ARG, "FSDP_BUCKET_GROUPED_AG needs shards and fulls, no FP32_MASTER");
+    for (int32_t j = 0; j < k; ++j)
+      if (d->params[j].dim0 % N)
+        return fail(FSDP_ERR_INVALID_ARG, "FSDP_BUCKET_GROUPED_AG needs every dim0 divisible by the world size");
+  }
 
   TableBuilder pack, unpack, rpack, rcopy, raccum, nvls, gaps, p2p_ag, p2p_rs;
   for (int32_t j = 0; j < k; ++j) {
@@ -109,7 +119,15 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
     const int64_t R = p.row_numel;
     const int64_t ag_end = (j + 1 < k) ? ag_off[j + 1] : ag_seg;
     const int64_t rs_end = (j + 1 < k) ? rs_off[j + 1] : rs_seg;
-    if (d->shards && direct) {
+    if (d->shards && grouped) {
+      // layout-only ctx: this rank's rows straight into the full parameter
+      // (with a communicator the group's all-gathers write every row)
+      const int64_t nb = own.c * R * ep;
+      pack.copy(reinterpret_cast<uint64_t>(d->shards[j]),
+                reinterpret_cast<uint64_t>(d->fulls[j]) + static_cast<uint64_t>(r * nb), nb, kAbsDst);
+      if (ag_zc)
+        gaps.zero(reinterpret_cast<uint64_t>(d->shards[0]) + ag_off[j] + nb, ag_end - ag_off[j] - nb);
+    } else if (d->shards && direct) {
       // own rows straight into the full parameter (used unless the collective
       // sends from segment storage itself)
       const uint64_t src = reinterpret_cast<uint64_t>(d->shards[0]);
@@ -135,7 +153,7 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
     }
     for (int32_t q = 0; q < N; ++q) {
       const ShardRows s = shard_rows(p.dim0, N, q);
-      if (d->fulls && s.v > 0 && !direct) {
+      if (d->fulls && s.v > 0 && !direct && !grouped) {
         // K3: valid rows of rank q's chunk -> rows [q c, q c + v) of the full param
         // (this rank's rows from its segment-layout storage when zero-copy).
         const uint64_t dst = reinterpret_cast<uint64_t>(d->fulls[j]) + static_cast<uint64_t>(s.begin * R * ep);
@@ -201,6 +219,12 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   b->ag_zero_copy = ag_zc;
   b->rs_zero_copy = rs_zc;
   b->ag_direct = direct;
+  b->ag_grouped = grouped;
+  if (grouped)
+    for (int32_t j = 0; j < k; ++j) {
+      b->shard_ptrs.push_back(d->shards[j]);
+      b->own_bytes.push_back((d->params[j].dim0 / N) * d->params[j].row_numel * ep);
+    }
   b->full0 = d->fulls ? static_cast<char*>(d->fulls[0]) : nullptr;
   b->members.assign(d->params, d->params + k);
   for (int32_t j = 0; j < k; ++j) {
@@ -260,9 +284,11 @@ extern "C" fsdp_status fsdp_bucket_query(const fsdp_bucket* b, fsdp_bucket_info*
   out->p2p_bytes[0] = b->p2p_ag.n ? b->p2p_ag.bytes_moved : 0;
   out->p2p_bytes[1] = b->p2p_rs.n ? b->p2p_rs.bytes_moved : 0;
   out->ag_direct = b->ag_direct ? 1 : 0;
-  out->reserved = 0;
   // a direct bucket with segment storage and a communicator never packs
   if (b->ag_direct && b->ag_zero_copy && b->ctx && b->ctx->comm) out->kernel_bytes[0] = 0;
+  // a grouped bucket with a communicator never packs (the group sends from the shards)
+  if (b->ag_grouped && b->ctx && b->ctx->comm) out->kernel_bytes[0] = 0;
+  out->ag_grouped = b->ag_grouped ? 1 : 0;
   return FSDP_OK;
 }
 
@@ -283,7 +309,9 @@ static bool comm_on(fsdp_ctx* c, bool with_comm) { return with_comm && c->comm !
 fsdp_status ag_pack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches) {
   // segment storage: the collective sends from it, no pack -- except for a
   // direct-gather bucket when no collective will write this rank's rows
-  const bool skip = b->ag_direct ? (b->ag_zero_copy && comm_on(c, with_comm)) : b->ag_zero_copy;
+  const bool skip = b->ag_grouped  ? comm_on(c, with_comm)
+                    : b->ag_direct ? (b->ag_zero_copy && comm_on(c, with_comm))
+                                   : b->ag_zero_copy;
   if (!skip) {
     FSDP_CUDA_TRY(launch_table(KK_AG_PACK, b->ag_pack, staging, 1.0f, cs, c->max_ctas));
     if (b->ag_pack.n && launches) ++*launches;
@@ -296,6 +324,22 @@ fsdp_status ag_pack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs,
 fsdp_status ag_collective(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t ms, bool with_comm, int* colls) {
   if (!comm_on(c, with_comm)) return FSDP_OK;
   FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_ag_packed, 0));
+  if (b->ag_grouped) {
+    // one NCCL group: shard j (this rank's c_j rows) -> rows of every rank in full j
+    FSDP_NCCL_TRY(ncclGroupStart());
+    for (size_t j = 0; j < b->shard_ptrs.size(); ++j) {
+      ncclResult_t r = ncclAllGather(b->shard_ptrs[j], b->fulls[j], static_cast<size_t>(b->own_bytes[j]), ncclInt8,
+                                     c->comm, ms);
+      if (r != ncclSuccess) {
+        ncclGroupEnd();
+        return fail(FSDP_ERR_NCCL, std::string("ncclAllGather (grouped): ") + ncclGetErrorString(r));
+      }
+    }
+    FSDP_NCCL_TRY(ncclGroupEnd());
+    FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_done, ms));
+    if (colls) ++*colls;
+    return FSDP_OK;
+  }
   // In place (sendbuff = recvbuff + rank * sendcount), or out of place from
   // segment-layout shard storage; bytes as ncclInt8.
   // A direct-gather bucket gathers into the full parameter itself.

@@ -227,6 +227,9 @@ struct fsdp_bucket {
   char* shard_seg = nullptr;   // this rank's AG segment in shard storage
   char* gshard_seg = nullptr;  // this rank's RS segment in grad-shard storage
   bool ag_direct = false;      // gathered buffer == the (single) full parameter
+  bool ag_grouped = false;     // FSDP_BUCKET_GROUPED_AG: per-member AGs in one NCCL group
+  std::vector<const void*> shard_ptrs;  // grouped: shards[j]
+  std::vector<int64_t> own_bytes;       // grouped: c_j * R_j * e_p
   char* full0 = nullptr;       // fulls[0]
   // members and their full-parameter / full-gradient pointers (linear-layer compute)
   std::vector<fsdp_param_desc> members;

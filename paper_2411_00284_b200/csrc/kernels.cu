@@ -61,6 +61,9 @@
 #ifndef FSDP_K9_MIN_BLOCKS
 #define FSDP_K9_MIN_BLOCKS FSDP_MIN_BLOCKS
 #endif
+#ifndef FSDP_PROXY_WAVES
+#define FSDP_PROXY_WAVES 16  // K7: short CTAs per (SM x ctas_per_sm) slot
+#endif
 #ifndef FSDP_BULK
 #define FSDP_BULK 0  // bulk engine for: 0 none, 1 K3, 2 all pure-copy kernels (K0, K1, K3, K6)
 #endif
@@ -816,8 +819,13 @@ __global__ void fsdp_p2p_epoch_advance_kernel(unsigned long long* base, unsigned
   if (threadIdx.x == 0 && blockIdx.x == 0) *base += inc;
 }
 
-// K7: persistent compute proxy.  Four independent FMA chains per thread; the
-// result is consumed behind an impossible branch so the loop survives.
+// K7: compute proxy.  Four independent FMA chains per thread; the result is
+// consumed behind an impossible branch so the loop survives.  The work is cut
+// into FSDP_PROXY_WAVES short CTAs per (SM x ctas_per_sm) slot, like the tiles
+// of a real GEMM: the block scheduler balances them over whatever SM room is
+// free, so a concurrent kernel (a collective, a copy) stretches the proxy in
+// proportion to the room it takes -- one long CTA per SM instead measured up to
+// 7.7x longer whenever the scheduler had to double CTAs up on some SMs.
 __global__ void __launch_bounds__(256) fsdp_compute_proxy_kernel(long long iters, float* sink) {
   extern __shared__ float smem[];
   float a0 = threadIdx.x * 1e-3f, a1 = a0 + 1.f, a2 = a0 + 2.f, a3 = a0 + 3.f;
@@ -949,7 +957,8 @@ cudaError_t launch_proxy(int64_t iters, int grid, int smem, float* sink, cudaStr
     if (e != cudaSuccess) return e;
   }
   (void)cudaGetLastError();
-  fsdp_compute_proxy_kernel<<<grid, 256, smem, s>>>(static_cast<long long>(iters), sink);
+  const long long per_cta = (static_cast<long long>(iters) + FSDP_PROXY_WAVES - 1) / FSDP_PROXY_WAVES;
+  fsdp_compute_proxy_kernel<<<grid * FSDP_PROXY_WAVES, 256, smem, s>>>(per_cta, sink);
   return cudaGetLastError();
 }
 

@@ -517,7 +517,9 @@ extern "C" fsdp_status fsdp_step_graph_create(fsdp_ctx* ctx, const fsdp_schedule
   g->graph = graph;
   g->kernel_launches = rep.kernel_launches;
   g->collectives = rep.collectives;
-  e = cudaGraphInstantiate(&g->exec, graph, 0);
+  // keep the captured per-kernel stream priorities (the comm stream's NCCL
+  // kernels must still overtake compute-stream CTAs, as in the eager step)
+  e = cudaGraphInstantiate(&g->exec, graph, cudaGraphInstantiateFlagUseNodePriority);
   if (e != cudaSuccess) {
     fsdp_step_graph_destroy(g);
     return fail(FSDP_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));

@@ -140,7 +140,8 @@ class Bucket:
         check(L.lib.fsdp_bucket_query(self.h, C.byref(i)))
         return dict(ag_seg=i.ag_seg_bytes, rs_seg=i.rs_seg_bytes, kernel_bytes=list(i.kernel_bytes),
                     kernel_chunks=list(i.kernel_chunks), ag_zero_copy=bool(i.ag_zero_copy),
-                    rs_zero_copy=bool(i.rs_zero_copy), p2p_bytes=list(i.p2p_bytes), ag_direct=bool(i.ag_direct))
+                    rs_zero_copy=bool(i.rs_zero_copy), p2p_bytes=list(i.p2p_bytes), ag_direct=bool(i.ag_direct),
+                    ag_grouped=bool(i.ag_grouped))
 
     def close(self):
         if self.h:

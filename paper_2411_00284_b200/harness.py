@@ -34,7 +34,8 @@ def _carve(sizes, align=ALIGN):
 
 class RankState:
     def __init__(self, specs, world, rank, fwd_plan, bwd_plan, ctx, param_dtype=L.BF16,
-                 device="cuda", seed=0, fill=True, segment_storage=True, ipc=False, nccl_register=None):
+                 device="cuda", seed=0, fill=True, segment_storage=True, ipc=False, nccl_register=None,
+                 ag_grouped=False):
         # ipc=True: the buffers peers read in the peer-memory path (shard
         # storage, gradient slots) come from fsdp_ipc_alloc so that other
         # processes can map them (setup_p2p_ipc).
@@ -126,6 +127,8 @@ class RankState:
                     flags |= L.BUCKET_SEGMENT_SHARDS
                 if phase == 1 and self._follows_segment(m, self.gs_offs, 4):
                     flags |= L.BUCKET_SEGMENT_GRAD_SHARDS
+                if ag_grouped and all(specs[j].dim0 % world == 0 for j in m):
+                    flags |= L.BUCKET_GROUPED_AG    # per-member AGs in one NCCL group, no copies
                 fbase = self.full_slots[b % 2].data_ptr()
                 gbase = self.grad_slots[b % 2].data_ptr()
                 bk = F.Bucket(ctx, [self.descs[j] for j in m],
