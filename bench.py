@@ -386,6 +386,17 @@ def main():
     if args.trace and rank == 0:
         rep_t = st.step(flags | L.SCHED_TIMING, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, want_log=True)
         H.chrome_trace(rep_t["log"], args.trace)
+    # model check (runs with real collectives): the two-stream simulator fed
+    # with THIS run's measured op durations (collectives included) against the
+    # measured eager step -- the gap is what the model leaves out (SM / HBM
+    # contention between the streams, launch gaps)
+    model_check = None
+    if (multi or p2p) and rank == 0:
+        rep_m = st.step(flags | L.SCHED_TIMING, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, want_log=True,
+                        gemm=gemm)
+        tot_m, exp_m, _, _ = F.simulate_schedule(rep_m["log"], [max(e[4], 0) for e in rep_m["log"]])
+        model_check = {"simulated_ms": round(tot_m / 1e6, 3), "simulated_exposed_ms": round(exp_m / 1e6, 3),
+                       "how": "fsdp_simulate_schedule on one timed step's measured op durations"}
     # (3) compute-stream-only baseline: same ops, no collective, no wait
     step(L.SCHED_NO_COMM)
     ms_compute, _ = timed_loop(L.SCHED_NO_COMM, args.steps)
@@ -564,6 +575,7 @@ def main():
             "exposed_comm_ms": round(ms_eager - ms_compute, 3), "compute_stream_ms": round(ms_compute, 3),
             "profiled_ms_per_step": round(ms_prof, 3),
             "predicted": predicted,
+            "model_check": dict(model_check, measured_eager_ms=round(ms_eager, 3)) if model_check else None,
             "linear_compute": gemm_report,
             "timing": "CUDA-graph replay of the step (fsdp_step_graph)" if sg is not None else "eager enqueue",
             "eager_ms_per_step": round(ms_eager, 3),
