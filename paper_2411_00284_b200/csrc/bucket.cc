@@ -113,6 +113,7 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   }
 
   TableBuilder pack, unpack, rpack, rcopy, raccum, nvls, gaps, p2p_ag, p2p_rs;
+  std::vector<TableBuilder> p2p_ag_by_peer(static_cast<size_t>(N));  // K8 chunks per source rank
   for (int32_t j = 0; j < k; ++j) {
     const fsdp_param_desc& p = d->params[j];
     const ShardRows own = shard_rows(p.dim0, N, r);
@@ -178,9 +179,9 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
       for (int32_t q = 0; q < N; ++q) {
         const ShardRows s = shard_rows(p.dim0, N, q);
         if (s.v > 0)
-          p2p_ag.copy(static_cast<uint64_t>(ag_off[j]),
-                      reinterpret_cast<uint64_t>(d->fulls[j]) + static_cast<uint64_t>(s.begin * R * ep),
-                      s.v * R * ep, static_cast<uint32_t>(q) << kPeerShift);
+          p2p_ag_by_peer[q].copy(static_cast<uint64_t>(ag_off[j]),
+                                 reinterpret_cast<uint64_t>(d->fulls[j]) + static_cast<uint64_t>(s.begin * R * ep),
+                                 s.v * R * ep, static_cast<uint32_t>(q) << kPeerShift);
       }
     }
     if (d->full_grads && d->grad_shards) {
@@ -202,6 +203,26 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
       nvls.nvls(static_cast<uint64_t>(r * rs_seg + rs_off[j]), reinterpret_cast<uint64_t>(d->grad_shards[j]),
                 own.c * R);
     }
+  }
+  // K8 chunk order: round-robin over the source ranks, starting at this rank's
+  // successor.  CTAs take chunks in table order, so at any moment a rank reads
+  // from every peer at once and the ranks start on different peers -- no
+  // peer's NVLink egress is the one all N - 1 readers queue on (as with every
+  // rank walking the sources 0, 1, ... in step).
+  {
+    std::vector<size_t> next(static_cast<size_t>(N), 0);
+    for (bool more = true; more;) {
+      more = false;
+      for (int32_t t = 1; t <= N; ++t) {
+        const int32_t q = (r + t) % N;
+        TableBuilder& src = p2p_ag_by_peer[q];
+        if (next[q] < src.chunks.size()) {
+          p2p_ag.chunks.push_back(src.chunks[next[q]++]);
+          more = true;
+        }
+      }
+    }
+    for (const TableBuilder& tb : p2p_ag_by_peer) p2p_ag.bytes_moved += tb.bytes_moved;
   }
   FSDP_CUDA_TRY(cudaSetDevice(ctx->device));
   fsdp_bucket* b = new fsdp_bucket();
