@@ -1,0 +1,36 @@
+#!/bin/bash
+# Multi-GPU measurement plan (one node, NVSwitch): run when more than one
+# B200 is available.  Writes JSON lines under gpurun_out/scale/.
+#   1. bench.py at N = 2, 4, 8 for the NCCL flat bucketing (default), the
+#      grouped all-gather, NCCL buffer registration (local / symmetric) and the
+#      fused peer-memory collectives;
+#   2. busbw sweeps + alpha/beta fits per (op, N) for NCCL and p2p, the inputs
+#      the greedy planner (Algorithm 1) needs.
+# Usage: bash tools/scale_check.sh [max_gpus]
+set -u
+MAX=${1:-8}
+O=gpurun_out/scale
+mkdir -p $O
+PORT=29900
+run() {  # run <n> <tag> <bench args...>
+  local n=$1 tag=$2
+  shift 2
+  timeout 1800 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+    --master-port $PORT bench.py --gpus $n "$@" > $O/bench_${tag}_N$n.json 2> $O/bench_${tag}_N$n.err
+  echo "N=$n $tag rc=$? $(tail -c 200 $O/bench_${tag}_N$n.json)"
+  PORT=$((PORT + 1))
+}
+for n in 2 4 8; do
+  [ $n -le $MAX ] || continue
+  run $n flat
+  run $n grouped --ag grouped
+  run $n reglocal --nccl-register local
+  run $n regsym --nccl-register symmetric
+  run $n p2p --collective p2p
+  for c in nccl p2p; do
+    timeout 1800 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+      --master-port $PORT tools/busbw_sweep.py --collective $c --out $O/busbw_${c}_N$n.json > $O/busbw_${c}_N$n.log 2>&1
+    echo "busbw N=$n $c rc=$?"
+    PORT=$((PORT + 1))
+  done
+done
