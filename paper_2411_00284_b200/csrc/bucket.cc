@@ -209,14 +209,17 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   // from every peer at once and the ranks start on different peers -- no
   // peer's NVLink egress is the one all N - 1 readers queue on (as with every
   // rank walking the sources 0, 1, ... in step).
+  // Runs of kPeerRun consecutive chunks (256 KiB) keep each source's reads
+  // and each destination's writes DRAM-page friendly.
   {
+    constexpr size_t kPeerRun = 8;
     std::vector<size_t> next(static_cast<size_t>(N), 0);
     for (bool more = true; more;) {
       more = false;
       for (int32_t t = 1; t <= N; ++t) {
         const int32_t q = (r + t) % N;
         TableBuilder& src = p2p_ag_by_peer[q];
-        if (next[q] < src.chunks.size()) {
+        for (size_t u = 0; u < kPeerRun && next[q] < src.chunks.size(); ++u) {
           p2p_ag.chunks.push_back(src.chunks[next[q]++]);
           more = true;
         }
