@@ -383,15 +383,18 @@ def main():
     # (2) the same K steps with a CUDA event pair around every op (per-kernel
     #     device time on the launching stream; synchronises once per step)
     ms_prof, reports = timed_loop(L.SCHED_TIMING, args.steps)
-    if args.trace and rank == 0:
+    # NOTE: every step below runs on EVERY rank (a step holds collectives / epoch
+    # handshakes); only the reporting is rank 0's
+    if args.trace:
         rep_t = st.step(flags | L.SCHED_TIMING, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, want_log=True)
-        H.chrome_trace(rep_t["log"], args.trace)
+        if rank == 0:
+            H.chrome_trace(rep_t["log"], args.trace)
     # model check (runs with real collectives): the two-stream simulator fed
     # with THIS run's measured op durations (collectives included) against the
     # measured eager step -- the gap is what the model leaves out (SM / HBM
     # contention between the streams, launch gaps)
     model_check = None
-    if (multi or p2p) and rank == 0:
+    if multi or p2p:
         rep_m = st.step(flags | L.SCHED_TIMING, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, want_log=True,
                         gemm=gemm)
         tot_m, exp_m, _, _ = F.simulate_schedule(rep_m["log"], [max(e[4], 0) for e in rep_m["log"]])
