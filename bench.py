@@ -60,9 +60,10 @@ def parse():
     ap.add_argument("--trace", default=None, help="write a Chrome trace of one profiled step to this path")
     ap.add_argument("--eager", action="store_true",
                     help="time the eager enqueue of every step instead of the CUDA-graph replay (fsdp_step_graph)")
-    ap.add_argument("--compute", default="proxy", choices=["proxy", "gemm"],
-                    help="bucket compute: calibrated proxy kernel (--tokens) or cuBLASLt linear layers on the "
-                         "gathered parameters (tokens = --tokens or 1024)")
+    ap.add_argument("--compute", default="proxy", choices=["proxy", "gemm", "llama"],
+                    help="bucket compute: calibrated proxy kernel (--tokens), cuBLASLt linear layers on the "
+                         "gathered parameters, or the real Llama-3 layers (attention, SwiGLU, norms, loss) "
+                         "through the schedule's compute hook (tokens = --tokens or 1024; eager timing)")
     ap.add_argument("--pg", default="auto", choices=["auto", "nccl", "gloo"],
                     help="torch.distributed backend for host plumbing (auto: nccl, gloo for p2p)")
     ap.add_argument("--same-device", action="store_true",
@@ -317,15 +318,24 @@ def main():
     if args.bwd_placement == "before":
         flags |= L.SCHED_BWD_AG_BEFORE_WAIT
 
-    gemm = None
+    gemm = model = None
+    if args.compute == "llama":
+        # the real model through the compute hook (fsdp_compute_hook): forward
+        # / backward of every bucket's layers on the gathered parameters, the
+        # weight gradients written where the reduce-scatter reads them
+        from paper_2411_00284_b200.llama_compute import LlamaCompute
+        model = LlamaCompute(st, tokens or 1024)
+        pf = pb = None
     if args.compute == "gemm":
         # linear-layer compute: cuBLASLt bf16 GEMMs on the gathered parameters,
         # the backward writing the gradients the reduce-scatter averages
         gemm = st.setup_gemm(tokens or 1024)
         pf = pb = None
 
+    hook = model.hook if model else None
+
     def step(extra=0):
-        return st.step(flags | extra, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, gemm=gemm)
+        return st.step(flags | extra, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, gemm=gemm, hook=hook)
 
     def barrier():
         if multi:
@@ -359,7 +369,7 @@ def main():
     #     --eager (the p2p path replays too: its epochs advance on the device);
     #     the eager enqueue of the same steps is timed beside it
     sg = None
-    if not args.eager:
+    if not args.eager and model is None:   # a Python hook cannot be baked into a graph
         sg = st.capture(flags, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, gemm=gemm)
         for _ in range(args.warmup):
             sg.launch(cs)
@@ -386,7 +396,8 @@ def main():
     # NOTE: every step below runs on EVERY rank (a step holds collectives / epoch
     # handshakes); only the reporting is rank 0's
     if args.trace:
-        rep_t = st.step(flags | L.SCHED_TIMING, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, want_log=True)
+        rep_t = st.step(flags | L.SCHED_TIMING, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, want_log=True,
+                        gemm=gemm, hook=hook)
         if rank == 0:
             H.chrome_trace(rep_t["log"], args.trace)
     # model check (runs with real collectives): the two-stream simulator fed
@@ -396,7 +407,7 @@ def main():
     model_check = None
     if multi or p2p:
         rep_m = st.step(flags | L.SCHED_TIMING, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, want_log=True,
-                        gemm=gemm)
+                        gemm=gemm, hook=hook)
         tot_m, exp_m, _, _ = F.simulate_schedule(rep_m["log"], [max(e[4], 0) for e in rep_m["log"]])
         model_check = {"simulated_ms": round(tot_m / 1e6, 3), "simulated_exposed_ms": round(exp_m / 1e6, 3),
                        "how": "fsdp_simulate_schedule on one timed step's measured op durations"}
@@ -417,10 +428,10 @@ def main():
     # the compute proxy at --predict-tokens), every collective at alpha + beta n
     # of modelled NVLink 5 (720 GB/s bus, 20 us); no contention modelled.
     predicted = None
-    if not multi and not p2p and (args.predict_tokens or gemm):
+    if not multi and not p2p and (args.predict_tokens or gemm or model):
         beta = round((world - 1) / world / 720e9 * 1e15)
         link = (20000, beta)
-        if gemm:   # the measured GEMMs of this run are the compute
+        if gemm or model:   # the measured compute of this run is the compute
             ppf = ppb = None
         else:
             ptf, ptb = per_param_compute_ns(specs, args.predict_tokens)
@@ -428,13 +439,16 @@ def main():
             ppf = H.proxy_iters(H.bucket_times(fplan, ptf), nspi)
             ppb = H.proxy_iters(H.bucket_times(bplan, ptb), nspi)
         tot, exp = H.predict_exposure(st, flags, cs, ms, ppf, ppb, link, link, args.proxy_ctas, args.proxy_smem,
-                                      gemm=gemm)
-        predicted = {"world": world, "tokens_per_gpu": gemm["tokens"] if gemm else args.predict_tokens,
-                     "compute": "cuBLASLt linear layers (measured)" if gemm else "calibrated proxy (per-op model)",
+                                      gemm=gemm, hook=hook)
+        predicted = {"world": world,
+                     "tokens_per_gpu": gemm["tokens"] if gemm else model.T if model else args.predict_tokens,
+                     "compute": ("cuBLASLt linear layers (measured)" if gemm else
+                                 "Llama-3 layers through the compute hook (measured)" if model else
+                                 "calibrated proxy (per-op model)"),
                      "link_alpha_ns": link[0], "link_beta_fs_per_byte": link[1], "total_ms": round(tot / 1e6, 3),
                      "exposed_ms": round(exp / 1e6, 3), "exposed_comm_ms": round(exp / 1e6, 3),
                      "model": "measured compute-stream ops + alpha/beta NVLink collectives, no contention"}
-        if not gemm and not args.no_variants:
+        if not gemm and not model and not args.no_variants:
             # the north star's comparison: exposure under the greedy plan (Alg. 1)
             # vs the unbucketed, unreordered baseline, same model, same compute
             variants = {}
@@ -460,6 +474,16 @@ def main():
 
     # linear-layer compute throughput (cuBLASLt, tensor cores) of the timed steps
     gemm_report = None
+    if model:
+        ops_ns = sum(r["op_ns"][L.OP_COMPUTE_F] + r["op_ns"][L.OP_COMPUTE_B] for r in reports) / len(reports)
+        tf = model.flops / (ops_ns * 1e-9) / 1e12
+        peak_tf = measured_peak_bf16()
+        gemm_report = {"tokens": model.T, "model": "Llama-3 layers (torch: cuBLAS GEMMs, SDPA causal GQA, RoPE, "
+                                                   "RMSNorm, SwiGLU, cross-entropy) via fsdp_compute_hook",
+                       "tflops_per_step": round(model.flops / 1e12, 2),
+                       "compute_ms_per_step": round(ops_ns / 1e6, 3), "achieved_TFLOPs": round(tf, 1),
+                       "peak_TFLOPs": peak_tf, "frac": round(tf / peak_tf, 3),
+                       "note": "model FLOPs / device time of the COMPUTE ops (library GEMM / attention kernels)"}
     if gemm:
         ops_ns = sum(r["op_ns"][L.OP_COMPUTE_F] + r["op_ns"][L.OP_COMPUTE_B] for r in reports) / len(reports)
         tf = st.gemm_flops / (ops_ns * 1e-9) / 1e12
@@ -515,12 +539,12 @@ def main():
         io = st.host_io(h_sh, h_gs, h2d_s.cuda_stream, d2h_s.cuda_stream)
         h2d_bytes = sum(b.ag_seg for b, p in zip(st.fwd, io["fwd_host_shards"]) if p)
         d2h_bytes = sum(b.rs_seg for b, p in zip(st.bwd, io["bwd_host_grads"]) if p)
-        st.step(flags, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, io=io)   # warm-up
+        st.step(flags, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, io=io, gemm=gemm, hook=hook)   # warm-up
         barrier()
         x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         x0.record(compute)
         for _ in range(args.e2e_steps):
-            st.step(flags, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, io=io)
+            st.step(flags, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, io=io, gemm=gemm, hook=hook)
         x1.record(compute)
         barrier()
         e2e_ms = max_over_ranks(x0.elapsed_time(x1) / args.e2e_steps)
@@ -547,7 +571,7 @@ def main():
     # workload, in a child process of its own (separate allocations and
     # timings), summarised beside the headline
     fused = None
-    if rank == 0 and not multi and not p2p and not args.no_fused_leg:
+    if rank == 0 and not multi and not p2p and not args.no_fused_leg and args.compute == "proxy":
         fused = fused_leg(args)
 
     if rank == 0:
@@ -569,7 +593,9 @@ def main():
                                "fused peer-memory kernels K8/K9 over CUDA IPC mappings of the peers" if multi else
                                "fused peer-memory kernels K8/K9 (peers simulated as separate HBM buffers)"),
                 "buckets_fwd": len(fplan), "buckets_bwd": len(bplan), "param_dtype": "bf16",
-                "reduce_dtype": "fp32", "proxy_tokens_per_gpu": tokens,
+                "reduce_dtype": "fp32", "compute": args.compute,
+                "proxy_tokens_per_gpu": tokens if args.compute == "proxy" else 0,
+                "compute_tokens_per_gpu": (model.T if model else gemm["tokens"] if gemm else tokens),
                 "value_def": "sum over ranks of full AG(fwd)+AG(bwd)+RS bucket bytes per second of step time",
                 "bytes_per_rank_step": ag_b + rs_b, "l2": "inputs > L2 (126 MB): 64 GB of bucket traffic per step",
                 "parallelism": "fsdp%d" % world if multi else "fsdp1 (simulated %d)" % world,

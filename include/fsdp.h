@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define FSDP_ABI_VERSION 1
+#define FSDP_ABI_VERSION 2  /* 2: fsdp_schedule.hook (fsdp_compute_hook) appended */
 
 typedef void* fsdp_stream_t; /* cudaStream_t */
 
@@ -338,7 +338,8 @@ fsdp_status fsdp_bucket_set_grad_accumulation(fsdp_bucket* b, int32_t on);
  *   reorder off: vanilla -- every collective right before its own wait.
  * Buckets are given in each phase's execution order; bucket b uses staging
  * slot b % 2 (ag_staging[2], rs_staging[2], each >= world * the largest
- * segment).  Compute of bucket b = compute-proxy kernel K7 with
+ * segment).  Compute of bucket b = the caller's hook (fsdp_compute_hook), else
+ * linear-layer GEMMs (fsdp_gemm_compute), else compute-proxy kernel K7 with
  * proxy_iters_{fwd,bwd}[b] iterations (NULL or 0 = none).
  * The op sequence is written to report->log (if non-NULL) in host enqueue
  * order as (phase, op, bucket, stream) with op codes FSDP_OP_*; stream 0 =
@@ -422,7 +423,30 @@ typedef struct {
   const fsdp_p2p_schedule* p2p; /* FSDP_SCHED_P2P only, else NULL */
   const struct fsdp_host_io* io; /* host-resident shards / gradient shards, else NULL */
   const struct fsdp_gemm_compute* gemm; /* real linear-layer compute instead of K7, else NULL */
+  const struct fsdp_compute_hook* hook; /* caller's model compute instead of K7 / gemm, else NULL */
 } fsdp_schedule;
+
+/* Caller-supplied model compute (the real block instead
+ * of the proxy).  With `hook` set, the schedule calls
+ *     rc = fn(user, phase, bucket, stream)
+ * on the host, at the point of the host enqueue order where COMPUTE_F (phase
+ * 0) or COMPUTE_B (phase 1) of `bucket` (index in that phase's execution
+ * order) belongs, with `stream` = s->compute.  fn must enqueue the bucket's
+ * compute on `stream` only (it runs after that bucket's WAIT_AG / UNPACK and
+ * before its PACK_RS in stream order): forward reads the gathered full
+ * parameters of the bucket's members; backward reads them and writes the
+ * members' full_grads, which PACK_RS then averages.  It must not synchronise
+ * the comm stream, and it runs once per step.  rc != 0 aborts the step with
+ * FSDP_ERR_INVALID_ARG ("compute hook failed"): work enqueued before it stays
+ * enqueued, so synchronise before reusing the buffers.  Captured by
+ * fsdp_step_graph_create like any other work: a hook that allocates or
+ * synchronises must not be used there.  `hook` takes precedence over `gemm`
+ * and the proxy iterations. */
+typedef int32_t (*fsdp_compute_fn)(void* user, int32_t phase, int32_t bucket, fsdp_stream_t stream);
+typedef struct fsdp_compute_hook {
+  fsdp_compute_fn fn;
+  void* user;
+} fsdp_compute_hook;
 
 /* Linear-layer compute instead of the proxy: every
  * member with row_numel > 1 is treated as a linear layer W [d, R] (out = d,

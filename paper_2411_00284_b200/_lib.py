@@ -108,6 +108,13 @@ class GemmCompute(C.Structure):
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64)]
 
 
+COMPUTE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p)
+
+
+class ComputeHook(C.Structure):
+    _fields_ = [("fn", COMPUTE_FN), ("user", C.c_void_p)]
+
+
 class Schedule(C.Structure):
     _fields_ = [("fwd", C.POINTER(C.c_void_p)), ("bwd", C.POINTER(C.c_void_p)),
                 ("proxy_iters_fwd", C.POINTER(C.c_int64)), ("proxy_iters_bwd", C.POINTER(C.c_int64)),
@@ -115,7 +122,8 @@ class Schedule(C.Structure):
                 ("compute", C.c_void_p), ("comm", C.c_void_p), ("n_fwd", C.c_int32),
                 ("n_bwd", C.c_int32), ("flags", C.c_uint32), ("proxy_ctas_per_sm", C.c_int32),
                 ("proxy_smem_bytes", C.c_int32), ("reserved", C.c_int32), ("p2p", C.POINTER(P2PSchedule)),
-                ("io", C.POINTER(HostIO)), ("gemm", C.POINTER(GemmCompute))]
+                ("io", C.POINTER(HostIO)), ("gemm", C.POINTER(GemmCompute)),
+                ("hook", C.POINTER(ComputeHook))]
 
 
 class LogEntry(C.Structure):

@@ -199,7 +199,8 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   if (s->proxy_ctas_per_sm < 0 || s->proxy_smem_bytes < 0)
     return fail(FSDP_ERR_INVALID_ARG, "bad proxy footprint");
   (void)max_seg;  // slot sizes are the caller's contract (>= world * largest segment)
-  if (s->gemm) {
+  if (s->hook && !s->hook->fn) return fail(FSDP_ERR_INVALID_ARG, "compute hook without fn");
+  if (s->gemm && !s->hook) {
     const fsdp_gemm_compute* g = s->gemm;
     if (g->tokens < 1 || g->tokens > INT32_MAX || !g->x || !g->dy || !g->y || g->workspace_bytes < 0 ||
         (g->workspace_bytes && !g->workspace))
@@ -304,6 +305,11 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   }
   // the compute of a bucket: linear-layer GEMMs (fsdp_gemm_compute) or the K7 proxy
   auto compute = [&](const Op& o, fsdp_bucket* b) -> fsdp_status {
+    if (s->hook) {
+      const int32_t rc = s->hook->fn(s->hook->user, o.phase, o.bucket, static_cast<fsdp_stream_t>(cs));
+      if (rc != 0) return fail(FSDP_ERR_INVALID_ARG, "compute hook failed (rc " + std::to_string(rc) + ")");
+      return FSDP_OK;
+    }
     if (s->gemm) return bucket_compute(ctx, b, s->gemm, o.op == FSDP_OP_COMPUTE_B, cs, &launches);
     const int64_t* it = o.op == FSDP_OP_COMPUTE_F ? s->proxy_iters_fwd : s->proxy_iters_bwd;
     if (it && it[o.bucket] > 0) {

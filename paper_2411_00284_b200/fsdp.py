@@ -165,13 +165,17 @@ def reduce_scatter_bucket(ctx, bucket, staging_ptr, compute=0, comm=0, flags=L.I
 
 def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0, comm=0, flags=0,
                  proxy_iters_fwd=None, proxy_iters_bwd=None, proxy_ctas_per_sm=1, proxy_smem_bytes=0,
-                 n_fwd=None, n_bwd=None, want_log=True, p2p=None, io=None, gemm=None, _capture=None):
+                 n_fwd=None, n_bwd=None, want_log=True, p2p=None, io=None, gemm=None, hook=None,
+                 _capture=None):
     """fsdp_run_schedule.  fwd / bwd: Bucket lists in execution order (or
     counts via n_fwd / n_bwd with FSDP_SCHED_DRY_RUN and ctx=None).  Returns the
     step report as a dict (log as a list of (phase, op, bucket, stream, ns)).
     p2p (with FSDP_SCHED_P2P): dict with ag_peers (rows of world pointers),
     rs_peers, ready_slots, done_slots, ready_flags, done_flags, epoch_base,
-    timeout_ns, error_flag."""
+    timeout_ns, error_flag.
+    hook (fsdp_compute_hook): a Python callable hook(phase, bucket, stream)
+    that enqueues the bucket's model compute on `stream` (a cudaStream_t
+    handle); an exception inside it aborts the step and is re-raised here."""
     nf = len(fwd) if fwd is not None else (n_fwd or 0)
     nb = len(bwd) if bwd is not None else (n_bwd or 0)
     s = L.Schedule()
@@ -214,6 +218,19 @@ def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0,
                            int(gemm.get("workspace_bytes", 0)))
         keep.append(gc)
         s.gemm = C.pointer(gc)
+    hook_exc = []
+    if hook is not None:
+        def _fn(user, phase, bucket, stream):
+            try:
+                hook(phase, bucket, stream or 0)
+                return 0
+            except BaseException as e:  # reported through the status, re-raised below
+                hook_exc.append(e)
+                return 1
+        cb = L.COMPUTE_FN(_fn)
+        hk = L.ComputeHook(cb, None)
+        keep += [cb, hk]
+        s.hook = C.pointer(hk)
     if _capture is not None:     # StepGraph: capture instead of run
         h = C.c_void_p()
         check(L.lib.fsdp_step_graph_create(ctx.h, C.byref(s), C.byref(h)))
@@ -222,7 +239,10 @@ def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0,
     log = (L.LogEntry * cap)() if want_log else None
     rep = L.StepReport()
     rep.log, rep.log_capacity = log, cap if want_log else 0
-    check(L.lib.fsdp_run_schedule(ctx.h if ctx is not None else None, C.byref(s), C.byref(rep)))
+    st = L.lib.fsdp_run_schedule(ctx.h if ctx is not None else None, C.byref(s), C.byref(rep))
+    if hook_exc:
+        raise hook_exc[0]
+    check(st)
     out = dict(step_ns=rep.step_ns, op_ns=list(rep.op_ns), op_count=list(rep.op_count),
                kernel_launches=rep.kernel_launches, collectives=rep.collectives, log_len=rep.log_len)
     if want_log:

@@ -144,6 +144,9 @@ class RankState:
         self.ag_st = [alloc("ag_st%d" % i, world * max_ag + ALIGN, zero=True, collective=True) for i in range(2)]
         self.rs_st = [alloc("rs_st%d" % i, world * max(max_rs, 16) + ALIGN, zero=True, collective=True)
                       for i in range(2)]
+        if torch.device(device).type == "cuda":
+            # fills / zeroing ran on torch's current stream; steps run on the caller's streams
+            torch.cuda.synchronize(device)
 
     def _segment_offsets(self, plan, elem_bytes):
         """Per-parameter byte offsets placing each bucket's members at the
@@ -306,7 +309,7 @@ class RankState:
         return self.gemm
 
     def step(self, flags, compute, comm, proxy_fwd=None, proxy_bwd=None, ctas_per_sm=1, smem=0,
-             want_log=False, io=None, gemm=None):
+             want_log=False, io=None, gemm=None, hook=None):
         p2p = None
         if flags & L.SCHED_P2P:
             p2p = self.p2p_schedule()   # the device epoch counter advances inside the step
@@ -315,7 +318,7 @@ class RankState:
                               rs_staging=(self.rs_st[0].data_ptr(), self.rs_st[1].data_ptr()),
                               compute=compute, comm=comm, flags=flags, proxy_iters_fwd=proxy_fwd,
                               proxy_iters_bwd=proxy_bwd, proxy_ctas_per_sm=ctas_per_sm,
-                              proxy_smem_bytes=smem, want_log=want_log, p2p=p2p, io=io, gemm=gemm)
+                              proxy_smem_bytes=smem, want_log=want_log, p2p=p2p, io=io, gemm=gemm, hook=hook)
 
     def capture(self, flags, compute, comm, proxy_fwd=None, proxy_bwd=None, ctas_per_sm=1, smem=0, gemm=None):
         """The same step captured into a CUDA graph (fsdp_step_graph_create)."""
@@ -420,14 +423,14 @@ def np_dtype(dt):
 
 
 def predict_exposure(st, flags, compute, comm, proxy_fwd, proxy_bwd, link_ag, link_rs, ctas_per_sm=1, smem=0,
-                     gemm=None):
+                     gemm=None, hook=None):
     """Two-stream prediction of the N-rank step (fsdp_simulate_schedule): one
     timed step of this rank gives every compute-stream op its MEASURED
     duration; every collective takes alpha + beta n of its full bucket bytes
     (fsdp_comm_time_ns).  Returns (total_ns, exposed_ns).  A model: no SM /
     HBM contention between the copies and the collectives."""
     rep = st.step(flags | L.SCHED_TIMING, compute, comm, proxy_fwd, proxy_bwd, ctas_per_sm, smem, want_log=True,
-                  gemm=gemm)
+                  gemm=gemm, hook=hook)
     durs = []
     for ph, op, b, _s, ns, _t in rep["log"]:
         bk = (st.fwd if ph == 0 else st.bwd)[b]
