@@ -102,7 +102,13 @@ def build(verbose=False, force=False, defines=None, variant=None):
     if force or variant or _stale(lib, objs):
         _run([nvcc, "-shared", *ARCH, "-o", lib, *objs, "-L", lib_nccl, "-l:libnccl.so.2",
               "-Xlinker", "-rpath," + lib_nccl, "-L", lib_blas, "-l:libcublasLt.so.12",
-              "-Xlinker", "-rpath," + lib_blas, "-cudart", "static"], verbose)
+              "-Xlinker", "-rpath," + lib_blas,
+              # DT_RPATH, not DT_RUNPATH: LD_LIBRARY_PATH (which holds the
+              # system CUDA 12.9 cuBLASLt) must not win over the wheel torch
+              # uses -- two cuBLASLt builds in one process made torch's own
+              # GEMMs fail with CUBLAS_STATUS_INVALID_VALUE when this library
+              # was loaded before torch
+              "-Xlinker", "--disable-new-dtags", "-cudart", "static"], verbose)
     if ptxas_log:
         with open(os.path.join(bdir, "ptxas.log"), "w") as f:
             f.write("\n".join(ptxas_log))

@@ -181,3 +181,20 @@ def test_toy_plan_parity():
         for mode in (PER_PARAM, MANUAL, GREEDY):
             pi = PlanInput(params, 2, tc, (10000, 1000), (10000, 1000), 10**9, mode, phase, param_bytes=4)
             _assert_same(*_both_plans(pi, L.FP32), mode)
+
+
+def test_one_cublaslt_in_process_whatever_the_import_order():
+    """The library loaded before torch must resolve the same cuBLASLt build as
+    torch (DT_RPATH over LD_LIBRARY_PATH): two builds in one process broke
+    torch's own GEMMs (CUBLAS_STATUS_INVALID_VALUE) in the Llama compute hook."""
+    import subprocess
+    import sys
+    code = ("from paper_2411_00284_b200 import _lib\n"
+            "import torch\n"
+            "m = open('/proc/self/maps').read()\n"
+            "print(sorted({l.split()[-1] for l in m.splitlines() if 'libcublasLt' in l}))\n")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr
+    libs = eval(out.stdout.strip().splitlines()[-1])
+    assert len(libs) == 1, libs

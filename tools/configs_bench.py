@@ -6,6 +6,8 @@
   c2  Llama-3-8B Table 5 / Table 6 variants with the compute proxy at T tokens:
       vanilla / +reorder / +bucket / +both / greedy+reorder, 4 placements
   c2w the same at world sizes 2 / 4 / 8 (vanilla, manual+reorder, greedy+reorder)
+  c2m the c2 variants with the real Llama-3 layers through the compute hook,
+      the greedy plan fed with per-parameter compute times measured on the B200
   c3  Llama-3-70B SIZE_CAP bucket-size sweep 25-500 MB at N = 8
   c4  Llama-3-405B one layer at N = 8: one whole-layer bucket vs per-parameter
 
@@ -27,7 +29,8 @@ sys.path.insert(0, ROOT)
 
 
 def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, tokens=0, steps=5, warmup=2,
-                link=(20000, 1500), param_dtype=None, nspi=None, predict_link=None, graph=False):
+                link=(20000, 1500), param_dtype=None, nspi=None, predict_link=None, graph=False, model_T=0,
+                profile=False):
     import torch
     import paper_2411_00284_b200 as F
     from paper_2411_00284_b200 import _lib as L
@@ -37,6 +40,11 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
     fplan, bplan = H.plans_for(specs, world, mode, t_fwd, t_bwd, link, link, mem_max, pdt)
     st = H.RankState(specs, world, 0, fplan, bplan, ctx, param_dtype=pdt)
     cs, ms = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+    hook = None
+    if model_T:   # the real Llama-3 layers through the compute hook instead of the proxy
+        from paper_2411_00284_b200.llama_compute import LlamaCompute
+        lc = LlamaCompute(st, model_T)
+        hook = lc.hook
     pf = pb = None
     if tokens and t_fwd is not None:
         pf = H.proxy_iters(H.bucket_times(fplan, t_fwd), nspi)
@@ -48,13 +56,13 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
         reps = []
         a.record(cs)
         for _ in range(n):
-            reps.append(st.step(flags | extra, cs.cuda_stream, ms.cuda_stream, pf, pb))
+            reps.append(st.step(flags | extra, cs.cuda_stream, ms.cuda_stream, pf, pb, hook=hook))
         b.record(cs)
         torch.cuda.synchronize()
         return a.elapsed_time(b) / n, reps
 
     for _ in range(warmup):
-        st.step(flags, cs.cuda_stream, ms.cuda_stream, pf, pb)
+        st.step(flags, cs.cuda_stream, ms.cuda_stream, pf, pb, hook=hook)
     ms_step, _ = loop(0, steps)
     _, reps = loop(L.SCHED_TIMING, steps)
     predicted = None
@@ -63,7 +71,7 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
         # compute-stream op at its MEASURED duration on this B200 (copies,
         # proxy compute), every collective at alpha + beta n of its bucket
         # (modelled NVLink; no SM / HBM contention)
-        rep = st.step(flags | L.SCHED_TIMING, cs.cuda_stream, ms.cuda_stream, pf, pb, want_log=True)
+        rep = st.step(flags | L.SCHED_TIMING, cs.cuda_stream, ms.cuda_stream, pf, pb, want_log=True, hook=hook)
         durs = []
         for ph, op, b, stream, ns, _t in rep["log"]:
             bk = (st.fwd if ph == 0 else st.bwd)[b]
@@ -75,8 +83,20 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
                 durs.append(max(ns, 0))
         tot, exp, _, _ = F.simulate_schedule(rep["log"], durs)
         predicted = dict(total_ms=round(tot / 1e6, 3), exposed_ms=round(exp / 1e6, 3))
+    measured_tc = None
+    if profile:
+        # per-bucket compute durations of the timed steps (the paper's profiler,
+        # P:219-221): with a per-parameter plan, T_c of every parameter
+        rep = st.step(flags | L.SCHED_TIMING, cs.cuda_stream, ms.cuda_stream, pf, pb, want_log=True, hook=hook)
+        tf, tb = [0] * len(specs), [0] * len(specs)
+        for ph, op, b, _s, ns, _t in rep["log"]:
+            if op in (L.OP_COMPUTE_F, L.OP_COMPUTE_B):
+                bk = (st.fwd if ph == 0 else st.bwd)[b]
+                for j in bk.members:   # a multi-member bucket's time goes to its first member
+                    (tf if ph == 0 else tb)[j] += max(ns, 0) if j == bk.members[0] else 0
+        measured_tc = (tf, tb)
     graph_ms = None
-    if graph:
+    if graph and hook is None:
         # the same step as one CUDA-graph launch (fsdp_step_graph): host enqueue cost removed
         sg = st.capture(flags, cs.cuda_stream, ms.cuda_stream, pf, pb)
         for _ in range(3):
@@ -103,6 +123,8 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
         res["predicted_N%d" % world] = predicted
     if graph_ms is not None:
         res["graph_ms_per_step"] = round(graph_ms, 4)
+    if measured_tc is not None:
+        res["_measured_tc"] = measured_tc
     del st, loop
     ctx.close()
     gc.collect()
@@ -185,6 +207,36 @@ def c2w(worlds=(2, 4, 8), T=1024):
     return out
 
 
+def c2m(tokens=(1024, 4096)):
+    """configs[2] with the REAL Llama-3-8B layers (attention, SwiGLU, norms,
+    loss; paper_2411_00284_b200/llama_compute.py) through the compute hook:
+    per-parameter compute times are first MEASURED with a per-parameter plan
+    (the paper's profiler) and fed to Algorithm 1 for the greedy
+    plan; then the Table 5 / Table 6 variants, each with its N = 8 exposure
+    predicted from its measured compute-stream ops (copies + real compute)."""
+    from paper_2411_00284_b200 import _lib as L
+    from workloads import llama
+    specs = llama("8b")
+    R, FB, BB = L.SCHED_REORDER, L.SCHED_FWD_AG_BEFORE_WAIT, L.SCHED_BWD_AG_BEFORE_WAIT
+    nvl = (20000, 1215)
+    out = {}
+    for T in tokens:
+        rows = {}
+        prof = run_variant(specs, 8, L.PLAN_PER_PARAM, 0, steps=2, warmup=1, link=nvl, predict_link=(nvl, nvl),
+                           model_T=T, profile=True)
+        f, b = prof.pop("_measured_tc")
+        rows["vanilla"] = prof
+        rows["measured_compute_ms"] = {"fwd": round(sum(f) / 1e6, 3), "bwd": round(sum(b) / 1e6, 3)}
+        for name, mode, flags in (("+reorder", L.PLAN_PER_PARAM, R | FB), ("+bucket", L.PLAN_MANUAL, 0),
+                                  ("+reorder&bucket", L.PLAN_MANUAL, R | FB),
+                                  ("greedy+reorder (measured T_c)", L.PLAN_GREEDY, R | FB),
+                                  ("place fwd-after/bwd-before", L.PLAN_MANUAL, R | BB)):
+            rows[name] = run_variant(specs, 8, mode, flags, f, b, mem_max=2 * 10**9, steps=2, warmup=1, link=nvl,
+                                     predict_link=(nvl, nvl), model_T=T)
+        out["T=%d" % T] = rows
+    return out
+
+
 def c3(caps_mb=(25, 50, 100, 200, 500)):
     from paper_2411_00284_b200 import _lib as L
     from workloads import llama
@@ -204,7 +256,8 @@ def c4():
 
 
 def main():
-    which = [a for a in sys.argv[1:] if a in ("c0", "c2", "c2w", "c3", "c4")] or ["c0", "c2", "c2w", "c3", "c4"]
+    which = [a for a in sys.argv[1:] if a in ("c0", "c2", "c2w", "c2m", "c3", "c4")] or ["c0", "c2", "c2w", "c3",
+                                                                                         "c4"]
     res = {}
     for w in which:
         res[w] = globals()[w]()
