@@ -448,6 +448,12 @@ def main():
                      "link_alpha_ns": link[0], "link_beta_fs_per_byte": link[1], "total_ms": round(tot / 1e6, 3),
                      "exposed_ms": round(exp / 1e6, 3), "exposed_comm_ms": round(exp / 1e6, 3),
                      "model": "measured compute-stream ops + alpha/beta NVLink collectives, no contention"}
+        # the paper's other metric (Tables 5 / 6): peak memory of the
+        # step's FSDP buffers under allocate-on-produce / free-after-use (G40),
+        # beside what this library's static two-slot pools hold
+        mp, pools = H.predict_memory(st, flags)
+        predicted["memory_model_peak_GiB"] = round(mp / 2 ** 30, 3)
+        predicted["static_pools_GiB"] = round(pools / 2 ** 30, 3)
         if not gemm and not model and not args.no_variants:
             # the north star's comparison: exposure under the greedy plan (Alg. 1)
             # vs the unbucketed, unreordered baseline, same model, same compute
@@ -463,13 +469,15 @@ def main():
                 vt, ve = H.predict_exposure(vst, vflags, cs, ms, vpf, vpb, link, link, args.proxy_ctas,
                                             args.proxy_smem)
                 variants[name] = {"buckets_fwd": len(vf), "buckets_bwd": len(vb),
-                                  "total_ms": round(vt / 1e6, 3), "exposed_ms": round(ve / 1e6, 3)}
+                                  "total_ms": round(vt / 1e6, 3), "exposed_ms": round(ve / 1e6, 3),
+                                  "memory_model_peak_GiB": round(H.predict_memory(vst, vflags)[0] / 2 ** 30, 3)}
                 del vst
                 gc.collect()
                 torch.cuda.empty_cache()
             variants["manual (per-block) + reorder [this run]"] = {
                 "buckets_fwd": len(fplan), "buckets_bwd": len(bplan),
-                "total_ms": predicted["total_ms"], "exposed_ms": predicted["exposed_ms"]}
+                "total_ms": predicted["total_ms"], "exposed_ms": predicted["exposed_ms"],
+                "memory_model_peak_GiB": predicted["memory_model_peak_GiB"]}
             predicted["variants"] = variants
 
     # linear-layer compute throughput (cuBLASLt, tensor cores) of the timed steps

@@ -546,6 +546,37 @@ fsdp_status fsdp_comm_time_ns(int64_t nbytes, const fsdp_link* link, int64_t* ns
 fsdp_status fsdp_simulate_schedule(const fsdp_log_entry* seq, int32_t n, const int64_t* dur_ns, int64_t* total_ns,
                                    int64_t* exposed_ns, int64_t* start_ns, int64_t* end_ns);
 
+/* fsdp_simulate_memory: peak memory of the step's FSDP buffers (memory is the
+ * paper's other metric, Tables 5 and 6) for an op sequence, as an
+ * allocate-on-produce / free-after-last-use allocator would hold them
+ * (reading G40), walked in sequence order:
+ *   PACK_AG (ph, b): + ag[ph][b]      the flat gathered bucket (N x AG segment)
+ *   UNPACK  (ph, b): + full[ph][b]    the full parameters, then - ag[ph][b]
+ *   COMPUTE_F b    : - full[0][b]     released after forward use
+ *   COMPUTE_B b    : + grad[b]        the full gradients, then - full[1][b]
+ *   PACK_RS b      : + rs[b]          the flat RS input (N x RS segment), then - grad[b]
+ *   COPYOUT_RS b   : - rs[b]
+ *   AG, RS, WAIT_* : nothing (in-place collectives).
+ * The peak is taken after each op's allocation, before its frees; resident
+ * shards, gradient shards and activations are outside the curve.  Bytes per
+ * bucket in the phase's execution order (arrays of n_fwd / n_bwd entries).
+ * Writes the peak and, if `live` is non-NULL, the live bytes after each of
+ * the n entries.  FSDP_ERR_INVALID_ARG for a bucket index out of range, a
+ * negative size or a live total that goes negative (a free before its
+ * allocation).  Host-only. */
+typedef struct {
+  const int64_t* ag_fwd;   /* n_fwd: N x AG segment bytes */
+  const int64_t* full_fwd; /* n_fwd: sum of the members' full parameter bytes */
+  const int64_t* ag_bwd;   /* n_bwd */
+  const int64_t* full_bwd; /* n_bwd */
+  const int64_t* grad_bwd; /* n_bwd: sum of the members' full gradient bytes */
+  const int64_t* rs_bwd;   /* n_bwd: N x RS segment bytes */
+  int32_t n_fwd;
+  int32_t n_bwd;
+} fsdp_mem_sizes;
+fsdp_status fsdp_simulate_memory(const fsdp_log_entry* seq, int32_t n, const fsdp_mem_sizes* sizes,
+                                 int64_t* peak_bytes, int64_t* live);
+
 /* ------------------------------------- peer-memory (fused) collectives
  * The same two collectives as one kernel each over peer memory (NVLink P2P on
  * a multi-GPU node, CUDA IPC mappings; on one GPU, buffers of simulated ranks):

@@ -52,3 +52,54 @@ def simulate(seq, dur, t_coll):
     total = max(t_cmp, t_comm)
     return dict(total=total, exposed=exposed, compute_busy=busy, comm_busy=comm_busy,
                 events=events)
+
+
+# --------------------------------------------------------------- memory curve
+# Memory is the paper's other metric (Table 5 and Table 6 report peak
+# GiB).  Reading G40: the FSDP buffers of a step live like tensors of an
+# allocate-on-produce / free-after-last-use allocator, walked in the
+# sequence's (stream) order:
+#   PACK_AG (ph, b)  allocates the flat gathered buffer  A(ph, b) (P:177 copy-in);
+#   UNPACK  (ph, b)  allocates the full parameters        F(ph, b) (P:177 copy-out),
+#                    then frees A(ph, b);
+#   COMPUTE_F b      frees F(0, b) afterwards: released after forward use;
+#   COMPUTE_B b      allocates the full gradients         G(b), then frees F(1, b);
+#   PACK_RS b        allocates the flat RS input          R(b) (P:179 copy-in),
+#                    then frees G(b);
+#   COPYOUT_RS b     frees R(b) (the gradient shard it fills is resident);
+#   AG, RS, WAIT_*   allocate nothing (in-place collectives).
+# The peak is taken after every allocation, before that op's frees.  Resident
+# shards / gradient shards and activations are outside the curve.
+from .schedule import UNPACK, COMPUTE_F, COMPUTE_B, COPYOUT_RS  # noqa: E402
+
+
+def memory_curve(seq, A, Fp, G, R):
+    """seq: O9 entries (phase, op, bucket, stream).  A(ph, b), Fp(ph, b): flat
+    gathered and full-parameter bytes of bucket b of phase ph; G(b), R(b): full
+    gradient and flat RS-input bytes of backward bucket b.
+    Returns dict(peak, live (after each entry), final)."""
+    live = 0
+    peak = 0
+    after = []
+    for ph, op, b, _stream in seq:
+        if op == PACK_AG:
+            live += A(ph, b)
+            peak = max(peak, live)
+        elif op == UNPACK:
+            live += Fp(ph, b)
+            peak = max(peak, live)
+            live -= A(ph, b)
+        elif op == COMPUTE_F:
+            live -= Fp(ph, b)
+        elif op == COMPUTE_B:
+            live += G(b)
+            peak = max(peak, live)
+            live -= Fp(ph, b)
+        elif op == PACK_RS:
+            live += R(b)
+            peak = max(peak, live)
+            live -= G(b)
+        elif op == COPYOUT_RS:
+            live -= R(b)
+        after.append(live)
+    return dict(peak=peak, live=after, final=live)

@@ -45,7 +45,7 @@ EXPORTED = [
     "fsdp_nvls_create", "fsdp_nvls_import", "fsdp_nvls_bind", "fsdp_nvls_destroy",
     "fsdp_nvls_reduce_scatter_bucket",
     "fsdp_step_graph_create", "fsdp_step_graph_launch", "fsdp_step_graph_info", "fsdp_step_graph_destroy",
-    "fsdp_comm_time_ns", "fsdp_simulate_schedule",
+    "fsdp_comm_time_ns", "fsdp_simulate_schedule", "fsdp_simulate_memory",
 ]
 
 
@@ -126,6 +126,13 @@ class Schedule(C.Structure):
                 ("hook", C.POINTER(ComputeHook))]
 
 
+class MemSizes(C.Structure):
+    _fields_ = [("ag_fwd", C.POINTER(C.c_int64)), ("full_fwd", C.POINTER(C.c_int64)),
+                ("ag_bwd", C.POINTER(C.c_int64)), ("full_bwd", C.POINTER(C.c_int64)),
+                ("grad_bwd", C.POINTER(C.c_int64)), ("rs_bwd", C.POINTER(C.c_int64)),
+                ("n_fwd", C.c_int32), ("n_bwd", C.c_int32)]
+
+
 class LogEntry(C.Structure):
     _fields_ = [("ns", C.c_int64), ("phase", C.c_int32), ("op", C.c_int32), ("bucket", C.c_int32),
                 ("stream", C.c_int32), ("start_ns", C.c_int64)]
@@ -188,6 +195,8 @@ _sigs = {
     "fsdp_simulate_schedule": (C.c_int, [C.POINTER(LogEntry), C.c_int32, C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int64)]),
+    "fsdp_simulate_memory": (C.c_int, [C.POINTER(LogEntry), C.c_int32, C.POINTER(MemSizes),
+                                       C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(lib, _name)

@@ -1,6 +1,7 @@
 // Cost model and two-stream timeline prediction of an op sequence
 // (the paper's auto-wrap estimates exposure from exactly these inputs: T_c per
 // compute node and alpha + beta n per collective).  Host-only.
+#include <algorithm>
 #include <map>
 #include <tuple>
 
@@ -57,5 +58,46 @@ extern "C" fsdp_status fsdp_simulate_schedule(const fsdp_log_entry* seq, int32_t
   }
   *total_ns = std::max(t_cmp, t_comm);
   *exposed_ns = exposed;
+  return FSDP_OK;
+}
+
+// Memory curve of the FSDP buffers (reading G40): allocate on produce, free
+// after the last use, peak after each op's allocation.
+extern "C" fsdp_status fsdp_simulate_memory(const fsdp_log_entry* seq, int32_t n, const fsdp_mem_sizes* sz,
+                                            int64_t* peak_bytes, int64_t* live_out) {
+  if (n < 0 || (n && !seq) || !sz || !peak_bytes || sz->n_fwd < 0 || sz->n_bwd < 0)
+    return fail(FSDP_ERR_INVALID_ARG, "bad simulate_memory arguments");
+  if ((sz->n_fwd && (!sz->ag_fwd || !sz->full_fwd)) ||
+      (sz->n_bwd && (!sz->ag_bwd || !sz->full_bwd || !sz->grad_bwd || !sz->rs_bwd)))
+    return fail(FSDP_ERR_INVALID_ARG, "simulate_memory: NULL size array");
+  int64_t live = 0, peak = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const fsdp_log_entry& e = seq[i];
+    const bool fwd = e.phase == 0;
+    if ((e.phase != 0 && e.phase != 1) || e.bucket < 0 || e.bucket >= (fwd ? sz->n_fwd : sz->n_bwd))
+      return fail(FSDP_ERR_INVALID_ARG, "simulate_memory: bucket out of range");
+    const int32_t b = e.bucket;
+    const int64_t ag = fwd ? sz->ag_fwd[b] : sz->ag_bwd[b];
+    const int64_t full = fwd ? sz->full_fwd[b] : sz->full_bwd[b];
+    const int64_t grad = fwd ? 0 : sz->grad_bwd[b];
+    const int64_t rs = fwd ? 0 : sz->rs_bwd[b];
+    if (ag < 0 || full < 0 || grad < 0 || rs < 0) return fail(FSDP_ERR_INVALID_ARG, "simulate_memory: negative size");
+    auto alloc = [&](int64_t x) {
+      live += x;
+      peak = std::max(peak, live);
+    };
+    switch (e.op) {
+      case FSDP_OP_PACK_AG: alloc(ag); break;
+      case FSDP_OP_UNPACK: alloc(full); live -= ag; break;
+      case FSDP_OP_COMPUTE_F: live -= full; break;
+      case FSDP_OP_COMPUTE_B: alloc(grad); live -= full; break;
+      case FSDP_OP_PACK_RS: alloc(rs); live -= grad; break;
+      case FSDP_OP_COPYOUT_RS: live -= rs; break;
+      default: break;  // AG, RS, WAIT_*: in place
+    }
+    if (live < 0) return fail(FSDP_ERR_INVALID_ARG, "simulate_memory: a buffer freed before it was allocated");
+    if (live_out) live_out[i] = live;
+  }
+  *peak_bytes = peak;
   return FSDP_OK;
 }

@@ -250,6 +250,22 @@ def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0,
     return out
 
 
+def simulate_memory(seq, ag_fwd, full_fwd, ag_bwd, full_bwd, grad_bwd, rs_bwd):
+    """fsdp_simulate_memory.  seq: (phase, op, bucket, stream[, ...]) tuples;
+    per-bucket byte lists in each phase's execution order.  Returns
+    (peak_bytes, live bytes after each entry)."""
+    n = len(seq)
+    arr = (L.LogEntry * max(n, 1))()
+    for i, e in enumerate(seq):
+        arr[i].ns, arr[i].phase, arr[i].op, arr[i].bucket, arr[i].stream = -1, e[0], e[1], e[2], e[3]
+    keep = [L.i64_array(x) for x in (ag_fwd, full_fwd, ag_bwd, full_bwd, grad_bwd, rs_bwd)]
+    sz = L.MemSizes(*keep, len(ag_fwd), len(ag_bwd))
+    peak = C.c_int64()
+    live = (C.c_int64 * max(n, 1))()
+    check(L.lib.fsdp_simulate_memory(arr, n, C.byref(sz), C.byref(peak), live))
+    return peak.value, list(live[:n])
+
+
 class StepGraph:
     """fsdp_step_graph_*: one step (same arguments as run_schedule) captured
     into a CUDA graph; .launch(stream) replays it."""

@@ -422,6 +422,33 @@ def np_dtype(dt):
     return np.uint16 if dt == L.BF16 else np.float32
 
 
+def memory_sizes(st):
+    """Per-bucket bytes of the G40 memory model (fsdp_simulate_memory), in each
+    phase's execution order: flat AG (N x segment), full parameters, full
+    gradients (bf16), flat RS input (N x fp32 segment)."""
+    def full(b):
+        return sum(st.full_numel[j] * st.ep for j in b.members)
+    return dict(ag_fwd=[st.world * b.ag_seg for b in st.fwd], full_fwd=[full(b) for b in st.fwd],
+                ag_bwd=[st.world * b.ag_seg for b in st.bwd], full_bwd=[full(b) for b in st.bwd],
+                grad_bwd=[sum(st.full_numel[j] * 2 for j in b.members) for b in st.bwd],
+                rs_bwd=[st.world * b.rs_seg for b in st.bwd])
+
+
+def predict_memory(st, flags):
+    """Peak bytes of the step's FSDP buffers under the G40 allocate-on-produce /
+    free-after-last-use model, for the op sequence this rank's step enqueues
+    with `flags` (host dry run); and the bytes this library's static pools hold
+    instead (two slots of each kind)."""
+    rep = F.run_schedule(None, None, None, n_fwd=len(st.fwd), n_bwd=len(st.bwd),
+                         flags=(flags & (L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT |
+                                         L.SCHED_BWD_AG_BEFORE_WAIT)) | L.SCHED_DRY_RUN)
+    sz = memory_sizes(st)
+    peak, _ = F.simulate_memory(rep["log"], sz["ag_fwd"], sz["full_fwd"], sz["ag_bwd"], sz["full_bwd"],
+                                sz["grad_bwd"], sz["rs_bwd"])
+    pools = 2 * (st.slot_bytes + st.gslot_bytes + st.ag_st[0].numel() + st.rs_st[0].numel())
+    return peak, pools
+
+
 def predict_exposure(st, flags, compute, comm, proxy_fwd, proxy_bwd, link_ag, link_rs, ctas_per_sm=1, smem=0,
                      gemm=None, hook=None):
     """Two-stream prediction of the N-rank step (fsdp_simulate_schedule): one

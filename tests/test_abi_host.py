@@ -162,6 +162,34 @@ def test_simulator_matches_oracle(kf, kb, reorder, fb, bb, seed):
             assert (s, f) == ev[e[:3]]
 
 
+@given(kf=st.integers(0, 12), kb=st.integers(0, 12), reorder=st.booleans(), fb=st.booleans(), bb=st.booleans(),
+       seed=st.integers(0, 2**31))
+@settings(max_examples=300, deadline=None)
+def test_memory_model_matches_oracle(kf, kb, reorder, fb, bb, seed):
+    """fsdp_simulate_memory == oracle.sim.memory_curve (G40), peak and every live value."""
+    from oracle.sim import memory_curve
+    seq = OS.step_sequence(kf, kb, reorder, OS.BEFORE if fb else OS.AFTER, OS.BEFORE if bb else OS.AFTER)
+    rng = np.random.Generator(np.random.Philox(seed))
+    big = lambda k: [int(x) for x in rng.integers(0, 2 ** 40, size=k)]   # noqa: E731  (> 2^32: 64-bit sums)
+    agf, fuf, agb, fub, grb, rsb = big(kf), big(kf), big(kb), big(kb), big(kb), big(kb)
+    ref = memory_curve(seq, lambda ph, b: (agf if ph == 0 else agb)[b], lambda ph, b: (fuf if ph == 0 else fub)[b],
+                       lambda b: grb[b], lambda b: rsb[b])
+    peak, live = F.simulate_memory(seq, agf, fuf, agb, fub, grb, rsb)
+    assert peak == ref["peak"] and live == ref["live"]
+
+
+def test_memory_model_rejects_bad_input():
+    seq = OS.step_sequence(1, 1, True)
+    one = [1]
+    with pytest.raises(L.FsdpError):
+        F.simulate_memory(seq, one, one, [], [], [], [])            # backward bucket out of range
+    with pytest.raises(L.FsdpError):
+        F.simulate_memory(seq, [-1], one, one, one, one, one)       # negative size
+    with pytest.raises(L.FsdpError):
+        F.simulate_memory([(0, OS.UNPACK, 0, 0), (0, OS.COMPUTE_F, 0, 0), (0, OS.COMPUTE_F, 0, 0)],
+                          one, one, [], [], [], [])                 # freed twice
+
+
 def test_simulator_spec_traces(golden):
     for ex in golden("spec_examples.json")["sim_traces"]:
         if ex["case"] == "compute_only":

@@ -155,3 +155,74 @@ def test_optimum_le_greedy(P, seed, phase):
     pp = PlanInput(params, 4, tc, pi.ag, pi.rs, 10**18, PER_PARAM, phase)
     singles, _ = plan(pp)
     assert best <= _plan_exposure(pp, singles, tc)["total"]
+
+
+# ------------------------------------------------------------ memory curve (G40)
+from oracle.sim import memory_curve  # noqa: E402
+
+
+def _mem(seq, A, Fp, G, R):
+    return memory_curve(seq, lambda ph, b: A[ph][b], lambda ph, b: Fp[ph][b], lambda b: G[b], lambda b: R[b])
+
+
+def test_memory_hand_example():
+    """Two buckets per phase, worked by hand from the G40 rules.
+    A = flat AG, F = full params (same in both phases), G = full grads, R = RS input.
+    Forward vanilla: 20 | 180 -> 160 | 0 | 10 | 90 -> 80 | 0                      peak 180
+    Forward before:  20, 30 | UNPACK 0: 190 -> 170 | C0: 10 | UNPACK 1: 90 -> 80 | 0   peak 190
+    Backward vanilla (fwd-order buckets reversed: b0 = A 10 / F 80 / G 80 / R 320,
+    b1 = A 20 / F 160 / G 160 / R 640):
+      b0: 10 | 90 -> 80 | +G 160 -> 80 | +R 400 -> 320 | 0
+      b1: 20 | 180 -> 160 | +G 320 -> 160 | +R 800 -> 640 | 0                      peak 800"""
+    A = {0: [20, 10], 1: [10, 20]}
+    Fp = {0: [160, 80], 1: [80, 160]}
+    G, R = [80, 160], [320, 640]
+    assert _mem(S.forward_sequence(2, reorder=False), A, Fp, G, R)["peak"] == 180
+    assert _mem(S.forward_sequence(2, reorder=True, placement=S.BEFORE), A, Fp, G, R)["peak"] == 190
+    assert _mem(S.forward_sequence(2, reorder=True, placement=S.AFTER), A, Fp, G, R)["peak"] == 180
+    r = _mem(S.backward_sequence(2, reorder=False), A, Fp, G, R)
+    assert r["peak"] == 800 and r["final"] == 0
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.integers(1, 9), st.integers(0, 10 ** 6))
+def test_memory_closed_forms(k, seed):
+    """Per-phase peaks in closed form (derived from the G40 rules, not by
+    walking the sequence):
+      forward vanilla          max_k A_k + F_k
+      forward before           max_k A_k + A_{k+1} + F_k          (A_K = 0)
+      forward after            max_k max(A_k + F_k, F_k + A_{k+1})
+      backward vanilla         max_j max(A_j + F_j, F_j + G_j, G_j + R_j)"""
+    rng = np.random.default_rng(seed)
+    A = {p: [int(x) for x in rng.integers(1, 10 ** 6, k)] for p in (0, 1)}
+    Fp = {p: [int(x) for x in rng.integers(1, 10 ** 7, k)] for p in (0, 1)}
+    G = [int(x) for x in rng.integers(1, 10 ** 7, k)]
+    R = [int(x) for x in rng.integers(1, 10 ** 7, k)]
+    A0n = A[0] + [0]
+    assert _mem(S.forward_sequence(k, reorder=False), A, Fp, G, R)["peak"] == max(
+        A[0][i] + Fp[0][i] for i in range(k))
+    assert _mem(S.forward_sequence(k, reorder=True, placement=S.BEFORE), A, Fp, G, R)["peak"] == max(
+        A0n[i] + A0n[i + 1] + Fp[0][i] for i in range(k))
+    assert _mem(S.forward_sequence(k, reorder=True, placement=S.AFTER), A, Fp, G, R)["peak"] == max(
+        max(A0n[i] + Fp[0][i], Fp[0][i] + A0n[i + 1]) for i in range(k))
+    assert _mem(S.backward_sequence(k, reorder=False), A, Fp, G, R)["peak"] == max(
+        max(A[1][j] + Fp[1][j], Fp[1][j] + G[j], G[j] + R[j]) for j in range(k))
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.integers(1, 8), st.integers(1, 8), st.integers(0, 10 ** 6),
+       st.sampled_from([S.BEFORE, S.AFTER]), st.sampled_from([S.BEFORE, S.AFTER]))
+def test_memory_conservation_and_reorder_costs_memory(kf, kb, seed, fp, bp):
+    """Every allocation is freed by the end of the step; prefetching (reorder)
+    never lowers the peak below the vanilla order's (Table 5: +reorder raises
+    memory, P:548)."""
+    rng = np.random.default_rng(seed)
+    A = {0: [int(x) for x in rng.integers(1, 10 ** 6, kf)], 1: [int(x) for x in rng.integers(1, 10 ** 6, kb)]}
+    Fp = {0: [int(x) for x in rng.integers(1, 10 ** 7, kf)], 1: [int(x) for x in rng.integers(1, 10 ** 7, kb)]}
+    G = [int(x) for x in rng.integers(1, 10 ** 7, kb)]
+    R = [int(x) for x in rng.integers(1, 10 ** 7, kb)]
+    van = _mem(S.step_sequence(kf, kb, reorder=False), A, Fp, G, R)
+    reo = _mem(S.step_sequence(kf, kb, reorder=True, fwd_placement=fp, bwd_placement=bp), A, Fp, G, R)
+    assert van["final"] == 0 and reo["final"] == 0
+    assert min(van["live"]) >= 0 and min(reo["live"]) >= 0
+    assert reo["peak"] >= van["peak"]

@@ -121,6 +121,12 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
                step_GBps=round((ag_b + rs_b) / (ms_step * 1e-3) / 1e9, 1))
     if predicted:
         res["predicted_N%d" % world] = predicted
+    # peak FSDP-buffer memory of this variant's op order under the G40 model
+    # (the paper's memory column, Tables 5 / 6) and the static pools this
+    # library actually holds
+    mp, pools = H.predict_memory(st, flags)
+    res["memory_model_peak_GiB"] = round(mp / 2 ** 30, 3)
+    res["static_pools_GiB"] = round(pools / 2 ** 30, 3)
     if graph_ms is not None:
         res["graph_ms_per_step"] = round(graph_ms, 4)
     if measured_tc is not None:
