@@ -136,6 +136,25 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def run_env(torch):
+    """GPU / host identity and library versions of this run (SURVEY §8(d)
+    protocol step 6)."""
+    cpu = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), None)
+    except OSError:
+        pass
+    try:
+        nccl = ".".join(str(x) for x in torch.cuda.nccl.version())
+    except Exception:
+        nccl = None
+    return {"gpu": torch.cuda.get_device_name(), "sm_count": torch.cuda.get_device_properties(0).multi_processor_count,
+            "torch": torch.__version__, "cuda_runtime": torch.version.cuda, "nccl": nccl,
+            "host_cpu": cpu, "host_cpus": os.cpu_count(), "affinity_cpus": len(os.sched_getaffinity(0)),
+            "nccl_env": {k: v for k, v in os.environ.items() if k.startswith("NCCL_")}}
+
+
 def measured_peak_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -349,14 +368,21 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    host_enqueue = []
+
     def timed_loop(extra, n, clocks=None):
-        """n steps bracketed by events on the compute stream; max over ranks."""
+        """n steps bracketed by events on the compute stream; max over ranks.
+        Also records the host time to enqueue each step (SURVEY §8(d) protocol
+        step 5: is the eager step launch-bound?)."""
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = []
         a.record(compute)
         for _ in range(n):
+            h0 = time.perf_counter()
             reps.append(step(extra))
+            if extra == 0:
+                host_enqueue.append(time.perf_counter() - h0)
         b.record(compute)
         barrier()
         return max_over_ranks(a.elapsed_time(b) / n), reps
@@ -616,6 +642,8 @@ def main():
             "linear_compute": gemm_report,
             "timing": "CUDA-graph replay of the step (fsdp_step_graph)" if sg is not None else "eager enqueue",
             "eager_ms_per_step": round(ms_eager, 3),
+            "host_enqueue_ms_per_step": (round(1e3 * sorted(host_enqueue)[len(host_enqueue) // 2], 3)
+                                         if host_enqueue else None),
             # the paper's other metric: peak device memory of this rank
             # (torch-allocated buffers: shards, slots, staging; the library's
             # own run tables are a few MB)
@@ -631,6 +659,7 @@ def main():
             "fused_p2p": fused,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
+            "env": run_env(torch),
         }
         print(json.dumps(line), flush=True)
     ctx_close = getattr(ctx, "close", None)

@@ -16,4 +16,5 @@ def test_c_abi_demo():
     assert r.returncode == 0, r.stdout + r.stderr
     assert "all-gather: bit-exact on every rank" in r.stdout
     assert "reduce-scatter(avg): bit-exact on every rank" in r.stdout
+    assert "scheduled step with a C compute hook: hook ran per phase, re-gather bit-exact" in r.stdout
     assert r.stdout.strip().endswith("OK")
