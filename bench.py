@@ -78,6 +78,8 @@ def parse():
                     help="N > 1 NCCL path: allocate the collective buffers with ncclMemAlloc and register them "
                          "(ncclCommRegister / symmetric ncclCommWindowRegister) for zero-copy NVLS / symmetric "
                          "kernels")
+    ap.add_argument("--nccl-max-ctas", type=int, default=0,
+                    help="N > 1 NCCL path: cap NCCL's CTAs per collective (fsdp_ctx_create_config; 0 = NCCL default)")
     ap.add_argument("--no-variants", action="store_true",
                     help="N=1: skip the predicted exposure of the vanilla and greedy plans")
     ap.add_argument("--ag", default="flat", choices=["flat", "grouped"],
@@ -296,7 +298,8 @@ def main():
         else:
             uid = [F.nccl_get_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
-            ctx = F.Ctx(world, rank, local, nccl_uid=uid[0])
+            cfg = dict(max_ctas=args.nccl_max_ctas) if args.nccl_max_ctas > 0 else None
+            ctx = F.Ctx(world, rank, local, nccl_uid=uid[0], nccl_config=cfg)
     else:
         world = args.sim_world
         ctx = F.Ctx(world, 0, local)   # layout-only: rank 0 of a simulated `world`-way job
@@ -554,6 +557,16 @@ def main():
     if multi or p2p:
         coll_ms = {"ag_ms_per_step": round(op_ns[L.OP_AG] / args.steps / 1e6, 3),
                    "rs_ms_per_step": round(op_ns[L.OP_RS] / args.steps / 1e6, 3)}
+    # NCCL's own estimate of this step's collectives (ncclGroupSimulateEnd,
+    # its topology-aware model) beside the event-measured collective time
+    if coll_ms is not None and not p2p:
+        try:
+            est = sum(ctx.nccl_estimate_ns(L.OP_AG, world * b.ag_seg) for b in st.fwd + st.bwd)
+            est_rs = sum(ctx.nccl_estimate_ns(L.OP_RS, world * b.rs_seg) for b in st.bwd)
+            coll_ms["nccl_estimate_ag_ms_per_step"] = round(est / 1e6, 3)
+            coll_ms["nccl_estimate_rs_ms_per_step"] = round(est_rs / 1e6, 3)
+        except Exception as e:   # reported, never fatal
+            coll_ms["nccl_estimate_error"] = str(e)[:200]
     busbw = None
     if multi and op_ns[L.OP_AG] > 0:
         busbw = {"ag": round((world - 1) / world * ag_b * args.steps / (op_ns[L.OP_AG] * 1e-9) / 1e9, 1),

@@ -101,6 +101,34 @@ fsdp_status fsdp_ctx_create(fsdp_ctx** out, int32_t world, int32_t rank, int32_t
                             const void* nccl_uid, void* borrowed_comm);
 fsdp_status fsdp_ctx_destroy(fsdp_ctx* ctx);
 
+/* The same with NCCL communicator settings (used with nccl_uid only; the
+ * library builds the communicator with ncclCommInitRankConfig): bound the SMs
+ * NCCL's kernels take from the compute they overlap -- min_ctas /
+ * max_ctas per collective, nvls_ctas for NVLS kernels, cta_policy
+ * (NCCL_CTA_POLICY_*).  A field <= 0 (cta_policy < 0) keeps NCCL's default.
+ * cfg NULL == fsdp_ctx_create.  FSDP_ERR_INVALID_ARG: cfg with a borrowed
+ * communicator or no nccl_uid, min_ctas > max_ctas. */
+typedef struct {
+  int32_t min_ctas;
+  int32_t max_ctas;
+  int32_t nvls_ctas;
+  int32_t cta_policy;
+} fsdp_nccl_config;
+fsdp_status fsdp_ctx_create_config(fsdp_ctx** out, int32_t world, int32_t rank, int32_t cuda_device,
+                                   const void* nccl_uid, const fsdp_nccl_config* cfg);
+
+/* NCCL's own time estimate for one bucket collective on this ctx's
+ * communicator (ncclGroupSimulateEnd: NCCL's topology-aware model, nothing is
+ * launched) -- a cross-check of the alpha + beta n model (the paper
+ * blames auto-wrap misses on that estimate) and an alternative planner
+ * input.  op: FSDP_OP_AG (bf16 gather of full_bytes in total) or FSDP_OP_RS
+ * (fp32 reduce-scatter, sum, of full_bytes in total).  Writes ns (NCCL's float
+ * microseconds x 1000, rounded).  FSDP_ERR_INVALID_ARG without a
+ * communicator, for another op, full_bytes not a multiple of world x element
+ * size; FSDP_ERR_NCCL if NCCL cannot simulate; FSDP_ERR_UNSUPPORTED if NCCL
+ * returns no estimate (it reports none for a 1-rank communicator). */
+fsdp_status fsdp_nccl_estimate_ns(fsdp_ctx* ctx, int32_t op, int64_t full_bytes, int64_t* ns);
+
 /* 2-D meshes (Tensor Parallel: a parameter "doubly sharded on both
  * Data Parallel (DP) and Tensor Parallel (TP) dimensions ... is first
  * redistributed (via an all-gather) on the DP sub-mesh"): the FSDP path runs

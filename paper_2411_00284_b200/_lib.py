@@ -35,7 +35,7 @@ REG_LOCAL, REG_SYMMETRIC = 0, 1
 
 EXPORTED = [
     "fsdp_last_error", "fsdp_abi_version", "fsdp_nccl_get_unique_id", "fsdp_ctx_create",
-    "fsdp_ctx_destroy", "fsdp_ctx_split", "fsdp_ctx_info", "fsdp_shard", "fsdp_plan_buckets", "fsdp_layout", "fsdp_bucket_create",
+    "fsdp_ctx_destroy", "fsdp_ctx_split", "fsdp_ctx_info", "fsdp_ctx_create_config", "fsdp_nccl_estimate_ns", "fsdp_shard", "fsdp_plan_buckets", "fsdp_layout", "fsdp_bucket_create",
     "fsdp_bucket_destroy", "fsdp_bucket_query", "fsdp_bucket_set_grad_accumulation",
     "fsdp_allgather_bucket", "fsdp_reduce_scatter_bucket",
     "fsdp_run_schedule", "fsdp_proxy_launch", "fsdp_proxy_calibrate",
@@ -133,6 +133,11 @@ class MemSizes(C.Structure):
                 ("n_fwd", C.c_int32), ("n_bwd", C.c_int32)]
 
 
+class NcclConfig(C.Structure):
+    _fields_ = [("min_ctas", C.c_int32), ("max_ctas", C.c_int32), ("nvls_ctas", C.c_int32),
+                ("cta_policy", C.c_int32)]
+
+
 class LogEntry(C.Structure):
     _fields_ = [("ns", C.c_int64), ("phase", C.c_int32), ("op", C.c_int32), ("bucket", C.c_int32),
                 ("stream", C.c_int32), ("start_ns", C.c_int64)]
@@ -152,6 +157,9 @@ _sigs = {
     "fsdp_nccl_get_unique_id": (C.c_int, [_P]),
     "fsdp_ctx_create": (C.c_int, [C.POINTER(_P), C.c_int32, C.c_int32, C.c_int32, _P, _P]),
     "fsdp_ctx_destroy": (C.c_int, [_P]),
+    "fsdp_ctx_create_config": (C.c_int, [C.POINTER(_P), C.c_int32, C.c_int32, C.c_int32, _P,
+                                         C.POINTER(NcclConfig)]),
+    "fsdp_nccl_estimate_ns": (C.c_int, [_P, C.c_int32, C.c_int64, C.POINTER(C.c_int64)]),
     "fsdp_ctx_split": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(_P)]),
     "fsdp_ctx_info": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "fsdp_shard": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(ParamDesc), C.c_int, _P, _P,

@@ -229,8 +229,8 @@ fsdp_status fsdp_nccl_get_unique_id(void* uid128) {
   return FSDP_OK;
 }
 
-fsdp_status fsdp_ctx_create(fsdp_ctx** out, int32_t world, int32_t rank, int32_t cuda_device,
-                            const void* nccl_uid, void* borrowed_comm) {
+static fsdp_status ctx_create(fsdp_ctx** out, int32_t world, int32_t rank, int32_t cuda_device,
+                              const void* nccl_uid, void* borrowed_comm, const fsdp_nccl_config* cfg) {
   if (!out) return fail(FSDP_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   if (world < 1 || rank < 0 || rank >= world) return fail(FSDP_ERR_INVALID_ARG, "bad world/rank");
@@ -262,17 +262,67 @@ fsdp_status fsdp_ctx_create(fsdp_ctx** out, int32_t world, int32_t rank, int32_t
   if (nccl_uid) {
     ncclUniqueId id;
     std::memcpy(&id, nccl_uid, sizeof(id));
-    ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+    ncclResult_t r;
+    if (cfg) {
+      ncclConfig_t nc = NCCL_CONFIG_INITIALIZER;
+      if (cfg->min_ctas > 0) nc.minCTAs = cfg->min_ctas;
+      if (cfg->max_ctas > 0) nc.maxCTAs = cfg->max_ctas;
+      if (cfg->nvls_ctas > 0) nc.nvlsCTAs = cfg->nvls_ctas;
+      if (cfg->cta_policy >= 0) nc.CTAPolicy = cfg->cta_policy;
+      r = ncclCommInitRankConfig(&c->comm, world, id, rank, &nc);
+    } else {
+      r = ncclCommInitRank(&c->comm, world, id, rank);
+    }
     if (r != ncclSuccess) {
       cudaFree(c->sink);
       delete c;
-      return fail(FSDP_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      return fail(FSDP_ERR_NCCL, std::string(cfg ? "ncclCommInitRankConfig: " : "ncclCommInitRank: ") +
+                                     ncclGetErrorString(r));
     }
     c->owns_comm = true;
   } else if (borrowed_comm) {
     c->comm = static_cast<ncclComm_t>(borrowed_comm);
   }
   *out = c;
+  return FSDP_OK;
+}
+
+fsdp_status fsdp_ctx_create(fsdp_ctx** out, int32_t world, int32_t rank, int32_t cuda_device,
+                            const void* nccl_uid, void* borrowed_comm) {
+  return ctx_create(out, world, rank, cuda_device, nccl_uid, borrowed_comm, nullptr);
+}
+
+fsdp_status fsdp_ctx_create_config(fsdp_ctx** out, int32_t world, int32_t rank, int32_t cuda_device,
+                                   const void* nccl_uid, const fsdp_nccl_config* cfg) {
+  if (cfg) {
+    if (!nccl_uid) return fail(FSDP_ERR_INVALID_ARG, "an NCCL config needs nccl_uid (the library builds the comm)");
+    if (cfg->min_ctas > 0 && cfg->max_ctas > 0 && cfg->min_ctas > cfg->max_ctas)
+      return fail(FSDP_ERR_INVALID_ARG, "min_ctas > max_ctas");
+  }
+  return ctx_create(out, world, rank, cuda_device, nccl_uid, nullptr, cfg);
+}
+
+fsdp_status fsdp_nccl_estimate_ns(fsdp_ctx* c, int32_t op, int64_t full_bytes, int64_t* ns) {
+  if (!c || !ns) return fail(FSDP_ERR_INVALID_ARG, "NULL argument");
+  if (!c->comm) return fail(FSDP_ERR_INVALID_ARG, "fsdp_nccl_estimate_ns needs a ctx with a communicator");
+  if (op != FSDP_OP_AG && op != FSDP_OP_RS) return fail(FSDP_ERR_INVALID_ARG, "op must be FSDP_OP_AG or FSDP_OP_RS");
+  const int64_t es = op == FSDP_OP_AG ? 2 : 4;
+  if (full_bytes < 0 || full_bytes % (c->world * es)) return fail(FSDP_ERR_INVALID_ARG, "bad full_bytes");
+  const size_t per_rank = static_cast<size_t>(full_bytes / c->world / es);
+  FSDP_CUDA_TRY(cudaSetDevice(c->device));
+  // nothing is launched: any non-NULL device pointer stands in for the buffers
+  void* dummy = c->sink;
+  ncclSimInfo_t si = NCCL_SIM_INFO_INITIALIZER;
+  FSDP_NCCL_TRY(ncclGroupStart());
+  ncclResult_t r = op == FSDP_OP_AG
+                       ? ncclAllGather(dummy, dummy, per_rank, ncclBfloat16, c->comm, nullptr)
+                       : ncclReduceScatter(dummy, dummy, per_rank, ncclFloat32, ncclSum, c->comm, nullptr);
+  ncclResult_t r2 = ncclGroupSimulateEnd(&si);
+  if (r != ncclSuccess || r2 != ncclSuccess)
+    return fail(FSDP_ERR_NCCL, std::string("ncclGroupSimulateEnd: ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
+  if (!(si.estimatedTime >= 0.0f))  // NCCL_UNDEF_FLOAT: no model for this communicator (e.g. world 1)
+    return fail(FSDP_ERR_UNSUPPORTED, "NCCL gave no time estimate for this communicator");
+  *ns = static_cast<int64_t>(static_cast<double>(si.estimatedTime) * 1000.0 + 0.5);
   return FSDP_OK;
 }
 

@@ -73,16 +73,29 @@ def plan_buckets(params, world, t_compute_ns, ag, rs, mem_max, mode, phase, para
 class Ctx:
     """fsdp_ctx_create / fsdp_ctx_destroy."""
 
-    def __init__(self, world, rank, device=0, nccl_uid=None, borrowed_comm=None):
+    def __init__(self, world, rank, device=0, nccl_uid=None, borrowed_comm=None, nccl_config=None):
+        """nccl_config: dict(min_ctas, max_ctas, nvls_ctas, cta_policy) ->
+        fsdp_ctx_create_config (needs nccl_uid)."""
         self.world, self.rank, self.device = world, rank, device
         h = C.c_void_p()
         uid = None
         if nccl_uid is not None:
             uid = (C.c_uint8 * 128).from_buffer_copy(nccl_uid)
-        check(L.lib.fsdp_ctx_create(C.byref(h), world, rank, device,
-                                    C.cast(uid, C.c_void_p) if uid is not None else None,
-                                    borrowed_comm))
+        uidp = C.cast(uid, C.c_void_p) if uid is not None else None
+        if nccl_config is not None:
+            cfg = L.NcclConfig(int(nccl_config.get("min_ctas", 0)), int(nccl_config.get("max_ctas", 0)),
+                               int(nccl_config.get("nvls_ctas", 0)), int(nccl_config.get("cta_policy", -1)))
+            check(L.lib.fsdp_ctx_create_config(C.byref(h), world, rank, device, uidp, C.byref(cfg)))
+        else:
+            check(L.lib.fsdp_ctx_create(C.byref(h), world, rank, device, uidp, borrowed_comm))
         self.h = h
+
+    def nccl_estimate_ns(self, op, full_bytes):
+        """fsdp_nccl_estimate_ns: NCCL's own estimate (ncclGroupSimulateEnd) for
+        one AG (op = OP_AG, bf16) or RS (op = OP_RS, fp32) of full_bytes."""
+        ns = C.c_int64()
+        check(L.lib.fsdp_nccl_estimate_ns(self.h, int(op), int(full_bytes), C.byref(ns)))
+        return ns.value
 
     def split(self, color, key):
         """fsdp_ctx_split: the sub-mesh ctx (a collective over this ctx's
