@@ -258,8 +258,18 @@ enum {
   FSDP_BUCKET_SEGMENT_SHARDS = 1u,
   FSDP_BUCKET_SEGMENT_GRAD_SHARDS = 2u,
   FSDP_BUCKET_FP32_MASTER = 4u,
-  FSDP_BUCKET_GROUPED_AG = 8u
+  FSDP_BUCKET_GROUPED_AG = 8u,
+  FSDP_BUCKET_BF16_GRAD_SHARDS = 16u
 };
+/* FSDP_BUCKET_BF16_GRAD_SHARDS (reading G41; the north star's "1 bf16 ulp
+ * after cast"): grad_shards[j] are bf16 [c_j, R_j]; the RS still reduces in
+ * fp32 (reduce_dtype) and K6 rounds this rank's fp32 segment to bf16
+ * (RNE, one rounding) while copying it out.  Bit-exact against the oracle's
+ * rank-order fp32 sum rounded once wherever the fp32 sums agree; within 1 bf16
+ * ulp where NCCL's summation order differs.  Excludes
+ * FSDP_BUCKET_SEGMENT_GRAD_SHARDS (the fp32 RS cannot land in bf16 storage),
+ * gradient accumulation, and the fp32-output peer-memory / NVLS reduce-scatters
+ * (K9, K10, FSDP_SCHED_P2P): those return FSDP_ERR_INVALID_ARG. */
 /* FSDP_BUCKET_GROUPED_AG (an alternative to copy-in / copy-out bucketing;
  * every member's dim0 divisible by the world size, shards and fulls bound,
  * no FP32_MASTER): the bucket's all-gather is ONE NCCL group of per-member

@@ -167,6 +167,13 @@ def rs_copyout(rs_out, dims, world, align=16):
     return res
 
 
+def rs_copyout_bf16(rs_out, dims, world, align=16):
+    """Read-out into bf16 gradient shards (reading G41; the north star's
+    "1 bf16 ulp after cast"): the fp32 RS result (reduce_dtype) is
+    rounded once, RNE, to bf16 bit patterns (O1 narrow)."""
+    return [bf16.narrow(x) for x in rs_copyout(rs_out, dims, world, align)]
+
+
 def accumulate_grad_shards(existing, new):
     """Gradient accumulation over micro-batches: the
     gradient shards read out of this reduce-scatter are added to the shards

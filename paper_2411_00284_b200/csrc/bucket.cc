@@ -45,7 +45,8 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   if (k < 1 || !d->params) return fail(FSDP_ERR_INVALID_ARG, "bucket needs >= 1 member");
   if (d->align_bytes < 1) return fail(FSDP_ERR_INVALID_ARG, "align_bytes < 1");
   if (d->reserved != 0 || (d->flags & ~(FSDP_BUCKET_SEGMENT_SHARDS | FSDP_BUCKET_SEGMENT_GRAD_SHARDS |
-                                        FSDP_BUCKET_FP32_MASTER | FSDP_BUCKET_GROUPED_AG)))
+                                        FSDP_BUCKET_FP32_MASTER | FSDP_BUCKET_GROUPED_AG |
+                                        FSDP_BUCKET_BF16_GRAD_SHARDS)))
     return fail(FSDP_ERR_INVALID_ARG, "unknown bucket flags");
   const int32_t ep = dtype_bytes(d->param_dtype), eg = dtype_bytes(d->grad_dtype);
   if (!ep || !eg) return fail(FSDP_ERR_INVALID_ARG, "unsupported dtype");
@@ -53,6 +54,10 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   const bool master = d->flags & FSDP_BUCKET_FP32_MASTER;
   if (master && (d->param_dtype != FSDP_BF16 || (d->flags & FSDP_BUCKET_SEGMENT_SHARDS)))
     return fail(FSDP_ERR_INVALID_ARG, "FSDP_BUCKET_FP32_MASTER needs param_dtype BF16 and no SEGMENT_SHARDS");
+  // bf16 gradient shards: K6 rounds the fp32 RS output (G41)
+  const bool gs_bf16 = d->flags & FSDP_BUCKET_BF16_GRAD_SHARDS;
+  if (gs_bf16 && (d->flags & FSDP_BUCKET_SEGMENT_GRAD_SHARDS))
+    return fail(FSDP_ERR_INVALID_ARG, "FSDP_BUCKET_BF16_GRAD_SHARDS excludes SEGMENT_GRAD_SHARDS");
   for (int32_t j = 0; j < k; ++j) {
     const fsdp_param_desc& p = d->params[j];
     if (p.dim0 < 1 || p.row_numel < 1 || p.reserved != 0)
@@ -184,7 +189,7 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
                                  s.v * R * ep, static_cast<uint32_t>(q) << kPeerShift);
       }
     }
-    if (d->full_grads && d->grad_shards) {
+    if (d->full_grads && d->grad_shards && !gs_bf16) {
       // K9 (peer-memory RS): rows of chunk r at the same offset from full_grads[0]
       // on every rank, summed in rank order into the fp32 shard; pad rows +0.0.
       const uint64_t rel = reinterpret_cast<uint64_t>(d->full_grads[j]) - reinterpret_cast<uint64_t>(d->full_grads[0]);
@@ -192,7 +197,11 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
       p2p_rs.peer_reduce(rel + static_cast<uint64_t>(own.begin * R * eg), dst, own.v * R, eg, N);
       p2p_rs.zero(dst + static_cast<uint64_t>(own.v * R * 4), (own.c - own.v) * R * 4);
     }
-    if (d->grad_shards) {
+    if (d->grad_shards && gs_bf16) {
+      // K6: own segment r -> bf16 gradient shard [c, R], one RNE rounding (G41)
+      rcopy.narrow(static_cast<uint64_t>(r * rs_seg + rs_off[j]), reinterpret_cast<uint64_t>(d->grad_shards[j]),
+                   own.c * R);
+    } else if (d->grad_shards) {
       // K6: own segment r -> fp32 gradient shard [c, R].
       rcopy.copy(static_cast<uint64_t>(r * rs_seg + rs_off[j]),
                  reinterpret_cast<uint64_t>(d->grad_shards[j]), own.c * R * 4);
@@ -244,6 +253,7 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   b->rs_zero_copy = rs_zc;
   b->ag_direct = direct;
   b->ag_grouped = grouped;
+  b->gshard_bf16 = gs_bf16;
   if (grouped)
     for (int32_t j = 0; j < k; ++j) {
       b->shard_ptrs.push_back(d->shards[j]);
@@ -504,6 +514,8 @@ extern "C" fsdp_status fsdp_reduce_scatter_bucket(fsdp_ctx* c, fsdp_bucket* b, v
 extern "C" fsdp_status fsdp_bucket_set_grad_accumulation(fsdp_bucket* b, int32_t on) {
   if (!b) return fail(FSDP_ERR_INVALID_ARG, "NULL bucket");
   if (on != 0 && on != 1) return fail(FSDP_ERR_INVALID_ARG, "on must be 0 or 1");
+  if (on && b->gshard_bf16)
+    return fail(FSDP_ERR_INVALID_ARG, "gradient accumulation needs fp32 gradient shards (FSDP_BUCKET_BF16_GRAD_SHARDS)");
   b->grad_accumulate = on != 0;
   return FSDP_OK;
 }

@@ -228,6 +228,7 @@ struct fsdp_bucket {
   char* gshard_seg = nullptr;  // this rank's RS segment in grad-shard storage
   bool ag_direct = false;      // gathered buffer == the (single) full parameter
   bool ag_grouped = false;     // FSDP_BUCKET_GROUPED_AG: per-member AGs in one NCCL group
+  bool gshard_bf16 = false;    // FSDP_BUCKET_BF16_GRAD_SHARDS: K6 rounds the fp32 RS output to bf16
   std::vector<const void*> shard_ptrs;  // grouped: shards[j]
   std::vector<int64_t> own_bytes;       // grouped: c_j * R_j * e_p
   char* full0 = nullptr;       // fulls[0]

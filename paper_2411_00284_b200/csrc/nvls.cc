@@ -245,6 +245,7 @@ extern "C" fsdp_status fsdp_nvls_reduce_scatter_bucket(fsdp_ctx* c, fsdp_bucket*
   if (!c || !b || !mc_staging) return fail(FSDP_ERR_INVALID_ARG, "NULL argument");
   if (b->ctx != c) return fail(FSDP_ERR_INVALID_ARG, "bucket belongs to another ctx");
   if (!b->has_gshards) return fail(FSDP_ERR_INVALID_ARG, "NVLS reduce-scatter needs bound grad_shards");
+  if (b->gshard_bf16) return fail(FSDP_ERR_INVALID_ARG, "NVLS reduce-scatter writes fp32 gradient shards");
   if (reinterpret_cast<uintptr_t>(mc_staging) % 16) return fail(FSDP_ERR_INVALID_ARG, "staging not 16-B aligned");
   FSDP_CUDA_TRY(cudaSetDevice(c->device));
   FSDP_CUDA_TRY(launch_nvls_reduce(b->nvls_rs, static_cast<const char*>(mc_staging), b->grad_accumulate,

@@ -43,6 +43,7 @@ extern "C" fsdp_status fsdp_p2p_reduce_scatter_bucket(fsdp_ctx* c, fsdp_bucket* 
   if (b->ctx != c) return fail(FSDP_ERR_INVALID_ARG, "bucket belongs to another ctx");
   if (!b->has_grads || !b->has_gshards)
     return fail(FSDP_ERR_INVALID_ARG, "peer reduce-scatter needs full_grads and grad_shards");
+  if (b->gshard_bf16) return fail(FSDP_ERR_INVALID_ARG, "peer reduce-scatter writes fp32 gradient shards");
   PeerTable pt;
   FSDP_TRY(peer_table(c, peer_grads, &pt, false));
   FSDP_CUDA_TRY(cudaSetDevice(c->device));

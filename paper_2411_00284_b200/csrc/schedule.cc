@@ -180,6 +180,9 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
       }
     }
     for (int32_t i = 0; i < s->n_bwd; ++i)
+      if (s->bwd[i]->gshard_bf16)
+        return fail(FSDP_ERR_INVALID_ARG, "FSDP_SCHED_P2P writes fp32 gradient shards (FSDP_BUCKET_BF16_GRAD_SHARDS)");
+    for (int32_t i = 0; i < s->n_bwd; ++i)
       for (int32_t q = 0; q < ctx->world; ++q) {
         const void* p = pp->rs_peers[static_cast<int64_t>(i) * ctx->world + q];
         if (!p || reinterpret_cast<uintptr_t>(p) % 16) return fail(FSDP_ERR_INVALID_ARG, "bad rs_peers entry");

@@ -37,3 +37,14 @@ class DevArray:
 def bits(a):
     a = np.ascontiguousarray(a)
     return a.view(np.uint16) if a.dtype.itemsize == 2 else a.view(np.uint32)
+
+
+def bf16_ulp_distance(a, b):
+    """Element-wise distance in bf16 units in the last place between two bf16
+    bit-pattern arrays (uint16): the patterns mapped to a monotone integer
+    order (+0 and -0 both 0, negatives below), then |ord(a) - ord(b)|.  The
+    north star's tolerance for gradients cast to bf16 after the fp32 RS."""
+    def order(u):
+        u = np.asarray(u, dtype=np.uint16).astype(np.int64)
+        return np.where(u < 0x8000, u, 0x8000 - u)
+    return np.abs(order(a) - order(b))

@@ -230,3 +230,41 @@ def test_accumulated_micro_batches_equal_exact_mean_sum():
         for j, (d, r) in enumerate(dims):
             want = shard(total[j].astype(np.float32), world, q)
             assert np.array_equal(acc[q][j].view(np.uint32), want.view(np.uint32))
+
+
+# ---------------------------------------------------- bf16 gradient shards (G41)
+def test_rs_bf16_shards_hand_ties():
+    """N = 2, one element: the fp32 mean is exact, the bf16 cast is one RNE
+    rounding.  (1.0 + 1.0078125) / 2 = 1 + 2^-8 lies halfway between bf16
+    1.0 (0x3F80, even) and 1.0078125 (0x3F81): -> 0x3F80.
+    (1.0078125 + 1.015625) / 2 = 1 + 3 * 2^-8 lies halfway between 0x3F81 and
+    0x3F82 (even): -> 0x3F82.  1.0 and 3.0 -> 2.0 exactly (0x4000)."""
+    from oracle.collectives import rs_copyout_bf16
+    for a, b, want in ((0x3F80, 0x3F81, 0x3F80), (0x3F81, 0x3F82, 0x3F82), (0x3F80, 0x4040, 0x4000)):
+        g = [[np.array([[a]], dtype=np.uint16)], [np.array([[b]], dtype=np.uint16)]]
+        _, outs, _ = bucketed_reduce_scatter(g, 2, 16)
+        got = [rs_copyout_bf16(o, [(1, 1)], 2, 16) for o in outs]
+        assert int(got[0][0][0, 0]) == want      # rank 0 owns the only row
+        assert got[1][0].shape == (1, 1) and int(got[1][0][0, 0]) == 0   # rank 1: one pad row, +0
+
+
+@given(dims=dims_st, k=st.integers(0, 3), seed=st.integers(0, 2**31))
+@settings(max_examples=100, deadline=None)
+def test_rs_bf16_shards_are_one_rounding_of_the_exact_mean(dims, k, seed):
+    """Exact-representable data at N = 2^k: the fp32 RS result is the exact
+    mean, so the bf16 shard must be the exact mean correctly rounded to bf16
+    (torch's float -> bfloat16 conversion of the fp64 mean, a library routine)."""
+    import torch
+    from oracle.collectives import rs_copyout_bf16
+    world = 2 ** k
+    rng = np.random.Generator(np.random.Philox(seed))
+    ks = [[rng.integers(-256, 257, size=(d, r)) for d, r in dims] for _ in range(world)]
+    g = [[(((x.astype(np.float32) * np.float32(2 ** -8)).view(np.uint32)) >> 16).astype(np.uint16) for x in kr]
+         for kr in ks]
+    _, outs, _ = bucketed_reduce_scatter(g, world, 16)
+    for q in range(world):
+        got = rs_copyout_bf16(outs[q], dims, world, 16)
+        for j, (d, r) in enumerate(dims):
+            mean = sum(ks[rr][j].astype(np.float64) for rr in range(world)) * 2.0 ** -8 / world
+            want = torch.from_numpy(shard(mean, world, q)).to(torch.float32).to(torch.bfloat16).view(torch.int16)
+            assert np.array_equal(got[j].view(np.int16), want.numpy())
