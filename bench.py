@@ -138,6 +138,22 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+# The paper's own numbers (H100, training TPS / peak memory -- it reports no
+# bus bandwidth or exposed-comm time): context beside this run, not a target.
+PAPER_CONTEXT = {
+    "hardware": "H100, 8 per node, NVLink intra-node (P:344); Llama 3.1; TorchTitan; C4",
+    "headline_vs_FSDP2_eager": {"peak_memory_reduction": "up to 28.54%", "throughput_gain": "up to 68.67%",
+                                "cite": "P:55"},
+    "8b_fsdp_vs_FSDP2_eager": {"memory": "-27.72%", "tps": "+7.49%", "gpus": "32/64/128", "cite": "P:414"},
+    "table5_1node_tps_mem": {"vanilla": [50976, 67.26], "+reorder": [54544, 68.72], "+bucket": [49168, 69.06],
+                             "+reorder&bucket": [52480, 69.08], "cite": "P:556-570 (8B, FSDP only, bs 1)"},
+    "table5_8node_tps_mem": {"vanilla": [333440, 56.42], "+reorder": [404032, 57.88], "+bucket": [405632, 58.15],
+                             "+reorder&bucket": [428352, 65.74], "cite": "P:556-570"},
+    "note": "context only: the paper's metrics are training TPS and peak GiB on H100; this line's are bucket "
+            "bytes per second, kernel HBM fractions and exposure predicted / measured on B200",
+}
+
+
 def run_env(torch):
     """GPU / host identity and library versions of this run (SURVEY §8(d)
     protocol step 6)."""
@@ -673,6 +689,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
             "env": run_env(torch),
+            "paper_context": PAPER_CONTEXT,
         }
         print(json.dumps(line), flush=True)
     ctx_close = getattr(ctx, "close", None)
