@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--plan", default="manual", choices=["manual", "greedy", "per_param", "size_cap"])
     ap.add_argument("--sim-world", type=int, default=8, help="layout world size at N=1")
+    ap.add_argument("--plan-file", default=None,
+                    help="JSON with plans.fwd / plans.bwd (buckets of forward indices in execution order), e.g. "
+                         "from tools/plan_search.py; overrides --plan")
     ap.add_argument("--tokens", type=int, default=None, help="proxy compute tokens/GPU (0 = none)")
     ap.add_argument("--no-reorder", action="store_true")
     ap.add_argument("--fwd-placement", default="before", choices=["before", "after"])
@@ -327,6 +330,13 @@ def main():
             "size_cap": L.PLAN_SIZE_CAP}[args.plan]
     link = (args.alpha_ns, args.beta_fs)
     fplan, bplan = H.plans_for(specs, world, mode, t_fwd, t_bwd, link, link, int(args.mem_limit))
+    if args.plan_file:
+        with open(args.plan_file) as f:
+            pj = json.load(f)["plans"]
+        fplan, bplan = pj["fwd"], pj["bwd"]
+        flat_f = sorted(j for b in fplan for j in b)
+        flat_b = sorted(j for b in bplan for j in b)
+        assert flat_f == flat_b == list(range(len(specs))), "plan file does not cover the model's parameters"
     reg = args.nccl_register if (multi and not p2p and args.nccl_register != "none") else None
     st = H.RankState(specs, world, rank if multi else 0, fplan, bplan, ctx, seed=1234 + rank,
                      ipc=multi and p2p, nccl_register=reg, ag_grouped=args.ag == "grouped")
@@ -644,7 +654,8 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic",
             "config": {
-                "workload": ("llama3-8b FSDP rank step, %s plan, %s" % (args.plan, "reorder fwd-%s/bwd-%s" % (
+                "workload": ("llama3-8b FSDP rank step, %s plan, %s" % (
+                    "file:" + os.path.basename(args.plan_file) if args.plan_file else args.plan, "reorder fwd-%s/bwd-%s" % (
                     args.fwd_placement, args.bwd_placement) if not args.no_reorder else "vanilla order")) +
                 ((", 1 GPU = rank 0 of a simulated %d-way job (pack/unpack only, no peers)" % world if not p2p else
                   ", 1 GPU = rank 0 of a simulated %d-way job (peers' buffers simulated in local HBM)" % world)

@@ -1,0 +1,42 @@
+"""Host logic of tools/plan_search.py (the simulator-guided plan search, a
+planner beyond the paper's Algorithm 1): on a 2-block Llama-3-8B slice the
+search returns a contiguous partition of every phase that covers each
+parameter once, respects the memory cap, and is never slower -- in the same
+two-stream model (fsdp_simulate_schedule) -- than the plan it started from."""
+import os
+import sys
+
+import pytest
+
+pytest.importorskip("paper_2411_00284_b200._lib", reason="libfsdp_b200.so not built")
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+
+import plan_search as PS  # noqa: E402
+from paper_2411_00284_b200 import _lib as L  # noqa: E402
+from paper_2411_00284_b200 import harness as H  # noqa: E402
+from workloads import llama  # noqa: E402
+from workloads.compute_model import per_param_compute_ns  # noqa: E402
+
+
+@pytest.mark.parametrize("phase", [0, 1])
+@pytest.mark.parametrize("mode", [L.PLAN_MANUAL, L.PLAN_GREEDY, L.PLAN_PER_PARAM])
+def test_search_never_worse_and_valid(phase, mode):
+    specs = llama("8b", n_layers=2)
+    P = len(specs)
+    tf, tb = per_param_compute_ns(specs, 1024)
+    link = (20000, 1215)
+    mem = int(6e8)
+    fp, bp = H.plans_for(specs, 8, mode, tf, tb, link, link, mem)
+    model = PS.PhaseModel(specs, 8, phase, tf if phase == 0 else tb, link, mem)
+    flags = L.SCHED_REORDER | (L.SCHED_FWD_AG_BEFORE_WAIT if phase == 0 else 0)
+    start = PS.cuts_of(fp if phase == 0 else bp, P, phase)
+    t_start = model.time(start, flags)[0]
+    cuts, t = PS.search(model, start, flags, budget_s=20)
+    assert t <= t_start and t == model.time(cuts, flags)[0]
+    assert cuts[0] == 0 and cuts[-1] == P and all(a < b for a, b in zip(cuts, cuts[1:]))
+    assert model.feasible(cuts)
+    plan = PS.plan_of(cuts, model)
+    assert sorted(j for b in plan for j in b) == list(range(P))
+    order = list(range(P)) if phase == 0 else list(range(P - 1, -1, -1))
+    assert [j for b in plan for j in b] == order          # contiguous, in execution order
