@@ -218,6 +218,36 @@ typedef struct {
 fsdp_status fsdp_plan_buckets(const fsdp_plan_in* in, int32_t* bucket_begin, int32_t* n_buckets,
                               fsdp_plan_trace* trace);
 
+/* fsdp_plan_search (beyond Algorithm 1): starting from a plan of
+ * the phase (start_begin: n_start + 1 increasing phase positions from 0 to
+ * n_params, e.g. fsdp_plan_buckets' output), hill-climb over contiguous
+ * partitions scored by the predicted phase time -- fsdp_simulate_schedule over
+ * the op sequence fsdp_run_schedule would enqueue with cost->sched_flags, with
+ * collectives at alpha + ceil(n beta) (in->ag / in->rs, n = N x segment), the
+ * copy-out K3 at 2 x full bytes / unpack_bytes_per_us + copy_launch_ns (none
+ * for a direct-gather bucket), the gradient pack K4 at (2 + reduce_bytes) B per
+ * element / pack_rs_bytes_per_us + copy_launch_ns, a bucket's compute at the
+ * sum of its t_compute_ns + compute_overhead_ns.  Moves, in this order, first
+ * strict improvement taken: remove each inner boundary, move it by -1, by +1;
+ * then split each bucket at its midpoint, first and last position.  A
+ * candidate is feasible when every bucket has M <= in->mem_max_bytes (M as in
+ * fsdp_plan_buckets) or a single parameter.  Stops when no move improves or
+ * after max_moves improvements (0 = no limit).  Writes the plan like
+ * fsdp_plan_buckets (bucket_begin: n_params + 1 entries, caller-allocated) and
+ * its predicted phase time.  Deterministic, host-only.  Errors: NULL
+ * arguments, a start plan that is not a partition or exceeds the memory cap,
+ * non-positive rates -> FSDP_ERR_INVALID_ARG. */
+typedef struct {
+  int64_t unpack_bytes_per_us;  /* K3 HBM rate, bytes per microsecond (6.47 TB/s = 6470000) */
+  int64_t pack_rs_bytes_per_us; /* K4 HBM rate */
+  int64_t copy_launch_ns;       /* launch + ramp + tail per copy kernel */
+  int64_t compute_overhead_ns;  /* per bucket, on top of its T_c */
+  uint32_t sched_flags;         /* FSDP_SCHED_REORDER and placement bits of the schedule to score */
+  int32_t max_moves;            /* 0 = until no move improves */
+} fsdp_search_cost;
+fsdp_status fsdp_plan_search(const fsdp_plan_in* in, const fsdp_search_cost* cost, const int32_t* start_begin,
+                             int32_t n_start, int32_t* bucket_begin, int32_t* n_buckets, int64_t* predicted_ns);
+
 /* Bucket layout, host-only: for k members (forward order) of
  * elem_bytes-byte elements at world N, offs[j] = byte offset of member j in a
  * rank segment, *seg_bytes = segment size; off_1 = 0, off_{j+1} =

@@ -46,7 +46,7 @@ EXPORTED = [
     "fsdp_nvls_create", "fsdp_nvls_import", "fsdp_nvls_bind", "fsdp_nvls_destroy",
     "fsdp_nvls_reduce_scatter_bucket",
     "fsdp_step_graph_create", "fsdp_step_graph_launch", "fsdp_step_graph_info", "fsdp_step_graph_destroy",
-    "fsdp_comm_time_ns", "fsdp_simulate_schedule", "fsdp_simulate_memory",
+    "fsdp_comm_time_ns", "fsdp_simulate_schedule", "fsdp_simulate_memory", "fsdp_plan_search",
 ]
 
 
@@ -139,6 +139,12 @@ class NcclConfig(C.Structure):
                 ("cta_policy", C.c_int32)]
 
 
+class SearchCost(C.Structure):
+    _fields_ = [("unpack_bytes_per_us", C.c_int64), ("pack_rs_bytes_per_us", C.c_int64),
+                ("copy_launch_ns", C.c_int64), ("compute_overhead_ns", C.c_int64), ("sched_flags", C.c_uint32),
+                ("max_moves", C.c_int32)]
+
+
 class LogEntry(C.Structure):
     _fields_ = [("ns", C.c_int64), ("phase", C.c_int32), ("op", C.c_int32), ("bucket", C.c_int32),
                 ("stream", C.c_int32), ("start_ns", C.c_int64)]
@@ -204,6 +210,8 @@ _sigs = {
     "fsdp_simulate_schedule": (C.c_int, [C.POINTER(LogEntry), C.c_int32, C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int64)]),
+    "fsdp_plan_search": (C.c_int, [C.POINTER(PlanIn), C.POINTER(SearchCost), C.POINTER(C.c_int32), C.c_int32,
+                                   C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
     "fsdp_simulate_memory": (C.c_int, [C.POINTER(LogEntry), C.c_int32, C.POINTER(MemSizes),
                                        C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
 }

@@ -70,6 +70,38 @@ def plan_buckets(params, world, t_compute_ns, ag, rs, mem_max, mode, phase, para
     return buckets, trace
 
 
+def plan_search(params, world, t_compute_ns, ag, rs, mem_max, phase, start_plan, cost, param_dtype=L.BF16,
+                align=16, mem_bytes=None, reduce_bytes=4):
+    """fsdp_plan_search.  start_plan: buckets (forward indices, execution order)
+    of this phase, e.g. from plan_buckets; cost: dict(unpack_bytes_per_us,
+    pack_rs_bytes_per_us, copy_launch_ns, compute_overhead_ns, sched_flags,
+    max_moves).  Returns (buckets, predicted phase ns)."""
+    params = list(params)
+    P = len(params)
+    pin = L.PlanIn()
+    keep = [L.descs(params), L.i64_array(t_compute_ns), L.i64_array(mem_bytes) if mem_bytes is not None else None]
+    pin.params, pin.t_compute_ns, pin.mem_bytes = keep
+    pin.ag = L.Link(int(ag[0]), int(ag[1]))
+    pin.rs = L.Link(int(rs[0]), int(rs[1]))
+    pin.mem_max_bytes = int(mem_max)
+    pin.n_params, pin.world, pin.align_bytes = P, world, align
+    pin.mode, pin.phase, pin.param_dtype, pin.reduce_bytes, pin.reserved = L.PLAN_GREEDY, phase, param_dtype, \
+        reduce_bytes, 0
+    starts = [0]
+    for b in start_plan:
+        starts.append(starts[-1] + len(b))
+    sb = (C.c_int32 * len(starts))(*starts)
+    c = L.SearchCost(int(cost["unpack_bytes_per_us"]), int(cost["pack_rs_bytes_per_us"]),
+                     int(cost["copy_launch_ns"]), int(cost["compute_overhead_ns"]), int(cost["sched_flags"]),
+                     int(cost.get("max_moves", 0)))
+    bb = (C.c_int32 * (P + 1))()
+    nb = C.c_int32()
+    t = C.c_int64()
+    check(L.lib.fsdp_plan_search(C.byref(pin), C.byref(c), sb, len(starts) - 1, bb, C.byref(nb), C.byref(t)))
+    order = list(range(P)) if phase == L.PHASE_FWD else list(range(P - 1, -1, -1))
+    return [order[bb[b]:bb[b + 1]] for b in range(nb.value)], t.value
+
+
 class Ctx:
     """fsdp_ctx_create / fsdp_ctx_destroy."""
 

@@ -458,14 +458,32 @@ def predict_exposure(st, flags, compute, comm, proxy_fwd, proxy_bwd, link_ag, li
     HBM contention between the copies and the collectives."""
     rep = st.step(flags | L.SCHED_TIMING, compute, comm, proxy_fwd, proxy_bwd, ctas_per_sm, smem, want_log=True,
                   gemm=gemm, hook=hook)
+    return simulate_n_rank(st, rep["log"], link_ag, link_rs)
+
+
+def simulate_n_rank(st, log, link_ag, link_rs):
+    """The N-rank step from one timed step's log of this rank: compute-stream
+    ops at their measured durations, except the copies a rank with a
+    communicator does not run -- the AG copy-in of segment-layout storage (the
+    collective sends from it) and the RS read-out into segment-layout gradient
+    storage (the collective writes it) -- which a layout-only rank still runs
+    (K1 own rows / K6) and which are charged 0 here; collectives at
+    alpha + beta n.  Returns (total_ns, exposed_ns)."""
     durs = []
-    for ph, op, b, _s, ns, _t in rep["log"]:
+    q = {}
+    for ph, op, b, _s, ns, _t in log:
         bk = (st.fwd if ph == 0 else st.bwd)[b]
+        if (ph, b) not in q:
+            q[(ph, b)] = bk.query()
+        info = q[(ph, b)]
         if op == L.OP_AG:
             durs.append(F.comm_time_ns(st.world * bk.ag_seg, link_ag))
         elif op == L.OP_RS:
             durs.append(F.comm_time_ns(st.world * bk.rs_seg, link_rs))
+        elif (op == L.OP_PACK_AG and info["ag_zero_copy"] and not info["ag_grouped"]) or \
+                (op == L.OP_COPYOUT_RS and info["rs_zero_copy"]):
+            durs.append(0)
         else:
             durs.append(max(ns, 0))
-    tot, exp, _, _ = F.simulate_schedule(rep["log"], durs)
+    tot, exp, _, _ = F.simulate_schedule(log, durs)
     return tot, exp

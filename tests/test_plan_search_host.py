@@ -40,3 +40,39 @@ def test_search_never_worse_and_valid(phase, mode):
     assert sorted(j for b in plan for j in b) == list(range(P))
     order = list(range(P)) if phase == 0 else list(range(P - 1, -1, -1))
     assert [j for b in plan for j in b] == order          # contiguous, in execution order
+
+
+@pytest.mark.parametrize("phase", [0, 1])
+@pytest.mark.parametrize("mode", [L.PLAN_MANUAL, L.PLAN_GREEDY, L.PLAN_PER_PARAM])
+def test_library_search_matches_reference(phase, mode):
+    """fsdp_plan_search (C++) == the Python reference in tools/plan_search.py:
+    same moves in the same order, same integer cost model -> the same plan and
+    the same predicted phase time, both run to convergence."""
+    import paper_2411_00284_b200 as F
+    specs = llama("8b", n_layers=2)
+    P = len(specs)
+    tf, tb = per_param_compute_ns(specs, 2048)
+    link = (20000, 1215)
+    mem = int(6e8)
+    fp, bp = H.plans_for(specs, 8, mode, tf, tb, link, link, mem)
+    t_c = tf if phase == 0 else tb
+    flags = L.SCHED_REORDER | (L.SCHED_FWD_AG_BEFORE_WAIT if phase == 0 else 0)
+    model = PS.PhaseModel(specs, 8, phase, t_c, link, mem)
+    start = fp if phase == 0 else bp
+    cuts, t = PS.search(model, PS.cuts_of(start, P, phase), flags, budget_s=1e9)
+    descs = [(s.dim0, s.row_numel, s.module_id) for s in specs]
+    plan, t_lib = F.plan_search(descs, 8, t_c, link, link, mem, phase, start, PS.library_cost(flags))
+    assert t_lib == t
+    assert plan == PS.plan_of(cuts, model)
+
+
+def test_library_search_rejects_bad_start():
+    import paper_2411_00284_b200 as F
+    specs = llama("8b", n_layers=1)
+    descs = [(s.dim0, s.row_numel, s.module_id) for s in specs]
+    tf, _ = per_param_compute_ns(specs, 1024)
+    cost = PS.library_cost(L.SCHED_REORDER)
+    with pytest.raises(L.FsdpError):    # does not cover every parameter
+        F.plan_search(descs, 8, tf, (1, 1), (1, 1), 10 ** 12, L.PHASE_FWD, [[0, 1]], cost)
+    with pytest.raises(L.FsdpError):    # start bucket over the memory cap
+        F.plan_search(descs, 8, tf, (1, 1), (1, 1), 10, L.PHASE_FWD, [list(range(len(specs)))], cost)

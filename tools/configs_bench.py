@@ -72,16 +72,7 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
         # proxy compute), every collective at alpha + beta n of its bucket
         # (modelled NVLink; no SM / HBM contention)
         rep = st.step(flags | L.SCHED_TIMING, cs.cuda_stream, ms.cuda_stream, pf, pb, want_log=True, hook=hook)
-        durs = []
-        for ph, op, b, stream, ns, _t in rep["log"]:
-            bk = (st.fwd if ph == 0 else st.bwd)[b]
-            if op == L.OP_AG:
-                durs.append(F.comm_time_ns(world * bk.ag_seg, predict_link[0]))
-            elif op == L.OP_RS:
-                durs.append(F.comm_time_ns(world * bk.rs_seg, predict_link[1]))
-            else:
-                durs.append(max(ns, 0))
-        tot, exp, _, _ = F.simulate_schedule(rep["log"], durs)
+        tot, exp = H.simulate_n_rank(st, rep["log"], predict_link[0], predict_link[1])
         predicted = dict(total_ms=round(tot / 1e6, 3), exposed_ms=round(exp / 1e6, 3))
     measured_tc = None
     if profile:

@@ -12,7 +12,10 @@ alpha + beta n on a FIFO comm stream, copy kernels (K3 copy-out, K4 gradient
 pack) at their measured HBM rates, per-parameter compute T_c -- under the
 memory cap M(bucket) <= M_max.  Moves: merge two neighbours, split a bucket,
 shift a boundary by one; first-improvement hill climbing from the manual,
-greedy and per-parameter plans, best result kept.  Host-only; the plans are
+greedy and per-parameter plans, best result kept.  The search itself is the
+library's fsdp_plan_search (C++); this file holds the Python reference of the
+same moves and model (`--python`; tests/test_plan_search_host.py checks that
+both give the same plan).  Host-only; the plans are
 then timed on the B200 with measured op durations
 (tools/plan_search_validate.sh, GPU; bench.py --plan-file).
 
@@ -29,10 +32,10 @@ sys.path.insert(0, ROOT)
 
 # copy-kernel model (profiles/r01_bench_default_final2.json): K3 6.47 TB/s,
 # K4 6.68 TB/s, ~6 us of launch + ramp + tail per copy launch; a bucket's
-# compute pays ~8 us of launch / ramp on top of its T_c (first validation
-# round: with 4 us and no compute overhead, 241-bucket plans were predicted
-# faster than they measured)
-K3_BPS, K4_BPS, LAUNCH_NS, COMPUTE_NS = 6.47e12, 6.68e12, 6000, 8000
+# compute pays ~16 us on top of its T_c (the median measured overhead of the
+# compute proxy over 582 per-parameter ops at T = 2048; with 4-8 us assumed,
+# plans of ~130 buckets were predicted faster than they measured)
+K3_BPUS, K4_BPUS, LAUNCH_NS, COMPUTE_NS = 6470000, 6680000, 6000, 16000   # rates in bytes per microsecond
 
 
 class PhaseModel:
@@ -59,12 +62,14 @@ class PhaseModel:
         rs_seg = F.layout(d, N, 4, 16)[1]
         full = sum(2 * x[0] * x[1] for x in d)
         direct = len(d) == 1 and d[0][0] % N == 0 and ag_seg == d[0][0] // N * d[0][1] * 2
-        unpack = 0 if direct else int(2 * full / K3_BPS * 1e9) + LAUNCH_NS
-        pack_rs = int(3 * full / K4_BPS * 1e9) + LAUNCH_NS if self.phase == 1 else 0
+        # integer ns, the same formulas as fsdp_plan_search (include/fsdp.h)
+        unpack = 0 if direct else 2 * full * 1000 // K3_BPUS + LAUNCH_NS
+        pack_rs = (full // 2) * 6 * 1000 // K4_BPUS + LAUNCH_NS if self.phase == 1 else 0
         comp = sum(self.t_c[j] for j in m) + COMPUTE_NS
         ag = F.comm_time_ns(N * ag_seg, self.link)
         rs = F.comm_time_ns(N * rs_seg, self.link) if self.phase == 1 else 0
-        r = (unpack, comp, pack_rs, ag, rs, N * ag_seg)
+        mem = sum(N * (-(-x[0] // N)) * x[1] * 2 for x in d)     # M_j = padded gathered bytes (G13)
+        r = (unpack, comp, pack_rs, ag, rs, mem)
         self.cache[key] = r
         return r
 
@@ -107,6 +112,12 @@ def plan_of(cuts, model):
     return [[model.order[i] for i in range(a, b)] for a, b in zip(cuts, cuts[1:])]
 
 
+def library_cost(flags):
+    """The same model as fsdp_search_cost for fsdp_plan_search."""
+    return dict(unpack_bytes_per_us=K3_BPUS, pack_rs_bytes_per_us=K4_BPUS, copy_launch_ns=LAUNCH_NS,
+                compute_overhead_ns=COMPUTE_NS, sched_flags=flags, max_moves=0)
+
+
 def search(model, start, flags, budget_s=60.0):
     best = list(start)
     best_t = model.time(best, flags)[0]
@@ -143,7 +154,9 @@ def main():
     ap.add_argument("--mem-limit", type=float, default=2e9)
     ap.add_argument("--budget-s", type=float, default=90.0)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--python", action="store_true", help="use the Python reference search instead of the library")
     a = ap.parse_args()
+    import paper_2411_00284_b200 as F
     from paper_2411_00284_b200 import _lib as L
     from paper_2411_00284_b200 import harness as H
     from workloads import llama
@@ -157,7 +170,7 @@ def main():
     for name, mode in (("manual", L.PLAN_MANUAL), ("greedy", L.PLAN_GREEDY), ("per_param", L.PLAN_PER_PARAM)):
         starts[name] = H.plans_for(specs, a.world, mode, tf, tb, link, link, int(a.mem_limit))
     out = {"world": a.world, "tokens_per_gpu": a.tokens, "link": link, "mem_max": a.mem_limit,
-           "copy_model": {"K3_Bps": K3_BPS, "K4_Bps": K4_BPS, "launch_ns": LAUNCH_NS,
+           "copy_model": {"K3_bytes_per_us": K3_BPUS, "K4_bytes_per_us": K4_BPUS, "launch_ns": LAUNCH_NS,
                           "compute_overhead_ns": COMPUTE_NS}, "phases": {}, "plans": {}}
     for phase, t_c in ((0, tf), (1, tb)):
         model = PhaseModel(specs, a.world, phase, t_c, link, a.mem_limit)
@@ -167,7 +180,13 @@ def main():
             cuts = cuts_of(fp if phase == 0 else bp, P, phase)
             t0, e0 = model.time(cuts, flags[phase])
             rows[name] = {"buckets": len(cuts) - 1, "total_ms": round(t0 / 1e6, 3), "exposed_ms": round(e0 / 1e6, 3)}
-            c, t = search(model, cuts, flags[phase], a.budget_s / 3)
+            if a.python:   # the reference implementation (time-bounded)
+                c, t = search(model, cuts, flags[phase], a.budget_s / 3)
+            else:          # fsdp_plan_search: the same moves and model, in C++, to convergence
+                descs = [(x.dim0, x.row_numel, x.module_id) for x in specs]
+                plan, t = F.plan_search(descs, a.world, t_c, link, link, int(a.mem_limit), phase,
+                                        fp if phase == 0 else bp, library_cost(flags[phase]))
+                c = cuts_of(plan, P, phase)
             e = model.time(c, flags[phase])[1]
             rows["search from " + name] = {"buckets": len(c) - 1, "total_ms": round(t / 1e6, 3),
                                            "exposed_ms": round(e / 1e6, 3)}
