@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="8b")
     ap.add_argument("--layers", type=int, default=None)
-    ap.add_argument("--plan", default="manual", choices=["manual", "greedy", "per_param", "size_cap"])
+    ap.add_argument("--plan", default="manual", choices=["manual", "greedy", "per_param", "size_cap", "search"],
+                    help="search: fsdp_plan_search (simulator-guided, beyond Algorithm 1) from the manual and "
+                         "greedy plans, with the per-op compute model at --tokens (or --predict-tokens)")
     ap.add_argument("--sim-world", type=int, default=8, help="layout world size at N=1")
     ap.add_argument("--plan-file", default=None,
                     help="JSON with plans.fwd / plans.bwd (buckets of forward indices in execution order), e.g. "
@@ -327,9 +329,14 @@ def main():
     specs = llama(args.model, n_layers=args.layers)
     t_fwd, t_bwd = per_param_compute_ns(specs, tokens) if tokens else ([0] * len(specs), [0] * len(specs))
     mode = {"manual": L.PLAN_MANUAL, "greedy": L.PLAN_GREEDY, "per_param": L.PLAN_PER_PARAM,
-            "size_cap": L.PLAN_SIZE_CAP}[args.plan]
+            "size_cap": L.PLAN_SIZE_CAP, "search": L.PLAN_GREEDY}[args.plan]
     link = (args.alpha_ns, args.beta_fs)
     fplan, bplan = H.plans_for(specs, world, mode, t_fwd, t_bwd, link, link, int(args.mem_limit))
+    if args.plan == "search":
+        st_tok = tokens or args.predict_tokens or 1024
+        sf, sb = per_param_compute_ns(specs, st_tok)
+        slink = (20000, round((world - 1) / world / 720e9 * 1e15)) if not multi else link
+        fplan, bplan = H.plans_search(specs, world, sf, sb, slink, slink, int(args.mem_limit))
     if args.plan_file:
         with open(args.plan_file) as f:
             pj = json.load(f)["plans"]
@@ -513,10 +520,14 @@ def main():
             # the north star's comparison: exposure under the greedy plan (Alg. 1)
             # vs the unbucketed, unreordered baseline, same model, same compute
             variants = {}
+            RF = L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT
             for name, vmode, vflags in (("vanilla (per-param, no reorder)", L.PLAN_PER_PARAM, 0),
-                                        ("greedy + reorder", L.PLAN_GREEDY,
-                                         L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT)):
-                vf, vb = H.plans_for(specs, world, vmode, ptf, ptb, link, link, int(args.mem_limit))
+                                        ("greedy + reorder", L.PLAN_GREEDY, RF),
+                                        ("search + reorder (fsdp_plan_search, beyond the paper)", "search", RF)):
+                if vmode == "search":
+                    vf, vb = H.plans_search(specs, world, ptf, ptb, link, link, int(args.mem_limit))
+                else:
+                    vf, vb = H.plans_for(specs, world, vmode, ptf, ptb, link, link, int(args.mem_limit))
                 vst = H.RankState(specs, world, 0, vf, vb, ctx, seed=99)
                 vpf = H.proxy_iters(H.bucket_times(vf, ptf), nspi)
                 vpb = H.proxy_iters(H.bucket_times(vb, ptb), nspi)

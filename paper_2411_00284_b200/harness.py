@@ -404,6 +404,33 @@ def plans_for(specs, world, mode, t_fwd=None, t_bwd=None, ag=(0, 0), rs=(0, 0), 
     return fb, bb
 
 
+# fsdp_plan_search cost model (tools/plan_search.py documents the numbers)
+SEARCH_COST = dict(unpack_bytes_per_us=6470000, pack_rs_bytes_per_us=6680000, copy_launch_ns=6000,
+                   compute_overhead_ns=16000, max_moves=0)
+
+
+def plans_search(specs, world, t_fwd, t_bwd, ag=(0, 0), rs=(0, 0), mem_max=0, flags=None, param_dtype=L.BF16):
+    """Per phase, fsdp_plan_search from the manual and the greedy plan; the
+    plan with the lower predicted phase time is kept."""
+    if flags is None:
+        flags = L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT
+    descs = [(p.dim0, p.row_numel, p.module_id) for p in specs]
+    starts = [plans_for(specs, world, m, t_fwd, t_bwd, ag, rs, mem_max, param_dtype)
+              for m in (L.PLAN_MANUAL, L.PLAN_GREEDY)]
+    out = []
+    for phase, t, ph_flags in ((L.PHASE_FWD, t_fwd, flags & ~L.SCHED_BWD_AG_BEFORE_WAIT),
+                               (L.PHASE_BWD, t_bwd, flags & ~L.SCHED_FWD_AG_BEFORE_WAIT)):
+        best = None
+        for st in starts:
+            cost = dict(SEARCH_COST, sched_flags=ph_flags)
+            plan, ns = F.plan_search(descs, world, t, ag, rs, mem_max, phase, st[phase], cost,
+                                     param_dtype=param_dtype)
+            if best is None or ns < best[1]:
+                best = (plan, ns)
+        out.append(best[0])
+    return out[0], out[1]
+
+
 def calibrate_proxy(ctx, stream, ctas_per_sm=1, smem=0, probe_iters=200000):
     """ns per proxy iteration on this device, now (clocks vary): median of 5."""
     ns = F.proxy_calibrate(ctx, probe_iters, ctas_per_sm, smem, 5, stream)

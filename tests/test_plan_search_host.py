@@ -76,3 +76,12 @@ def test_library_search_rejects_bad_start():
         F.plan_search(descs, 8, tf, (1, 1), (1, 1), 10 ** 12, L.PHASE_FWD, [[0, 1]], cost)
     with pytest.raises(L.FsdpError):    # start bucket over the memory cap
         F.plan_search(descs, 8, tf, (1, 1), (1, 1), 10, L.PHASE_FWD, [list(range(len(specs)))], cost)
+
+
+def test_plans_search_covers_every_parameter():
+    specs = llama("8b", n_layers=3)
+    tf, tb = per_param_compute_ns(specs, 1024)
+    f, b = H.plans_search(specs, 8, tf, tb, (20000, 1215), (20000, 1215), int(2e9))
+    P = len(specs)
+    assert [j for bk in f for j in bk] == list(range(P))
+    assert [j for bk in b for j in bk] == list(range(P - 1, -1, -1))
