@@ -33,6 +33,7 @@
 // __fmul_rn by fl32(1/N).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "internal.h"
@@ -63,6 +64,9 @@
 #endif
 #ifndef FSDP_PROXY_WAVES
 #define FSDP_PROXY_WAVES 16  // K7: short CTAs per (SM x ctas_per_sm) slot
+#endif
+#ifndef FSDP_PROXY_MIN_ITERS
+#define FSDP_PROXY_MIN_ITERS 512  // K7: fewest iterations per CTA before another wave is added
 #endif
 #ifndef FSDP_BULK
 #define FSDP_BULK 0  // bulk engine for: 0 none, 1 K3, 2 all pure-copy kernels (K0, K1, K3, K6)
@@ -957,8 +961,13 @@ cudaError_t launch_proxy(int64_t iters, int grid, int smem, float* sink, cudaStr
     if (e != cudaSuccess) return e;
   }
   (void)cudaGetLastError();
-  const long long per_cta = (static_cast<long long>(iters) + FSDP_PROXY_WAVES - 1) / FSDP_PROXY_WAVES;
-  fsdp_compute_proxy_kernel<<<grid * FSDP_PROXY_WAVES, 256, smem, s>>>(per_cta, sink);
+  // up to FSDP_PROXY_WAVES waves of short CTAs; a short op gets fewer waves
+  // (>= FSDP_PROXY_MIN_ITERS iterations per CTA) so that a 3 us norm is not
+  // charged the scheduling of thousands of near-empty CTAs
+  const long long it = static_cast<long long>(iters);
+  const long long waves = std::max(1LL, std::min<long long>(FSDP_PROXY_WAVES, it / FSDP_PROXY_MIN_ITERS));
+  const long long per_cta = (it + waves - 1) / waves;
+  fsdp_compute_proxy_kernel<<<static_cast<unsigned>(grid * waves), 256, smem, s>>>(per_cta, sink);
   return cudaGetLastError();
 }
 

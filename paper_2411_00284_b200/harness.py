@@ -432,13 +432,26 @@ def plans_search(specs, world, t_fwd, t_bwd, ag=(0, 0), rs=(0, 0), mem_max=0, fl
 
 
 def calibrate_proxy(ctx, stream, ctas_per_sm=1, smem=0, probe_iters=200000):
-    """ns per proxy iteration on this device, now (clocks vary): median of 5."""
-    ns = F.proxy_calibrate(ctx, probe_iters, ctas_per_sm, smem, 5, stream)
-    return ns / probe_iters
+    """Proxy duration model on this device, now (clocks vary): K7 timed (median
+    of 5) at probe_iters and probe_iters / 10 -> (ns per iteration, fixed ns
+    per launch), an affine fit: the 16 waves of short CTAs cost a fixed
+    launch / drain time on top of the iterations (a pure ratio ran
+    100 us - 1 ms ops 10-13 % long)."""
+    lo = probe_iters // 10
+    t_hi = F.proxy_calibrate(ctx, probe_iters, ctas_per_sm, smem, 5, stream)
+    t_lo = F.proxy_calibrate(ctx, lo, ctas_per_sm, smem, 5, stream)
+    slope = (t_hi - t_lo) / (probe_iters - lo)
+    if slope <= 0:
+        return (t_hi / probe_iters, 0.0)
+    return (slope, max(0.0, t_lo - slope * lo))
 
 
-def proxy_iters(t_ns_per_bucket, ns_per_iter):
-    return [int(round(t / ns_per_iter)) if t > 0 else 0 for t in t_ns_per_bucket]
+def proxy_iters(t_ns_per_bucket, cal):
+    """Iterations of K7 that take t ns: cal = calibrate_proxy's (ns per
+    iteration, fixed ns) or a plain ns-per-iteration; the fixed part is taken
+    off ops longer than twice it (shorter ops keep half their time)."""
+    slope, fixed = cal if isinstance(cal, tuple) else (cal, 0.0)
+    return [int(round(max(t - fixed, 0.5 * t) / slope)) if t > 0 else 0 for t in t_ns_per_bucket]
 
 
 def bucket_times(plan, t_per_param):

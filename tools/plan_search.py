@@ -32,9 +32,10 @@ sys.path.insert(0, ROOT)
 
 # copy-kernel model (profiles/r01_bench_default_final2.json): K3 6.47 TB/s,
 # K4 6.68 TB/s, ~6 us of launch + ramp + tail per copy launch; a bucket's
-# compute pays ~16 us on top of its T_c (the median measured overhead of the
-# compute proxy over 582 per-parameter ops at T = 2048; with 4-8 us assumed,
-# plans of ~130 buckets were predicted faster than they measured)
+# compute is charged 16 us on top of its T_c (the median overhead the compute
+# proxy measured over 582 per-parameter ops at T = 2048 before its affine
+# calibration; now 2-8 us, so the charge is conservative: it keeps the search
+# from plans of hundreds of buckets whose launch costs a real model pays)
 K3_BPUS, K4_BPUS, LAUNCH_NS, COMPUTE_NS = 6470000, 6680000, 6000, 16000   # rates in bytes per microsecond
 
 
