@@ -156,7 +156,7 @@ def c2(tokens=(1024, 2048)):
     nspi = H.calibrate_proxy(ctx, s.cuda_stream)
     ctx.close()
     R, FB, BB = L.SCHED_REORDER, L.SCHED_FWD_AG_BEFORE_WAIT, L.SCHED_BWD_AG_BEFORE_WAIT
-    out = {"proxy_ns_per_iter": nspi}
+    out = {"proxy_cal": nspi}
     for T in tokens:
         f, b = per_param_compute_ns(specs, T)
         rows = {}
@@ -192,7 +192,7 @@ def c2w(worlds=(2, 4, 8), T=1024):
     ctx.close()
     R, FB = L.SCHED_REORDER, L.SCHED_FWD_AG_BEFORE_WAIT
     f, b = per_param_compute_ns(specs, T)
-    out = {"tokens_per_gpu": T, "proxy_ns_per_iter": nspi}
+    out = {"tokens_per_gpu": T, "proxy_cal": nspi}
     for w in worlds:
         nvl = (20000, round((w - 1) / w / 720e9 * 1e15))
         rows = {}
@@ -234,12 +234,33 @@ def c2m(tokens=(1024, 4096)):
     return out
 
 
-def c3(caps_mb=(25, 50, 100, 200, 500)):
+def c3(caps_mb=(25, 50, 100, 200, 500), T=2048):
+    """configs[3]: Llama-3-70B at N = 8, SIZE_CAP bucket-size sweep, with the
+    compute proxy at T tokens and the predicted N = 8 step / exposure (same
+    model as c2), plus the greedy plan and the per-block plan for reference."""
+    import torch
+    import paper_2411_00284_b200 as F
     from paper_2411_00284_b200 import _lib as L
+    from paper_2411_00284_b200 import harness as H
     from workloads import llama
+    from workloads.compute_model import per_param_compute_ns
     specs = llama("70b")
-    return {"%d MB" % m: run_variant(specs, 8, L.PLAN_SIZE_CAP, L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT,
-                                     mem_max=m * 10**6, steps=3, warmup=1) for m in caps_mb}
+    ctx = F.Ctx(8, 0)
+    s = torch.cuda.Stream()
+    nspi = H.calibrate_proxy(ctx, s.cuda_stream)
+    ctx.close()
+    f, b = per_param_compute_ns(specs, T)
+    nvl = (20000, 1215)
+    RF = L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT
+    out = {"tokens_per_gpu": T, "proxy_cal": nspi}
+    for m in caps_mb:
+        out["size_cap %d MB" % m] = run_variant(specs, 8, L.PLAN_SIZE_CAP, RF, f, b, mem_max=m * 10**6, tokens=T,
+                                                nspi=nspi, steps=2, warmup=1, link=nvl, predict_link=(nvl, nvl))
+    out["manual (per block)"] = run_variant(specs, 8, L.PLAN_MANUAL, RF, f, b, mem_max=2 * 10**9, tokens=T,
+                                            nspi=nspi, steps=2, warmup=1, link=nvl, predict_link=(nvl, nvl))
+    out["greedy (M_max 2 GB)"] = run_variant(specs, 8, L.PLAN_GREEDY, RF, f, b, mem_max=2 * 10**9, tokens=T,
+                                             nspi=nspi, steps=2, warmup=1, link=nvl, predict_link=(nvl, nvl))
+    return out
 
 
 def c4():
