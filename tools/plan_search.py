@@ -153,6 +153,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=1024)
     ap.add_argument("--world", type=int, default=8)
     ap.add_argument("--mem-limit", type=float, default=2e9)
+    ap.add_argument("--model", default="8b")
     ap.add_argument("--budget-s", type=float, default=90.0)
     ap.add_argument("--out", default=None)
     ap.add_argument("--python", action="store_true", help="use the Python reference search instead of the library")
@@ -162,7 +163,7 @@ def main():
     from paper_2411_00284_b200 import harness as H
     from workloads import llama
     from workloads.compute_model import per_param_compute_ns
-    specs = llama("8b")
+    specs = llama(a.model)
     P = len(specs)
     tf, tb = per_param_compute_ns(specs, a.tokens)
     link = (20000, round((a.world - 1) / a.world / 720e9 * 1e15))
@@ -170,7 +171,7 @@ def main():
     starts = {}
     for name, mode in (("manual", L.PLAN_MANUAL), ("greedy", L.PLAN_GREEDY), ("per_param", L.PLAN_PER_PARAM)):
         starts[name] = H.plans_for(specs, a.world, mode, tf, tb, link, link, int(a.mem_limit))
-    out = {"world": a.world, "tokens_per_gpu": a.tokens, "link": link, "mem_max": a.mem_limit,
+    out = {"model": "llama3-" + a.model, "world": a.world, "tokens_per_gpu": a.tokens, "link": link, "mem_max": a.mem_limit,
            "copy_model": {"K3_bytes_per_us": K3_BPUS, "K4_bytes_per_us": K4_BPUS, "launch_ns": LAUNCH_NS,
                           "compute_overhead_ns": COMPUTE_NS}, "phases": {}, "plans": {}}
     for phase, t_c in ((0, tf), (1, tb)):
