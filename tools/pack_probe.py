@@ -10,6 +10,7 @@ shard at N = 8 (16032 x 4096 bf16 = 131 MB) and one 8B block at N = 8:
   k3_unpack   K3 of the two-member bucket
   k6_copy     K6 copy-out of the block's RS segment
   k6_accum    K6 in gradient-accumulation mode (shard += segment)
+  k6_bf16     K6 rounding into bf16 gradient shards (FSDP_BUCKET_BF16_GRAD_SHARDS)
   torch_copy  torch copy_ of the same bytes (reference point)
 Prints one JSON object; GB/s are algorithmic bytes (read + write) / time.
 """
@@ -104,6 +105,14 @@ def main():
         F.reduce_scatter_bucket(ctx, b, rst[i].data_ptr(), cs, 0, L.ISSUE)   # latch the mode
     out["k6_accum"] = timed(lambda i: F.reduce_scatter_bucket(ctx, ba[i], rst[i].data_ptr(), cs, 0, L.WAIT),
                             3 * rseg, s)
+    del ba
+    # K6 rounding into bf16 gradient shards (FSDP_BUCKET_BF16_GRAD_SHARDS, G41): 4 B read + 2 B written
+    gsh16 = [[torch.zeros(-(-dd // world) * rr, dtype=torch.int16, device="cuda") for dd, rr, _ in descs]
+             for _ in range(SETS)]
+    b16 = [F.Bucket(ctx, descs, grad_shards=[g.data_ptr() for g in gsh16[i]], flags=L.BUCKET_BF16_GRAD_SHARDS)
+           for i in range(SETS)]
+    out["k6_bf16"] = timed(lambda i: F.reduce_scatter_bucket(ctx, b16[i], rst[i].data_ptr(), cs, 0, L.WAIT),
+                           rseg + rseg // 2, s)
     torch.cuda.synchronize()
     print(json.dumps(out))
 
