@@ -431,8 +431,24 @@ def main():
     #     --eager (the p2p path replays too: its epochs advance on the device);
     #     the eager enqueue of the same steps is timed beside it
     sg = None
-    if not args.eager and model is None:   # a Python hook cannot be baked into a graph
+    if not args.eager and model is None:
         sg = st.capture(flags, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, gemm=gemm)
+        for _ in range(args.warmup):
+            sg.launch(cs)
+    elif not args.eager:
+        # the model's torch ops through the hook: torch captures the whole step
+        # (library kernels, collectives and the hook's ops) into one graph
+        tg = st.capture_with_torch(flags, compute, ms, pf, pb, args.proxy_ctas, args.proxy_smem, gemm=gemm,
+                                   hook=hook)
+
+        class _TorchGraph:
+            def launch(self, stream):
+                with torch.cuda.stream(compute):
+                    tg.replay()
+
+            def close(self):
+                pass
+        sg = _TorchGraph()
         for _ in range(args.warmup):
             sg.launch(cs)
 
@@ -691,7 +707,9 @@ def main():
             "predicted": predicted,
             "model_check": dict(model_check, measured_eager_ms=round(ms_eager, 3)) if model_check else None,
             "linear_compute": gemm_report,
-            "timing": "CUDA-graph replay of the step (fsdp_step_graph)" if sg is not None else "eager enqueue",
+            "timing": ("eager enqueue" if sg is None else "CUDA-graph replay of the step (fsdp_step_graph)"
+                       if model is None else "CUDA-graph replay of the step incl. the hook's torch ops "
+                                             "(torch.cuda.graph)"),
             "eager_ms_per_step": round(ms_eager, 3),
             "host_enqueue_ms_per_step": (round(1e3 * sorted(host_enqueue)[len(host_enqueue) // 2], 3)
                                          if host_enqueue else None),

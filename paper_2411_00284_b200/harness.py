@@ -330,6 +330,21 @@ class RankState:
                            proxy_iters_bwd=proxy_bwd, proxy_ctas_per_sm=ctas_per_sm, proxy_smem_bytes=smem,
                            gemm=gemm)
 
+    def capture_with_torch(self, flags, compute_stream, comm, proxy_fwd=None, proxy_bwd=None, ctas_per_sm=1,
+                           smem=0, gemm=None, hook=None):
+        """The step -- library kernels and collectives AND a PyTorch compute
+        hook's ops -- captured into one CUDA graph by torch (torch.cuda.graph
+        on `compute_stream`, a torch.cuda.Stream, with torch's private memory
+        pool for the hook's tensors; the comm stream joins through the
+        library's events).  fsdp_step_graph cannot hold a hook that allocates
+        through torch; this can.  Returns the torch.cuda.CUDAGraph (replay()
+        on any stream)."""
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=compute_stream, capture_error_mode="thread_local"):
+            self.step(flags, compute_stream.cuda_stream, comm, proxy_fwd, proxy_bwd, ctas_per_sm, smem,
+                      gemm=gemm, hook=hook)
+        return g
+
     # -------------------------------------------------------------- accounting
     def step_bytes(self):
         """Full (gathered / reduced) bucket bytes one step moves through its

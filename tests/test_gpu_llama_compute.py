@@ -88,3 +88,32 @@ def test_hook_called_in_schedule_order():
     assert calls == want and len(calls) == len(st.fwd) + len(st.bwd)
     del st
     ctx.close()
+
+
+def test_hooked_step_as_one_torch_graph():
+    """The whole step -- gathers, Llama layers (torch ops through the hook),
+    gradient pack, reduce-scatter, read-out -- captured into one CUDA graph
+    (RankState.capture_with_torch) and replayed: same loss, same gradient
+    shards as the eager step (within autograd's nondeterministic attention
+    backward)."""
+    specs, ctx, st = _state(L.PLAN_MANUAL, True)
+    lc = LC.LlamaCompute(st, T, seed=9)
+    cs, ms = torch.cuda.Stream(), torch.cuda.Stream()
+    flags = L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT
+    for _ in range(2):     # warm-up (cuBLAS handles, allocator)
+        st.step(flags, cs.cuda_stream, ms.cuda_stream, hook=lc.hook)
+    torch.cuda.synchronize()
+    want_loss = lc.state[0].clone()
+    want = st.gshard_buf.clone()
+    g = st.capture_with_torch(flags, cs, ms.cuda_stream, hook=lc.hook)
+    st.gshard_buf.fill_(0x11)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(cs):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(lc.state[0], want_loss)
+    got, ref = st.gshard_buf.view(torch.float32), want.view(torch.float32)
+    assert torch.isfinite(got).all()
+    assert ((got - ref).norm() / ref.norm()).item() < 1e-2
+    del g, lc, st
+    ctx.close()
