@@ -562,6 +562,36 @@ def main():
                 "memory_model_peak_GiB": predicted["memory_model_peak_GiB"]}
             predicted["variants"] = variants
 
+    # MEASURED exposure of the N-rank step with emulated collectives (K11,
+    # fsdp_comm_emulation): every AG / RS runs on the comm stream with the
+    # modelled NVLink duration, 32 CTAs and the HBM traffic a rank sees, so
+    # (step - compute-only step) includes the SM / HBM contention the
+    # two-stream prediction leaves out.  Timing only (no peers, no real data).
+    emulated = None
+    if not multi and not p2p and args.predict_tokens and not gemm and not model:
+        em = dict(ag=link, rs=link, ctas=32)   # 16 CTAs could not move an 8B block's RS bytes in time
+
+        def em_loop(extra, emulate, n):
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(compute)
+            for _ in range(n):
+                st.step(flags | extra, cs, ms, ppf, ppb, args.proxy_ctas, args.proxy_smem, emulate=emulate)
+            b.record(compute)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / n
+        em_loop(0, em, 1)   # warm-up
+        em_step = em_loop(0, em, args.steps)
+        em_comp = em_loop(L.SCHED_NO_COMM, None, args.steps)
+        emulated = {"world": world, "tokens_per_gpu": args.predict_tokens, "link_alpha_ns": link[0],
+                    "link_beta_fs_per_byte": link[1], "ctas_per_collective": 32,
+                    "step_ms": round(em_step, 3), "compute_only_ms": round(em_comp, 3),
+                    "exposed_ms": round(em_step - em_comp, 3),
+                    "predicted_exposed_ms": predicted["exposed_ms"] if predicted else None,
+                    "how": "same plan and proxy compute as `predicted`, collectives emulated on the comm stream "
+                           "(kernel K11: modelled duration, 32 CTAs, the rank's HBM traffic); measured with "
+                           "CUDA events, eager enqueue"}
+
     # linear-layer compute throughput (cuBLASLt, tensor cores) of the timed steps
     gemm_report = None
     if model:
@@ -705,6 +735,7 @@ def main():
             "exposed_comm_ms": round(ms_eager - ms_compute, 3), "compute_stream_ms": round(ms_compute, 3),
             "profiled_ms_per_step": round(ms_prof, 3),
             "predicted": predicted,
+            "emulated": emulated,
             "model_check": dict(model_check, measured_eager_ms=round(ms_eager, 3)) if model_check else None,
             "linear_compute": gemm_report,
             "timing": ("eager enqueue" if sg is None else "CUDA-graph replay of the step (fsdp_step_graph)"

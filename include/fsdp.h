@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define FSDP_ABI_VERSION 2  /* 2: fsdp_schedule.hook (fsdp_compute_hook) appended */
+#define FSDP_ABI_VERSION 3  /* 2: fsdp_schedule.hook appended; 3: fsdp_schedule.emulate appended */
 
 typedef void* fsdp_stream_t; /* cudaStream_t */
 
@@ -492,7 +492,29 @@ typedef struct {
   const struct fsdp_host_io* io; /* host-resident shards / gradient shards, else NULL */
   const struct fsdp_gemm_compute* gemm; /* real linear-layer compute instead of K7, else NULL */
   const struct fsdp_compute_hook* hook; /* caller's model compute instead of K7 / gemm, else NULL */
+  const struct fsdp_comm_emulation* emulate; /* emulated N-rank collectives on a layout-only ctx, else NULL */
 } fsdp_schedule;
+
+/* Emulated collectives (a measurement device, like the compute proxy K7): on
+ * a layout-only ctx (no peers) every AG / RS of the step runs as kernel K11 on
+ * the comm stream, with the collective's buffers, SM footprint and duration:
+ * `ctas` CTAs of 512 threads (NCCL runs one CTA per channel) move the bytes a
+ * rank's HBM sees -- AG: this rank's segment copied into the other N - 1 slots
+ * of the gathered buffer; RS: the N fp32 segments summed into this rank's
+ * output -- and then hold their SMs until alpha + ceil(n beta / 1e6) ns (n =
+ * the collective's full bucket bytes, fsdp_comm_time_ns) have passed since the
+ * kernel began.  So the step's exposed time, measured on ONE GPU as (step -
+ * compute-only step), includes the SM and HBM contention between the
+ * collectives and the compute that the two-stream model leaves out.  The data
+ * the emulated collectives leave behind are not the gathered / reduced values
+ * (there are no peers): timing only.  Needs a ctx without a communicator, not
+ * FSDP_SCHED_P2P, no FSDP_BUCKET_GROUPED_AG buckets; 1 <= ctas <= 148. */
+typedef struct fsdp_comm_emulation {
+  fsdp_link ag;
+  fsdp_link rs;
+  int32_t ctas;
+  int32_t reserved; /* must be 0 */
+} fsdp_comm_emulation;
 
 /* Caller-supplied model compute (the real block instead
  * of the proxy).  With `hook` set, the schedule calls

@@ -109,6 +109,10 @@ class GemmCompute(C.Structure):
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64)]
 
 
+class CommEmulation(C.Structure):
+    _fields_ = [("ag", Link), ("rs", Link), ("ctas", C.c_int32), ("reserved", C.c_int32)]
+
+
 COMPUTE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p)
 
 
@@ -124,7 +128,7 @@ class Schedule(C.Structure):
                 ("n_bwd", C.c_int32), ("flags", C.c_uint32), ("proxy_ctas_per_sm", C.c_int32),
                 ("proxy_smem_bytes", C.c_int32), ("reserved", C.c_int32), ("p2p", C.POINTER(P2PSchedule)),
                 ("io", C.POINTER(HostIO)), ("gemm", C.POINTER(GemmCompute)),
-                ("hook", C.POINTER(ComputeHook))]
+                ("hook", C.POINTER(ComputeHook)), ("emulate", C.POINTER(CommEmulation))]
 
 
 class MemSizes(C.Structure):

@@ -338,7 +338,7 @@ namespace fsdp {
 // Per-bucket steps, shared by the public calls and the schedule executor.
 // `launches` / `colls` (nullable) count enqueued kernels / collectives;
 // with_comm = false (FSDP_SCHED_NO_COMM) skips collectives and waits.
-static bool comm_on(fsdp_ctx* c, bool with_comm) { return with_comm && c->comm != nullptr; }
+static bool comm_on(fsdp_ctx* c, bool with_comm) { return with_comm && (c->comm != nullptr || c->emul != nullptr); }
 
 fsdp_status ag_pack(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream_t cs, bool with_comm, int* launches) {
   // segment storage: the collective sends from it, no pack -- except for a
@@ -379,6 +379,14 @@ fsdp_status ag_collective(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream
   // A direct-gather bucket gathers into the full parameter itself.
   char* recv = b->ag_direct ? b->full0 : staging;
   const char* send = b->ag_zero_copy ? b->shard_seg : recv + c->rank * b->ag_seg;
+  if (!c->comm) {  // emulated collective (fsdp_comm_emulation): K11 on the comm stream
+    int64_t ns = 0;
+    FSDP_TRY(fsdp_comm_time_ns(c->world * b->ag_seg, &c->emul->ag, &ns));
+    FSDP_CUDA_TRY(launch_comm_emulation(false, send, recv, b->ag_seg, c->world, c->rank, ns, c->emul->ctas, ms));
+    FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_done, ms));
+    if (colls) ++*colls;
+    return FSDP_OK;
+  }
   FSDP_NCCL_TRY(ncclAllGather(send, recv, static_cast<size_t>(b->ag_seg), ncclInt8, c->comm, ms));
   FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_done, ms));
   if (colls) ++*colls;
@@ -426,6 +434,14 @@ fsdp_status rs_collective(fsdp_ctx* c, fsdp_bucket* b, char* staging, cudaStream
   // recvcount) or straight into segment-layout gradient-shard storage.
   // (accumulation needs the result beside the shards, so it goes to staging)
   char* recv = (b->rs_zero_copy && !b->rs_accum_issued) ? b->gshard_seg : staging + c->rank * b->rs_seg;
+  if (!c->comm) {  // emulated collective (fsdp_comm_emulation): K11 on the comm stream
+    int64_t ns = 0;
+    FSDP_TRY(fsdp_comm_time_ns(c->world * b->rs_seg, &c->emul->rs, &ns));
+    FSDP_CUDA_TRY(launch_comm_emulation(true, staging, recv, b->rs_seg, c->world, c->rank, ns, c->emul->ctas, ms));
+    FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_done, ms));
+    if (colls) ++*colls;
+    return FSDP_OK;
+  }
   FSDP_NCCL_TRY(ncclReduceScatter(staging, recv, static_cast<size_t>(b->rs_seg / 4), ncclFloat32, ncclSum,
                                   c->comm, ms));
   FSDP_CUDA_TRY(cudaEventRecord(b->ev_rs_done, ms));

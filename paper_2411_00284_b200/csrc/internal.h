@@ -141,6 +141,11 @@ enum KernelKind { KK_SHARD = 0, KK_AG_PACK, KK_AG_UNPACK, KK_RS_PACK, KK_RS_COPY
 cudaError_t launch_table(KernelKind kind, const DevTable& t, char* base, float scale, cudaStream_t s,
                          int max_ctas);
 cudaError_t launch_proxy(int64_t iters, int grid, int smem, float* sink, cudaStream_t s);
+// K11: emulated collective (fsdp_comm_emulation).  AG: `src` (seg bytes) copied
+// into the N - 1 slots q != rank of `dst` (N x seg); RS: dst (seg bytes) = sum
+// over q of the fp32 slots of `src` (N x seg); then hold until target_ns.
+cudaError_t launch_comm_emulation(bool reduce, const char* src, char* dst, int64_t seg, int32_t world, int32_t rank,
+                                  int64_t target_ns, int ctas, cudaStream_t s);
 cudaError_t launch_p2p_allgather(const DevTable& t, const PeerTable& pt, cudaStream_t s, int max_ctas);
 // Epoch handshake fused into K9 (scheduled step): wait for wait_flags[q] >=
 // wait_value before reading, store signal_value into every signal_slots[q]
@@ -206,6 +211,7 @@ struct fsdp_ctx {
   std::vector<cudaEvent_t> io_events;      // pool for host I/O ordering (fsdp_host_io)
   cudaStream_t own_h2d = nullptr, own_d2h = nullptr;
   void* gemm_cache = nullptr;              // cuBLASLt handle + plans (gemm.cc)
+  const fsdp_comm_emulation* emul = nullptr;  // set by fsdp_run_schedule for the call (emulated collectives)
   // NCCL registrations (ncclmem.cc): base pointer -> local handle / window
   std::vector<std::pair<void*, void*>> nccl_regs;
   std::vector<std::pair<void*, ncclWindow_t>> nccl_wins;

@@ -954,6 +954,58 @@ cudaError_t launch_p2p_wait(const void* flags, int world, uint64_t value, int64_
   return cudaGetLastError();
 }
 
+// K11: an emulated collective (measurement device, fsdp_comm_emulation).
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(512) fsdp_comm_emulate_kernel(int reduce, const char* __restrict__ src,
+                                                                 char* __restrict__ dst, long long seg, int world,
+                                                                 int rank, long long target_ns) {
+  const unsigned long long t0 = global_ns();
+  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long nth = static_cast<long long>(gridDim.x) * blockDim.x;
+  if (!reduce) {
+    // this rank's segment into every other slot (16-B units; seg is 16-B aligned)
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    const long long n = seg / 16;
+    for (int q = 0; q < world; ++q) {
+      if (q == rank) continue;
+      uint4* d = reinterpret_cast<uint4*>(dst + static_cast<long long>(q) * seg);
+      for (long long i = tid; i < n; i += nth) d[i] = s[i];
+    }
+  } else {
+    // fp32 sum of the N slots into this rank's output
+    const float4* s = reinterpret_cast<const float4*>(src);
+    float4* d = reinterpret_cast<float4*>(dst);
+    const long long n = seg / 16;
+    for (long long i = tid; i < n; i += nth) {
+      float4 a = s[i];
+      for (int q = 1; q < world; ++q) {
+        const float4 b = s[static_cast<long long>(q) * n + i];
+        a.x += b.x;
+        a.y += b.y;
+        a.z += b.z;
+        a.w += b.w;
+      }
+      d[i] = a;
+    }
+  }
+  // hold the SMs for the collective's modelled duration, like NCCL's CTAs
+  if (threadIdx.x == 0)
+    while (global_ns() - t0 < static_cast<unsigned long long>(target_ns)) __nanosleep(256);
+  __syncthreads();
+}
+
+cudaError_t launch_comm_emulation(bool reduce, const char* src, char* dst, int64_t seg, int32_t world, int32_t rank,
+                                  int64_t target_ns, int ctas, cudaStream_t s) {
+  (void)cudaGetLastError();
+  fsdp_comm_emulate_kernel<<<ctas, 512, 0, s>>>(reduce ? 1 : 0, src, dst, seg, world, rank, target_ns);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_proxy(int64_t iters, int grid, int smem, float* sink, cudaStream_t s) {
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fsdp_compute_proxy_kernel,
@@ -978,6 +1030,7 @@ cudaError_t launch_proxy(int64_t iters, int grid, int smem, float* sink, cudaStr
 cudaError_t preload_kernels() {
   cudaFuncAttributes a;
   const void* fns[] = {
+      reinterpret_cast<const void*>(fsdp_comm_emulate_kernel),
       reinterpret_cast<const void*>(fsdp_shard_kernel), reinterpret_cast<const void*>(fsdp_ag_pack_kernel),
       reinterpret_cast<const void*>(fsdp_ag_unpack_kernel), reinterpret_cast<const void*>(fsdp_rs_pack_kernel),
       reinterpret_cast<const void*>(fsdp_rs_copyout_kernel), reinterpret_cast<const void*>(fsdp_shard_bulk_kernel),

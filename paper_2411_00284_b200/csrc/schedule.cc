@@ -220,6 +220,23 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
         return fail(FSDP_ERR_INVALID_ARG, "host I/O: backward buckets need FSDP_BUCKET_SEGMENT_GRAD_SHARDS");
   }
 
+  if (s->emulate) {
+    const fsdp_comm_emulation* em = s->emulate;
+    if (ctx->comm || p2p) return fail(FSDP_ERR_INVALID_ARG, "emulated collectives need a layout-only ctx, no P2P");
+    if (em->ctas < 1 || em->ctas > 148 || em->reserved != 0 || em->ag.alpha_ns < 0 || em->ag.beta_fs_per_byte < 0 ||
+        em->rs.alpha_ns < 0 || em->rs.beta_fs_per_byte < 0)
+      return fail(FSDP_ERR_INVALID_ARG, "bad fsdp_comm_emulation");
+    for (int32_t i = 0; i < s->n_fwd + s->n_bwd; ++i)
+      if ((i < s->n_fwd ? s->fwd[i] : s->bwd[i - s->n_fwd])->ag_grouped)
+        return fail(FSDP_ERR_INVALID_ARG, "emulated collectives do not cover FSDP_BUCKET_GROUPED_AG");
+  }
+  // the emulated collectives (fsdp_comm_emulation) stand in for a communicator for this call only
+  struct EmulGuard {
+    fsdp_ctx* c;
+    ~EmulGuard() { c->emul = nullptr; }
+  } emul_guard{ctx};
+  ctx->emul = s->emulate;
+
   FSDP_CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t cs = static_cast<cudaStream_t>(s->compute);
   cudaStream_t ms = resolve_comm(ctx, s->comm);

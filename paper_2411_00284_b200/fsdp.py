@@ -211,13 +211,15 @@ def reduce_scatter_bucket(ctx, bucket, staging_ptr, compute=0, comm=0, flags=L.I
 def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0, comm=0, flags=0,
                  proxy_iters_fwd=None, proxy_iters_bwd=None, proxy_ctas_per_sm=1, proxy_smem_bytes=0,
                  n_fwd=None, n_bwd=None, want_log=True, p2p=None, io=None, gemm=None, hook=None,
-                 _capture=None):
+                 emulate=None, _capture=None):
     """fsdp_run_schedule.  fwd / bwd: Bucket lists in execution order (or
     counts via n_fwd / n_bwd with FSDP_SCHED_DRY_RUN and ctx=None).  Returns the
     step report as a dict (log as a list of (phase, op, bucket, stream, ns)).
     p2p (with FSDP_SCHED_P2P): dict with ag_peers (rows of world pointers),
     rs_peers, ready_slots, done_slots, ready_flags, done_flags, epoch_base,
     timeout_ns, error_flag.
+    emulate (fsdp_comm_emulation): dict(ag=(alpha, beta), rs=(alpha, beta),
+    ctas) -- emulated N-rank collectives on a layout-only ctx (timing only).
     hook (fsdp_compute_hook): a Python callable hook(phase, bucket, stream)
     that enqueues the bucket's model compute on `stream` (a cudaStream_t
     handle); an exception inside it aborts the step and is re-raised here."""
@@ -276,6 +278,12 @@ def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0,
         hk = L.ComputeHook(cb, None)
         keep += [cb, hk]
         s.hook = C.pointer(hk)
+    if emulate is not None:
+        # emulate: dict(ag=(alpha_ns, beta_fs), rs=(alpha_ns, beta_fs), ctas) -- fsdp_comm_emulation
+        em = L.CommEmulation(L.Link(*[int(x) for x in emulate["ag"]]), L.Link(*[int(x) for x in emulate["rs"]]),
+                             int(emulate.get("ctas", 16)), 0)
+        keep.append(em)
+        s.emulate = C.pointer(em)
     if _capture is not None:     # StepGraph: capture instead of run
         h = C.c_void_p()
         check(L.lib.fsdp_step_graph_create(ctx.h, C.byref(s), C.byref(h)))

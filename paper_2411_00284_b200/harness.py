@@ -309,7 +309,7 @@ class RankState:
         return self.gemm
 
     def step(self, flags, compute, comm, proxy_fwd=None, proxy_bwd=None, ctas_per_sm=1, smem=0,
-             want_log=False, io=None, gemm=None, hook=None):
+             want_log=False, io=None, gemm=None, hook=None, emulate=None):
         p2p = None
         if flags & L.SCHED_P2P:
             p2p = self.p2p_schedule()   # the device epoch counter advances inside the step
@@ -318,7 +318,8 @@ class RankState:
                               rs_staging=(self.rs_st[0].data_ptr(), self.rs_st[1].data_ptr()),
                               compute=compute, comm=comm, flags=flags, proxy_iters_fwd=proxy_fwd,
                               proxy_iters_bwd=proxy_bwd, proxy_ctas_per_sm=ctas_per_sm,
-                              proxy_smem_bytes=smem, want_log=want_log, p2p=p2p, io=io, gemm=gemm, hook=hook)
+                              proxy_smem_bytes=smem, want_log=want_log, p2p=p2p, io=io, gemm=gemm, hook=hook,
+                              emulate=emulate)
 
     def capture(self, flags, compute, comm, proxy_fwd=None, proxy_bwd=None, ctas_per_sm=1, smem=0, gemm=None):
         """The same step captured into a CUDA graph (fsdp_step_graph_create)."""
