@@ -569,7 +569,7 @@ def main():
     # two-stream prediction leaves out.  Timing only (no peers, no real data).
     emulated = None
     if not multi and not p2p and args.predict_tokens and not gemm and not model:
-        em = dict(ag=link, rs=link, ctas=32)   # 16 CTAs could not move an 8B block's RS bytes in time
+        em = dict(ag=link, rs=link, ctas=H.emulation_ctas(world))   # 32 at N = 8 (16 could not keep up)
 
         def em_loop(extra, emulate, n):
             torch.cuda.synchronize()
@@ -584,12 +584,12 @@ def main():
         em_step = em_loop(0, em, args.steps)
         em_comp = em_loop(L.SCHED_NO_COMM, None, args.steps)
         emulated = {"world": world, "tokens_per_gpu": args.predict_tokens, "link_alpha_ns": link[0],
-                    "link_beta_fs_per_byte": link[1], "ctas_per_collective": 32,
+                    "link_beta_fs_per_byte": link[1], "ctas_per_collective": em["ctas"],
                     "step_ms": round(em_step, 3), "compute_only_ms": round(em_comp, 3),
                     "exposed_ms": round(em_step - em_comp, 3),
                     "predicted_exposed_ms": predicted["exposed_ms"] if predicted else None,
                     "how": "same plan and proxy compute as `predicted`, collectives emulated on the comm stream "
-                           "(kernel K11: modelled duration, 32 CTAs, the rank's HBM traffic); measured with "
+                           "(kernel K11: modelled duration, enough CTAs for the rank's HBM traffic); measured with "
                            "CUDA events, eager enqueue"}
 
     # linear-layer compute throughput (cuBLASLt, tensor cores) of the timed steps

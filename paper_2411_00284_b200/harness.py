@@ -447,6 +447,20 @@ def plans_search(specs, world, t_fwd, t_bwd, ag=(0, 0), rs=(0, 0), mem_max=0, fl
     return out[0], out[1]
 
 
+def emulation_ctas(world, bus_gbps=720.0, per_cta_gbps=29.0):
+    """CTAs for the emulated collectives (K11) of an N-rank job: enough to move
+    a reduce-scatter's HBM bytes (the N fp32 segments read + this rank's
+    segment written, (1 + 1/N) x the bucket) at the modelled bus rate, at the
+    ~29 GB/s per CTA K11 sustained on B200 (32 CTAs hold an 8B block's RS at
+    N = 8 to its modelled time; 16 did not).  32 at N = 8, 42 at N = 4, 75 at
+    N = 2."""
+    import math
+    if world < 2:
+        return 32
+    rate = (1.0 + 1.0 / world) * bus_gbps * world / (world - 1)
+    return int(min(148, max(32, math.ceil(rate / per_cta_gbps))))
+
+
 def calibrate_proxy(ctx, stream, ctas_per_sm=1, smem=0, probe_iters=200000):
     """Proxy duration model on this device, now (clocks vary): K7 timed (median
     of 5) at probe_iters and probe_iters / 10 -> (ns per iteration, fixed ns

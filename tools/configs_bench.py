@@ -37,7 +37,10 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
     from paper_2411_00284_b200 import harness as H
     pdt = L.BF16 if param_dtype is None else param_dtype
     ctx = F.Ctx(world, 0)
-    fplan, bplan = H.plans_for(specs, world, mode, t_fwd, t_bwd, link, link, mem_max, pdt)
+    if mode == "search":    # fsdp_plan_search (beyond Algorithm 1) from the manual and greedy plans
+        fplan, bplan = H.plans_search(specs, world, t_fwd, t_bwd, link, link, mem_max, param_dtype=pdt)
+    else:
+        fplan, bplan = H.plans_for(specs, world, mode, t_fwd, t_bwd, link, link, mem_max, pdt)
     st = H.RankState(specs, world, 0, fplan, bplan, ctx, param_dtype=pdt)
     cs, ms = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
     hook = None
@@ -65,7 +68,7 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
         st.step(flags, cs.cuda_stream, ms.cuda_stream, pf, pb, hook=hook)
     ms_step, _ = loop(0, steps)
     _, reps = loop(L.SCHED_TIMING, steps)
-    predicted = None
+    predicted = emulated = None
     if predict_link is not None:
         # the N-rank step predicted by the library's two-stream model: every
         # compute-stream op at its MEASURED duration on this B200 (copies,
@@ -74,6 +77,23 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
         rep = st.step(flags | L.SCHED_TIMING, cs.cuda_stream, ms.cuda_stream, pf, pb, want_log=True, hook=hook)
         tot, exp = H.simulate_n_rank(st, rep["log"], predict_link[0], predict_link[1])
         predicted = dict(total_ms=round(tot / 1e6, 3), exposed_ms=round(exp / 1e6, 3))
+        # and MEASURED with emulated collectives (K11): contention included
+        em = dict(ag=predict_link[0], rs=predict_link[1], ctas=H.emulation_ctas(world))
+
+        def em_loop(extra, emulate, n):
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(cs)
+            for _ in range(n):
+                st.step(flags | extra, cs.cuda_stream, ms.cuda_stream, pf, pb, hook=hook, emulate=emulate)
+            b.record(cs)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / n
+        em_loop(0, em, 1)
+        e_step = em_loop(0, em, steps)
+        e_comp = em_loop(L.SCHED_NO_COMM, None, steps)
+        emulated = dict(step_ms=round(e_step, 3), compute_only_ms=round(e_comp, 3),
+                        exposed_ms=round(e_step - e_comp, 3))
     measured_tc = None
     if profile:
         # per-bucket compute durations of the timed steps (the paper's profiler,
@@ -112,6 +132,8 @@ def run_variant(specs, world, mode, flags, t_fwd=None, t_bwd=None, mem_max=0, to
                step_GBps=round((ag_b + rs_b) / (ms_step * 1e-3) / 1e9, 1))
     if predicted:
         res["predicted_N%d" % world] = predicted
+    if emulated:
+        res["emulated_N%d" % world] = emulated
     # peak FSDP-buffer memory of this variant's op order under the G40 model
     # (the paper's memory column, Tables 5 / 6) and the static pools this
     # library actually holds
@@ -163,6 +185,7 @@ def c2(tokens=(1024, 2048)):
         variants = [("vanilla", L.PLAN_PER_PARAM, 0), ("+reorder", L.PLAN_PER_PARAM, R | FB),
                     ("+bucket", L.PLAN_MANUAL, 0), ("+reorder&bucket", L.PLAN_MANUAL, R | FB),
                     ("greedy+reorder", L.PLAN_GREEDY, R | FB),
+                    ("search+reorder", "search", R | FB),
                     ("place fwd-before/bwd-before", L.PLAN_MANUAL, R | FB | BB),
                     ("place fwd-after/bwd-before", L.PLAN_MANUAL, R | BB),
                     ("place fwd-after/bwd-after", L.PLAN_MANUAL, R)]
@@ -227,6 +250,7 @@ def c2m(tokens=(1024, 4096)):
         for name, mode, flags in (("+reorder", L.PLAN_PER_PARAM, R | FB), ("+bucket", L.PLAN_MANUAL, 0),
                                   ("+reorder&bucket", L.PLAN_MANUAL, R | FB),
                                   ("greedy+reorder (measured T_c)", L.PLAN_GREEDY, R | FB),
+                                  ("search+reorder (measured T_c)", "search", R | FB),
                                   ("place fwd-after/bwd-before", L.PLAN_MANUAL, R | BB)):
             rows[name] = run_variant(specs, 8, mode, flags, f, b, mem_max=2 * 10**9, steps=2, warmup=1, link=nvl,
                                      predict_link=(nvl, nvl), model_T=T)
