@@ -271,7 +271,7 @@ def fused_leg(args):
     """bench.py --collective p2p at N = 1 on the same workload (child process)."""
     cmd = [sys.executable, os.path.abspath(__file__), "--collective", "p2p", "--steps", str(args.steps),
            "--warmup", str(args.warmup), "--no-e2e", "--no-cpu-baseline", "--no-fused-leg",
-           "--predict-tokens", "0", "--plan", args.plan, "--model", args.model, "--sim-world", str(args.sim_world)]
+           "--predict-tokens", str(args.predict_tokens), "--plan", args.plan, "--model", args.model, "--sim-world", str(args.sim_world)]
     try:
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
         d = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
@@ -280,6 +280,7 @@ def fused_leg(args):
     return {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"],
             "collective": d["config"]["collective"], "kernels": d["kernels"], "roofline": d["roofline"],
             "gpu_launches": d["gpu_launches"], "p2p_wait_timeouts": d["p2p_wait_timeouts"],
+            "emulated": d.get("emulated"),
             "how": "bench.py --collective p2p (same workload, same K/W, own process)"}
 
 
@@ -568,8 +569,17 @@ def main():
     # (step - compute-only step) includes the SM / HBM contention the
     # two-stream prediction leaves out.  Timing only (no peers, no real data).
     emulated = None
-    if not multi and not p2p and args.predict_tokens and not gemm and not model:
-        em = dict(ag=link, rs=link, ctas=H.emulation_ctas(world))   # 32 at N = 8 (16 could not keep up)
+    if not multi and p2p and args.predict_tokens and not gemm and not model:
+        # the fused peer-memory path: K8 / K9 against the simulated peers, paced to
+        # the modelled link time (fsdp_comm_emulation with FSDP_SCHED_P2P)
+        link = (20000, round((world - 1) / world / 720e9 * 1e15))
+        ptf, ptb = per_param_compute_ns(specs, args.predict_tokens)
+        nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
+        ppf = H.proxy_iters(H.bucket_times(fplan, ptf), nspi)
+        ppb = H.proxy_iters(H.bucket_times(bplan, ptb), nspi)
+    if not multi and args.predict_tokens and not gemm and not model:
+        em = dict(ag=link, rs=link,   # 32 CTAs at N = 8 for K11 (16 could not keep up); 57 for paced K8 / K9
+                  ctas=H.emulation_ctas_p2p(world) if p2p else H.emulation_ctas(world))
 
         def em_loop(extra, emulate, n):
             torch.cuda.synchronize()
@@ -588,9 +598,12 @@ def main():
                     "step_ms": round(em_step, 3), "compute_only_ms": round(em_comp, 3),
                     "exposed_ms": round(em_step - em_comp, 3),
                     "predicted_exposed_ms": predicted["exposed_ms"] if predicted else None,
-                    "how": "same plan and proxy compute as `predicted`, collectives emulated on the comm stream "
-                           "(kernel K11: modelled duration, enough CTAs for the rank's HBM traffic); measured with "
-                           "CUDA events, eager enqueue"}
+                    "how": ("same plan and proxy compute as `predicted`, collectives emulated on the comm stream "
+                            "(kernel K11: modelled duration, enough CTAs for the rank's HBM traffic); measured with "
+                            "CUDA events, eager enqueue" if not p2p else
+                            "fused peer-memory kernels K8 / K9 against the simulated peers on a grid of that many "
+                            "CTAs, each held to the modelled link time (AG: bf16 bucket; RS: the bf16 gradients "
+                            "K9 pulls); proxy compute at the same T; CUDA events, eager enqueue")}
 
     # linear-layer compute throughput (cuBLASLt, tensor cores) of the timed steps
     gemm_report = None

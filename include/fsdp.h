@@ -507,8 +507,12 @@ typedef struct {
  * compute-only step), includes the SM and HBM contention between the
  * collectives and the compute that the two-stream model leaves out.  The data
  * the emulated collectives leave behind are not the gathered / reduced values
- * (there are no peers): timing only.  Needs a ctx without a communicator, not
- * FSDP_SCHED_P2P, no FSDP_BUCKET_GROUPED_AG buckets; 1 <= ctas <= 148. */
+ * (there are no peers): timing only.  With FSDP_SCHED_P2P the peer-memory
+ * kernels K8 / K9 themselves do the work (against simulated peers) on a grid
+ * of `ctas` CTAs and each CTA stays until the link time has passed (AG: the
+ * gathered bucket; RS: the bucket's gradients in their dtype); their results
+ * are then the real ones.  Needs a ctx without a communicator, no
+ * FSDP_BUCKET_GROUPED_AG buckets; 1 <= ctas <= 148. */
 typedef struct fsdp_comm_emulation {
   fsdp_link ag;
   fsdp_link rs;

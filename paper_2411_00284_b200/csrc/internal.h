@@ -146,7 +146,10 @@ cudaError_t launch_proxy(int64_t iters, int grid, int smem, float* sink, cudaStr
 // over q of the fp32 slots of `src` (N x seg); then hold until target_ns.
 cudaError_t launch_comm_emulation(bool reduce, const char* src, char* dst, int64_t seg, int32_t world, int32_t rank,
                                   int64_t target_ns, int ctas, cudaStream_t s);
-cudaError_t launch_p2p_allgather(const DevTable& t, const PeerTable& pt, cudaStream_t s, int max_ctas);
+// hold_ns > 0 (emulated NVLink, fsdp_comm_emulation): each CTA stays until
+// hold_ns after it began, so the kernel lasts the modelled link time.
+cudaError_t launch_p2p_allgather(const DevTable& t, const PeerTable& pt, cudaStream_t s, int max_ctas,
+                                 int64_t hold_ns = 0);
 // Epoch handshake fused into K9 (scheduled step): wait for wait_flags[q] >=
 // wait_value before reading, store signal_value into every signal_slots[q]
 // once the whole grid is done; counter: a zeroed device word per stream.
@@ -160,7 +163,8 @@ struct P2PSync {
   unsigned int* counter;  // NULL = no fused handshake
 };
 cudaError_t launch_p2p_reduce_scatter(const DevTable& t, const PeerTable& pt, int world, float scale,
-                                      bool accumulate, cudaStream_t s, int max_ctas, const P2PSync* sync = nullptr);
+                                      bool accumulate, cudaStream_t s, int max_ctas, const P2PSync* sync = nullptr,
+                                      int64_t hold_ns = 0);
 // K10: src offsets relative to the multicast mapping of the RS staging.
 cudaError_t launch_nvls_reduce(const DevTable& t, const char* mc_base, bool accumulate, cudaStream_t s,
                                int max_ctas);

@@ -90,6 +90,20 @@ namespace fsdp {
 namespace {
 
 constexpr int kThreads = FSDP_THREADS;
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Emulated link time (fsdp_comm_emulation): the CTA stays until hold_ns after t0.
+__device__ __forceinline__ void hold_until(unsigned long long t0, long long hold_ns) {
+  if (hold_ns <= 0) return;
+  if (threadIdx.x == 0)
+    while (global_ns() - t0 < static_cast<unsigned long long>(hold_ns)) __nanosleep(256);
+  __syncthreads();
+}
 constexpr int kUnroll = FSDP_UNROLL;
 constexpr int kStages = FSDP_BULK_STAGES;
 
@@ -701,8 +715,11 @@ __device__ __forceinline__ void run_peer_reduce(const Chunk* __restrict__ tab, i
 }  // namespace
 
 // K8: fused all-gather + copy-out over peer memory.
-__global__ void FSDP_LSU_BOUNDS fsdp_p2p_allgather_kernel(const Chunk* tab, int n, const __grid_constant__ PeerTable pt) {
+__global__ void FSDP_LSU_BOUNDS fsdp_p2p_allgather_kernel(const Chunk* tab, int n, const __grid_constant__ PeerTable pt,
+                                                          long long hold_ns) {
+  const unsigned long long t0 = hold_ns > 0 ? global_ns() : 0ull;
   run_peer_copy(tab, n, pt);
+  hold_until(t0, hold_ns);
 }
 namespace {
 // Spin (lanes q < world of the calling warp) until flags[q] >= value at system
@@ -745,12 +762,14 @@ __device__ __forceinline__ void store_flags(const PeerTable& slots, int world, u
 // wait / signal launches around the reduction.
 __global__ void __launch_bounds__(kThreads, FSDP_K9_MIN_BLOCKS) fsdp_p2p_reduce_scatter_kernel(
     const Chunk* tab, int n, const __grid_constant__ PeerTable pt, int world, float scale, int accum,
-    const __grid_constant__ P2PSync sync) {
+    const __grid_constant__ P2PSync sync, long long hold_ns) {
   if (sync.counter) {
     if (threadIdx.x < 32) wait_flags(sync.wait_flags, world, sync.wait_value, sync.timeout_ns, sync.err);
     __syncthreads();
   }
+  const unsigned long long t0 = hold_ns > 0 ? global_ns() : 0ull;
   run_peer_reduce(tab, n, pt, world, scale, accum != 0);
+  hold_until(t0, hold_ns);
   if (sync.counter) {
     __syncthreads();  // every thread of this CTA is done reading peer memory
     if (threadIdx.x == 0) {
@@ -902,22 +921,24 @@ cudaError_t launch_table(KernelKind kind, const DevTable& t, char* base, float s
   return cudaGetLastError();
 }
 
-cudaError_t launch_p2p_allgather(const DevTable& t, const PeerTable& pt, cudaStream_t s, int max_ctas) {
+cudaError_t launch_p2p_allgather(const DevTable& t, const PeerTable& pt, cudaStream_t s, int max_ctas,
+                                 int64_t hold_ns) {
   if (t.n == 0) return cudaSuccess;
   (void)cudaGetLastError();
-  fsdp_p2p_allgather_kernel<<<t.n < max_ctas ? t.n : max_ctas, kThreads, 0, s>>>(t.d, t.n, pt);
+  fsdp_p2p_allgather_kernel<<<t.n < max_ctas ? t.n : max_ctas, kThreads, 0, s>>>(t.d, t.n, pt, hold_ns);
   return cudaGetLastError();
 }
 
 cudaError_t launch_p2p_reduce_scatter(const DevTable& t, const PeerTable& pt, int world, float scale,
-                                      bool accumulate, cudaStream_t s, int max_ctas, const P2PSync* sync) {
+                                      bool accumulate, cudaStream_t s, int max_ctas, const P2PSync* sync,
+                                      int64_t hold_ns) {
   P2PSync none{};
   if (t.n == 0 && !sync) return cudaSuccess;
   (void)cudaGetLastError();
   // a fused handshake needs >= 1 CTA even for an empty table
   const int grid = t.n == 0 ? 1 : (t.n < max_ctas ? t.n : max_ctas);
   fsdp_p2p_reduce_scatter_kernel<<<grid, kThreads, 0, s>>>(t.d, t.n, pt, world, scale, accumulate ? 1 : 0,
-                                                           sync ? *sync : none);
+                                                           sync ? *sync : none, hold_ns);
   return cudaGetLastError();
 }
 
@@ -955,11 +976,6 @@ cudaError_t launch_p2p_wait(const void* flags, int world, uint64_t value, int64_
 }
 
 // K11: an emulated collective (measurement device, fsdp_comm_emulation).
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 __global__ void __launch_bounds__(512) fsdp_comm_emulate_kernel(int reduce, const char* __restrict__ src,
                                                                  char* __restrict__ dst, long long seg, int world,

@@ -222,7 +222,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
 
   if (s->emulate) {
     const fsdp_comm_emulation* em = s->emulate;
-    if (ctx->comm || p2p) return fail(FSDP_ERR_INVALID_ARG, "emulated collectives need a layout-only ctx, no P2P");
+    if (ctx->comm) return fail(FSDP_ERR_INVALID_ARG, "emulated collectives need a ctx without a communicator");
     if (em->ctas < 1 || em->ctas > 148 || em->reserved != 0 || em->ag.alpha_ns < 0 || em->ag.beta_fs_per_byte < 0 ||
         em->rs.alpha_ns < 0 || em->rs.beta_fs_per_byte < 0)
       return fail(FSDP_ERR_INVALID_ARG, "bad fsdp_comm_emulation");
@@ -235,7 +235,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     fsdp_ctx* c;
     ~EmulGuard() { c->emul = nullptr; }
   } emul_guard{ctx};
-  ctx->emul = s->emulate;
+  ctx->emul = p2p ? nullptr : s->emulate;
 
   FSDP_CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t cs = static_cast<cudaStream_t>(s->compute);
@@ -248,6 +248,17 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   int launches = 0, colls = 0;
   // ---- peer-memory mode: epoch protocol of include/fsdp.h (FSDP_SCHED_P2P)
   const fsdp_p2p_schedule* pp = p2p ? s->p2p : nullptr;
+  // emulated NVLink (fsdp_comm_emulation) for the peer-memory kernels: a grid of
+  // emulate->ctas CTAs that stay for alpha + beta n (AG: the gathered bf16
+  // bucket; RS: the bucket's gradients in their dtype, the bytes K9 pulls)
+  const int p2p_ctas = (pp && s->emulate) ? s->emulate->ctas : ctx->max_ctas;
+  auto p2p_hold = [&](fsdp_bucket* bk, bool rs) -> int64_t {
+    if (!pp || !s->emulate) return 0;
+    int64_t ns = 0;
+    if (rs) fsdp_comm_time_ns(ctx->world * bk->rs_seg / 4 * bk->grad_bytes, &s->emulate->rs, &ns);
+    else fsdp_comm_time_ns(ctx->world * bk->ag_seg, &s->emulate->ag, &ns);
+    return ns;
+  };
   PeerTable ready_slots{}, done_slots{};
   auto epoch = [&](int64_t b) { return pp->epoch_base + 2 + static_cast<uint64_t>(b); };
   const uint64_t* ebase = pp ? pp->epoch_counter : nullptr;  // device epoch counter (nullable)
@@ -361,7 +372,8 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
           if (with_comm) {
             FSDP_CUDA_TRY(cudaStreamWaitEvent(ms, b->ev_ag_packed, 0));
             const int64_t row = o.phase == 0 ? o.bucket : s->n_fwd + o.bucket;
-            FSDP_CUDA_TRY(launch_p2p_allgather(b->p2p_ag, peer_row(pp->ag_peers, row), ms, ctx->max_ctas));
+            FSDP_CUDA_TRY(launch_p2p_allgather(b->p2p_ag, peer_row(pp->ag_peers, row), ms, p2p_ctas,
+                                               p2p_hold(b, false)));
             FSDP_CUDA_TRY(cudaEventRecord(b->ev_ag_done, ms));
             ++launches;
             ++colls;
@@ -395,12 +407,12 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
                          static_cast<long long>(pp->timeout_ns), pp->error_flag, done_slots, epoch(o.bucket),
                          ctx->p2p_counter};
             FSDP_CUDA_TRY(launch_p2p_reduce_scatter(b->p2p_rs, peer_row(pp->rs_peers, o.bucket), ctx->world, inv,
-                                                    b->grad_accumulate, ms, ctx->max_ctas, &sync));
+                                                    b->grad_accumulate, ms, p2p_ctas, &sync, p2p_hold(b, true)));
             ++launches;
 #else
             FSDP_TRY(p2p_wait(pp->ready_flags, epoch(o.bucket), ms));
             FSDP_CUDA_TRY(launch_p2p_reduce_scatter(b->p2p_rs, peer_row(pp->rs_peers, o.bucket), ctx->world, inv,
-                                                    b->grad_accumulate, ms, ctx->max_ctas));
+                                                    b->grad_accumulate, ms, p2p_ctas, nullptr, p2p_hold(b, true)));
             ++launches;
             FSDP_TRY(p2p_signal(done_slots, epoch(o.bucket), ms));  // done reading peers' b
 #endif

@@ -461,6 +461,19 @@ def emulation_ctas(world, bus_gbps=720.0, per_cta_gbps=29.0):
     return int(min(148, max(32, math.ceil(rate / per_cta_gbps))))
 
 
+def emulation_ctas_p2p(world, bus_gbps=720.0, per_cta_gbps=29.0):
+    """CTAs for the paced peer-memory kernels (K8 / K9 under
+    fsdp_comm_emulation): K8 reads all N segments (the simulated peers live in
+    local HBM) and writes the full parameters, 2 x the bucket within the link
+    time of (N - 1) / N of it -> 2 x bus x N / (N - 1) of HBM traffic; 57 CTAs
+    at N = 8."""
+    import math
+    if world < 2:
+        return 32
+    rate = 2.0 * bus_gbps * world / (world - 1)
+    return int(min(148, max(32, math.ceil(rate / per_cta_gbps))))
+
+
 def calibrate_proxy(ctx, stream, ctas_per_sm=1, smem=0, probe_iters=200000):
     """Proxy duration model on this device, now (clocks vary): K7 timed (median
     of 5) at probe_iters and probe_iters / 10 -> (ns per iteration, fixed ns

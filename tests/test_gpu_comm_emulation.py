@@ -91,3 +91,33 @@ def test_emulation_rejections():
         st2.step(0, cs.cuda_stream, ms.cuda_stream, emulate=dict(EM, ctas=0))
     del st2
     ctx2.close()
+
+
+def test_paced_peer_kernels_keep_their_results_and_take_the_link_time():
+    """FSDP_SCHED_P2P with fsdp_comm_emulation: K8 / K9 run on a grid of
+    `ctas` CTAs held to alpha + beta n -- same bytes as without pacing, and
+    every collective op lasts at least its modelled time."""
+    specs = llama("8b", n_layers=1)
+    world = 8
+    ctx = F.Ctx(world, 0)
+    fplan, bplan = H.plans_for(specs, world, L.PLAN_MANUAL)
+    st = H.RankState(specs, world, 0, fplan, bplan, ctx, seed=6)
+    st.setup_p2p_simulated(seed=7)
+    cs, ms = torch.cuda.Stream(), torch.cuda.Stream()
+    flags = L.SCHED_REORDER | L.SCHED_P2P
+    st.step(flags, cs.cuda_stream, ms.cuda_stream)
+    torch.cuda.synchronize()
+    want_g = st.gshard_buf.clone()
+    want_f = [t.clone() for t in st.full_slots]
+    st.gshard_buf.fill_(0x33)
+    torch.cuda.synchronize()
+    rep = st.step(flags | L.SCHED_TIMING, cs.cuda_stream, ms.cuda_stream, emulate=EM)
+    torch.cuda.synchronize()
+    assert int(st.p2p_err.item()) == 0
+    assert torch.equal(st.gshard_buf, want_g)
+    assert all(torch.equal(a, b) for a, b in zip(st.full_slots, want_f))
+    ag = sum(F.comm_time_ns(world * b.ag_seg, LINK) for b in st.fwd + st.bwd)
+    rs = sum(F.comm_time_ns(world * b.rs_seg // 2, LINK) for b in st.bwd)     # bf16 gradients on the wire
+    assert rep["op_ns"][L.OP_AG] >= ag and rep["op_ns"][L.OP_RS] >= rs
+    del st
+    ctx.close()
