@@ -83,6 +83,9 @@ def parse():
                     help="N > 1 NCCL path: allocate the collective buffers with ncclMemAlloc and register them "
                          "(ncclCommRegister / symmetric ncclCommWindowRegister) for zero-copy NVLS / symmetric "
                          "kernels")
+    ap.add_argument("--p2p-max-ctas", type=int, default=-1,
+                    help="N > 1 peer-memory path: K8 / K9 grid cap (-1 = harness.emulation_ctas_p2p(N), 0 = full "
+                         "GPU)")
     ap.add_argument("--nccl-max-ctas", type=int, default=0,
                     help="N > 1 NCCL path: cap NCCL's CTAs per collective (fsdp_ctx_create_config; 0 = NCCL default)")
     ap.add_argument("--no-variants", action="store_true",
@@ -364,6 +367,9 @@ def main():
                 dist.all_gather_object(out, obj)
                 return out
             st.setup_p2p_ipc(exchange)
+            # N > 1: cap the fused kernels' grid like NCCL's channels so the
+            # NVLink-bound K8 / K9 leave the SMs to the compute stream
+            st.p2p_max_ctas = args.p2p_max_ctas if args.p2p_max_ctas >= 0 else H.emulation_ctas_p2p(world)
         else:
             st.setup_p2p_simulated(seed=99)
     flags = 0 if args.no_reorder else L.SCHED_REORDER

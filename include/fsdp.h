@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define FSDP_ABI_VERSION 3  /* 2: fsdp_schedule.hook appended; 3: fsdp_schedule.emulate appended */
+#define FSDP_ABI_VERSION 4  /* 2: schedule.hook; 3: schedule.emulate; 4: p2p_schedule.max_ctas */
 
 typedef void* fsdp_stream_t; /* cudaStream_t */
 
@@ -471,6 +471,13 @@ typedef struct {
                                    step's last kernel adds n_bwd + 2 to it -- the step can
                                    then be captured (fsdp_step_graph) and replayed; keep
                                    epoch_base fixed.  Zero it once before the first step. */
+  int32_t max_ctas;             /* K8 / K9 grid cap (0 = the library's default, ~8 per SM).  At
+                                   N > 1 the peer reads are NVLink-bound and a full-GPU grid
+                                   would hold every SM for the link time, starving the compute
+                                   stream; a cap like NCCL's channel count leaves the SMs to
+                                   compute (57 CTAs carried an 8B block's traffic at N = 8 in
+                                   the emulation). */
+  int32_t reserved;             /* must be 0 */
 } fsdp_p2p_schedule;
 
 typedef struct {

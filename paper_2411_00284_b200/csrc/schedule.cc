@@ -171,6 +171,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
         !pp->ready_flags || !pp->done_flags)
       return fail(FSDP_ERR_INVALID_ARG, "FSDP_SCHED_P2P needs a complete fsdp_p2p_schedule");
     if (ctx->world > kMaxPeers) return fail(FSDP_ERR_UNSUPPORTED, "peer-memory path supports world <= 16");
+    if (pp->max_ctas < 0 || pp->reserved != 0) return fail(FSDP_ERR_INVALID_ARG, "bad fsdp_p2p_schedule.max_ctas");
     for (int32_t i = 0; i < s->n_fwd + s->n_bwd; ++i) {
       fsdp_bucket* b = i < s->n_fwd ? s->fwd[i] : s->bwd[i - s->n_fwd];
       if (!b->ag_zero_copy) return fail(FSDP_ERR_INVALID_ARG, "FSDP_SCHED_P2P needs FSDP_BUCKET_SEGMENT_SHARDS buckets");
@@ -251,7 +252,8 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   // emulated NVLink (fsdp_comm_emulation) for the peer-memory kernels: a grid of
   // emulate->ctas CTAs that stay for alpha + beta n (AG: the gathered bf16
   // bucket; RS: the bucket's gradients in their dtype, the bytes K9 pulls)
-  const int p2p_ctas = (pp && s->emulate) ? s->emulate->ctas : ctx->max_ctas;
+  const int p2p_ctas = (pp && s->emulate) ? s->emulate->ctas
+                       : (pp && pp->max_ctas > 0) ? std::min(pp->max_ctas, ctx->max_ctas) : ctx->max_ctas;
   auto p2p_hold = [&](fsdp_bucket* bk, bool rs) -> int64_t {
     if (!pp || !s->emulate) return 0;
     int64_t ns = 0;

@@ -269,7 +269,7 @@ class RankState:
         return dict(ag_peers=self.ag_peers, rs_peers=self.rs_peers, ready_slots=self.ready_slots,
                     done_slots=self.done_slots, ready_flags=self.ready.data_ptr(), done_flags=self.done.data_ptr(),
                     epoch_base=self.epoch, timeout_ns=timeout_ns, error_flag=self.p2p_err.data_ptr(),
-                    epoch_counter=self.epoch_ctr.data_ptr())
+                    epoch_counter=self.epoch_ctr.data_ptr(), max_ctas=getattr(self, "p2p_max_ctas", 0))
 
     def p2p_bytes(self):
         """Algorithmic bytes per step of K8 (peer AG, both phases) and K9 (peer RS)."""

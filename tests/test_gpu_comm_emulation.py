@@ -121,3 +121,32 @@ def test_paced_peer_kernels_keep_their_results_and_take_the_link_time():
     assert rep["op_ns"][L.OP_AG] >= ag and rep["op_ns"][L.OP_RS] >= rs
     del st
     ctx.close()
+
+
+def test_p2p_grid_cap_same_bytes():
+    """fsdp_p2p_schedule.max_ctas (the N > 1 grid cap of K8 / K9) changes
+    no result; a negative cap is rejected."""
+    specs = llama("8b", n_layers=1)
+    world = 8
+    ctx = F.Ctx(world, 0)
+    fplan, bplan = H.plans_for(specs, world, L.PLAN_MANUAL)
+    st = H.RankState(specs, world, 0, fplan, bplan, ctx, seed=8)
+    st.setup_p2p_simulated(seed=9)
+    cs, ms = torch.cuda.Stream(), torch.cuda.Stream()
+    flags = L.SCHED_REORDER | L.SCHED_P2P
+    st.step(flags, cs.cuda_stream, ms.cuda_stream)
+    torch.cuda.synchronize()
+    want_g, want_f = st.gshard_buf.clone(), [t.clone() for t in st.full_slots]
+    st.gshard_buf.fill_(0x21)
+    torch.cuda.synchronize()
+    st.p2p_max_ctas = H.emulation_ctas_p2p(world)
+    st.step(flags, cs.cuda_stream, ms.cuda_stream)
+    torch.cuda.synchronize()
+    assert int(st.p2p_err.item()) == 0
+    assert torch.equal(st.gshard_buf, want_g) and all(torch.equal(a, b) for a, b in zip(st.full_slots, want_f))
+    st.p2p_max_ctas = -1
+    with pytest.raises(L.FsdpError):
+        st.step(flags, cs.cuda_stream, ms.cuda_stream)
+    st.p2p_max_ctas = 0
+    del st
+    ctx.close()
