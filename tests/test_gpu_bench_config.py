@@ -147,7 +147,10 @@ def test_host_io_step():
     del toy_mlp
 
 
-def test_llama8b_bench_step_sampled_parity():
+@pytest.mark.parametrize("graph", [False, True])
+def test_llama8b_bench_step_sampled_parity(graph):
+    """graph=True: the step as bench.py times it -- captured once into a CUDA
+    graph (fsdp_step_graph) and replayed."""
     world = 8
     specs = llama("8b")
     ctx = F.Ctx(world, 0)
@@ -158,6 +161,15 @@ def test_llama8b_bench_step_sampled_parity():
     flags = L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT
     rep = st.step(flags, cs.cuda_stream, ms.cuda_stream, want_log=True)
     torch.cuda.synchronize()
+    if graph:   # scrub the outputs, then replay the captured step
+        sg = st.capture(flags, cs.cuda_stream, ms.cuda_stream)
+        st.gshard_buf.fill_(0xCD)
+        for t in st.full_slots:
+            t.fill_(0xEE)
+        torch.cuda.synchronize()
+        sg.launch(cs.cuda_stream)
+        torch.cuda.synchronize()
+        sg.close()
     # 35 buckets per phase; shards live in segment layout, so no pack (K1):
     # forward unpack, backward unpack + grad pack + copy-out (no peers: K6 runs)
     assert st.zero_copy()["ag_buckets"] == 70
