@@ -469,3 +469,25 @@ def test_degenerate_steps_and_zero_row_ranks():
     assert rep["op_count"][L.OP_PACK_AG] == 1 and rep["op_count"][L.OP_RS] == 0
     # rank 1's own rows [5, 10) are in place; rank 0's rows come from a peer (none here)
     assert np.array_equal(out.get()[5:], p[5:])
+
+
+def test_bulk_copy_engine_variant_parity():
+    """The TMA bulk-copy engine build (FSDP_BULK=2: cp.async.bulk global ->
+    shared -> global for the 16-B-aligned copy chunks of K0 / K1 / K3 / K6;
+    measured slower than the LSU engine on B200 and off by default, DESIGN.md
+    §6) moves the same bytes: the all-gather and reduce-scatter parity tests
+    pass against it."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    from paper_2411_00284_b200 import build as B
+    lib = os.path.join(B.BUILD, "variants", "bulk", "libfsdp_b200.so")
+    if not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(B.LIB):   # stale vs the main build
+        lib = B.build(defines=["FSDP_BULK=2"], variant="bulk")
+    env = dict(os.environ, FSDP_B200_LIB=lib)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k",
+                        "allgather or reduce_scatter or zero_copy", os.path.join(root, "tests", "test_gpu_parity.py")],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
