@@ -9,6 +9,6 @@ for T in 1024 2048 4096; do
     timeout 600 $B --tokens $T --predict-tokens $T $flags > gpurun_out/psv_${name}_T$T.json 2> gpurun_out/psv_${name}_T$T.err
     python -c "
 import json; d=json.loads(open('gpurun_out/psv_${name}_T$T.json').read().strip().splitlines()[-1]); p=d['predicted']
-print(json.dumps({'T': $T, 'plan': '$name', 'buckets': [d['config']['buckets_fwd'], d['config']['buckets_bwd']], 'total_ms': p['total_ms'], 'exposed_ms': p['exposed_ms'], 'memory_model_peak_GiB': p['memory_model_peak_GiB']}))"
+print(json.dumps({'T': $T, 'plan': '$name', 'buckets': [d['config']['buckets_fwd'], d['config']['buckets_bwd']], 'total_ms': p['total_ms'], 'exposed_ms': p['exposed_ms'], 'memory_model_peak_GiB': p['memory_model_peak_GiB'], 'emulated_step_ms': (d.get('emulated') or {}).get('step_ms'), 'emulated_exposed_ms': (d.get('emulated') or {}).get('exposed_ms')}))"
   done
 done

@@ -8,5 +8,5 @@ for v in "manual:--plan manual" "greedy:--plan greedy" "size_cap_500MB:--plan si
   timeout 900 $B $flags > gpurun_out/psv70_${name}.json 2> gpurun_out/psv70_${name}.err
   python -c "
 import json; d=json.loads(open('gpurun_out/psv70_${name}.json').read().strip().splitlines()[-1]); p=d['predicted']
-print(json.dumps({'model': '70b', 'T': 2048, 'plan': '$name', 'buckets': [d['config']['buckets_fwd'], d['config']['buckets_bwd']], 'total_ms': p['total_ms'], 'exposed_ms': p['exposed_ms'], 'memory_model_peak_GiB': p['memory_model_peak_GiB']}))"
+print(json.dumps({'model': '70b', 'T': 2048, 'plan': '$name', 'buckets': [d['config']['buckets_fwd'], d['config']['buckets_bwd']], 'total_ms': p['total_ms'], 'exposed_ms': p['exposed_ms'], 'memory_model_peak_GiB': p['memory_model_peak_GiB'], 'emulated_step_ms': (d.get('emulated') or {}).get('step_ms'), 'emulated_exposed_ms': (d.get('emulated') or {}).get('exposed_ms')}))"
 done
