@@ -52,6 +52,9 @@ def parse():
                          "from tools/plan_search.py; overrides --plan")
     ap.add_argument("--tokens", type=int, default=None, help="proxy compute tokens/GPU (0 = none)")
     ap.add_argument("--no-reorder", action="store_true")
+    ap.add_argument("--keep-last", action="store_true",
+                    help="FSDP_SCHED_KEEP_LAST_GATHERED (G42): the first backward bucket reuses the last forward "
+                         "bucket's gathered parameters (no re-gather; FSDP2-style, beyond the paper)")
     ap.add_argument("--fwd-placement", default="before", choices=["before", "after"])
     ap.add_argument("--bwd-placement", default="after", choices=["before", "after"])
     ap.add_argument("--mem-limit", type=float, default=2e9)
@@ -379,6 +382,8 @@ def main():
         flags |= L.SCHED_FWD_AG_BEFORE_WAIT
     if args.bwd_placement == "before":
         flags |= L.SCHED_BWD_AG_BEFORE_WAIT
+    if args.keep_last:
+        flags |= L.SCHED_KEEP_LAST_GATHERED
 
     gemm = model = None
     if args.compute == "llama":

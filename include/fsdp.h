@@ -450,8 +450,18 @@ enum {
   FSDP_SCHED_NO_COMM = 8u,
   FSDP_SCHED_DRY_RUN = 16u,
   FSDP_SCHED_TIMING = 32u,
-  FSDP_SCHED_P2P = 64u
+  FSDP_SCHED_P2P = 64u,
+  FSDP_SCHED_KEEP_LAST_GATHERED = 128u
 };
+/* FSDP_SCHED_KEEP_LAST_GATHERED (reading G42; FSDP2's reshard-after-forward
+ * off for the boundary module, which the paper does not describe -- P:137
+ * re-gathers every parameter): the first backward bucket reuses the full
+ * parameters the last forward bucket gathered, so its re-gather (PACK_AG, AG,
+ * WAIT_AG, UNPACK) is left out of the sequence and the log.  Needs
+ * bwd[0] to bind the same members and the same full-parameter pointers as
+ * fwd[n_fwd - 1] (else FSDP_ERR_INVALID_ARG); those parameters stay live
+ * across the forward / backward boundary.  Saves that bucket's all-gather,
+ * which is otherwise fully exposed (nothing precedes it in the backward). */
 
 /* Peer tables of one rank for FSDP_SCHED_P2P (device pointers valid in this
  * process; `world` entries per row). */
@@ -653,7 +663,9 @@ fsdp_status fsdp_simulate_schedule(const fsdp_log_entry* seq, int32_t n, const i
  * (reading G40), walked in sequence order:
  *   PACK_AG (ph, b): + ag[ph][b]      the flat gathered bucket (N x AG segment)
  *   UNPACK  (ph, b): + full[ph][b]    the full parameters, then - ag[ph][b]
- *   COMPUTE_F b    : - full[0][b]     released after forward use
+ *   COMPUTE_F b    : - full[0][b]     released after forward use -- except the
+ *                                      last forward bucket when backward bucket 0 has no
+ *                                      UNPACK (FSDP_SCHED_KEEP_LAST_GATHERED, G42)
  *   COMPUTE_B b    : + grad[b]        the full gradients, then - full[1][b]
  *   PACK_RS b      : + rs[b]          the flat RS input (N x RS segment), then - grad[b]
  *   COPYOUT_RS b   : - rs[b]

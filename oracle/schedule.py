@@ -44,7 +44,19 @@ def forward_sequence(k, reorder=True, placement=BEFORE):
     return s
 
 
-def backward_sequence(k, reorder=True, placement=AFTER):
+def backward_sequence(k, reorder=True, placement=AFTER, keep_first=False):
+    """keep_first (reading G42, an FSDP2-style option the paper does not
+    describe -- P:137 re-gathers every parameter): the first backward bucket
+    reuses the parameters the last forward bucket gathered, so its re-gather
+    (PACK_AG, AG, WAIT_AG, UNPACK of bucket 0) is left out of the sequence;
+    everything else is unchanged."""
+    s = _backward_sequence(k, reorder, placement)
+    if keep_first:
+        s = [e for e in s if not (e[2] == 0 and e[1] in (PACK_AG, AG, WAIT_AG, UNPACK))]
+    return s
+
+
+def _backward_sequence(k, reorder, placement):
     s = []
     if not reorder:
         for b in range(k):
@@ -67,9 +79,9 @@ def backward_sequence(k, reorder=True, placement=AFTER):
     return s
 
 
-def step_sequence(k_fwd, k_bwd, reorder=True, fwd_placement=BEFORE, bwd_placement=AFTER):
+def step_sequence(k_fwd, k_bwd, reorder=True, fwd_placement=BEFORE, bwd_placement=AFTER, keep_first=False):
     return (forward_sequence(k_fwd, reorder, fwd_placement)
-            + backward_sequence(k_bwd, reorder, bwd_placement))
+            + backward_sequence(k_bwd, reorder, bwd_placement, keep_first and k_fwd > 0))
 
 
 def dependencies_respected(seq):
@@ -77,7 +89,8 @@ def dependencies_respected(seq):
     AG after its PACK_AG, WAIT_AG after its AG, UNPACK after its WAIT_AG,
     COMPUTE after its UNPACK, PACK_RS after its COMPUTE_B, RS after its
     PACK_RS, WAIT_RS after its RS, COPYOUT_RS after its WAIT_RS; every op
-    appears exactly once."""
+    appears exactly once.  A backward bucket 0 without its re-gather (G42)
+    computes on the last forward bucket's parameters: after its COMPUTE_F."""
     pos = {}
     for i, (ph, op, b, _) in enumerate(seq):
         key = (ph, op, b)
@@ -86,9 +99,13 @@ def dependencies_respected(seq):
         pos[key] = i
     need = {AG: PACK_AG, WAIT_AG: AG, UNPACK: WAIT_AG, COMPUTE_F: UNPACK, COMPUTE_B: UNPACK,
             PACK_RS: COMPUTE_B, RS: PACK_RS, WAIT_RS: RS, COPYOUT_RS: WAIT_RS}
+    last_f = max([b for (ph, op, b) in pos if ph == 0 and op == COMPUTE_F], default=None)
     for (ph, op, b), i in pos.items():
         if op in need:
-            j = pos.get((ph, need[op], b))
+            dep = (ph, need[op], b)
+            if (ph, op, b) == (1, COMPUTE_B, 0) and dep not in pos and last_f is not None:
+                dep = (0, COMPUTE_F, last_f)      # kept from the forward (G42)
+            j = pos.get(dep)
             if j is None or j > i:
                 return False
     return True

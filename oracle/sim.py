@@ -68,6 +68,9 @@ def simulate(seq, dur, t_coll):
 #                    then frees G(b);
 #   COPYOUT_RS b     frees R(b) (the gradient shard it fills is resident);
 #   AG, RS, WAIT_*   allocate nothing (in-place collectives).
+# A backward bucket 0 without UNPACK reuses the last forward bucket's gathered
+# parameters (G42): that bucket's COMPUTE_F then frees nothing, and COMPUTE_B 0
+# frees them.
 # The peak is taken after every allocation, before that op's frees.  Resident
 # shards / gradient shards and activations are outside the curve.
 from .schedule import UNPACK, COMPUTE_F, COMPUTE_B, COPYOUT_RS  # noqa: E402
@@ -81,6 +84,9 @@ def memory_curve(seq, A, Fp, G, R):
     live = 0
     peak = 0
     after = []
+    ops = {(e[0], e[1], e[2]) for e in seq}
+    keep = (1, COMPUTE_B, 0) in ops and (1, UNPACK, 0) not in ops
+    last_f = max([e[2] for e in seq if e[0] == 0 and e[1] == COMPUTE_F], default=None)
     for ph, op, b, _stream in seq:
         if op == PACK_AG:
             live += A(ph, b)
@@ -90,7 +96,8 @@ def memory_curve(seq, A, Fp, G, R):
             peak = max(peak, live)
             live -= A(ph, b)
         elif op == COMPUTE_F:
-            live -= Fp(ph, b)
+            if not (keep and b == last_f):
+                live -= Fp(ph, b)
         elif op == COMPUTE_B:
             live += G(b)
             peak = max(peak, live)

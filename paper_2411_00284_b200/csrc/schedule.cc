@@ -58,41 +58,51 @@ void forward_ops(std::vector<Op>& s, int32_t K, bool reorder, bool before) {
 
 // Backward: re-gather with AG(j+1) after (default) or before Wa(j);
 // "Wr12 is placed before RS34": Wr(j-1) and its read-out precede RS(j).
-void backward_ops(std::vector<Op>& s, int32_t K, bool reorder, bool before) {
+void backward_ops(std::vector<Op>& s, int32_t K, bool reorder, bool before, bool keep_first) {
+  // keep_first (G42): bucket 0 reuses the last forward bucket's gathered
+  // parameters -- its PACK_AG / AG / WAIT_AG / UNPACK are left out
+  const size_t start = s.size();
   if (!reorder) {
     for (int32_t b = 0; b < K; ++b)
       for (int32_t op : {FSDP_OP_PACK_AG, FSDP_OP_AG, FSDP_OP_WAIT_AG, FSDP_OP_UNPACK, FSDP_OP_COMPUTE_B,
                          FSDP_OP_PACK_RS, FSDP_OP_RS, FSDP_OP_WAIT_RS, FSDP_OP_COPYOUT_RS})
         s.push_back({1, op, b});
-    return;
-  }
-  if (K > 0) {
-    s.push_back({1, FSDP_OP_PACK_AG, 0});
-    s.push_back({1, FSDP_OP_AG, 0});
-  }
-  for (int32_t b = 0; b < K; ++b) {
-    auto prefetch = [&] {
-      if (b + 1 < K) {
-        s.push_back({1, FSDP_OP_PACK_AG, b + 1});
-        s.push_back({1, FSDP_OP_AG, b + 1});
-      }
-    };
-    if (before) prefetch();
-    s.push_back({1, FSDP_OP_WAIT_AG, b});
-    s.push_back({1, FSDP_OP_UNPACK, b});
-    if (!before) prefetch();
-    s.push_back({1, FSDP_OP_COMPUTE_B, b});
-    s.push_back({1, FSDP_OP_PACK_RS, b});
-    if (b >= 1) {
-      s.push_back({1, FSDP_OP_WAIT_RS, b - 1});
-      s.push_back({1, FSDP_OP_COPYOUT_RS, b - 1});
+  } else {
+    if (K > 0) {
+      s.push_back({1, FSDP_OP_PACK_AG, 0});
+      s.push_back({1, FSDP_OP_AG, 0});
     }
-    s.push_back({1, FSDP_OP_RS, b});
+    for (int32_t b = 0; b < K; ++b) {
+      auto prefetch = [&] {
+        if (b + 1 < K) {
+          s.push_back({1, FSDP_OP_PACK_AG, b + 1});
+          s.push_back({1, FSDP_OP_AG, b + 1});
+        }
+      };
+      if (before) prefetch();
+      s.push_back({1, FSDP_OP_WAIT_AG, b});
+      s.push_back({1, FSDP_OP_UNPACK, b});
+      if (!before) prefetch();
+      s.push_back({1, FSDP_OP_COMPUTE_B, b});
+      s.push_back({1, FSDP_OP_PACK_RS, b});
+      if (b >= 1) {
+        s.push_back({1, FSDP_OP_WAIT_RS, b - 1});
+        s.push_back({1, FSDP_OP_COPYOUT_RS, b - 1});
+      }
+      s.push_back({1, FSDP_OP_RS, b});
+    }
+    if (K > 0) {
+      s.push_back({1, FSDP_OP_WAIT_RS, K - 1});
+      s.push_back({1, FSDP_OP_COPYOUT_RS, K - 1});
+    }
   }
-  if (K > 0) {
-    s.push_back({1, FSDP_OP_WAIT_RS, K - 1});
-    s.push_back({1, FSDP_OP_COPYOUT_RS, K - 1});
-  }
+  if (keep_first)
+    s.erase(std::remove_if(s.begin() + static_cast<std::ptrdiff_t>(start), s.end(),
+                           [](const Op& o) {
+                             return o.bucket == 0 && (o.op == FSDP_OP_PACK_AG || o.op == FSDP_OP_AG ||
+                                                      o.op == FSDP_OP_WAIT_AG || o.op == FSDP_OP_UNPACK);
+                           }),
+            s.end());
 }
 
 int64_t max_seg(fsdp_bucket* const* bs, int32_t n, bool ag) {
@@ -115,7 +125,8 @@ fsdp_status grow_events(fsdp_ctx* c, size_t n) {
 extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, fsdp_step_report* out) {
   if (!s) return fail(FSDP_ERR_INVALID_ARG, "NULL schedule");
   const uint32_t known = FSDP_SCHED_REORDER | FSDP_SCHED_FWD_AG_BEFORE_WAIT | FSDP_SCHED_BWD_AG_BEFORE_WAIT |
-                         FSDP_SCHED_NO_COMM | FSDP_SCHED_DRY_RUN | FSDP_SCHED_TIMING | FSDP_SCHED_P2P;
+                         FSDP_SCHED_NO_COMM | FSDP_SCHED_DRY_RUN | FSDP_SCHED_TIMING | FSDP_SCHED_P2P |
+                         FSDP_SCHED_KEEP_LAST_GATHERED;
   if (s->flags & ~known) return fail(FSDP_ERR_INVALID_ARG, "unknown schedule flag");
   if (s->n_fwd < 0 || s->n_bwd < 0) return fail(FSDP_ERR_INVALID_ARG, "negative bucket count");
   const bool p2p = s->flags & FSDP_SCHED_P2P;
@@ -127,7 +138,8 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   seq.reserve(5 * s->n_fwd + 9 * s->n_bwd + 4);
   const bool reorder = s->flags & FSDP_SCHED_REORDER;
   forward_ops(seq, s->n_fwd, reorder, s->flags & FSDP_SCHED_FWD_AG_BEFORE_WAIT);
-  backward_ops(seq, s->n_bwd, reorder, s->flags & FSDP_SCHED_BWD_AG_BEFORE_WAIT);
+  const bool keep_last = (s->flags & FSDP_SCHED_KEEP_LAST_GATHERED) && s->n_fwd > 0 && s->n_bwd > 0;
+  backward_ops(seq, s->n_bwd, reorder, s->flags & FSDP_SCHED_BWD_AG_BEFORE_WAIT, keep_last);
 
   if (out) {
     if (out->log && out->log_capacity < static_cast<int32_t>(seq.size()))
@@ -165,6 +177,18 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     if (!s->bwd[i] || s->bwd[i]->ctx != ctx || !s->bwd[i]->has_shards || !s->bwd[i]->has_fulls ||
         !s->bwd[i]->has_grads || !s->bwd[i]->has_gshards)
       return fail(FSDP_ERR_INVALID_ARG, "backward bucket missing, foreign or without AG/RS pointers");
+  if (keep_last) {
+    // the first backward bucket must bind exactly the last forward bucket's gathered parameters
+    const fsdp_bucket* f = s->fwd[s->n_fwd - 1];
+    const fsdp_bucket* g = s->bwd[0];
+    bool same = f->fulls == g->fulls && f->members.size() == g->members.size() && f->param_bytes == g->param_bytes;
+    for (size_t j = 0; same && j < f->members.size(); ++j)
+      same = f->members[j].dim0 == g->members[j].dim0 && f->members[j].row_numel == g->members[j].row_numel;
+    if (!same)
+      return fail(FSDP_ERR_INVALID_ARG,
+                  "FSDP_SCHED_KEEP_LAST_GATHERED: the first backward bucket does not bind the last forward "
+                  "bucket's full parameters");
+  }
   if (p2p) {
     const fsdp_p2p_schedule* pp = s->p2p;
     if (!pp || !pp->ag_peers || (s->n_bwd && !pp->rs_peers) || !pp->ready_slots || !pp->done_slots ||

@@ -71,6 +71,17 @@ extern "C" fsdp_status fsdp_simulate_memory(const fsdp_log_entry* seq, int32_t n
       (sz->n_bwd && (!sz->ag_bwd || !sz->full_bwd || !sz->grad_bwd || !sz->rs_bwd)))
     return fail(FSDP_ERR_INVALID_ARG, "simulate_memory: NULL size array");
   int64_t live = 0, peak = 0;
+  // a backward bucket 0 without UNPACK reuses the last forward bucket's
+  // parameters (G42): that bucket's COMPUTE_F frees nothing
+  bool has_unpack0 = false, has_compute_b0 = false;
+  int32_t last_f = -1;
+  for (int32_t i = 0; i < n; ++i) {
+    const fsdp_log_entry& e = seq[i];
+    if (e.phase == 1 && e.bucket == 0 && e.op == FSDP_OP_UNPACK) has_unpack0 = true;
+    if (e.phase == 1 && e.bucket == 0 && e.op == FSDP_OP_COMPUTE_B) has_compute_b0 = true;
+    if (e.phase == 0 && e.op == FSDP_OP_COMPUTE_F) last_f = std::max(last_f, e.bucket);
+  }
+  const bool keep = has_compute_b0 && !has_unpack0;
   for (int32_t i = 0; i < n; ++i) {
     const fsdp_log_entry& e = seq[i];
     const bool fwd = e.phase == 0;
@@ -89,7 +100,9 @@ extern "C" fsdp_status fsdp_simulate_memory(const fsdp_log_entry* seq, int32_t n
     switch (e.op) {
       case FSDP_OP_PACK_AG: alloc(ag); break;
       case FSDP_OP_UNPACK: alloc(full); live -= ag; break;
-      case FSDP_OP_COMPUTE_F: live -= full; break;
+      case FSDP_OP_COMPUTE_F:
+        if (!(keep && b == last_f)) live -= full;
+        break;
       case FSDP_OP_COMPUTE_B: alloc(grad); live -= full; break;
       case FSDP_OP_PACK_RS: alloc(rs); live -= grad; break;
       case FSDP_OP_COPYOUT_RS: live -= rs; break;

@@ -116,6 +116,10 @@ class RankState:
         sp = self.shard_buf.data_ptr()
         gp = self.gshard_buf.data_ptr()
         self.fwd, self.bwd = [], []
+        # backward bucket b gathers into full-parameter slot (b + off) % 2 with off
+        # chosen so that backward bucket 0 uses the last forward bucket's slot:
+        # with FSDP_SCHED_KEEP_LAST_GATHERED (G42) it reuses those parameters
+        self._bwd_slot_off = (len(fwd_plan) - 1) % 2 if len(fwd_plan) else 0
         max_ag = max_rs = 0
         for phase, plan, out in ((0, fwd_plan, self.fwd), (1, bwd_plan, self.bwd)):
             for b, members in enumerate(plan):
@@ -129,7 +133,7 @@ class RankState:
                     flags |= L.BUCKET_SEGMENT_GRAD_SHARDS
                 if ag_grouped and all(specs[j].dim0 % world == 0 for j in m):
                     flags |= L.BUCKET_GROUPED_AG    # per-member AGs in one NCCL group, no copies
-                fbase = self.full_slots[b % 2].data_ptr()
+                fbase = self.full_slots[self.full_slot_index(phase, b)].data_ptr()
                 gbase = self.grad_slots[b % 2].data_ptr()
                 bk = F.Bucket(ctx, [self.descs[j] for j in m],
                               shards=[sp + self.shard_offs[j] for j in m],
@@ -147,6 +151,11 @@ class RankState:
         if torch.device(device).type == "cuda":
             # fills / zeroing ran on torch's current stream; steps run on the caller's streams
             torch.cuda.synchronize(device)
+
+    def full_slot_index(self, phase, b):
+        """Full-parameter slot of bucket b of a phase (forward b % 2; backward
+        shifted so that its bucket 0 shares the last forward bucket's slot)."""
+        return b % 2 if phase == 0 else (b + self._bwd_slot_off) % 2
 
     def _segment_offsets(self, plan, elem_bytes):
         """Per-parameter byte offsets placing each bucket's members at the

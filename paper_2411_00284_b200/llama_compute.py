@@ -155,8 +155,10 @@ class LlamaCompute:
                     o = st.shard_offs[j]
                     st.shard_buf[o:o + 2 * v].view(torch.bfloat16).fill_(1.0)
         # views of every member's gathered parameter / full gradient, per phase and bucket
-        self.views = (self._views(st.fwd, st.full_slots), self._views(st.bwd, st.full_slots))
-        self.gviews = self._views(st.bwd, st.grad_slots)
+        slot_of = getattr(st, "full_slot_index", lambda phase, b: b % 2)
+        self.views = (self._views(st.fwd, st.full_slots, lambda b: slot_of(0, b)),
+                      self._views(st.bwd, st.full_slots, lambda b: slot_of(1, b)))
+        self.gviews = self._views(st.bwd, st.grad_slots, lambda b: b % 2)
         self.saved = {}
         self.gstate = None
         self.state = ()
@@ -167,14 +169,14 @@ class LlamaCompute:
             # the fills above ran on torch's current stream; the step's streams are not ordered after it
             torch.cuda.synchronize(dev)
 
-    def _views(self, buckets, slots):
+    def _views(self, buckets, slots, slot_of):
         out = []
         for b, bk in enumerate(buckets):
             offs, _ = _carve([self.st.full_numel[j] * 2 for j in bk.members])
             d = {}
             for j, o in zip(bk.members, offs):
                 s = self.st.specs[j]
-                v = slots[b % 2][o:o + 2 * s.dim0 * s.row_numel].view(torch.bfloat16)
+                v = slots[slot_of(b)][o:o + 2 * s.dim0 * s.row_numel].view(torch.bfloat16)
                 d[j] = v.view(s.dim0, s.row_numel) if s.row_numel > 1 else v
             out.append(d)
         return out

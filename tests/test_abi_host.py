@@ -125,14 +125,17 @@ def test_plan_rejects_bad_input():
         F.plan_buckets([(0, 1, 0)], 2, [0], (0, 0), (0, 0), 0, L.PLAN_GREEDY, L.PHASE_FWD)
 
 
-@given(kf=st.integers(0, 40), kb=st.integers(0, 40), reorder=st.booleans(), fb=st.booleans(), bb=st.booleans())
-@settings(max_examples=200, deadline=None)
-def test_dry_run_schedule_log_equals_oracle(kf, kb, reorder, fb, bb):
+@given(kf=st.integers(0, 40), kb=st.integers(0, 40), reorder=st.booleans(), fb=st.booleans(), bb=st.booleans(),
+       keep=st.booleans())
+@settings(max_examples=300, deadline=None)
+def test_dry_run_schedule_log_equals_oracle(kf, kb, reorder, fb, bb, keep):
     flags = L.SCHED_DRY_RUN | (L.SCHED_REORDER if reorder else 0)
     flags |= (L.SCHED_FWD_AG_BEFORE_WAIT if fb else 0) | (L.SCHED_BWD_AG_BEFORE_WAIT if bb else 0)
+    flags |= L.SCHED_KEEP_LAST_GATHERED if keep else 0
     rep = F.run_schedule(None, None, None, flags=flags, n_fwd=kf, n_bwd=kb)
     got = [e[:4] for e in rep["log"]]
-    want = OS.step_sequence(kf, kb, reorder, OS.BEFORE if fb else OS.AFTER, OS.BEFORE if bb else OS.AFTER)
+    want = OS.step_sequence(kf, kb, reorder, OS.BEFORE if fb else OS.AFTER, OS.BEFORE if bb else OS.AFTER,
+                            keep_first=keep)
     assert got == want
     assert all(e[4] == -1 for e in rep["log"])
 
@@ -166,12 +169,15 @@ def test_simulator_matches_oracle(kf, kb, reorder, fb, bb, seed):
        seed=st.integers(0, 2**31))
 @settings(max_examples=300, deadline=None)
 def test_memory_model_matches_oracle(kf, kb, reorder, fb, bb, seed):
-    """fsdp_simulate_memory == oracle.sim.memory_curve (G40), peak and every live value."""
+    """fsdp_simulate_memory == oracle.sim.memory_curve (G40, G42), peak and every live value."""
     from oracle.sim import memory_curve
-    seq = OS.step_sequence(kf, kb, reorder, OS.BEFORE if fb else OS.AFTER, OS.BEFORE if bb else OS.AFTER)
+    seq = OS.step_sequence(kf, kb, reorder, OS.BEFORE if fb else OS.AFTER, OS.BEFORE if bb else OS.AFTER,
+                           keep_first=bool(seed % 2))
     rng = np.random.Generator(np.random.Philox(seed))
     big = lambda k: [int(x) for x in rng.integers(0, 2 ** 40, size=k)]   # noqa: E731  (> 2^32: 64-bit sums)
     agf, fuf, agb, fub, grb, rsb = big(kf), big(kf), big(kb), big(kb), big(kb), big(kb)
+    if seed % 2 and kf and kb:
+        fub[0] = fuf[kf - 1]     # G42: backward bucket 0 binds the last forward bucket's parameters
     ref = memory_curve(seq, lambda ph, b: (agf if ph == 0 else agb)[b], lambda ph, b: (fuf if ph == 0 else fub)[b],
                        lambda b: grb[b], lambda b: rsb[b])
     peak, live = F.simulate_memory(seq, agf, fuf, agb, fub, grb, rsb)

@@ -194,7 +194,7 @@ def test_llama8b_bench_step_sampled_parity(graph):
     for b in (len(st.bwd) - 1, len(st.bwd) - 2):
         bk = st.bwd[b]
         offs, _ = H._carve([st.full_numel[j] * 2 for j in bk.members])
-        slot = st.full_slots[b % 2]
+        slot = st.full_slots[st.full_slot_index(1, b)]
         for j, o in zip(bk.members, offs):
             full = slot[o:o + 2 * st.full_numel[j]]
             n = st.shard_numel[j]

@@ -226,3 +226,46 @@ def test_memory_conservation_and_reorder_costs_memory(kf, kb, seed, fp, bp):
     assert van["final"] == 0 and reo["final"] == 0
     assert min(van["live"]) >= 0 and min(reo["live"]) >= 0
     assert reo["peak"] >= van["peak"]
+
+
+# ------------------------------------------------- keep the last gathered (G42)
+def test_keep_first_hand_sequence():
+    """k_fwd = k_bwd = 2, reordered, default placements: the backward loses
+    exactly bucket 0's PACK_AG / AG / WAIT_AG / UNPACK; COMPUTE_B 0 follows the
+    forward's last COMPUTE_F."""
+    F_, B_ = 0, 1
+    # full: PACK_AG 0, AG 0 | WAIT_AG 0, UNPACK 0, PACK_AG 1, AG 1, COMPUTE_B 0, PACK_RS 0, RS 0 |
+    #       WAIT_AG 1, UNPACK 1, COMPUTE_B 1, PACK_RS 1, WAIT_RS 0, COPYOUT_RS 0, RS 1 | WAIT_RS 1, COPYOUT_RS 1
+    want = [(B_, S.PACK_AG, 1), (B_, S.AG, 1), (B_, S.COMPUTE_B, 0), (B_, S.PACK_RS, 0), (B_, S.RS, 0),
+            (B_, S.WAIT_AG, 1), (B_, S.UNPACK, 1), (B_, S.COMPUTE_B, 1), (B_, S.PACK_RS, 1),
+            (B_, S.WAIT_RS, 0), (B_, S.COPYOUT_RS, 0), (B_, S.RS, 1), (B_, S.WAIT_RS, 1), (B_, S.COPYOUT_RS, 1)]
+    got = [e[:3] for e in S.backward_sequence(2, True, S.AFTER, keep_first=True)]
+    assert got == want
+    full = [e[:3] for e in S.backward_sequence(2, True, S.AFTER)]
+    assert [e for e in full if not (e[2] == 0 and e[1] in (S.PACK_AG, S.AG, S.WAIT_AG, S.UNPACK))] == got
+    seq = S.step_sequence(2, 2, keep_first=True)
+    assert S.dependencies_respected(seq)
+    i_f = seq.index((F_, S.COMPUTE_F, 1, 0))
+    i_b = seq.index((B_, S.COMPUTE_B, 0, 0))
+    assert i_f < i_b
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.integers(1, 8), st.integers(1, 8), st.booleans(), st.integers(0, 10 ** 6),
+       st.sampled_from([S.BEFORE, S.AFTER]), st.sampled_from([S.BEFORE, S.AFTER]))
+def test_keep_first_never_costs_time_or_leaks_memory(kf, kb, reorder, seed, fp, bp):
+    rng = np.random.default_rng(seed)
+    base = S.step_sequence(kf, kb, reorder, fp, bp)
+    keep = S.step_sequence(kf, kb, reorder, fp, bp, keep_first=True)
+    assert S.dependencies_respected(keep) and len(keep) == len(base) - 4
+    dur = {e[:3]: int(rng.integers(0, 50000)) for e in base}
+    f = lambda ph, op, b: dur[(ph, op, b)]   # noqa: E731
+    assert simulate(keep, f, f)["total"] <= simulate(base, f, f)["total"]
+    A = {p: [int(x) for x in rng.integers(1, 10 ** 6, n)] for p, n in ((0, kf), (1, kb))}
+    Fp = {0: [int(x) for x in rng.integers(1, 10 ** 7, kf)], 1: None}
+    Fp[1] = [int(x) for x in rng.integers(1, 10 ** 7, kb)]
+    Fp[1][0] = Fp[0][kf - 1]            # bucket 0 of the backward = the forward's last bucket
+    G = [int(x) for x in rng.integers(1, 10 ** 7, kb)]
+    R = [int(x) for x in rng.integers(1, 10 ** 7, kb)]
+    r = _mem(keep, A, Fp, G, R)
+    assert r["final"] == 0 and min(r["live"]) >= 0
