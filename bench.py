@@ -52,6 +52,9 @@ def parse():
                          "from tools/plan_search.py; overrides --plan")
     ap.add_argument("--tokens", type=int, default=None, help="proxy compute tokens/GPU (0 = none)")
     ap.add_argument("--no-reorder", action="store_true")
+    ap.add_argument("--grad-slots", type=int, default=2,
+                    help="full-gradient slots the backward buckets rotate through (peer-memory path: the backward "
+                         "of bucket b waits for the peers' K9 of bucket b - slots)")
     ap.add_argument("--keep-last", action="store_true",
                     help="FSDP_SCHED_KEEP_LAST_GATHERED (G42): the first backward bucket reuses the last forward "
                          "bucket's gathered parameters (no re-gather; FSDP2-style, beyond the paper)")
@@ -353,7 +356,8 @@ def main():
         assert flat_f == flat_b == list(range(len(specs))), "plan file does not cover the model's parameters"
     reg = args.nccl_register if (multi and not p2p and args.nccl_register != "none") else None
     st = H.RankState(specs, world, rank if multi else 0, fplan, bplan, ctx, seed=1234 + rank,
-                     ipc=multi and p2p, nccl_register=reg, ag_grouped=args.ag == "grouped")
+                     ipc=multi and p2p, nccl_register=reg, ag_grouped=args.ag == "grouped",
+                     grad_slots=args.grad_slots)
     compute = torch.cuda.Stream()
     comm = torch.cuda.Stream(priority=-1)
     cs, ms = compute.cuda_stream, comm.cuda_stream

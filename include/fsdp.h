@@ -487,7 +487,10 @@ typedef struct {
                                    stream; a cap like NCCL's channel count leaves the SMs to
                                    compute (57 CTAs carried an 8B block's traffic at N = 8 in
                                    the emulation). */
-  int32_t reserved;             /* must be 0 */
+  int32_t grad_slots;           /* gradient slots the backward buckets rotate through (0 = 2):
+                                   K9 reads peers' full gradients in place, so the backward of
+                                   bucket b first waits until every peer has consumed bucket
+                                   b - grad_slots (the same slot); more slots = more slack */
 } fsdp_p2p_schedule;
 
 typedef struct {

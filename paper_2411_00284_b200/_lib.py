@@ -98,7 +98,7 @@ class P2PSchedule(C.Structure):
                 ("ready_slots", C.POINTER(C.c_void_p)), ("done_slots", C.POINTER(C.c_void_p)),
                 ("ready_flags", C.c_void_p), ("done_flags", C.c_void_p), ("epoch_base", C.c_uint64),
                 ("timeout_ns", C.c_int64), ("error_flag", C.c_void_p), ("epoch_counter", C.c_void_p),
-                ("max_ctas", C.c_int32), ("reserved", C.c_int32)]
+                ("max_ctas", C.c_int32), ("grad_slots", C.c_int32)]
 
 
 class HostIO(C.Structure):

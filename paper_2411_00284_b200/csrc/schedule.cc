@@ -195,7 +195,8 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
         !pp->ready_flags || !pp->done_flags)
       return fail(FSDP_ERR_INVALID_ARG, "FSDP_SCHED_P2P needs a complete fsdp_p2p_schedule");
     if (ctx->world > kMaxPeers) return fail(FSDP_ERR_UNSUPPORTED, "peer-memory path supports world <= 16");
-    if (pp->max_ctas < 0 || pp->reserved != 0) return fail(FSDP_ERR_INVALID_ARG, "bad fsdp_p2p_schedule.max_ctas");
+    if (pp->max_ctas < 0 || pp->grad_slots < 0 || pp->grad_slots == 1)
+      return fail(FSDP_ERR_INVALID_ARG, "bad fsdp_p2p_schedule.max_ctas / grad_slots");
     for (int32_t i = 0; i < s->n_fwd + s->n_bwd; ++i) {
       fsdp_bucket* b = i < s->n_fwd ? s->fwd[i] : s->bwd[i - s->n_fwd];
       if (!b->ag_zero_copy) return fail(FSDP_ERR_INVALID_ARG, "FSDP_SCHED_P2P needs FSDP_BUCKET_SEGMENT_SHARDS buckets");
@@ -410,9 +411,10 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
           break;
         case FSDP_OP_COMPUTE_F:
         case FSDP_OP_COMPUTE_B: {
-          // the backward of bucket b overwrites gradient slot b % 2: peers must be done with b - 2
-          if (o.op == FSDP_OP_COMPUTE_B && with_comm && o.bucket >= 2)
-            FSDP_TRY(p2p_wait(pp->done_flags, epoch(o.bucket - 2), cs));
+          // the backward of bucket b overwrites gradient slot b % G: peers must be done with b - G
+          const int32_t gslots = pp->grad_slots > 0 ? pp->grad_slots : 2;
+          if (o.op == FSDP_OP_COMPUTE_B && with_comm && o.bucket >= gslots)
+            FSDP_TRY(p2p_wait(pp->done_flags, epoch(o.bucket - gslots), cs));
           FSDP_TRY(compute(o, b));
           break;
         }

@@ -248,7 +248,7 @@ def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0,
         ps.epoch_base, ps.timeout_ns = int(p2p["epoch_base"]), int(p2p.get("timeout_ns", 10**10))
         ps.error_flag = p2p.get("error_flag") or None
         ps.epoch_counter = p2p.get("epoch_counter") or None
-        ps.max_ctas, ps.reserved = int(p2p.get("max_ctas", 0)), 0
+        ps.max_ctas, ps.grad_slots = int(p2p.get("max_ctas", 0)), int(p2p.get("grad_slots", 0))
         keep.append(ps)
         s.p2p = C.pointer(ps)
     if io is not None:

@@ -35,7 +35,7 @@ def _carve(sizes, align=ALIGN):
 class RankState:
     def __init__(self, specs, world, rank, fwd_plan, bwd_plan, ctx, param_dtype=L.BF16,
                  device="cuda", seed=0, fill=True, segment_storage=True, ipc=False, nccl_register=None,
-                 ag_grouped=False):
+                 ag_grouped=False, grad_slots=2):
         # ipc=True: the buffers peers read in the peer-memory path (shard
         # storage, gradient slots) come from fsdp_ipc_alloc so that other
         # processes can map them (setup_p2p_ipc).
@@ -100,7 +100,9 @@ class RankState:
         self.slot_bytes = max(_carve([self.full_numel[j] * ep for j in sorted(b)])[1] for b in buckets)
         self.gslot_bytes = max(_carve([self.full_numel[j] * 2 for j in sorted(b)])[1] for b in buckets)
         self.full_slots = [alloc("fulls%d" % i, self.slot_bytes, collective=True) for i in range(2)]
-        self.grad_slots = [alloc("grads%d" % i, self.gslot_bytes, peer=True) for i in range(2)]
+        # backward bucket b produces its full gradients in slot b % n_grad_slots
+        self.n_grad_slots = int(grad_slots)
+        self.grad_slots = [alloc("grads%d" % i, self.gslot_bytes, peer=True) for i in range(self.n_grad_slots)]
         if fill:
             g = torch.Generator(device=device).manual_seed(seed)
             # N(0, 0.02) bf16 parameters and N(0, 1e-3) bf16 gradients (DESIGN.md input recipe)
@@ -134,7 +136,7 @@ class RankState:
                 if ag_grouped and all(specs[j].dim0 % world == 0 for j in m):
                     flags |= L.BUCKET_GROUPED_AG    # per-member AGs in one NCCL group, no copies
                 fbase = self.full_slots[self.full_slot_index(phase, b)].data_ptr()
-                gbase = self.grad_slots[b % 2].data_ptr()
+                gbase = self.grad_slots[b % self.n_grad_slots].data_ptr()
                 bk = F.Bucket(ctx, [self.descs[j] for j in m],
                               shards=[sp + self.shard_offs[j] for j in m],
                               fulls=[fbase + o for o in offs],
@@ -235,8 +237,8 @@ class RankState:
         self.ready = fl[:8 * W].view(torch.int64)
         self.done = fl[8 * W:].view(torch.int64)
         self.p2p_err = torch.zeros(1, dtype=torch.int32, device=self.shard_buf.device)
-        mine = dict(rank=r, shards=self.ipc_handles["shards"], g0=self.ipc_handles["grads0"],
-                    g1=self.ipc_handles["grads1"], flags=flags_h)
+        mine = dict(rank=r, shards=self.ipc_handles["shards"], flags=flags_h,
+                    grads=[self.ipc_handles["grads%d" % i] for i in range(self.n_grad_slots)])
         allh = sorted(exchange(mine), key=lambda d: d["rank"])
         self._opened = []
         shard_base, grad_base, flag_base = [], [], []
@@ -246,11 +248,11 @@ class RankState:
                 grad_base.append([t.data_ptr() for t in self.grad_slots])
                 flag_base.append(flags_ptr)
                 continue
-            ptrs = [F.ipc_open(h[k]) for k in ("shards", "g0", "g1", "flags")]
+            ptrs = [F.ipc_open(h["shards"]), F.ipc_open(h["flags"])] + [F.ipc_open(g) for g in h["grads"]]
             self._opened += ptrs
             shard_base.append(ptrs[0])
-            grad_base.append([ptrs[1], ptrs[2]])
-            flag_base.append(ptrs[3])
+            flag_base.append(ptrs[1])
+            grad_base.append(ptrs[2:])
         self.ready_slots = [flag_base[q] + 8 * r for q in range(W)]
         self.done_slots = [flag_base[q] + 8 * W + 8 * r for q in range(W)]
         self._p2p_tables(shard_base, grad_base)
@@ -270,7 +272,7 @@ class RankState:
     def _p2p_tables(self, shard_base, grad_base):
         W = self.world
         self.ag_peers = [[shard_base[q] + self.shard_offs[b.members[0]] for q in range(W)] for b in self.fwd + self.bwd]
-        self.rs_peers = [[grad_base[q][i % 2] for q in range(W)] for i, b in enumerate(self.bwd)]
+        self.rs_peers = [[grad_base[q][i % self.n_grad_slots] for q in range(W)] for i, b in enumerate(self.bwd)]
         self.epoch = 0   # fixed epoch_base: the epochs advance on the device (epoch_counter)
         self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=self.shard_buf.device)
 
@@ -278,7 +280,8 @@ class RankState:
         return dict(ag_peers=self.ag_peers, rs_peers=self.rs_peers, ready_slots=self.ready_slots,
                     done_slots=self.done_slots, ready_flags=self.ready.data_ptr(), done_flags=self.done.data_ptr(),
                     epoch_base=self.epoch, timeout_ns=timeout_ns, error_flag=self.p2p_err.data_ptr(),
-                    epoch_counter=self.epoch_ctr.data_ptr(), max_ctas=getattr(self, "p2p_max_ctas", 0))
+                    epoch_counter=self.epoch_ctr.data_ptr(), max_ctas=getattr(self, "p2p_max_ctas", 0),
+                    grad_slots=self.n_grad_slots)
 
     def p2p_bytes(self):
         """Algorithmic bytes per step of K8 (peer AG, both phases) and K9 (peer RS)."""

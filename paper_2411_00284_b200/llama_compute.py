@@ -158,7 +158,8 @@ class LlamaCompute:
         slot_of = getattr(st, "full_slot_index", lambda phase, b: b % 2)
         self.views = (self._views(st.fwd, st.full_slots, lambda b: slot_of(0, b)),
                       self._views(st.bwd, st.full_slots, lambda b: slot_of(1, b)))
-        self.gviews = self._views(st.bwd, st.grad_slots, lambda b: b % 2)
+        ng = getattr(st, "n_grad_slots", 2)
+        self.gviews = self._views(st.bwd, st.grad_slots, lambda b: b % ng)
         self.saved = {}
         self.gstate = None
         self.state = ()

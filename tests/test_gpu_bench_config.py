@@ -180,7 +180,7 @@ def test_llama8b_bench_step_sampled_parity(graph):
     rng = np.random.Generator(np.random.Philox(5))
     gs_u8 = st.gshard_buf
     for b, bk in enumerate(st.bwd):
-        slot = st.grad_slots[b % 2]
+        slot = st.grad_slots[b % st.n_grad_slots]
         offs, _ = H._carve([st.full_numel[j] * 2 for j in bk.members])
         for j, goff in zip(bk.members, offs):
             n = st.shard_numel[j]               # rank 0 owns rows [0, c): the first n elements
