@@ -532,7 +532,7 @@ typedef struct {
  * of `ctas` CTAs and each CTA stays until the link time has passed (AG: the
  * gathered bucket; RS: the bucket's gradients in their dtype); their results
  * are then the real ones.  Needs a ctx without a communicator, no
- * FSDP_BUCKET_GROUPED_AG buckets; 1 <= ctas <= 148. */
+ * FSDP_BUCKET_GROUPED_AG buckets; 1 <= ctas <= 4 x SMs (all resident at once). */
 typedef struct fsdp_comm_emulation {
   fsdp_link ag;
   fsdp_link rs;

@@ -249,7 +249,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   if (s->emulate) {
     const fsdp_comm_emulation* em = s->emulate;
     if (ctx->comm) return fail(FSDP_ERR_INVALID_ARG, "emulated collectives need a ctx without a communicator");
-    if (em->ctas < 1 || em->ctas > 148 || em->reserved != 0 || em->ag.alpha_ns < 0 || em->ag.beta_fs_per_byte < 0 ||
+    if (em->ctas < 1 || em->ctas > 4 * ctx->sm_count || em->reserved != 0 || em->ag.alpha_ns < 0 || em->ag.beta_fs_per_byte < 0 ||
         em->rs.alpha_ns < 0 || em->rs.beta_fs_per_byte < 0)
       return fail(FSDP_ERR_INVALID_ARG, "bad fsdp_comm_emulation");
     for (int32_t i = 0; i < s->n_fwd + s->n_bwd; ++i)
