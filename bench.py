@@ -584,15 +584,19 @@ def main():
     # (step - compute-only step) includes the SM / HBM contention the
     # two-stream prediction leaves out.  Timing only (no peers, no real data).
     emulated = None
-    if not multi and p2p and args.predict_tokens and not gemm and not model:
+    if not multi and p2p and (args.predict_tokens or gemm or model):
         # the fused peer-memory path: K8 / K9 against the simulated peers, paced to
         # the modelled link time (fsdp_comm_emulation with FSDP_SCHED_P2P)
         link = (20000, round((world - 1) / world / 720e9 * 1e15))
-        ptf, ptb = per_param_compute_ns(specs, args.predict_tokens)
-        nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
-        ppf = H.proxy_iters(H.bucket_times(fplan, ptf), nspi)
-        ppb = H.proxy_iters(H.bucket_times(bplan, ptb), nspi)
-    if not multi and args.predict_tokens and not gemm and not model:
+        ppf = ppb = None
+        if not gemm and not model:
+            ptf, ptb = per_param_compute_ns(specs, args.predict_tokens)
+            nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
+            ppf = H.proxy_iters(H.bucket_times(fplan, ptf), nspi)
+            ppb = H.proxy_iters(H.bucket_times(bplan, ptb), nspi)
+    if not multi and (args.predict_tokens or gemm or model):
+        # with --compute gemm / llama the compute is the real tensor-core work, a
+        # more faithful co-runner for the collectives than the ALU-bound proxy
         em = dict(ag=link, rs=link,   # 32 CTAs at N = 8 for K11 (16 could not keep up); 57 for paced K8 / K9
                   ctas=H.emulation_ctas_p2p(world) if p2p else H.emulation_ctas(world))
 
@@ -601,24 +605,27 @@ def main():
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(compute)
             for _ in range(n):
-                st.step(flags | extra, cs, ms, ppf, ppb, args.proxy_ctas, args.proxy_smem, emulate=emulate)
+                st.step(flags | extra, cs, ms, ppf, ppb, args.proxy_ctas, args.proxy_smem, emulate=emulate,
+                        gemm=gemm, hook=hook)
             b.record(compute)
             torch.cuda.synchronize()
             return a.elapsed_time(b) / n
         em_loop(0, em, 1)   # warm-up
         em_step = em_loop(0, em, args.steps)
         em_comp = em_loop(L.SCHED_NO_COMM, None, args.steps)
-        emulated = {"world": world, "tokens_per_gpu": args.predict_tokens, "link_alpha_ns": link[0],
+        emulated = {"world": world, "compute": args.compute,
+                    "tokens_per_gpu": (gemm["tokens"] if gemm else model.T if model else args.predict_tokens),
+                    "link_alpha_ns": link[0],
                     "link_beta_fs_per_byte": link[1], "ctas_per_collective": em["ctas"],
                     "step_ms": round(em_step, 3), "compute_only_ms": round(em_comp, 3),
                     "exposed_ms": round(em_step - em_comp, 3),
                     "predicted_exposed_ms": predicted["exposed_ms"] if predicted else None,
-                    "how": ("same plan and proxy compute as `predicted`, collectives emulated on the comm stream "
+                    "how": ("same plan and compute as `predicted`, collectives emulated on the comm stream "
                             "(kernel K11: modelled duration, enough CTAs for the rank's HBM traffic); measured with "
                             "CUDA events, eager enqueue" if not p2p else
                             "fused peer-memory kernels K8 / K9 against the simulated peers on a grid of that many "
                             "CTAs, each held to the modelled link time (AG: bf16 bucket; RS: the bf16 gradients "
-                            "K9 pulls); proxy compute at the same T; CUDA events, eager enqueue")}
+                            "K9 pulls); the run's compute (see `compute`); CUDA events, eager enqueue")}
 
     # linear-layer compute throughput (cuBLASLt, tensor cores) of the timed steps
     gemm_report = None
