@@ -154,6 +154,8 @@ def main():
     ap.add_argument("--world", type=int, default=8)
     ap.add_argument("--mem-limit", type=float, default=2e9)
     ap.add_argument("--model", default="8b")
+    ap.add_argument("--f-eff", type=float, default=1.0e15,
+                    help="achieved dense bf16 FLOP/s of the compute model (1.33e15 = the cuBLASLt GEMMs measured)")
     ap.add_argument("--budget-s", type=float, default=90.0)
     ap.add_argument("--out", default=None)
     ap.add_argument("--python", action="store_true", help="use the Python reference search instead of the library")
@@ -165,7 +167,7 @@ def main():
     from workloads.compute_model import per_param_compute_ns
     specs = llama(a.model)
     P = len(specs)
-    tf, tb = per_param_compute_ns(specs, a.tokens)
+    tf, tb = per_param_compute_ns(specs, a.tokens, f_eff=a.f_eff)
     link = (20000, round((a.world - 1) / a.world / 720e9 * 1e15))
     flags = {0: L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT, 1: L.SCHED_REORDER}
     starts = {}
