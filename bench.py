@@ -19,6 +19,15 @@ gradient pack (K4), NCCL reduce-scatter, copy-out (K6) for all 35 buckets.
 value = sum over ranks of the full bucket bytes the step's collectives carry
 (forward AG + backward AG in bf16, RS in fp32) / step time, in GB/s.  Inputs
 (64.3 GB of bucket traffic per rank-step) are far larger than the 126 MB L2.
+
+Beside the contract keys the line carries (N = 1): `roofline` (dominant
+kernel vs the measured HBM peak), `kernels` (per-kernel GB/s), `predicted`
+(the N-rank step from measured op durations and alpha + beta n links, with
+vanilla / greedy / searched plan variants and the G40 memory peak),
+`emulated` (the N-rank step MEASURED with emulated collectives, contention
+included), `fused_p2p` (the fused peer-memory path K8 / K9, with its own
+`emulated`), `e2e` (host I/O through fsdp_run_schedule), `cpu_baseline`
+(the oracle on one host core), `clocks`, `env` and `paper_context`.
 """
 import argparse
 import gc
