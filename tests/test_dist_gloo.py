@@ -98,6 +98,18 @@ def _worker(rank, world, port, errq):
         allp = [None] * world
         dist.all_gather_object(allp, plans)
         assert all(p == allp[0] for p in allp)
+        # ... and the same searched plans (fsdp_plan_search, via harness.plans_search)
+        from paper_2411_00284_b200 import harness as H
+        searched = H.plans_search(ls, world, f, b_, (20000, 1500), (20000, 1500), 10**9)
+        alls = [None] * world
+        dist.all_gather_object(alls, searched)
+        assert all(x == alls[0] for x in alls)
+        # ... and the same dry-run step sequence, with the boundary bucket kept (G42)
+        seq = F.run_schedule(None, None, None, n_fwd=len(searched[0]), n_bwd=len(searched[1]),
+                             flags=L.SCHED_DRY_RUN | L.SCHED_REORDER | L.SCHED_KEEP_LAST_GATHERED)["log"]
+        allq = [None] * world
+        dist.all_gather_object(allq, seq)
+        assert all(x == allq[0] for x in allq)
         dist.barrier()
         dist.destroy_process_group()
     except BaseException as e:  # noqa: BLE001
