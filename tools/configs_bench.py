@@ -284,6 +284,8 @@ def c3(caps_mb=(25, 50, 100, 200, 500), T=2048):
                                             nspi=nspi, steps=2, warmup=1, link=nvl, predict_link=(nvl, nvl))
     out["greedy (M_max 2 GB)"] = run_variant(specs, 8, L.PLAN_GREEDY, RF, f, b, mem_max=2 * 10**9, tokens=T,
                                              nspi=nspi, steps=2, warmup=1, link=nvl, predict_link=(nvl, nvl))
+    out["search (M_max 2 GB)"] = run_variant(specs, 8, "search", RF, f, b, mem_max=2 * 10**9, tokens=T,
+                                             nspi=nspi, steps=2, warmup=1, link=nvl, predict_link=(nvl, nvl))
     return out
 
 
