@@ -2,8 +2,10 @@
 # Multi-GPU measurement plan (one node, NVSwitch): run when more than one
 # B200 is available.  Writes JSON lines under gpurun_out/scale/.
 #   1. bench.py at N = 2, 4, 8 for the NCCL flat bucketing (default), the
-#      grouped all-gather, NCCL buffer registration (local / symmetric) and the
-#      fused peer-memory collectives;
+#      grouped all-gather, NCCL buffer registration (local / symmetric), the
+#      fused peer-memory collectives (grid-capped and full grid), the searched
+#      plans, keep-last, real GEMM compute and a bounded NCCL CTA count --
+#      the measured counterparts of this round's emulated results;
 #   2. busbw sweeps + alpha/beta fits per (op, N) for NCCL and p2p, the inputs
 #      the greedy planner (Algorithm 1) needs.
 # Usage: bash tools/scale_check.sh [max_gpus]
@@ -27,6 +29,12 @@ for n in 2 4 8; do
   run $n reglocal --nccl-register local
   run $n regsym --nccl-register symmetric
   run $n p2p --collective p2p
+  run $n p2p_fullgrid --collective p2p --p2p-max-ctas 0      # grid cap off (full GPU) vs the default cap
+  run $n search --plan search                               # fsdp_plan_search (beyond Algorithm 1)
+  run $n search_p2p --plan search --collective p2p
+  run $n keeplast --keep-last                               # G42: no re-gather of the boundary bucket
+  run $n gemm_p2p_search --compute gemm --collective p2p --plan search   # real GEMMs between the collectives
+  run $n nccl_maxctas16 --nccl-max-ctas 16                  # NCCL's SM footprint bounded
   for c in nccl p2p; do
     timeout 1800 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
       --master-port $PORT tools/busbw_sweep.py --collective $c --out $O/busbw_${c}_N$n.json > $O/busbw_${c}_N$n.log 2>&1
