@@ -111,6 +111,9 @@ def parse():
     ap.add_argument("--dist", action="store_true",
                     help="run the torch.distributed / NCCL-communicator path even at --gpus 1 (world 1 with a "
                          "real communicator: checks the N > 1 plumbing on one GPU)")
+    ap.add_argument("--no-gemm-comparison", action="store_true",
+                    help="N=1: skip the emulated N-rank step with GEMM compute for per-block NCCL vs searched fused "
+                         "(two child runs)")
     ap.add_argument("--no-fused-leg", action="store_true",
                     help="N=1 with --collective nccl: skip the extra run of the fused peer-memory mode whose "
                          "summary is reported under 'fused_p2p'")
@@ -288,7 +291,7 @@ def run_reference(args, rank):
 def fused_leg(args):
     """bench.py --collective p2p at N = 1 on the same workload (child process)."""
     cmd = [sys.executable, os.path.abspath(__file__), "--collective", "p2p", "--steps", str(args.steps),
-           "--warmup", str(args.warmup), "--no-e2e", "--no-cpu-baseline", "--no-fused-leg",
+           "--warmup", str(args.warmup), "--no-e2e", "--no-cpu-baseline", "--no-fused-leg", "--no-gemm-comparison",
            "--predict-tokens", str(args.predict_tokens), "--plan", args.plan, "--model", args.model, "--sim-world", str(args.sim_world)]
     try:
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
@@ -300,6 +303,32 @@ def fused_leg(args):
             "gpu_launches": d["gpu_launches"], "p2p_wait_timeouts": d["p2p_wait_timeouts"],
             "emulated": d.get("emulated"),
             "how": "bench.py --collective p2p (same workload, same K/W, own process)"}
+
+
+def gemm_comparison(args):
+    """The N = 8 step with real tensor-core compute (cuBLASLt linear layers,
+    T = 1024) and emulated collectives, measured for the paper-style design
+    (per-block buckets, NCCL + copy kernels) and the B200-native one (searched
+    buckets, fused peer-memory kernels K8 / K9) -- child processes."""
+    out = {}
+    for name, extra in (("per-block + NCCL + copy kernels", ["--plan", "manual", "--collective", "nccl"]),
+                        ("searched + fused K8/K9", ["--plan", "search", "--collective", "p2p"])):
+        cmd = [sys.executable, os.path.abspath(__file__), "--compute", "gemm", "--tokens", "1024", "--steps",
+               str(args.steps), "--warmup", str(args.warmup), "--no-e2e", "--no-cpu-baseline", "--no-fused-leg",
+               "--no-variants", "--no-gemm-comparison", "--model", args.model,
+               "--sim-world", str(args.sim_world)] + extra
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+            d = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+            e = d["emulated"]
+            out[name] = {"emulated_step_ms": e["step_ms"], "compute_only_ms": e["compute_only_ms"],
+                         "exposed_ms": e["exposed_ms"], "buckets": [d["config"]["buckets_fwd"],
+                                                                    d["config"]["buckets_bwd"]]}
+        except Exception as ex:  # reported, never fatal to the headline
+            out[name] = {"error": "%s: %s" % (type(ex).__name__, str(ex)[:200])}
+    out["how"] = ("bench.py --compute gemm --tokens 1024 (cuBLASLt bf16 linear layers on the gathered parameters) "
+                  "with the N-rank collectives emulated (K11 / paced K8-K9), own processes")
+    return out
 
 
 def main():
@@ -747,6 +776,10 @@ def main():
     fused = None
     if rank == 0 and not multi and not p2p and not args.no_fused_leg and args.compute == "proxy":
         fused = fused_leg(args)
+    gemm_cmp = None
+    if rank == 0 and not multi and not p2p and not args.no_gemm_comparison and args.compute == "proxy" \
+            and args.model == "8b":
+        gemm_cmp = gemm_comparison(args)
 
     if rank == 0:
         line = {
@@ -801,6 +834,7 @@ def main():
             "zero_copy": st.zero_copy(),
             "p2p_wait_timeouts": int(st.p2p_err.item()) if p2p else None,
             "fused_p2p": fused,
+            "emulated_gemm_comparison": gemm_cmp,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
             "env": run_env(torch),

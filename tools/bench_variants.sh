@@ -1,7 +1,7 @@
 #!/bin/bash
 # Robustness sweep of bench.py variants on one B200 (gpurun): plans, collectives, compute modes,
 # model sizes, layout worlds.  Writes gpurun_out/sw_<name>.json; summarised in profiles/r01_bench_variants.json.
-B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-fused-leg --no-e2e --predict-tokens 0"
+B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-fused-leg --no-gemm-comparison --no-e2e --predict-tokens 0"
 run() { name=$1; shift; timeout 600 $B "$@" > gpurun_out/sw_$name.json 2> gpurun_out/sw_$name.err; echo "$name rc=$? $(tail -c 300 gpurun_out/sw_$name.json | grep -o '"ms_per_step": [0-9.]*' | head -1)"; }
 run greedy --plan greedy --tokens 1024
 run pp_noreorder --plan per_param --no-reorder

@@ -3,7 +3,7 @@
 # layout world N = 2 / 4 / 8 with the compute proxy at T = 1024 and the
 # collectives emulated (K11 for NCCL + copy kernels, paced K8 / K9 for the
 # fused path).  One JSON line per (N, collective).
-B="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-fused-leg --no-e2e --no-variants --predict-tokens 1024"
+B="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-fused-leg --no-gemm-comparison --no-e2e --no-variants --predict-tokens 1024"
 for N in 2 4 8; do
   for c in nccl p2p; do
     timeout 600 $B --sim-world $N --collective $c > gpurun_out/es_${c}_$N.json 2> gpurun_out/es_${c}_$N.err

@@ -7,7 +7,7 @@
 set -u
 O=gpurun_out/ncu
 mkdir -p $O
-B="bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-fused-leg --no-variants --predict-tokens 0"
+B="bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-fused-leg --no-gemm-comparison --no-variants --predict-tokens 0"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $O/launches.csv python $B > $O/launches_bench.log 2>&1
 echo "launch list rc=$?"
 for k in fsdp_ag_unpack_kernel fsdp_rs_pack_kernel fsdp_rs_copyout_kernel; do
@@ -15,7 +15,7 @@ for k in fsdp_ag_unpack_kernel fsdp_rs_pack_kernel fsdp_rs_copyout_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on -k $k -s 4 -c 2 -o $O/full_$k python $B > $O/full_$k.log 2>&1
   echo "$k rc=$?"
 done
-P="bench.py --collective p2p --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-fused-leg --no-variants --predict-tokens 0"
+P="bench.py --collective p2p --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-fused-leg --no-gemm-comparison --no-variants --predict-tokens 0"
 for k in fsdp_p2p_allgather_kernel fsdp_p2p_reduce_scatter_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on -k $k -s 4 -c 2 -o $O/full_$k python $P > $O/full_$k.log 2>&1
   echo "$k rc=$?"
