@@ -118,6 +118,27 @@ def test_plan_hand_examples(golden):
         assert [[pos[j] for j in bb] for bb in cb] == ex["buckets"]
 
 
+def test_plan_world3_hand_examples(golden):
+    """C++ planner against the world-3 hand-worked Alg. 1 examples (G8 / G13 world factor)."""
+    g = golden("alg1_world3_examples.json")
+    st_ = g["setup"]
+    params = [(d, r, i) for i, (d, r) in enumerate(st_["params_forward_order"])]
+    for key in ("forward_time", "forward_memory", "backward"):
+        ex = g[key]
+        pi = PlanInput(params, st_["world"], ex["t_c_ns"], (st_["alpha_ns"], st_["beta_ag_fs"]),
+                       (st_["alpha_ns"], st_["beta_rs_fs"]), ex["mem_max"], GREEDY,
+                       FWD if ex["phase"] == "fwd" else BWD)
+        ob, otr, cb, ctr = _both_plans(pi, L.BF16)
+        _assert_same(ob, otr, cb, ctr, GREEDY)
+        assert [[j + 1 for j in bb] for bb in cb] == ex["buckets"]
+        assert [(t["param"] + 1, t["t_lhs"], t["t_rhs"], t["m_lhs"], bool(t["accept"])) for t in ctr] == \
+            [(t["param"], t["t_lhs"], t["t_rhs"], t["m_lhs"], t["accept"]) for t in ex["trace"]]
+        # the library's own default M_i (mem_bytes NULL): N ceil(d/N) R e_p
+        cb2, ctr2 = F.plan_buckets(pi.params, 3, pi.t_compute_ns, pi.ag, pi.rs, pi.mem_max, L.PLAN_GREEDY,
+                                   PHASES[pi.phase], param_dtype=L.BF16, want_trace=True)
+        assert (cb2, ctr2) == (cb, ctr)
+
+
 def test_plan_rejects_bad_input():
     with pytest.raises(F.FsdpError):
         F.plan_buckets([], 2, [], (0, 0), (0, 0), 0, L.PLAN_GREEDY, L.PHASE_FWD)

@@ -175,3 +175,68 @@ def test_toy_greedy_plan_runs():
                        param_bytes=4)
         b, _ = plan(pi)
         assert verify_greedy(pi, b)
+
+
+def _world3_input(ex, setup):
+    params = [(d, r, i) for i, (d, r) in enumerate(setup["params_forward_order"])]
+    return PlanInput(params, setup["world"], ex["t_c_ns"], (setup["alpha_ns"], setup["beta_ag_fs"]),
+                     (setup["alpha_ns"], setup["beta_rs_fs"]), ex["mem_max"], GREEDY,
+                     FWD if ex["phase"] == "fwd" else BWD, param_bytes=setup["param_bytes"],
+                     reduce_bytes=setup["reduce_bytes"], align=setup["align"])   # default M_i (G13)
+
+
+def _labelled(buckets, trace):
+    return ([[j + 1 for j in b] for b in buckets],
+            [dict(param=t["param"] + 1, t_lhs=t["t_lhs"], t_rhs=t["t_rhs"], m_lhs=t["m_lhs"],
+                  accept=t["accept"]) for t in trace])
+
+
+@pytest.mark.parametrize("case", ["forward_time", "forward_memory", "backward"])
+def test_alg1_world3_hand_examples(golden, case):
+    """World factor pins (P:222 n = transmitted bytes; P:237 M_ci; G8 / G13):
+    hand-worked at N = 3 with uneven dim 0 and the default M_i."""
+    g = golden("alg1_world3_examples.json")
+    ex = g[case]
+    pi = _world3_input(ex, g["setup"])
+    assert pi.mem_bytes == [12, 720000, 480000, 720000, 12, 720000]   # N ceil(d/N) R e_p by hand
+    buckets, trace = plan(pi)
+    got_b, got_t = _labelled(buckets, trace)
+    assert got_b == ex["buckets"]
+    assert got_t == ex["trace"]
+    assert verify_greedy(pi, buckets)
+
+
+def test_alg1_world3_examples_detect_a_dropped_world_factor(golden, monkeypatch):
+    """The examples are sensitive: the oracle with N dropped from n (AG, RS) or
+    from the default M_i disagrees with at least one of them."""
+    from oracle import planner as OP
+    from oracle.cost import comm_time
+    from oracle.layout import bucket_layout
+    g = golden("alg1_world3_examples.json")
+
+    def all_match():
+        out = []
+        for case in ("forward_time", "forward_memory", "backward"):
+            ex = g[case]
+            pi = _world3_input(ex, g["setup"])
+            b, t = plan(pi)
+            out.append(_labelled(b, t) == (ex["buckets"], ex["trace"]))
+        return all(out)
+
+    assert all_match()
+    with monkeypatch.context() as m:
+        m.setattr(OP.PlanInput, "t_ag", lambda self, mem: comm_time(
+            bucket_layout(self.dims(mem), self.world, self.param_bytes, self.align)[1], *self.ag))
+        assert not all_match()
+    with monkeypatch.context() as m:
+        m.setattr(OP.PlanInput, "t_rs", lambda self, mem: comm_time(
+            bucket_layout(self.dims(mem), self.world, self.reduce_bytes, self.align)[1], *self.rs))
+        assert not all_match()
+    orig_init = OP.PlanInput.__init__
+
+    def init_no_n(self, *a, **k):
+        orig_init(self, *a, **k)
+        self.mem_bytes = [(-(-d // self.world)) * r * self.param_bytes for d, r, _ in self.params]
+    with monkeypatch.context() as m:
+        m.setattr(OP.PlanInput, "__init__", init_no_n)
+        assert not all_match()

@@ -48,9 +48,23 @@ def test_sequences_are_linear_extensions(kf, kb, reorder, fp, bp):
     assert sum(1 for e in seq if e[1] == S.AG) == kf + kb       # alpha count = buckets
     assert sum(1 for e in seq if e[1] == S.RS) == kb
     assert all((e[3] == 1) == (e[1] in S.COMM_OPS) for e in seq)
-    if reorder:
-        # prefetch depth 1: never two AG issued ahead of the current wait
-        pass
+    # prefetch depth (G16 = 1, P:189 'prefetch bucket i+1 during compute of
+    # bucket i'): when WAIT_AG k of a phase is enqueued, exactly k + 1 AGs of
+    # that phase have been issued (vanilla, or reorder with the AG placed after
+    # the wait) or k + 2 (reorder with the AG placed before the wait), never more;
+    # under reorder AG k+1 is always issued before COMPUTE k.
+    for ph, kk, place in ((0, kf, fp), (1, kb, bp)):
+        for k in range(kk):
+            w = _idx(seq, ph, S.WAIT_AG, k)
+            issued = sum(1 for e in seq[:w] if e[0] == ph and e[1] == S.AG)
+            ahead = 1 if (reorder and place == S.BEFORE and k + 1 < kk) else 0
+            assert issued == k + 1 + ahead
+            if reorder and k + 1 < kk:
+                comp = S.COMPUTE_F if ph == 0 else S.COMPUTE_B
+                assert _idx(seq, ph, S.AG, k + 1) < _idx(seq, ph, comp, k)
+            if not reorder and k + 1 < kk:
+                comp = S.COMPUTE_F if ph == 0 else S.COMPUTE_B
+                assert _idx(seq, ph, S.AG, k + 1) > _idx(seq, ph, comp, k)
 
 
 def _two_bucket(ex):
