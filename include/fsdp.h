@@ -41,7 +41,8 @@
 extern "C" {
 #endif
 
-#define FSDP_ABI_VERSION 4  /* 2: schedule.hook; 3: schedule.emulate; 4: p2p_schedule.max_ctas */
+#define FSDP_ABI_VERSION 5  /* 2: schedule.hook; 3: schedule.emulate; 4: p2p_schedule.max_ctas;
+                              5: fsdp_bucket_launch_kernel */
 
 typedef void* fsdp_stream_t; /* cudaStream_t */
 
@@ -398,6 +399,20 @@ fsdp_status fsdp_reduce_scatter_bucket(fsdp_ctx* ctx, fsdp_bucket* b, void* rs_s
  * NULL bucket, on not 0/1. */
 fsdp_status fsdp_bucket_set_grad_accumulation(fsdp_bucket* b, int32_t on);
 
+/* One data kernel of a bucket, alone (measurement; no event, no collective,
+ * no wait): op = FSDP_OP_PACK_AG (K1), FSDP_OP_UNPACK (K3), FSDP_OP_PACK_RS
+ * (K4) or FSDP_OP_COPYOUT_RS (K6), launched on `stream` exactly as
+ * fsdp_run_schedule launches it for this ctx (same run table, grid and
+ * staging slot semantics; skipped where the step skips it, e.g. K1 of
+ * segment-layout storage, K6 of segment grad storage with a communicator).
+ * *launched (nullable) = 1 if a kernel was enqueued, else 0.  Stream-ordered,
+ * capturable into a CUDA graph; the caller orders it against the data it
+ * reads.  Errors: NULL ctx / bucket / staging, bucket of another ctx,
+ * unaligned staging, an op outside the four, unbound buffers the op needs.
+ * (ABI version 5.) */
+fsdp_status fsdp_bucket_launch_kernel(fsdp_ctx* ctx, fsdp_bucket* b, int32_t op, void* staging,
+                                      fsdp_stream_t stream, int32_t* launched);
+
 /* ------------------------------------------------ 5. fsdp_run_schedule
  * One training step's communication path (Table 6):
  *   reorder on : forward prefetch depth 1 -- AG(k+1) before (default) or after
@@ -475,7 +490,12 @@ typedef struct {
   const void* done_flags;       /* this rank's consumed-flag array (world uint64) */
   uint64_t epoch_base;
   int64_t timeout_ns;           /* per wait; 0 = forever */
-  int32_t* error_flag;          /* device int set to 1 by a timed-out wait (nullable) */
+  int32_t* error_flag;          /* device int set to 1 by a timed-out wait (nullable).  A set
+                                   flag means a kernel went ahead without its peers: the step's
+                                   results are INVALID.  FSDP_SCHED_TIMING steps read it after
+                                   their final synchronisation and fail with FSDP_ERR_CUDA;
+                                   otherwise the caller must read it after the step and treat
+                                   a nonzero value as a failed step (the flag stays set). */
   uint64_t* epoch_counter;      /* nullable device uint64: if set, every epoch above is
                                    epoch_base + *epoch_counter (read on the device) and the
                                    step's last kernel adds n_bwd + 2 to it -- the step can

@@ -39,7 +39,7 @@ EXPORTED = [
     "fsdp_last_error", "fsdp_abi_version", "fsdp_nccl_get_unique_id", "fsdp_ctx_create",
     "fsdp_ctx_destroy", "fsdp_ctx_split", "fsdp_ctx_info", "fsdp_ctx_create_config", "fsdp_nccl_estimate_ns", "fsdp_shard", "fsdp_plan_buckets", "fsdp_layout", "fsdp_bucket_create",
     "fsdp_bucket_destroy", "fsdp_bucket_query", "fsdp_bucket_set_grad_accumulation",
-    "fsdp_allgather_bucket", "fsdp_reduce_scatter_bucket",
+    "fsdp_allgather_bucket", "fsdp_reduce_scatter_bucket", "fsdp_bucket_launch_kernel",
     "fsdp_run_schedule", "fsdp_proxy_launch", "fsdp_proxy_calibrate",
     "fsdp_p2p_allgather_bucket", "fsdp_p2p_reduce_scatter_bucket", "fsdp_p2p_signal", "fsdp_p2p_wait",
     "fsdp_ipc_alloc", "fsdp_ipc_open", "fsdp_ipc_close", "fsdp_ipc_free",
@@ -188,6 +188,7 @@ _sigs = {
     "fsdp_bucket_set_grad_accumulation": (C.c_int, [_P, C.c_int32]),
     "fsdp_allgather_bucket": (C.c_int, [_P, _P, _P, _P, _P, C.c_uint32]),
     "fsdp_reduce_scatter_bucket": (C.c_int, [_P, _P, _P, _P, _P, C.c_uint32]),
+    "fsdp_bucket_launch_kernel": (C.c_int, [_P, _P, C.c_int32, _P, _P, C.POINTER(C.c_int32)]),
     "fsdp_run_schedule": (C.c_int, [_P, C.POINTER(Schedule), C.POINTER(StepReport)]),
     "fsdp_proxy_launch": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, _P]),
     "fsdp_proxy_calibrate": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _P,

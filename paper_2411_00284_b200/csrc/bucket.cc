@@ -527,6 +527,47 @@ extern "C" fsdp_status fsdp_reduce_scatter_bucket(fsdp_ctx* c, fsdp_bucket* b, v
   return FSDP_OK;
 }
 
+extern "C" fsdp_status fsdp_bucket_launch_kernel(fsdp_ctx* c, fsdp_bucket* b, int32_t op, void* staging,
+                                                 fsdp_stream_t stream, int32_t* launched) {
+  if (launched) *launched = 0;
+  if (!c || !b || !staging) return fail(FSDP_ERR_INVALID_ARG, "NULL argument");
+  if (b->ctx != c) return fail(FSDP_ERR_INVALID_ARG, "bucket belongs to another ctx");
+  if (reinterpret_cast<uintptr_t>(staging) % 16) return fail(FSDP_ERR_INVALID_ARG, "staging not 16-B aligned");
+  const bool ag = op == FSDP_OP_PACK_AG || op == FSDP_OP_UNPACK;
+  if (!ag && op != FSDP_OP_PACK_RS && op != FSDP_OP_COPYOUT_RS)
+    return fail(FSDP_ERR_INVALID_ARG, "op must be PACK_AG, UNPACK, PACK_RS or COPYOUT_RS");
+  if ((op == FSDP_OP_PACK_AG && !b->has_shards) || (op == FSDP_OP_UNPACK && !b->has_fulls) ||
+      (op == FSDP_OP_PACK_RS && !b->has_grads) || (op == FSDP_OP_COPYOUT_RS && !b->has_gshards))
+    return fail(FSDP_ERR_INVALID_ARG, "the op's buffers are not bound");
+  FSDP_CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  char* st = static_cast<char*>(staging);
+  int n = 0;
+  switch (op) {
+    case FSDP_OP_PACK_AG: {
+      // the step's skip rule (ag_pack) with the ctx's collective state
+      const bool coll = comm_on(c, true);
+      const bool skip = b->ag_grouped ? coll : b->ag_direct ? (b->ag_zero_copy && coll) : b->ag_zero_copy;
+      if (!skip) {
+        FSDP_CUDA_TRY(launch_table(KK_AG_PACK, b->ag_pack, st, 1.0f, cs, c->max_ctas));
+        n = b->ag_pack.n ? 1 : 0;
+      }
+      break;
+    }
+    case FSDP_OP_UNPACK:
+      FSDP_TRY(ag_unpack(c, b, st, cs, &n));
+      break;
+    case FSDP_OP_PACK_RS:
+      FSDP_CUDA_TRY(launch_table(KK_RS_PACK, b->rs_pack, st, 1.0f / static_cast<float>(c->world), cs, c->max_ctas));
+      n = b->rs_pack.n ? 1 : 0;
+      break;
+    default:
+      FSDP_TRY(rs_copyout(c, b, st, cs, true, &n));
+  }
+  if (launched) *launched = n;
+  return FSDP_OK;
+}
+
 extern "C" fsdp_status fsdp_bucket_set_grad_accumulation(fsdp_bucket* b, int32_t on) {
   if (!b) return fail(FSDP_ERR_INVALID_ARG, "NULL bucket");
   if (on != 0 && on != 1) return fail(FSDP_ERR_INVALID_ARG, "on must be 0 or 1");

@@ -977,18 +977,23 @@ cudaError_t launch_p2p_wait(const void* flags, int world, uint64_t value, int64_
 
 // K11: an emulated collective (measurement device, fsdp_comm_emulation).
 
-__global__ void __launch_bounds__(512) fsdp_comm_emulate_kernel(int reduce, const char* __restrict__ src,
-                                                                 char* __restrict__ dst, long long seg, int world,
-                                                                 int rank, long long target_ns) {
+// src / dst may alias (the RS runs in place: dst = this rank's slot of src),
+// so neither is __restrict__; each output element is read from every slot by
+// the one thread that then writes it.  seg is a multiple of 16 (checked by
+// fsdp_run_schedule) and both pointers are 16-B aligned.
+__global__ void __launch_bounds__(512) fsdp_comm_emulate_kernel(int reduce, const char* src, char* dst, long long seg,
+                                                                 int world, int rank, long long target_ns) {
   const unsigned long long t0 = global_ns();
   const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long nth = static_cast<long long>(gridDim.x) * blockDim.x;
   if (!reduce) {
-    // this rank's segment into every other slot (16-B units; seg is 16-B aligned)
+    // this rank's segment into every slot (16-B units); its own slot only when
+    // the gather runs out of place (send != recv + rank * seg), as NCCL's would
     const uint4* s = reinterpret_cast<const uint4*>(src);
     const long long n = seg / 16;
+    const bool in_place = src == dst + static_cast<long long>(rank) * seg;
     for (int q = 0; q < world; ++q) {
-      if (q == rank) continue;
+      if (q == rank && in_place) continue;
       uint4* d = reinterpret_cast<uint4*>(dst + static_cast<long long>(q) * seg);
       for (long long i = tid; i < n; i += nth) d[i] = s[i];
     }

@@ -252,9 +252,18 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     if (em->ctas < 1 || em->ctas > 4 * ctx->sm_count || em->reserved != 0 || em->ag.alpha_ns < 0 || em->ag.beta_fs_per_byte < 0 ||
         em->rs.alpha_ns < 0 || em->rs.beta_fs_per_byte < 0)
       return fail(FSDP_ERR_INVALID_ARG, "bad fsdp_comm_emulation");
-    for (int32_t i = 0; i < s->n_fwd + s->n_bwd; ++i)
-      if ((i < s->n_fwd ? s->fwd[i] : s->bwd[i - s->n_fwd])->ag_grouped)
+    for (int32_t i = 0; i < s->n_fwd + s->n_bwd; ++i) {
+      const fsdp_bucket* bk = i < s->n_fwd ? s->fwd[i] : s->bwd[i - s->n_fwd];
+      if (bk->ag_grouped)
         return fail(FSDP_ERR_INVALID_ARG, "emulated collectives do not cover FSDP_BUCKET_GROUPED_AG");
+      // K11 moves 16-B units: segments built with align_bytes < 16 may not be
+      auto mis = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 != 0; };
+      if (bk->ag_seg % 16 != 0 || (i >= s->n_fwd && bk->rs_seg % 16 != 0) ||
+          (bk->ag_zero_copy && mis(bk->shard_seg)) || (bk->ag_direct && mis(bk->full0)) ||
+          (i >= s->n_fwd && bk->rs_zero_copy && mis(bk->gshard_seg)))
+        return fail(FSDP_ERR_INVALID_ARG,
+                    "emulated collectives need 16-B multiple segments (align_bytes 16) and 16-B aligned buffers");
+    }
   }
   // the emulated collectives (fsdp_comm_emulation) stand in for a communicator for this call only
   struct EmulGuard {
@@ -533,6 +542,13 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
         }
       }
     }
+  }
+  if (timing && pp && with_comm && pp->error_flag) {
+    // the step has completed (synchronised above): a timed-out epoch wait means
+    // a kernel went ahead without its peers -- the results are invalid
+    int32_t flag = 0;
+    FSDP_CUDA_TRY(cudaMemcpy(&flag, pp->error_flag, sizeof(flag), cudaMemcpyDeviceToHost));
+    if (flag) return fail(FSDP_ERR_CUDA, "peer-memory epoch wait timed out: this step's results are invalid");
   }
   return FSDP_OK;
 }

@@ -208,6 +208,15 @@ def reduce_scatter_bucket(ctx, bucket, staging_ptr, compute=0, comm=0, flags=L.I
     check(L.lib.fsdp_reduce_scatter_bucket(ctx.h, bucket.h, staging_ptr, compute or None, comm or None, flags))
 
 
+def bucket_launch_kernel(ctx, bucket, op, staging_ptr, stream=0):
+    """fsdp_bucket_launch_kernel: one data kernel of the bucket alone (op =
+    OP_PACK_AG / OP_UNPACK / OP_PACK_RS / OP_COPYOUT_RS) as the step launches
+    it; returns 1 if a kernel was enqueued, 0 if the step skips it."""
+    n = C.c_int32()
+    check(L.lib.fsdp_bucket_launch_kernel(ctx.h, bucket.h, int(op), staging_ptr, stream or None, C.byref(n)))
+    return n.value
+
+
 def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0, comm=0, flags=0,
                  proxy_iters_fwd=None, proxy_iters_bwd=None, proxy_ctas_per_sm=1, proxy_smem_bytes=0,
                  n_fwd=None, n_bwd=None, want_log=True, p2p=None, io=None, gemm=None, hook=None,

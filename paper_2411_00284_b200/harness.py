@@ -283,6 +283,14 @@ class RankState:
                     epoch_counter=self.epoch_ctr.data_ptr(), max_ctas=getattr(self, "p2p_max_ctas", 0),
                     grad_slots=self.n_grad_slots)
 
+    def check_p2p(self):
+        """Raise if a peer-memory epoch wait timed out since setup: a kernel then
+        went ahead without its peers and the step's results are invalid
+        (include/fsdp.h, fsdp_p2p_schedule.error_flag).  Synchronises."""
+        err = getattr(self, "p2p_err", None)
+        if err is not None and int(err.item()) != 0:
+            raise RuntimeError("peer-memory epoch wait timed out: the step's results are invalid")
+
     def p2p_bytes(self):
         """Algorithmic bytes per step of K8 (peer AG, both phases) and K9 (peer RS)."""
         k8 = sum(b.query()["p2p_bytes"][0] for b in self.fwd + self.bwd)

@@ -29,7 +29,7 @@ def test_exports_every_declared_symbol():
     assert declared == set(L.EXPORTED)
     for name in declared:
         assert hasattr(L.lib, name), name
-    assert F.abi_version() == 4
+    assert F.abi_version() == 5
 
 
 @given(d=st.integers(1, 10**6), world=st.integers(1, 64), data=st.data())

@@ -15,7 +15,7 @@ from workloads import llama
 pytestmark = pytest.mark.gpu
 
 LINK = (20000, 1215)
-EM = dict(ag=LINK, rs=LINK, ctas=32)
+EM = dict(ag=LINK, rs=LINK, ctas=64)   # K11 now also writes the own slot of out-of-place gathers
 
 
 def _state(world=8):
