@@ -2,32 +2,42 @@
 """Benchmark of the SimpleFSDP hot path on B200 -- one JSON line on rank 0.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
 
-A step is one pass of the whole hot path for one rank of a Llama-3-8B FSDP
-job (BASELINE.json configs[1]: bf16 params, fp32 reduce, per-transformer-block
+A step is one pass of the whole hot path for one rank of a Llama-3-8B FSDP job
+(BASELINE.json configs[1]: bf16 params, fp32 reduce, per-transformer-block
 buckets = MANUAL wrapping, reordered with the Table 6 default placements):
-forward all-gathers (pack K1, NCCL AG, unpack K3) and backward re-gathers,
-gradient pack (K4), NCCL reduce-scatter, copy-out (K6) for all 35 buckets.
+the forward all-gathers and backward re-gathers (NCCL AG + copy-out K3, or the
+fused peer-memory K8 with --collective p2p), the gradient pack K4 and the
+reduce-scatter (NCCL RS, or K9) for all 35 buckets.  No model compute runs in
+the headline step (--tokens 0): it times the communication path itself.
 
-* N = 1 (default): one GPU holds rank 0 of an 8-way job (layout world 8,
-  "1 GPU (pack/unpack only)" in BASELINE.json) -- every kernel runs at the
-  8-GPU per-rank size; the collectives are absent because there are no peers.
-* N > 1 (torchrun): one process per GPU, an NCCL communicator of N ranks,
-  real in-place all-gather / reduce-scatter on a high-priority comm stream,
-  a calibrated compute proxy per bucket (--tokens, default 1024 tokens/GPU).
+value (the headline, whole job):
+* N > 1: bus bytes per second summed over the ranks -- per rank (N-1)/N x the
+  full bucket bytes of the step's collectives (nccl-tests busbw convention,
+  reading G28; AG in bf16, RS in fp32 on the NCCL path / the bf16 gradients K9
+  pulls on the peer-memory path) / step time, times N.
+* N = 1: there are no peers, so no bus: the GPU holds rank 0 of a simulated
+  8-way job (G36) and runs every pack / copy-out kernel at its per-rank size;
+  value = the algorithmic HBM bytes of the step's data kernels / step time
+  (`value_kind`: "hbm"), reported beside `ms_per_step` and the dominant
+  kernel's roofline fraction.
 
-value = sum over ranks of the full bucket bytes the step's collectives carry
-(forward AG + backward AG in bf16, RS in fp32) / step time, in GB/s.  Inputs
-(64.3 GB of bucket traffic per rank-step) are far larger than the 126 MB L2.
-
-Beside the contract keys the line carries (N = 1): `roofline` (dominant
-kernel vs the measured HBM peak), `kernels` (per-kernel GB/s), `predicted`
-(the N-rank step from measured op durations and alpha + beta n links, with
-vanilla / greedy / searched plan variants and the G40 memory peak),
-`emulated` (the N-rank step MEASURED with emulated collectives, contention
-included), `fused_p2p` (the fused peer-memory path K8 / K9, with its own
-`emulated`), `e2e` (host I/O through fsdp_run_schedule), `cpu_baseline`
-(the oracle on one host core), `clocks`, `env` and `paper_context`.
+Legs beside the headline (all measured on the device; `predicted` and
+`emulated` are labelled models):
+* every N: `kernels` (per kernel: in-step event-timed GB/s and the same
+  launches back to back in a CUDA graph), `roofline`, `e2e` (host I/O through
+  fsdp_run_schedule), `clocks`, `env`;
+* N > 1: `parity` (sampled outputs of the step's own buckets checked against
+  the CPU oracle: AG bit-exact, RS within G7's bound / bit-exact where it must
+  be), `busbw_block` (an isolated 8B-block AG and RS in the nccl-tests
+  convention vs 900 GB/s), `alpha_beta` (a size sweep fitted to T = alpha +
+  beta n per op at this N), `exposure` (measured exposed-comm ms/step
+  at --exposure-tokens for vanilla / per-block + reorder / greedy + reorder
+  planned with the fitted alpha, beta), `nccl_info` (NCCL_DEBUG=INFO lines);
+* N = 1: `predicted` (the N-rank step from measured op durations + ASSUMED
+  alpha / beta links: a model), `fused_p2p` (K8 / K9 against simulated
+  peers), `cpu_baseline` (the oracle on the host cores).
 """
 import argparse
 import gc
@@ -42,9 +52,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "AG/RS bus GB/s and exposed-comm ms/step, Llama-3-8B shards, 1/2/4/8 B200"
+NVLINK_GBS = 900.0      # NVLink 5, per direction per GPU (SURVEY §8(d) roofline)
+ASSUMED_LINK = (20000, 1215)   # 20 us, (N-1)/N / 720 GB/s at N = 8: used only where nothing was measured
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -52,72 +64,49 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="8b")
     ap.add_argument("--layers", type=int, default=None)
-    ap.add_argument("--plan", default="manual", choices=["manual", "greedy", "per_param", "size_cap", "search"],
-                    help="search: fsdp_plan_search (simulator-guided, beyond Algorithm 1) from the manual and "
-                         "greedy plans, with the per-op compute model at --tokens (or --predict-tokens)")
-    ap.add_argument("--sim-world", type=int, default=8, help="layout world size at N=1")
+    ap.add_argument("--plan", default="manual", choices=["manual", "greedy", "per_param", "size_cap", "search"])
     ap.add_argument("--plan-file", default=None,
-                    help="JSON with plans.fwd / plans.bwd (buckets of forward indices in execution order), e.g. "
-                         "from tools/plan_search.py; overrides --plan")
-    ap.add_argument("--tokens", type=int, default=None, help="proxy compute tokens/GPU (0 = none)")
+                    help="JSON with plans.fwd / plans.bwd (buckets of forward indices in execution order)")
+    ap.add_argument("--sim-world", type=int, default=8, help="layout world size at N=1")
+    ap.add_argument("--tokens", type=int, default=0, help="compute tokens/GPU inside the headline step (0 = none)")
     ap.add_argument("--no-reorder", action="store_true")
-    ap.add_argument("--grad-slots", type=int, default=2,
-                    help="full-gradient slots the backward buckets rotate through (peer-memory path: the backward "
-                         "of bucket b waits for the peers' K9 of bucket b - slots)")
-    ap.add_argument("--keep-last", action="store_true",
-                    help="FSDP_SCHED_KEEP_LAST_GATHERED (G42): the first backward bucket reuses the last forward "
-                         "bucket's gathered parameters (no re-gather; FSDP2-style, beyond the paper)")
+    ap.add_argument("--grad-slots", type=int, default=2)
+    ap.add_argument("--keep-last", action="store_true", help="G42 (beyond the paper): no re-gather of the boundary bucket")
     ap.add_argument("--fwd-placement", default="before", choices=["before", "after"])
     ap.add_argument("--bwd-placement", default="after", choices=["before", "after"])
     ap.add_argument("--mem-limit", type=float, default=2e9)
-    ap.add_argument("--alpha-ns", type=int, default=20000)
-    ap.add_argument("--beta-fs", type=int, default=1500)
+    ap.add_argument("--alpha-ns", type=int, default=ASSUMED_LINK[0], help="assumed link for planning where none is measured")
+    ap.add_argument("--beta-fs", type=int, default=ASSUMED_LINK[1])
+    ap.add_argument("--collective", default="nccl", choices=["nccl", "p2p"],
+                    help="nccl: pack + NCCL + copy-out (the paper's bucketing); p2p: fused peer-memory K8/K9")
+    ap.add_argument("--compute", default="proxy", choices=["proxy", "gemm", "llama"])
+    ap.add_argument("--proxy-ctas", type=int, default=1)
+    ap.add_argument("--proxy-smem", type=int, default=0)
+    ap.add_argument("--eager", action="store_true", help="time the eager enqueue instead of the CUDA-graph replay")
+    ap.add_argument("--trace", default=None, help="Chrome trace of one profiled step")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--proxy-ctas", type=int, default=1)
-    ap.add_argument("--proxy-smem", type=int, default=0)
-    ap.add_argument("--trace", default=None, help="write a Chrome trace of one profiled step to this path")
-    ap.add_argument("--eager", action="store_true",
-                    help="time the eager enqueue of every step instead of the CUDA-graph replay (fsdp_step_graph)")
-    ap.add_argument("--compute", default="proxy", choices=["proxy", "gemm", "llama"],
-                    help="bucket compute: calibrated proxy kernel (--tokens), cuBLASLt linear layers on the "
-                         "gathered parameters, or the real Llama-3 layers (attention, SwiGLU, norms, loss) "
-                         "through the schedule's compute hook (tokens = --tokens or 1024; eager timing)")
-    ap.add_argument("--pg", default="auto", choices=["auto", "nccl", "gloo"],
-                    help="torch.distributed backend for host plumbing (auto: nccl, gloo for p2p)")
+    ap.add_argument("--no-fused-leg", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="N>1: skip the busbw sweep / alpha-beta fit")
+    ap.add_argument("--exposure-tokens", type=int, default=1024,
+                    help="N>1: tokens/GPU of the compute proxy for the measured exposure variants (0 = skip)")
+    ap.add_argument("--quick", action="store_true", help="headline only (no parity / sweep / exposure / side legs)")
+    ap.add_argument("--predict-tokens", type=int, default=1024, help="N=1: tokens/GPU of the modelled N-rank step")
+    ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--emulate", action="store_true",
+                    help="N=1: also run the N-rank step with emulated collectives (K11; a model device)")
+    ap.add_argument("--no-gemm-comparison", action="store_true", help="(accepted for old scripts; no effect)")
+    ap.add_argument("--pg", default="gloo", choices=["gloo"], help="torch.distributed backend of the host plumbing")
     ap.add_argument("--same-device", action="store_true",
-                    help="TEST ONLY: put every rank on cuda:0 (exercises the multi-process p2p path on one GPU; "
-                         "timings are meaningless)")
-    ap.add_argument("--predict-tokens", type=int, default=1024,
-                    help="N=1: tokens/GPU of the compute proxy for the predicted N-rank exposure (0 = off)")
-    ap.add_argument("--collective", default="nccl", choices=["nccl", "p2p"],
-                    help="nccl: pack + NCCL + copy-out (the paper's bucketing); p2p: fused peer-memory "
-                         "kernels K8/K9 (1 GPU: the 7 peers are simulated as separate buffers)")
-    ap.add_argument("--nccl-register", default="none", choices=["none", "local", "symmetric"],
-                    help="N > 1 NCCL path: allocate the collective buffers with ncclMemAlloc and register them "
-                         "(ncclCommRegister / symmetric ncclCommWindowRegister) for zero-copy NVLS / symmetric "
-                         "kernels")
-    ap.add_argument("--p2p-max-ctas", type=int, default=-1,
-                    help="N > 1 peer-memory path: K8 / K9 grid cap (-1 = harness.emulation_ctas_p2p(N), 0 = full "
-                         "GPU)")
-    ap.add_argument("--nccl-max-ctas", type=int, default=0,
-                    help="N > 1 NCCL path: cap NCCL's CTAs per collective (fsdp_ctx_create_config; 0 = NCCL default)")
-    ap.add_argument("--no-variants", action="store_true",
-                    help="N=1: skip the predicted exposure of the vanilla and greedy plans")
-    ap.add_argument("--ag", default="flat", choices=["flat", "grouped"],
-                    help="flat: the paper's bucketing (copy-in, one AG of the flat buffer, copy-out); grouped: one "
-                         "NCCL group of per-member AGs straight into the full parameters (FSDP_BUCKET_GROUPED_AG)")
-    ap.add_argument("--dist", action="store_true",
-                    help="run the torch.distributed / NCCL-communicator path even at --gpus 1 (world 1 with a "
-                         "real communicator: checks the N > 1 plumbing on one GPU)")
-    ap.add_argument("--no-gemm-comparison", action="store_true",
-                    help="N=1: skip the emulated N-rank step with GEMM compute for per-block NCCL vs searched fused "
-                         "(two child runs)")
-    ap.add_argument("--no-fused-leg", action="store_true",
-                    help="N=1 with --collective nccl: skip the extra run of the fused peer-memory mode whose "
-                         "summary is reported under 'fused_p2p'")
-    return ap.parse_args()
+                    help="TEST ONLY: every rank on cuda:0 (multi-process p2p path on one GPU; timings meaningless)")
+    ap.add_argument("--dist", action="store_true", help="the N>1 code path at --gpus 1 (world 1, real communicator)")
+    ap.add_argument("--nccl-register", default="none", choices=["none", "local", "symmetric"])
+    ap.add_argument("--p2p-max-ctas", type=int, default=-1)
+    ap.add_argument("--nccl-max-ctas", type=int, default=0)
+    ap.add_argument("--ag", default="flat", choices=["flat", "grouped"])
+    return ap.parse_args(argv)
 
 
 # ------------------------------------------------------------------ clocks
@@ -170,19 +159,15 @@ PAPER_CONTEXT = {
     "hardware": "H100, 8 per node, NVLink intra-node (P:344); Llama 3.1; TorchTitan; C4",
     "headline_vs_FSDP2_eager": {"peak_memory_reduction": "up to 28.54%", "throughput_gain": "up to 68.67%",
                                 "cite": "P:55"},
-    "8b_fsdp_vs_FSDP2_eager": {"memory": "-27.72%", "tps": "+7.49%", "gpus": "32/64/128", "cite": "P:414"},
     "table5_1node_tps_mem": {"vanilla": [50976, 67.26], "+reorder": [54544, 68.72], "+bucket": [49168, 69.06],
                              "+reorder&bucket": [52480, 69.08], "cite": "P:556-570 (8B, FSDP only, bs 1)"},
     "table5_8node_tps_mem": {"vanilla": [333440, 56.42], "+reorder": [404032, 57.88], "+bucket": [405632, 58.15],
                              "+reorder&bucket": [428352, 65.74], "cite": "P:556-570"},
-    "note": "context only: the paper's metrics are training TPS and peak GiB on H100; this line's are bucket "
-            "bytes per second, kernel HBM fractions and exposure predicted / measured on B200",
+    "note": "context only: the paper reports training TPS and peak GiB on H100, no bus bandwidth or exposure",
 }
 
 
 def run_env(torch):
-    """GPU / host identity and library versions of this run (SURVEY §8(d)
-    protocol step 6)."""
     cpu = None
     try:
         with open("/proc/cpuinfo") as f:
@@ -194,8 +179,9 @@ def run_env(torch):
     except Exception:
         nccl = None
     return {"gpu": torch.cuda.get_device_name(), "sm_count": torch.cuda.get_device_properties(0).multi_processor_count,
-            "torch": torch.__version__, "cuda_runtime": torch.version.cuda, "nccl": nccl,
-            "host_cpu": cpu, "host_cpus": os.cpu_count(), "affinity_cpus": len(os.sched_getaffinity(0)),
+            "devices": torch.cuda.device_count(), "torch": torch.__version__, "cuda_runtime": torch.version.cuda,
+            "nccl_torch": nccl, "host_cpu": cpu, "host_cpus": os.cpu_count(),
+            "affinity_cpus": len(os.sched_getaffinity(0)),
             "nccl_env": {k: v for k, v in os.environ.items() if k.startswith("NCCL_")}}
 
 
@@ -208,8 +194,6 @@ def measured_peak_hbm():
 
 
 def measured_peak_bf16():
-    """Sustained dense bf16 TFLOP/s (MEASURED_PEAKS.json; for a kernel timed
-    inside a long step), else the guide's fallback."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["bf16_tflops_sustained"])
@@ -218,8 +202,8 @@ def measured_peak_bf16():
 
 
 def ncu_traffic(op_name):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu
-    --set full capture (profiles/ncu_traffic.json), else None."""
+    """DRAM bytes per launch of a kernel from the committed ncu --set full
+    capture (profiles/ncu_traffic.json), else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             return json.load(f).get(op_name)
@@ -231,27 +215,40 @@ def ncu_traffic(op_name):
 class CpuOracleSample:
     """The oracle as it stands, on a bounded sample of the same workload:
     whole 8B-block tensors (attention_norm, wq, wk, wv, wo, ffn_norm) at world
-    N -- forward AG (shard + pack all ranks + gather + unpack), the backward
-    re-gather, and the bucketed RS (pack every rank, rank-order sum, copy-out).
-    Inputs are generated once; run() times one step of the oracle."""
+    N -- forward AG, the backward re-gather and the bucketed RS over all N
+    simulated ranks.  Inputs are generated once; run() times one step.
 
-    def __init__(self, world):
+    Its value is stated in the headline's unit for the same N: bus bytes (N >
+    1: N x (N-1)/N x full bucket bytes) or, at N = 1, the algorithmic HBM bytes
+    the N ranks' data kernels would move (per rank: K3 2 x valid full bytes
+    per gather, K4 6 B per gradient element, K6 8 B per shard element) -- the
+    oracle does every rank's work."""
+
+    def __init__(self, world, kind="bus"):
         from oracle.layout import bucket_layout
         from workloads import llama
         from workloads.data import grad_tensor, param_tensor
-        self.world = world
+        self.world, self.kind = world, kind
         specs = [s for s in llama("8b", n_layers=1, with_embeddings=False)
                  if s.name.split(".")[-2] in ("attention_norm", "wq", "wk", "wv", "wo", "ffn_norm")]
         self.params = [param_tensor(s, "bf16", 1 + i) for i, s in enumerate(specs)]
         self.grads = [[grad_tensor(s, "bf16", 2, r) for s in specs] for r in range(world)]
         dims = [(s.dim0, s.row_numel) for s in specs]
-        self.bytes = 2 * world * bucket_layout(dims, world, 2, 16)[1] + world * bucket_layout(dims, world, 4, 16)[1]
+        full_bytes = 2 * world * bucket_layout(dims, world, 2, 16)[1] + world * bucket_layout(dims, world, 4, 16)[1]
         n = sum(s.dim0 * s.row_numel for s in specs)
+        shard_elems = sum(-(-s.dim0 // world) * s.row_numel for s in specs)
+        if kind == "bus":
+            self.bytes = world * (world - 1) / world * full_bytes
+            how = "N x (N-1)/N x full bucket bytes"
+        else:
+            self.bytes = world * (2 * 2 * 2 * n + 6 * n + 8 * shard_elems)
+            how = "N ranks x the data kernels' algorithmic HBM bytes (K3 x 2, K4, K6)"
         self.desc = ("oracle (NumPy, 1 thread) on %d tensors / %.1f M params of one Llama-3-8B block at N=%d: "
-                     "fwd AG + bwd AG + RS over all %d simulated ranks per step" % (len(specs), n / 1e6, world, world))
+                     "fwd AG + bwd AG + RS over all %d simulated ranks per step; value = %s / time"
+                     % (len(specs), n / 1e6, world, world, how))
 
     def run(self):
-        """Returns (GB/s in the bench's unit, seconds)."""
+        """Returns (GB/s in the headline's unit, seconds)."""
         from oracle import collectives as OC
         t0 = time.perf_counter()
         OC.bucketed_all_gather(self.params, self.world, 16)     # forward
@@ -266,79 +263,324 @@ def run_reference(args, rank):
         return
     world = args.sim_world if args.gpus == 1 else args.gpus
     t0 = time.perf_counter()
-    sample = CpuOracleSample(world)
-    desc = sample.desc
-    vals = []
-    for _ in range(args.warmup + args.steps):
-        vals.append(sample.run())
+    sample = CpuOracleSample(world, "hbm" if args.gpus == 1 else "bus")
+    vals = [sample.run() for _ in range(args.warmup + args.steps)]
     timed = vals[args.warmup:]
     v = sum(x[0] for x in timed) / len(timed)
     ms = 1e3 * sum(x[1] for x in timed) / len(timed)
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "GB/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic",
+            "value_kind": sample.kind, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "llama3-8b FSDP rank step sample (see cpu_baseline.sample)",
                        "world": world, "plan": "one bucket of the sampled tensors"},
             "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                             "sample": desc, "host_cpus": os.cpu_count()},
+                             "sample": sample.desc, "host_cpus": os.cpu_count()},
             "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": round(time.perf_counter() - t0, 1)}
     print(json.dumps(line), flush=True)
 
 
-# -------------------------------------------------------------------- ours
+# --------------------------------------------------------- parity (N ranks)
+# Verification leg (after the timed region): sampled outputs of the step's own
+# buckets, produced by the same library calls, kernels and communicator as the
+# step, against the CPU oracle computing those elements.  With the CPU
+# baseline this is the only part of bench.py that calls oracle/; the product
+# path never does.
+
+def sample_local_rows(c, seed, n=6):
+    """Deterministic local row indices in [0, c): the first and last row of
+    a chunk plus n - 2 seeded ones (same on every rank)."""
+    import numpy as np
+    if c <= n:
+        return list(range(c))
+    rng = np.random.Generator(np.random.Philox(seed))
+    mid = sorted(set(int(x) for x in rng.integers(1, c - 1, size=n - 2)))
+    return sorted(set([0, c - 1] + mid))
+
+
+def sample_buckets(n):
+    return sorted({0, 1, n // 2, n - 2, n - 1} & set(range(n)))
+
+
+def expected_ag_rows(d, world, rows, shard_rows_by_rank):
+    """Oracle O2 / O4 one element at a time: global row g of the gathered
+    parameter = local row g - row_begin_q of the shard of its owner q.
+    shard_rows_by_rank[q][t] = rank q's shard row t (bytes).  Returns
+    {g: bytes}."""
+    from oracle.shard import shard_rows
+    out = {}
+    for g in rows:
+        for q in range(world):
+            _, begin, v = shard_rows(d, world, q)
+            if begin <= g < begin + v:
+                out[g] = shard_rows_by_rank[q][g - begin]
+                break
+    return out
+
+
+def expected_rs_rows(d, R, world, rank, local_rows, grad_rows_by_rank):
+    """Oracle O5 on the sampled elements: rank `rank`'s gradient-shard rows
+    `local_rows` = the rank-order fp32 sum of fl32(widen(g_q) x fl32(1/N))
+    over q.  grad_rows_by_rank[q][g] = rank q's bf16 full-gradient row g
+    (uint16 [R]).  Built as a small bucket whose chunk of every rank holds the
+    sampled rows of that rank's chunk, then oracle.bucketed_reduce_scatter.
+    Returns (expected fp32 [n, R], abs-sum scale fp64 [n, R]) for the valid rows."""
+    import numpy as np
+    from oracle.collectives import bucketed_reduce_scatter, inv_world_f32
+    from oracle import bf16 as OB
+    c = -(-d // world)
+    n = len(local_rows)
+    fakes = []
+    for q in range(world):
+        f = np.zeros((world * n, R), dtype=np.uint16)
+        for rp in range(world):
+            for i, t in enumerate(local_rows):
+                g = rp * c + t
+                if g < d:
+                    f[rp * n + i] = grad_rows_by_rank[q][g]
+        fakes.append([f])
+    _, _, shards = bucketed_reduce_scatter(fakes, world, 16)
+    exp = shards[rank][0]
+    inv = float(inv_world_f32(world))
+    scale = np.zeros((n, R), dtype=np.float64)
+    for q in range(world):
+        scale += np.abs(OB.widen(fakes[q][0][rank * n:(rank + 1) * n]).astype(np.float64)) * inv
+    return exp, scale
+
+
+def rs_tolerance(world, scale):
+    """G7: |gpu - oracle| <= 1.01 N 2^-24 sum_r |g_r| / N, element-wise."""
+    return 1.01 * world * 2.0 ** -24 * scale
+
+
+def ag_check(world, rank, members, exchange, acc):
+    """Host side of the AG check for one bucket.  members: list of dicts
+    {key, d, ep, own: {t: bytes of this rank's shard row t}, got: {g: bytes of
+    the gathered row g}}.  Exchanges the shard rows over the host process
+    group, compares every gathered row with expected_ag_rows bit for bit and
+    adds to acc (elements, mismatches)."""
+    allown = exchange({m["key"]: m["own"] for m in members})
+    for m in members:
+        exp = expected_ag_rows(m["d"], world, sorted(m["got"]), [allown[q][m["key"]] for q in range(world)])
+        for g, b in m["got"].items():
+            acc["elements"] += len(b) // m["ep"]
+            if exp.get(g) != b:
+                acc["mismatches"] += 1
+
+
+def rs_check(world, rank, members, exchange, acc):
+    """Host side of the RS check for one bucket.  members: list of dicts {key,
+    d, R, loc (sampled local rows), own (those valid on this rank), grads: {g:
+    uint16 [R] full-gradient row g of this rank}, got: fp32 [len(own), R] this
+    rank's gradient-shard rows}.  Exchanges the gradient rows, computes the
+    oracle's rows (expected_rs_rows) and adds to acc (elements, bit mismatches,
+    max error / G7 bound)."""
+    import numpy as np
+    allg = exchange({m["key"]: m["grads"] for m in members})
+    for m in members:
+        if not m["own"]:
+            continue
+        exp, scale = expected_rs_rows(m["d"], m["R"], world, rank, m["loc"], [allg[q][m["key"]] for q in range(world)])
+        sel = [m["loc"].index(t) for t in m["own"]]
+        exp, scale, got = exp[sel], scale[sel], m["got"]
+        err = np.abs(got.astype(np.float64) - exp.astype(np.float64))
+        tol = rs_tolerance(world, scale)
+        acc["elements"] += got.size
+        acc["mismatches"] += int(np.count_nonzero(got.view(np.uint32) != exp.view(np.uint32)))
+        if got.size:
+            acc["max_err_over_bound"] = max(acc["max_err_over_bound"], float(np.max(err / np.maximum(tol, 1e-300))))
+
+
+def parity_verdict(ag, rs, world, p2p):
+    """AG must be bit-exact; the RS bit-exact where the summation order cannot
+    matter or is the oracle's (K9 sums in rank order; N <= 2 is one
+    commutative add), else within G7's bound."""
+    exact_required = p2p or world <= 2
+    rs_ok = rs["mismatches"] == 0 if exact_required else rs["max_err_over_bound"] <= 1.0
+    ok = ag["mismatches"] == 0 and ag["elements"] > 0 and rs_ok and rs["elements"] > 0
+    return bool(ok), ("bit-exact" if exact_required else "G7 bound 1.01 N 2^-24 sum|g|/N")
+
+
+def parity_leg(st, ctx, cs, ms, p2p, world, rank, exchange, barrier):
+    import numpy as np
+    import torch
+    import paper_2411_00284_b200 as F
+    from paper_2411_00284_b200 import _lib as L
+    ep = st.ep
+    pdt = np.uint16 if ep == 2 else np.uint32
+
+    def rows_of(buf, off, rows, row_bytes, dtype):
+        if not rows:
+            return np.zeros((0, row_bytes // np.dtype(dtype).itemsize), dtype=dtype)
+        idx = torch.tensor(rows, dtype=torch.int64, device=buf.device)
+        t = buf[off:off + (max(rows) + 1) * row_bytes].view(-1, row_bytes).index_select(0, idx)
+        return t.cpu().numpy().view(dtype)
+
+    ag = {"buckets": [], "elements": 0, "mismatches": 0}
+    for k in sample_buckets(len(st.fwd)):
+        bk = st.fwd[k]
+        barrier()
+        if p2p:
+            F.p2p_allgather_bucket(ctx, bk, st.ag_peers[k], cs)
+        else:
+            F.allgather_bucket(ctx, bk, st.ag_st[k % 2].data_ptr(), cs, ms, L.ISSUE | L.WAIT)
+        torch.cuda.synchronize()
+        slot = st.full_slots[bk.full_slot]
+        members = []
+        for j, foff in zip(bk.members, bk.full_offs):
+            d, R = st.specs[j].dim0, st.specs[j].row_numel
+            c = -(-d // world)
+            loc = sample_local_rows(c, 1000 + j)
+            grows = sorted({q * c + t for q in range(world) for t in loc if q * c + t < d})
+            own = [t for t in loc if rank * c + t < d]
+            sh = rows_of(st.shard_buf, st.shard_offs[j], own, R * ep, pdt)
+            fr = rows_of(slot, foff, grows, R * ep, pdt)
+            members.append({"key": j, "d": d, "ep": ep, "own": {t: sh[i].tobytes() for i, t in enumerate(own)},
+                            "got": {g: fr[i].tobytes() for i, g in enumerate(grows)}})
+        ag_check(world, rank, members, exchange, ag)
+        ag["buckets"].append(k)
+    rs = {"buckets": [], "elements": 0, "max_err_over_bound": 0.0, "mismatches": 0}
+    for b in sample_buckets(len(st.bwd)):
+        bk = st.bwd[b]
+        barrier()
+        if p2p:
+            F.p2p_reduce_scatter_bucket(ctx, bk, st.rs_peers[b], cs)
+        else:
+            F.reduce_scatter_bucket(ctx, bk, st.rs_st[b % 2].data_ptr(), cs, ms, L.ISSUE | L.WAIT)
+        torch.cuda.synchronize()
+        gslot = st.grad_slots[bk.grad_slot]
+        members = []
+        for j, goff in zip(bk.members, bk.grad_offs):
+            d, R = st.specs[j].dim0, st.specs[j].row_numel
+            c = -(-d // world)
+            loc = sample_local_rows(c, 2000 + j)
+            grows = sorted({q * c + t for q in range(world) for t in loc if q * c + t < d})
+            gr = rows_of(gslot, goff, grows, R * 2, np.uint16)
+            own = [t for t in loc if rank * c + t < d]
+            members.append({"key": j, "d": d, "R": R, "loc": loc, "own": own,
+                            "grads": {g: gr[i].copy() for i, g in enumerate(grows)},
+                            "got": rows_of(st.gshard_buf, st.gs_offs[j], own, R * 4, np.float32)})
+        rs_check(world, rank, members, exchange, rs)
+        rs["buckets"].append(b)
+    barrier()
+    ok, required = parity_verdict(ag, rs, world, p2p)
+    return {"ok": ok, "ag": dict(ag, bit_exact=ag["mismatches"] == 0),
+            "rs": dict(rs, bit_exact=rs["mismatches"] == 0, required=required),
+            "how": ("sampled rows (first / last / seeded) of every member of buckets %s (fwd AG) / %s (bwd RS) of "
+                    "the bench's own state, run through the same calls and communicator as the step, compared "
+                    "with the CPU oracle (O2/O4 AG, O5 RS) on inputs exchanged over the host process group"
+                    % (ag["buckets"], rs["buckets"]))}
+
+
+# ------------------------------------------------------------ NCCL INFO log
+def nccl_log_path(rank):
+    return "/tmp/fsdp_bench_nccl.%d.%d.log" % (os.getpid(), rank)
+
+
+def nccl_info_summary(path, limit=24):
+    """The communicator's own account of itself (NCCL_DEBUG=INFO): version,
+    ranks / channels, NVLS and P2P transport, tuning choices."""
+    keys = ("NCCL version", "nRanks", "NVLS", "nvls", "Channel 00", "channels", "P2P/", "via P2P", "CollNet",
+            "Init COMPLETE", "algorithm", "Algo", "proto", "NCCL_")
+    try:
+        with open(path, errors="ignore") as f:
+            lines = [ln.rstrip() for ln in f]
+    except OSError:
+        return {"lines": [], "note": "no NCCL log (NCCL_DEBUG set by the caller?)"}
+    pick = [ln for ln in lines if any(k in ln for k in keys)]
+    nvls = [ln for ln in lines if "NVLS" in ln or "nvls" in ln]
+    return {"lines": pick[:limit], "n_lines": len(lines), "nvls_lines": nvls[:6],
+            "nvls_mentioned": bool(nvls), "file": path}
+
+
+# ------------------------------------------------------------------ helpers
 def fused_leg(args):
-    """bench.py --collective p2p at N = 1 on the same workload (child process)."""
+    """bench.py --collective p2p at N = 1 on the same workload (child process):
+    K8 / K9 against 7 simulated peers' buffers in local HBM."""
     cmd = [sys.executable, os.path.abspath(__file__), "--collective", "p2p", "--steps", str(args.steps),
-           "--warmup", str(args.warmup), "--no-e2e", "--no-cpu-baseline", "--no-fused-leg", "--no-gemm-comparison",
-           "--predict-tokens", str(args.predict_tokens), "--plan", args.plan, "--model", args.model, "--sim-world", str(args.sim_world)]
+           "--warmup", str(args.warmup), "--no-e2e", "--no-cpu-baseline", "--no-fused-leg", "--predict-tokens", "0",
+           "--plan", args.plan, "--model", args.model, "--sim-world", str(args.sim_world)]
     try:
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
         d = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
     except Exception as e:  # reported, never fatal to the headline
         return {"error": "%s: %s" % (type(e).__name__, str(e)[:200])}
-    return {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"],
-            "collective": d["config"]["collective"], "kernels": d["kernels"], "roofline": d["roofline"],
-            "gpu_launches": d["gpu_launches"], "p2p_wait_timeouts": d["p2p_wait_timeouts"],
-            "emulated": d.get("emulated"),
-            "how": "bench.py --collective p2p (same workload, same K/W, own process)"}
+    return {"ms_per_step": d["ms_per_step"], "value": d["value"], "unit": d["unit"], "value_kind": d["value_kind"],
+            "kernels": d["kernels"], "roofline": d["roofline"], "gpu_launches": d["gpu_launches"],
+            "how": "bench.py --collective p2p (same workload, own process; the 7 peers simulated in local HBM)"}
 
 
-def gemm_comparison(args):
-    """The N = 8 step with real tensor-core compute (cuBLASLt linear layers,
-    T = 1024) and emulated collectives, measured for the paper-style design
-    (per-block buckets, NCCL + copy kernels) and the B200-native one (searched
-    buckets, fused peer-memory kernels K8 / K9) -- child processes."""
+def kernel_table(st, ctx, names, kbytes, klaunch, op_ns, steps, cs_stream, peak):
+    """Per data kernel: (a) in-step, event-timed -- an event pair around every
+    launch in the profiled steps (FSDP_SCHED_TIMING), which also counts each
+    launch's event / launch latency (~8 us per launch, tools/
+    launch_overhead_probe.py); (b) back to back -- this step's launches of
+    that kernel alone (fsdp_bucket_launch_kernel, same tables, staging slots
+    and order), captured into one CUDA graph, timed with CUDA events around
+    three replays on the launching stream."""
+    import torch
+    import paper_2411_00284_b200 as F
+    from paper_2411_00284_b200 import _lib as L
     out = {}
-    for name, extra in (("per-block + NCCL + copy kernels", ["--plan", "manual", "--collective", "nccl"]),
-                        ("searched + fused K8/K9", ["--plan", "search", "--collective", "p2p"])):
-        cmd = [sys.executable, os.path.abspath(__file__), "--compute", "gemm", "--tokens", "1024", "--steps",
-               str(args.steps), "--warmup", str(args.warmup), "--no-e2e", "--no-cpu-baseline", "--no-fused-leg",
-               "--no-variants", "--no-gemm-comparison", "--model", args.model,
-               "--sim-world", str(args.sim_world)] + extra
+    for op in kbytes:
+        if kbytes[op] <= 0 or op_ns.get(op, 0) <= 0:
+            continue
+        ev_gbs = kbytes[op] * steps / (op_ns[op] * 1e-9) / 1e9
+        row = {"GB/s_in_step_event": round(ev_gbs, 1), "frac_in_step_event": round(ev_gbs / peak, 4),
+               "ms_per_step_in_step_event": round(op_ns[op] / steps / 1e6, 3),
+               "launches_per_step": klaunch[op], "bytes_per_step": kbytes[op]}
+        seq = []
+        if op in (L.OP_PACK_AG, L.OP_UNPACK):
+            seq = [(bk, st.ag_st[b % 2]) for bs in (st.fwd, st.bwd) for b, bk in enumerate(bs)]
+        elif op in (L.OP_PACK_RS, L.OP_COPYOUT_RS):
+            seq = [(bk, st.rs_st[b % 2]) for b, bk in enumerate(st.bwd)]
         try:
-            r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
-            d = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
-            e = d["emulated"]
-            out[name] = {"emulated_step_ms": e["step_ms"], "compute_only_ms": e["compute_only_ms"],
-                         "exposed_ms": e["exposed_ms"], "buckets": [d["config"]["buckets_fwd"],
-                                                                    d["config"]["buckets_bwd"]]}
-        except Exception as ex:  # reported, never fatal to the headline
-            out[name] = {"error": "%s: %s" % (type(ex).__name__, str(ex)[:200])}
-    out["how"] = ("bench.py --compute gemm --tokens 1024 (cuBLASLt bf16 linear layers on the gathered parameters) "
-                  "with the N-rank collectives emulated (K11 / paced K8-K9), own processes")
+            s = torch.cuda.Stream()
+            g = torch.cuda.CUDAGraph()
+            n = 0
+            with torch.cuda.graph(g, stream=s):
+                for bk, stg in seq:
+                    n += F.bucket_launch_kernel(ctx, bk, op, stg.data_ptr(), s.cuda_stream)
+            with torch.cuda.stream(s):
+                g.replay()
+            s.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            with torch.cuda.stream(s):
+                for _ in range(3):
+                    g.replay()
+            b.record(s)
+            b.synchronize()
+            ms_b2b = a.elapsed_time(b) / 3
+            gbs = kbytes[op] / (ms_b2b * 1e-3) / 1e9
+            row.update({"GB/s": round(gbs, 1), "frac": round(gbs / peak, 4), "ms_per_step": round(ms_b2b, 3),
+                        "launches_back_to_back": n})
+            del g
+        except Exception as e:   # reported, never fatal
+            row["back_to_back_error"] = str(e)[:200]
+        out[names[op]] = row
     return out
 
 
-def main():
-    args = parse()
+# -------------------------------------------------------------------- ours
+def main(argv=None):
+    args = parse(argv)
     rank = int(os.environ.get("RANK", "0"))
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank)
+    multi = args.gpus > 1 or args.dist
+    p2p = args.collective == "p2p"
+    quick = args.quick
+    if multi and not p2p and os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("", "VERSION", "WARN"):
+        # the communicator's own account (version, channels, NVLS, tuning), one file per rank
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS,TUNING,ENV")
+        os.environ["NCCL_DEBUG_FILE"] = nccl_log_path(rank)
 
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -350,20 +592,14 @@ def main():
 
     assert torch.cuda.is_available(), "bench.py needs a B200"
     if args.same_device:
-        local = 0    # test only: every rank on cuda:0 (exercises the multi-process path on one GPU)
+        local = 0
     torch.cuda.set_device(local)
-    multi = args.gpus > 1 or args.dist
-    p2p = args.collective == "p2p"
-    pg = args.pg if args.pg != "auto" else ("gloo" if (p2p or args.same_device) else "nccl")
     if multi:
         assert world_env == args.gpus, "launch with torchrun --nproc-per-node %d" % args.gpus
-        if pg == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group("gloo")
+        dist.init_process_group("gloo")      # host plumbing only; the data path is the library's
         world = args.gpus
         if p2p:
-            ctx = F.Ctx(world, rank, local)   # peer-memory collectives need no NCCL communicator
+            ctx = F.Ctx(world, rank, local)  # peer-memory collectives need no NCCL communicator
         else:
             uid = [F.nccl_get_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
@@ -372,8 +608,26 @@ def main():
     else:
         world = args.sim_world
         ctx = F.Ctx(world, 0, local)   # layout-only: rank 0 of a simulated `world`-way job
-    tokens = args.tokens if args.tokens is not None else (1024 if multi else 0)
+    my_rank = rank if multi else 0
 
+    def exchange(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    def barrier():
+        torch.cuda.synchronize()
+        if multi:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if not multi:
+            return x
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    tokens = args.tokens
     specs = llama(args.model, n_layers=args.layers)
     t_fwd, t_bwd = per_param_compute_ns(specs, tokens) if tokens else ([0] * len(specs), [0] * len(specs))
     mode = {"manual": L.PLAN_MANUAL, "greedy": L.PLAN_GREEDY, "per_param": L.PLAN_PER_PARAM,
@@ -381,39 +635,28 @@ def main():
     link = (args.alpha_ns, args.beta_fs)
     fplan, bplan = H.plans_for(specs, world, mode, t_fwd, t_bwd, link, link, int(args.mem_limit))
     if args.plan == "search":
-        st_tok = tokens or args.predict_tokens or 1024
-        sf, sb = per_param_compute_ns(specs, st_tok)
-        slink = (20000, round((world - 1) / world / 720e9 * 1e15)) if not multi else link
-        fplan, bplan = H.plans_search(specs, world, sf, sb, slink, slink, int(args.mem_limit))
+        sf, sb = per_param_compute_ns(specs, tokens or 1024)
+        fplan, bplan = H.plans_search(specs, world, sf, sb, link, link, int(args.mem_limit))
     if args.plan_file:
         with open(args.plan_file) as f:
             pj = json.load(f)["plans"]
         fplan, bplan = pj["fwd"], pj["bwd"]
-        flat_f = sorted(j for b in fplan for j in b)
-        flat_b = sorted(j for b in bplan for j in b)
-        assert flat_f == flat_b == list(range(len(specs))), "plan file does not cover the model's parameters"
+        assert sorted(j for b in fplan for j in b) == sorted(j for b in bplan for j in b) == list(range(len(specs)))
     reg = args.nccl_register if (multi and not p2p and args.nccl_register != "none") else None
-    st = H.RankState(specs, world, rank if multi else 0, fplan, bplan, ctx, seed=1234 + rank,
-                     ipc=multi and p2p, nccl_register=reg, ag_grouped=args.ag == "grouped",
-                     grad_slots=args.grad_slots)
+    st = H.RankState(specs, world, my_rank, fplan, bplan, ctx, seed=1234 + my_rank, ipc=multi and p2p,
+                     nccl_register=reg, ag_grouped=args.ag == "grouped", grad_slots=args.grad_slots)
     compute = torch.cuda.Stream()
     comm = torch.cuda.Stream(priority=-1)
     cs, ms = compute.cuda_stream, comm.cuda_stream
 
     pf = pb = None
-    if tokens:
+    if tokens and args.compute == "proxy":
         nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
         pf = H.proxy_iters(H.bucket_times(fplan, t_fwd), nspi)
         pb = H.proxy_iters(H.bucket_times(bplan, t_bwd), nspi)
     if p2p:
         if multi:
-            def exchange(obj):
-                out = [None] * world
-                dist.all_gather_object(out, obj)
-                return out
             st.setup_p2p_ipc(exchange)
-            # N > 1: cap the fused kernels' grid like NCCL's channels so the
-            # NVLink-bound K8 / K9 leave the SMs to the compute stream
             st.p2p_max_ctas = args.p2p_max_ctas if args.p2p_max_ctas >= 0 else H.emulation_ctas_p2p(world)
         else:
             st.setup_p2p_simulated(seed=99)
@@ -429,41 +672,18 @@ def main():
 
     gemm = model = None
     if args.compute == "llama":
-        # the real model through the compute hook (fsdp_compute_hook): forward
-        # / backward of every bucket's layers on the gathered parameters, the
-        # weight gradients written where the reduce-scatter reads them
         from paper_2411_00284_b200.llama_compute import LlamaCompute
         model = LlamaCompute(st, tokens or 1024)
-        pf = pb = None
     if args.compute == "gemm":
-        # linear-layer compute: cuBLASLt bf16 GEMMs on the gathered parameters,
-        # the backward writing the gradients the reduce-scatter averages
         gemm = st.setup_gemm(tokens or 1024)
-        pf = pb = None
-
     hook = model.hook if model else None
 
     def step(extra=0):
         return st.step(flags | extra, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, gemm=gemm, hook=hook)
 
-    def barrier():
-        if multi:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    def max_over_ranks(x):
-        if not multi:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda" if pg == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
     host_enqueue = []
 
-    def timed_loop(extra, n, clocks=None):
-        """n steps bracketed by events on the compute stream; max over ranks.
-        Also records the host time to enqueue each step (SURVEY §8(d) protocol
-        step 5: is the eager step launch-bound?)."""
+    def timed_loop(extra, n):
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = []
@@ -479,19 +699,13 @@ def main():
 
     for _ in range(args.warmup):
         step()
-    # (1) the headline: K plain steps, no instrumentation -- replayed as one
-    #     CUDA graph per step (fsdp_step_graph: the library's whole step,
-    #     kernels + NCCL collectives + cross-stream events, captured once) unless
-    #     --eager (the p2p path replays too: its epochs advance on the device);
-    #     the eager enqueue of the same steps is timed beside it
+    # (1) the headline: K plain steps, each replayed as one CUDA graph
+    #     (fsdp_step_graph: kernels + collectives + cross-stream events captured
+    #     once) unless --eager; the eager enqueue of the same steps beside it
     sg = None
     if not args.eager and model is None:
         sg = st.capture(flags, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, gemm=gemm)
-        for _ in range(args.warmup):
-            sg.launch(cs)
     elif not args.eager:
-        # the model's torch ops through the hook: torch captures the whole step
-        # (library kernels, collectives and the hook's ops) into one graph
         tg = st.capture_with_torch(flags, compute, ms, pf, pb, args.proxy_ctas, args.proxy_smem, gemm=gemm,
                                    hook=hook)
 
@@ -503,6 +717,7 @@ def main():
             def close(self):
                 pass
         sg = _TorchGraph()
+    if sg is not None:
         for _ in range(args.warmup):
             sg.launch(cs)
 
@@ -517,222 +732,83 @@ def main():
         return max_over_ranks(a.elapsed_time(b) / n)
 
     with ClockSampler(local) as clk:
-        if sg is not None:
-            ms_step = graph_loop(args.steps)
-        else:
-            ms_step, _ = timed_loop(0, args.steps)
+        ms_step = graph_loop(args.steps) if sg is not None else timed_loop(0, args.steps)[0]
+    st.check_p2p()
     ms_eager = timed_loop(0, args.steps)[0] if sg is not None else ms_step
-    # (2) the same K steps with a CUDA event pair around every op (per-kernel
-    #     device time on the launching stream; synchronises once per step)
+    # (2) the same K steps with an event pair around every op (per-op device
+    #     time on the launching stream; synchronises once per step)
     ms_prof, reports = timed_loop(L.SCHED_TIMING, args.steps)
-    # NOTE: every step below runs on EVERY rank (a step holds collectives / epoch
-    # handshakes); only the reporting is rank 0's
     if args.trace:
         rep_t = st.step(flags | L.SCHED_TIMING, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, want_log=True,
                         gemm=gemm, hook=hook)
         if rank == 0:
             H.chrome_trace(rep_t["log"], args.trace)
-    # model check (runs with real collectives): the two-stream simulator fed
-    # with THIS run's measured op durations (collectives included) against the
-    # measured eager step -- the gap is what the model leaves out (SM / HBM
-    # contention between the streams, launch gaps)
-    model_check = None
-    if multi or p2p:
-        rep_m = st.step(flags | L.SCHED_TIMING, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, want_log=True,
-                        gemm=gemm, hook=hook)
-        tot_m, exp_m, _, _ = F.simulate_schedule(rep_m["log"], [max(e[4], 0) for e in rep_m["log"]])
-        model_check = {"simulated_ms": round(tot_m / 1e6, 3), "simulated_exposed_ms": round(exp_m / 1e6, 3),
-                       "how": "fsdp_simulate_schedule on one timed step's measured op durations"}
     # (3) compute-stream-only baseline: same ops, no collective, no wait
     step(L.SCHED_NO_COMM)
     ms_compute, _ = timed_loop(L.SCHED_NO_COMM, args.steps)
-
+    st.check_p2p()
     if sg is not None:
         sg.close()
 
+    # ---- headline value
     ag_b, rs_b = st.step_bytes()
-    ranks = world_env if multi else 1
-    value = ranks * (ag_b + rs_b) / (ms_step * 1e-3) / 1e9
-
-    # N = 1 has no peers, so exposure cannot be measured; report the library's
-    # two-stream PREDICTION for the N-rank job instead (fsdp_simulate_schedule):
-    # every compute-stream op at its duration measured here (copy kernels and
-    # the compute proxy at --predict-tokens), every collective at alpha + beta n
-    # of modelled NVLink 5 (720 GB/s bus, 20 us); no contention modelled.
-    predicted = None
-    if not multi and not p2p and (args.predict_tokens or gemm or model):
-        beta = round((world - 1) / world / 720e9 * 1e15)
-        link = (20000, beta)
-        if gemm or model:   # the measured compute of this run is the compute
-            ppf = ppb = None
-        else:
-            ptf, ptb = per_param_compute_ns(specs, args.predict_tokens)
-            nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
-            ppf = H.proxy_iters(H.bucket_times(fplan, ptf), nspi)
-            ppb = H.proxy_iters(H.bucket_times(bplan, ptb), nspi)
-        tot, exp = H.predict_exposure(st, flags, cs, ms, ppf, ppb, link, link, args.proxy_ctas, args.proxy_smem,
-                                      gemm=gemm, hook=hook)
-        predicted = {"world": world,
-                     "tokens_per_gpu": gemm["tokens"] if gemm else model.T if model else args.predict_tokens,
-                     "compute": ("cuBLASLt linear layers (measured)" if gemm else
-                                 "Llama-3 layers through the compute hook (measured)" if model else
-                                 "calibrated proxy (per-op model)"),
-                     "link_alpha_ns": link[0], "link_beta_fs_per_byte": link[1], "total_ms": round(tot / 1e6, 3),
-                     "exposed_ms": round(exp / 1e6, 3), "exposed_comm_ms": round(exp / 1e6, 3),
-                     "model": "measured compute-stream ops + alpha/beta NVLink collectives, no contention"}
-        # the paper's other metric (Tables 5 / 6): peak memory of the
-        # step's FSDP buffers under allocate-on-produce / free-after-use (G40),
-        # beside what this library's static two-slot pools hold
-        mp, pools = H.predict_memory(st, flags)
-        predicted["memory_model_peak_GiB"] = round(mp / 2 ** 30, 3)
-        predicted["static_pools_GiB"] = round(pools / 2 ** 30, 3)
-        if not gemm and not model and not args.no_variants:
-            # the north star's comparison: exposure under the greedy plan (Alg. 1)
-            # vs the unbucketed, unreordered baseline, same model, same compute
-            variants = {}
-            RF = L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT
-            for name, vmode, vflags in (("vanilla (per-param, no reorder)", L.PLAN_PER_PARAM, 0),
-                                        ("greedy + reorder", L.PLAN_GREEDY, RF),
-                                        ("search + reorder (fsdp_plan_search, beyond the paper)", "search", RF)):
-                if vmode == "search":
-                    vf, vb = H.plans_search(specs, world, ptf, ptb, link, link, int(args.mem_limit))
-                else:
-                    vf, vb = H.plans_for(specs, world, vmode, ptf, ptb, link, link, int(args.mem_limit))
-                vst = H.RankState(specs, world, 0, vf, vb, ctx, seed=99)
-                vpf = H.proxy_iters(H.bucket_times(vf, ptf), nspi)
-                vpb = H.proxy_iters(H.bucket_times(vb, ptb), nspi)
-                vst.step(vflags, cs, ms, vpf, vpb, args.proxy_ctas, args.proxy_smem)   # warm-up
-                vt, ve = H.predict_exposure(vst, vflags, cs, ms, vpf, vpb, link, link, args.proxy_ctas,
-                                            args.proxy_smem)
-                variants[name] = {"buckets_fwd": len(vf), "buckets_bwd": len(vb),
-                                  "total_ms": round(vt / 1e6, 3), "exposed_ms": round(ve / 1e6, 3),
-                                  "memory_model_peak_GiB": round(H.predict_memory(vst, vflags)[0] / 2 ** 30, 3)}
-                del vst
-                gc.collect()
-                torch.cuda.empty_cache()
-            variants["manual (per-block) + reorder [this run]"] = {
-                "buckets_fwd": len(fplan), "buckets_bwd": len(bplan),
-                "total_ms": predicted["total_ms"], "exposed_ms": predicted["exposed_ms"],
-                "memory_model_peak_GiB": predicted["memory_model_peak_GiB"]}
-            predicted["variants"] = variants
-
-    # MEASURED exposure of the N-rank step with emulated collectives (K11,
-    # fsdp_comm_emulation): every AG / RS runs on the comm stream with the
-    # modelled NVLink duration, 32 CTAs and the HBM traffic a rank sees, so
-    # (step - compute-only step) includes the SM / HBM contention the
-    # two-stream prediction leaves out.  Timing only (no peers, no real data).
-    emulated = None
-    if not multi and p2p and (args.predict_tokens or gemm or model):
-        # the fused peer-memory path: K8 / K9 against the simulated peers, paced to
-        # the modelled link time (fsdp_comm_emulation with FSDP_SCHED_P2P)
-        link = (20000, round((world - 1) / world / 720e9 * 1e15))
-        ppf = ppb = None
-        if not gemm and not model:
-            ptf, ptb = per_param_compute_ns(specs, args.predict_tokens)
-            nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
-            ppf = H.proxy_iters(H.bucket_times(fplan, ptf), nspi)
-            ppb = H.proxy_iters(H.bucket_times(bplan, ptb), nspi)
-    if not multi and (args.predict_tokens or gemm or model):
-        # with --compute gemm / llama the compute is the real tensor-core work, a
-        # more faithful co-runner for the collectives than the ALU-bound proxy
-        em = dict(ag=link, rs=link,   # 32 CTAs at N = 8 for K11 (16 could not keep up); 57 for paced K8 / K9
-                  ctas=H.emulation_ctas_p2p(world) if p2p else H.emulation_ctas(world))
-
-        def em_loop(extra, emulate, n):
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(compute)
-            for _ in range(n):
-                st.step(flags | extra, cs, ms, ppf, ppb, args.proxy_ctas, args.proxy_smem, emulate=emulate,
-                        gemm=gemm, hook=hook)
-            b.record(compute)
-            torch.cuda.synchronize()
-            return a.elapsed_time(b) / n
-        em_loop(0, em, 1)   # warm-up
-        em_step = em_loop(0, em, args.steps)
-        em_comp = em_loop(L.SCHED_NO_COMM, None, args.steps)
-        emulated = {"world": world, "compute": args.compute,
-                    "tokens_per_gpu": (gemm["tokens"] if gemm else model.T if model else args.predict_tokens),
-                    "link_alpha_ns": link[0],
-                    "link_beta_fs_per_byte": link[1], "ctas_per_collective": em["ctas"],
-                    "step_ms": round(em_step, 3), "compute_only_ms": round(em_comp, 3),
-                    "exposed_ms": round(em_step - em_comp, 3),
-                    "predicted_exposed_ms": predicted["exposed_ms"] if predicted else None,
-                    "how": ("same plan and compute as `predicted`, collectives emulated on the comm stream "
-                            "(kernel K11: modelled duration, enough CTAs for the rank's HBM traffic); measured with "
-                            "CUDA events, eager enqueue" if not p2p else
-                            "fused peer-memory kernels K8 / K9 against the simulated peers on a grid of that many "
-                            "CTAs, each held to the modelled link time (AG: bf16 bucket; RS: the bf16 gradients "
-                            "K9 pulls); the run's compute (see `compute`); CUDA events, eager enqueue")}
-
-    # linear-layer compute throughput (cuBLASLt, tensor cores) of the timed steps
-    gemm_report = None
-    if model:
-        ops_ns = sum(r["op_ns"][L.OP_COMPUTE_F] + r["op_ns"][L.OP_COMPUTE_B] for r in reports) / len(reports)
-        tf = model.flops / (ops_ns * 1e-9) / 1e12
-        peak_tf = measured_peak_bf16()
-        gemm_report = {"tokens": model.T, "model": "Llama-3 layers (torch: cuBLAS GEMMs, SDPA causal GQA, RoPE, "
-                                                   "RMSNorm, SwiGLU, cross-entropy) via fsdp_compute_hook",
-                       "tflops_per_step": round(model.flops / 1e12, 2),
-                       "compute_ms_per_step": round(ops_ns / 1e6, 3), "achieved_TFLOPs": round(tf, 1),
-                       "peak_TFLOPs": peak_tf, "frac": round(tf / peak_tf, 3),
-                       "note": "model FLOPs / device time of the COMPUTE ops (library GEMM / attention kernels)"}
-    if gemm:
-        ops_ns = sum(r["op_ns"][L.OP_COMPUTE_F] + r["op_ns"][L.OP_COMPUTE_B] for r in reports) / len(reports)
-        tf = st.gemm_flops / (ops_ns * 1e-9) / 1e12
-        peak_tf = measured_peak_bf16()
-        gemm_report = {"tokens": gemm["tokens"], "tflops_per_step": round(st.gemm_flops / 1e12, 2),
-                       "compute_ms_per_step": round(ops_ns / 1e6, 3), "achieved_TFLOPs": round(tf, 1),
-                       "peak_TFLOPs": peak_tf, "frac": round(tf / peak_tf, 3),
-                       "note": "library GEMMs (cuBLASLt), bf16 in/out, fp32 accumulate"}
-
-    # per-op device time from the timed steps' events -> dominant data kernel
-    op_ns = [sum(r["op_ns"][i] for r in reports) for i in range(L.N_OPS)]
-    op_cnt = [sum(r["op_count"][i] for r in reports) for i in range(L.N_OPS)]
+    op_ns = {i: sum(r["op_ns"][i] for r in reports) for i in range(L.N_OPS)}
     if p2p:
         k8, k9 = st.p2p_bytes()
         kbytes = {L.OP_AG: k8, L.OP_RS: k9}
         klaunch = {L.OP_AG: len(st.fwd) + len(st.bwd), L.OP_RS: len(st.bwd)}
         names = {L.OP_AG: "fsdp_p2p_allgather_kernel", L.OP_RS: "fsdp_p2p_reduce_scatter_kernel"}
+        wire_rs = rs_b // 2      # K9 pulls the bf16 gradients: half the fp32 RS bytes
     else:
         kbytes, klaunch = st.kernel_bytes(), st.kernel_launches()
         names = {L.OP_PACK_AG: "fsdp_ag_pack_kernel", L.OP_UNPACK: "fsdp_ag_unpack_kernel",
                  L.OP_PACK_RS: "fsdp_rs_pack_kernel", L.OP_COPYOUT_RS: "fsdp_rs_copyout_kernel"}
-    live = [op for op in kbytes if kbytes[op] > 0 and op_ns[op] > 0]
-    dom = max(live, key=lambda op: op_ns[op])
+        wire_rs = rs_b
+    hbm_bytes = sum(kbytes.values())
+    bus_world = world if multi else 1
+    bus_bytes_rank = (bus_world - 1) / bus_world * (ag_b + wire_rs)
+    if bus_world > 1:
+        value = bus_world * bus_bytes_rank / (ms_step * 1e-3) / 1e9
+        value_kind = "bus"
+        value_def = ("whole-job bus GB/s: N x (N-1)/N x full bucket bytes of the step's collectives (fwd AG + bwd AG "
+                     "bf16, RS %s) / step time (nccl-tests busbw convention, G28, summed over ranks)"
+                     % ("bf16 gradients pulled by K9" if p2p else "fp32"))
+    else:
+        value = hbm_bytes / (ms_step * 1e-3) / 1e9
+        value_kind = "hbm"
+        value_def = ("N = 1 has no peers and no bus: algorithmic HBM bytes of the step's data kernels (%s) / step "
+                     "time, rank 0 of a simulated %d-way job" % (", ".join(names[o] for o in kbytes if kbytes[o]),
+                                                                world))
+
+    # ---- per-kernel table and the roofline of the dominant kernel
     peak, peak_src = measured_peak_hbm()
+    live = [op for op in kbytes if kbytes[op] > 0 and op_ns.get(op, 0) > 0]
+    dom = max(live, key=lambda op: op_ns[op])
     achieved = kbytes[dom] * args.steps / (op_ns[dom] * 1e-9) / 1e9
-    per_kernel = {names[op]: {"GB/s": round(kbytes[op] * args.steps / (op_ns[op] * 1e-9) / 1e9, 1),
-                              "ms_per_step": round(op_ns[op] / args.steps / 1e6, 3),
-                              "launches_per_step": klaunch[op],
-                              "bytes_per_step": kbytes[op]} for op in live}
+    per_kernel = (kernel_table(st, ctx, names, kbytes, klaunch, op_ns, args.steps, cs, peak) if not p2p else
+                  {names[op]: {"GB/s_in_step_event": round(kbytes[op] * args.steps / (op_ns[op] * 1e-9) / 1e9, 1),
+                               "ms_per_step_in_step_event": round(op_ns[op] / args.steps / 1e6, 3),
+                               "launches_per_step": klaunch[op], "bytes_per_step": kbytes[op]} for op in live})
     launches = sum(r["kernel_launches"] for r in reports)
-    # device time of the collective ops (event pairs on the comm stream); at
-    # N = 1 with the NCCL design no collective exists (no peers): null
     coll_ms = None
+    busbw_step = None
     if multi or p2p:
         coll_ms = {"ag_ms_per_step": round(op_ns[L.OP_AG] / args.steps / 1e6, 3),
                    "rs_ms_per_step": round(op_ns[L.OP_RS] / args.steps / 1e6, 3)}
-    # NCCL's own estimate of this step's collectives (ncclGroupSimulateEnd,
-    # its topology-aware model) beside the event-measured collective time
-    if coll_ms is not None and not p2p:
-        try:
-            est = sum(ctx.nccl_estimate_ns(L.OP_AG, world * b.ag_seg) for b in st.fwd + st.bwd)
-            est_rs = sum(ctx.nccl_estimate_ns(L.OP_RS, world * b.rs_seg) for b in st.bwd)
-            coll_ms["nccl_estimate_ag_ms_per_step"] = round(est / 1e6, 3)
-            coll_ms["nccl_estimate_rs_ms_per_step"] = round(est_rs / 1e6, 3)
-        except Exception as e:   # reported, never fatal
-            coll_ms["nccl_estimate_error"] = str(e)[:200]
-    busbw = None
-    if multi and op_ns[L.OP_AG] > 0:
-        busbw = {"ag": round((world - 1) / world * ag_b * args.steps / (op_ns[L.OP_AG] * 1e-9) / 1e9, 1),
-                 "rs": round((world - 1) / world * rs_b * args.steps / (op_ns[L.OP_RS] * 1e-9) / 1e9, 1)}
+    if multi and world > 1 and op_ns[L.OP_AG] > 0:
+        # the step's collectives alone (event pairs on the comm stream), per GPU
+        busbw_step = {"ag": round((world - 1) / world * ag_b * args.steps / (op_ns[L.OP_AG] * 1e-9) / 1e9, 1),
+                      "rs": round((world - 1) / world * wire_rs * args.steps / (op_ns[L.OP_RS] * 1e-9) / 1e9, 1),
+                      "nvlink_GBps": NVLINK_GBS,
+                      "how": "(N-1)/N x full bytes / comm-stream event time of the step's AG / RS, per GPU"}
 
-    # e2e through the public call with HOST buffers: fsdp_run_schedule with
-    # fsdp_host_io streams the rank's parameter shards in from pinned host
-    # memory and its fp32 gradient shards back out, bucket by bucket,
-    # overlapped with the device path; the step ends when the gradients are
-    # on the host.
+    # ---- N > 1 verification: sampled oracle parity on the step's own buckets
+    parity = None
+    if multi and not quick and not args.no_parity and args.compute == "proxy":
+        parity = parity_leg(st, ctx, cs, ms, p2p, world, my_rank, exchange, barrier)
+        st.check_p2p()
+
+    # ---- e2e through the public call with HOST buffers
     e2e = None
     if not args.no_e2e:
         h_sh = torch.empty(st.shard_buf.numel(), dtype=torch.uint8, pin_memory=True)
@@ -750,104 +826,274 @@ def main():
             st.step(flags, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, io=io, gemm=gemm, hook=hook)
         x1.record(compute)
         barrier()
+        st.check_p2p()
         e2e_ms = max_over_ranks(x0.elapsed_time(x1) / args.e2e_steps)
-        e2e = {"value": round(ranks * (ag_b + rs_b) / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
-               "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(h2d_bytes),
-               "d2h_bytes_per_step": int(d2h_bytes),
-               "how": "fsdp_run_schedule with fsdp_host_io: per-bucket H2D of shards / D2H of grad shards "
-                      "from/to pinned host memory inside the call, overlapped with the device path"}
+        e2e_val = (bus_world * bus_bytes_rank if bus_world > 1 else hbm_bytes) / (e2e_ms * 1e-3) / 1e9
+        e2e = {"value": round(e2e_val, 3), "unit": "GB/s", "ms_per_step": round(e2e_ms, 3),
+               "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h_bytes),
+               "how": "fsdp_run_schedule with fsdp_host_io: per-bucket H2D of shards / D2H of fp32 grad shards "
+                      "from / to pinned host memory inside the call, overlapped with the device path; value "
+                      "defined as the headline's (%s)" % value_kind}
         del h_sh, h_gs
 
+    zero_copy = st.zero_copy()
+    n_fwd, n_bwd = len(fplan), len(bplan)
+
+    # ---- N = 1: the modelled N-rank step (assumed links; labelled a model)
+    predicted = None
+    if not multi and not p2p and not quick and args.predict_tokens and args.compute == "proxy":
+        plink = (ASSUMED_LINK[0], round((world - 1) / world / 720e9 * 1e15))
+        ptf, ptb = per_param_compute_ns(specs, args.predict_tokens)
+        nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
+        ppf = H.proxy_iters(H.bucket_times(fplan, ptf), nspi)
+        ppb = H.proxy_iters(H.bucket_times(bplan, ptb), nspi)
+        tot, exp = H.predict_exposure(st, flags, cs, ms, ppf, ppb, plink, plink, args.proxy_ctas, args.proxy_smem)
+        predicted = {"kind": "MODEL, not a measurement: this rank's measured compute-stream ops + ASSUMED links "
+                             "(alpha 20 us, 720 GB/s busbw = 80 % of NVLink 5), no contention",
+                     "world": world, "tokens_per_gpu": args.predict_tokens, "link_alpha_ns": plink[0],
+                     "link_beta_fs_per_byte": plink[1], "total_ms": round(tot / 1e6, 3),
+                     "exposed_ms": round(exp / 1e6, 3)}
+        mp, pools = H.predict_memory(st, flags)
+        predicted["memory_model_peak_GiB"] = round(mp / 2 ** 30, 3)
+        if not args.no_variants:
+            variants = {}
+            RF = L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT
+            for name, vmode, vflags in (("vanilla (per-param, no reorder)", L.PLAN_PER_PARAM, 0),
+                                        ("greedy + reorder (assumed links)", L.PLAN_GREEDY, RF)):
+                vf, vb = H.plans_for(specs, world, vmode, ptf, ptb, plink, plink, int(args.mem_limit))
+                vst = H.RankState(specs, world, 0, vf, vb, ctx, seed=99)
+                vpf = H.proxy_iters(H.bucket_times(vf, ptf), nspi)
+                vpb = H.proxy_iters(H.bucket_times(vb, ptb), nspi)
+                vst.step(vflags, cs, ms, vpf, vpb, args.proxy_ctas, args.proxy_smem)   # warm-up
+                vt, ve = H.predict_exposure(vst, vflags, cs, ms, vpf, vpb, plink, plink, args.proxy_ctas,
+                                            args.proxy_smem)
+                variants[name] = {"buckets_fwd": len(vf), "buckets_bwd": len(vb), "total_ms": round(vt / 1e6, 3),
+                                  "exposed_ms": round(ve / 1e6, 3)}
+                del vst
+                gc.collect()
+                torch.cuda.empty_cache()
+            variants["per-block + reorder [this run's plan]"] = {"buckets_fwd": n_fwd, "buckets_bwd": n_bwd,
+                                                                "total_ms": predicted["total_ms"],
+                                                                "exposed_ms": predicted["exposed_ms"]}
+            predicted["variants"] = variants
+
+    emulated = None
+    if not multi and not quick and args.emulate and args.compute == "proxy":
+        elink = (ASSUMED_LINK[0], round((world - 1) / world / 720e9 * 1e15))
+        ptf, ptb = per_param_compute_ns(specs, args.predict_tokens or 1024)
+        nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
+        epf = H.proxy_iters(H.bucket_times(fplan, ptf), nspi)
+        epb = H.proxy_iters(H.bucket_times(bplan, ptb), nspi)
+        em = dict(ag=elink, rs=elink, ctas=H.emulation_ctas_p2p(world) if p2p else 64)
+
+        def em_loop(extra, emulate, n):
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(compute)
+            for _ in range(n):
+                st.step(flags | extra, cs, ms, epf, epb, args.proxy_ctas, args.proxy_smem, emulate=emulate)
+            b.record(compute)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / n
+        em_loop(0, em, 1)
+        es, ec = em_loop(0, em, args.steps), em_loop(L.SCHED_NO_COMM, None, args.steps)
+        emulated = {"kind": "MODEL DEVICE, not a multi-GPU measurement: collectives emulated on one GPU (K11 / "
+                            "paced K8-K9) at ASSUMED links (720 GB/s busbw, 20 us)",
+                    "world": world, "step_ms": round(es, 3), "compute_only_ms": round(ec, 3),
+                    "exposed_ms": round(es - ec, 3)}
+
+    # free the headline state before the N > 1 sweeps / variants
+    st.check_p2p()
+    if p2p and multi:
+        barrier()
+        st.close_ipc()
+    st.close_nccl_mem()
+    del st
+    gc.collect()
+    torch.cuda.empty_cache()
+
+    # ---- N > 1: isolated 8B-block busbw, alpha / beta fit, measured exposure
+    busbw_block = alpha_beta = exposure = None
+    if multi and world > 1 and not quick:
+        from workloads.shapes import ParamSpec
+        kw = dict(p2p=p2p, exchange=exchange, max_over_ranks=max_over_ranks)
+        block = [p for p in llama("8b", n_layers=1, with_embeddings=False)]
+        barrier()
+        r = H.time_bucket_collectives(block, world, my_rank, ctx, cs, ms, reps=20, warmup=5, **kw)
+        wire_rs_block = r["rs_bytes"] // 2 if p2p else r["rs_bytes"]
+        bb_ag = (world - 1) / world * r["ag_bytes"] / r["ag_ns"]
+        bb_rs = (world - 1) / world * wire_rs_block / r["rs_ns"]
+        busbw_block = {"ag_GBps": round(bb_ag, 1), "rs_GBps": round(bb_rs, 1),
+                       "ag_frac_nvlink": round(bb_ag / NVLINK_GBS, 4), "rs_frac_nvlink": round(bb_rs / NVLINK_GBS, 4),
+                       "ag_ms": round(r["ag_ns"] / 1e6, 4), "rs_ms": round(r["rs_ns"] / 1e6, 4),
+                       "ag_full_bytes": r["ag_bytes"], "rs_full_bytes": r["rs_bytes"],
+                       "rs_wire_dtype": "bf16 (K9 pulls the gradients)" if p2p else "fp32",
+                       "target_GBps": 0.8 * NVLINK_GBS,
+                       "how": "one Llama-3-8B transformer block as one bucket, alone; median of 20 after 5 warm-up, "
+                              "CUDA events around the collective on the comm stream, max over ranks; busbw = "
+                              "(N-1)/N x full bytes / t (nccl-tests)"}
+        if not args.no_sweep:
+            rows = []
+            for n in [2 ** 13, 2 ** 16, 2 ** 19, 2 ** 22, 2 ** 25, 2 ** 26, 2 ** 27, 2 ** 28, 2 ** 29, 2 ** 30]:
+                d = max(world, (n // 2048) // world * world)
+                barrier()
+                rows.append(H.time_bucket_collectives([ParamSpec("x", d, 1024, 0)], world, my_rank, ctx, cs, ms,
+                                                      reps=10, warmup=3, **kw))
+            fa, fr = H.fit_link(rows, "ag_bytes", "ag_ns"), H.fit_link(rows, "rs_bytes", "rs_ns")
+            alpha_beta = {"ag": {"alpha_ns": fa[0], "beta_fs_per_byte": fa[1]},
+                          "rs": {"alpha_ns": fr[0], "beta_fs_per_byte": fr[1]},
+                          "source": "measured at this N (fit: alpha = t at 8 KiB; beta = least-squares slope over "
+                                    "n >= 64 MiB; n = full bucket bytes, bf16 AG / fp32 RS, G8)",
+                          "rows": [{k: (round(v, 1) if isinstance(v, float) else v) for k, v in x.items()}
+                                   for x in rows]}
+        if args.exposure_tokens:
+            exposure = exposure_leg(args, specs, world, my_rank, ctx, cs, ms, compute, p2p, exchange, barrier,
+                                    max_over_ranks, alpha_beta)
+    elif not multi:
+        alpha_beta = {"ag": {"alpha_ns": args.alpha_ns, "beta_fs_per_byte": args.beta_fs},
+                      "rs": {"alpha_ns": args.alpha_ns, "beta_fs_per_byte": args.beta_fs},
+                      "source": "assumed (N = 1: no collective to measure)"}
+
+    nccl_info = None
+    if multi and not p2p and rank == 0 and os.environ.get("NCCL_DEBUG_FILE") == nccl_log_path(rank):
+        nccl_info = nccl_info_summary(nccl_log_path(rank))
+
     cpu = None
-    if rank == 0 and not multi and not args.no_cpu_baseline:
-        sample = CpuOracleSample(world)
+    if rank == 0 and not multi and not args.no_cpu_baseline and not quick:
+        sample = CpuOracleSample(world, "hbm")
         runs = []
-        while sum(r[1] for r in runs) < 10.0:     # ~10 s of timed oracle work
+        while sum(r_[1] for r_ in runs) < 10.0:     # ~10 s of timed oracle work
             runs.append(sample.run())
-        dt = sum(r[1] for r in runs)
-        v = len(runs) * sample.bytes / dt / 1e9
-        desc = sample.desc + "; %d repetitions" % len(runs)
-        cpu = {"value": round(v, 3), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc,
-               "seconds": round(dt, 2), "host_cpus": os.cpu_count()}
+        dt = sum(r_[1] for r_ in runs)
+        cpu = {"value": round(len(runs) * sample.bytes / dt / 1e9, 3), "unit": "GB/s", "cores": 1,
+               "kind": "oracle", "sample": sample.desc + "; %d repetitions" % len(runs), "seconds": round(dt, 2),
+               "host_cpus": os.cpu_count()}
 
-    # the fused peer-memory path (K8/K9) on the same
-    # workload, in a child process of its own (separate allocations and
-    # timings), summarised beside the headline
     fused = None
-    if rank == 0 and not multi and not p2p and not args.no_fused_leg and args.compute == "proxy":
+    if rank == 0 and not multi and not p2p and not args.no_fused_leg and not quick and args.compute == "proxy":
         fused = fused_leg(args)
-    gemm_cmp = None
-    if rank == 0 and not multi and not p2p and not args.no_gemm_comparison and args.compute == "proxy" \
-            and args.model == "8b":
-        gemm_cmp = gemm_comparison(args)
 
+    workload = "llama3-8b FSDP rank step, %s plan, %s, %s" % (
+        "file:" + os.path.basename(args.plan_file) if args.plan_file else args.plan,
+        "reorder fwd-%s/bwd-%s" % (args.fwd_placement, args.bwd_placement) if not args.no_reorder else "vanilla order",
+        "compute: none (the communication path alone)" if not tokens and args.compute == "proxy"
+        else "compute: %s at %d tokens/GPU" % (args.compute, tokens or 1024))
+    if not multi:
+        workload += ", 1 GPU = rank 0 of a simulated %d-way job (%s)" % (
+            world, "peers simulated in local HBM" if p2p else "pack/unpack only, no peers")
+    else:
+        workload += ", %d ranks over %s%s" % (world, "peer memory (CUDA IPC)" if p2p else "NCCL",
+                                             " [TEST: one GPU]" if args.same_device else "")
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic",
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "value_kind": value_kind,
+            "value_def": value_def, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded N(0, 0.02) bf16 params, N(0, 1e-3) bf16 grads)",
             "config": {
-                "workload": ("llama3-8b FSDP rank step, %s plan, %s" % (
-                    "file:" + os.path.basename(args.plan_file) if args.plan_file else args.plan, "reorder fwd-%s/bwd-%s" % (
-                    args.fwd_placement, args.bwd_placement) if not args.no_reorder else "vanilla order")) +
-                ((", 1 GPU = rank 0 of a simulated %d-way job (pack/unpack only, no peers)" % world if not p2p else
-                  ", 1 GPU = rank 0 of a simulated %d-way job (peers' buffers simulated in local HBM)" % world)
-                 if not multi
-                 else ", %d ranks over %s%s" % (world, "peer memory (CUDA IPC)" if p2p else "NCCL",
-                                               " [TEST: all ranks on one GPU]" if args.same_device else "")),
+                "workload": workload,
                 "model": "llama3-8b shapes (Table 2; vocab 128256, 8 KV heads)", "layout_world": world,
-                "collective": ("NCCL all-gather / reduce-scatter with pack + copy-out kernels" if not p2p else
-                               "fused peer-memory kernels K8/K9 over CUDA IPC mappings of the peers" if multi else
-                               "fused peer-memory kernels K8/K9 (peers simulated as separate HBM buffers)"),
-                "buckets_fwd": len(fplan), "buckets_bwd": len(bplan), "param_dtype": "bf16",
-                "reduce_dtype": "fp32", "compute": args.compute,
-                "proxy_tokens_per_gpu": tokens if args.compute == "proxy" else 0,
-                "compute_tokens_per_gpu": (model.T if model else gemm["tokens"] if gemm else tokens),
-                "value_def": "sum over ranks of full AG(fwd)+AG(bwd)+RS bucket bytes per second of step time",
-                "bytes_per_rank_step": ag_b + rs_b, "l2": "inputs > L2 (126 MB): 64 GB of bucket traffic per step",
+                "collective": ("NCCL all-gather / reduce-scatter with copy kernels" if not p2p else
+                               "fused peer-memory kernels K8/K9"),
+                "buckets_fwd": n_fwd, "buckets_bwd": n_bwd, "param_dtype": "bf16", "reduce_dtype": "fp32",
+                "compute": args.compute if tokens or args.compute != "proxy" else "none",
+                "tokens_per_gpu": tokens, "bus_bytes_per_rank_step": int(bus_bytes_rank),
+                "full_bucket_bytes_per_rank_step": ag_b + rs_b, "hbm_algorithmic_bytes_per_step": hbm_bytes,
+                "l2": "inputs > L2 (126 MB): every bucket but the 8 KB norms exceeds it",
                 "parallelism": "fsdp%d" % world if multi else "fsdp1 (simulated %d)" % world,
                 "nccl_register": reg or "none", "ag": args.ag},
-            # measured exposure: eager step - the same eager step without collectives / waits
             "exposed_comm_ms": round(ms_eager - ms_compute, 3), "compute_stream_ms": round(ms_compute, 3),
-            "profiled_ms_per_step": round(ms_prof, 3),
-            "predicted": predicted,
-            "emulated": emulated,
-            "model_check": dict(model_check, measured_eager_ms=round(ms_eager, 3)) if model_check else None,
-            "linear_compute": gemm_report,
-            "timing": ("eager enqueue" if sg is None else "CUDA-graph replay of the step (fsdp_step_graph)"
-                       if model is None else "CUDA-graph replay of the step incl. the hook's torch ops "
-                                             "(torch.cuda.graph)"),
-            "eager_ms_per_step": round(ms_eager, 3),
+            "eager_ms_per_step": round(ms_eager, 3), "profiled_ms_per_step": round(ms_prof, 3),
+            "timing": "eager enqueue" if sg is None else "CUDA-graph replay of the step",
             "host_enqueue_ms_per_step": (round(1e3 * sorted(host_enqueue)[len(host_enqueue) // 2], 3)
                                          if host_enqueue else None),
-            # the paper's other metric: peak device memory of this rank
-            # (torch-allocated buffers: shards, slots, staging; the library's
-            # own run tables are a few MB)
-            "peak_device_mem_GiB": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
-            "collectives": coll_ms, "busbw_GBps": busbw, "kernels": per_kernel,
+            "collectives": coll_ms, "busbw_step": busbw_step, "busbw_block": busbw_block,
+            "alpha_beta": alpha_beta, "exposure": exposure, "parity": parity, "nccl_info": nccl_info,
+            "kernels": per_kernel,
             "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "achieved_how": "algorithmic bytes / in-step event-timed launch duration (conservative: "
+                                         "includes each launch's event / launch latency)",
                          "traffic": ncu_traffic(names[dom]),
                          "traffic_launch_algorithmic_bytes": ncu_traffic(names[dom] + "_algorithmic"),
                          "algorithmic_bytes_per_launch": kbytes[dom] // max(1, klaunch[dom])},
-            "zero_copy": st.zero_copy(),
-            "p2p_wait_timeouts": int(st.p2p_err.item()) if p2p else None,
-            "fused_p2p": fused,
-            "emulated_gemm_comparison": gemm_cmp,
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(),
-            "env": run_env(torch),
-            "paper_context": PAPER_CONTEXT,
+            "zero_copy": zero_copy, "predicted": predicted, "emulated": emulated, "fused_p2p": fused,
+            "peak_device_mem_GiB": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "p2p_wait_timeouts": 0 if p2p else None,
+            "clocks": clk.summary(), "env": run_env(torch), "paper_context": PAPER_CONTEXT,
         }
         print(json.dumps(line), flush=True)
-    ctx_close = getattr(ctx, "close", None)
-    st.close_nccl_mem()
-    del st
-    if ctx_close:
-        ctx_close()
+    ctx.close()
     if multi:
         dist.destroy_process_group()
+
+
+def exposure_leg(args, specs, world, rank, ctx, cs, ms, compute, p2p, exchange, barrier, max_over_ranks, alpha_beta):
+    """BASELINE configs[2] at this N, MEASURED: the step with the compute proxy
+    at --exposure-tokens tokens/GPU per variant; exposed = step - the same
+    step with no collective and no wait (FSDP_SCHED_NO_COMM), both CUDA-graph
+    replays timed with events, max over ranks.  Greedy (Algorithm 1) is
+    planned with the alpha / beta fitted at this N.  `predicted_exposed_ms` =
+    the two-stream model (fsdp_simulate_schedule) from a timed step's
+    compute-stream ops + alpha + beta n collectives (the estimate P:600 blames
+    for auto-wrap's misses), beside the measurement."""
+    import torch
+    from paper_2411_00284_b200 import _lib as L
+    from paper_2411_00284_b200 import harness as H
+    from workloads.compute_model import per_param_compute_ns
+    T = args.exposure_tokens
+    tf, tb = per_param_compute_ns(specs, T)
+    if alpha_beta and "ag" in alpha_beta:
+        lag = (alpha_beta["ag"]["alpha_ns"], alpha_beta["ag"]["beta_fs_per_byte"])
+        lrs = (alpha_beta["rs"]["alpha_ns"], alpha_beta["rs"]["beta_fs_per_byte"])
+        src = "fitted at this N"
+    else:
+        lag = lrs = ASSUMED_LINK
+        src = "assumed (no sweep)"
+    nspi = H.calibrate_proxy(ctx, cs, args.proxy_ctas, args.proxy_smem)
+    RF = L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT
+    out = {"tokens_per_gpu": T, "links": {"ag": lag, "rs": lrs, "source": src}, "variants": {}}
+    for name, vmode, vflags in (("vanilla (per-param, no reorder)", L.PLAN_PER_PARAM, 0),
+                                ("per-block + reorder (manual wrap)", L.PLAN_MANUAL, RF),
+                                ("greedy + reorder (Algorithm 1, fitted links)", L.PLAN_GREEDY, RF)):
+        vf, vb = H.plans_for(specs, world, vmode, tf, tb, lag, lrs, int(args.mem_limit))
+        vst = H.RankState(specs, world, rank, vf, vb, ctx, seed=77 + rank, ipc=p2p)
+        if p2p:
+            vst.setup_p2p_ipc(exchange)
+            vst.p2p_max_ctas = args.p2p_max_ctas if args.p2p_max_ctas >= 0 else H.emulation_ctas_p2p(world)
+        fl = vflags | (L.SCHED_P2P if p2p else 0)
+        vpf = H.proxy_iters(H.bucket_times(vf, tf), nspi)
+        vpb = H.proxy_iters(H.bucket_times(vb, tb), nspi)
+        res = {"buckets_fwd": len(vf), "buckets_bwd": len(vb)}
+        for key, extra in (("step_ms", 0), ("compute_only_ms", L.SCHED_NO_COMM)):
+            for _ in range(2):
+                vst.step(fl | extra, cs, ms, vpf, vpb, args.proxy_ctas, args.proxy_smem)
+            g = vst.capture(fl | extra, cs, ms, vpf, vpb, args.proxy_ctas, args.proxy_smem)
+            for _ in range(2):
+                g.launch(cs)
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(compute)
+            for _ in range(args.steps):
+                g.launch(cs)
+            b.record(compute)
+            barrier()
+            res[key] = round(max_over_ranks(a.elapsed_time(b) / args.steps), 3)
+            g.close()
+        vst.check_p2p()
+        res["exposed_ms"] = round(res["step_ms"] - res["compute_only_ms"], 3)
+        rep = vst.step(fl | L.SCHED_TIMING, cs, ms, vpf, vpb, args.proxy_ctas, args.proxy_smem, want_log=True)
+        ptot, pexp = H.simulate_n_rank(vst, rep["log"], lag, lrs)
+        res["predicted_exposed_ms"] = round(max_over_ranks(pexp / 1e6), 3)
+        res["predicted_step_ms"] = round(max_over_ranks(ptot / 1e6), 3)
+        out["variants"][name] = res
+        barrier()
+        if p2p:
+            vst.close_ipc()
+        del vst
+        gc.collect()
+        torch.cuda.empty_cache()
+    return out
 
 
 if __name__ == "__main__":

@@ -745,11 +745,11 @@ fsdp_status fsdp_p2p_reduce_scatter_bucket(fsdp_ctx* ctx, fsdp_bucket* b, const 
  * NVLink SHARP: the NVSwitch reduces a load issued to a *multicast* address
  * across every GPU of the team (multimem.ld_reduce), so a rank reads only its
  * own reduced chunk -- 1/N of the RS bytes on its NVLink ingress instead of
- * (N-1)/N.  Setup, one team per buffer (fabric handles, 64 B, exchanged by the
- * caller, e.g. torch.distributed.all_gather_object):
- *   rank 0   : fsdp_nvls_create(ctx, bytes, handle64, &m)  -- the multicast
+ * (N-1)/N.  Setup, one team per buffer (a FSDP_NVLS_HANDLE_BYTES handle,
+ * exchanged by the caller, e.g. torch.distributed.broadcast_object_list):
+ *   rank 0   : fsdp_nvls_create(ctx, bytes, handle, &m)  -- the multicast
  *              object for ctx's world devices, its handle, this GPU added;
- *   others   : fsdp_nvls_import(ctx, handle64, bytes, &m)  -- this GPU added;
+ *   others   : fsdp_nvls_import(ctx, handle, bytes, &m)  -- this GPU added;
  *   (host barrier: every rank added)
  *   every rank: fsdp_nvls_bind(m, &uc, &mc, &bytes)  -- this GPU's physical
  *              memory bound, mapped at `uc` (unicast, this GPU only) and at
@@ -761,9 +761,23 @@ fsdp_status fsdp_p2p_reduce_scatter_bucket(fsdp_ctx* ctx, fsdp_bucket* b, const 
  * accumulation mode); the next pack into the same staging needs another
  * barrier (every rank done reading).  The switch's summation order is its
  * own: results match the oracle within G7's fp32 bound (bit-exact at N <= 2).
- * Errors: FSDP_ERR_UNSUPPORTED without multicast / fabric-handle support. */
+ * Handle (fsdp_nvls_handle, FSDP_NVLS_HANDLE_BYTES): create exports a FABRIC
+ * handle where the platform has one (IMEX / NVSwitch fabric), else a POSIX
+ * file descriptor (type FSDP_NVLS_POSIX_FD: `fd` is valid in the creating
+ * process `pid` only -- the caller passes it to each peer, e.g. SCM_RIGHTS over
+ * a unix socket as the Python binding does, and writes the RECEIVED fd into
+ * the handle before fsdp_nvls_import, which takes ownership of it and closes
+ * it).  Errors: FSDP_ERR_UNSUPPORTED without multicast support or where the
+ * platform refuses the object (e.g. a one-GPU fabric partition). */
 typedef struct fsdp_nvls fsdp_nvls;
-enum { FSDP_NVLS_HANDLE_BYTES = 64 };
+enum { FSDP_NVLS_HANDLE_BYTES = 80, FSDP_NVLS_FABRIC = 1, FSDP_NVLS_POSIX_FD = 2 };
+typedef struct {
+  int32_t type;          /* FSDP_NVLS_FABRIC or FSDP_NVLS_POSIX_FD (0 = a team of one: no handle) */
+  int32_t fd;            /* POSIX_FD: the descriptor, valid in the process that holds it */
+  int32_t pid;           /* POSIX_FD: the creating process */
+  int32_t reserved;
+  uint8_t fabric[64];    /* FABRIC: CUmemFabricHandle */
+} fsdp_nvls_handle;
 fsdp_status fsdp_nvls_create(fsdp_ctx* ctx, int64_t bytes, void* handle_out, fsdp_nvls** out);
 fsdp_status fsdp_nvls_import(fsdp_ctx* ctx, const void* handle, int64_t bytes, fsdp_nvls** out);
 fsdp_status fsdp_nvls_bind(fsdp_nvls* m, void** uc_ptr, void** mc_ptr, int64_t* bytes);

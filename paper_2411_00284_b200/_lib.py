@@ -24,7 +24,8 @@ BF16, FP32 = 0, 1
 PLAN_PER_PARAM, PLAN_MANUAL, PLAN_SIZE_CAP, PLAN_GREEDY = range(4)
 PHASE_FWD, PHASE_BWD = 0, 1
 ISSUE, WAIT, NO_COLLECTIVE = 1, 2, 4
-NVLS_HANDLE_BYTES = 64
+NVLS_HANDLE_BYTES = 80
+NVLS_FABRIC, NVLS_POSIX_FD = 1, 2
 (OP_PACK_AG, OP_AG, OP_WAIT_AG, OP_UNPACK, OP_COMPUTE_F, OP_COMPUTE_B, OP_PACK_RS, OP_RS,
  OP_WAIT_RS, OP_COPYOUT_RS) = range(10)
 N_OPS = 10

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <unistd.h>
 
 #include "internal.h"
 
@@ -94,7 +95,8 @@ struct fsdp_nvls {
   bool added = false, bound = false, uc_mapped = false, mc_mapped = false;
 };
 
-static fsdp_status nvls_begin(fsdp_ctx* c, int64_t bytes, fsdp_nvls** out, CUmulticastObjectProp* prop) {
+static fsdp_status nvls_begin(fsdp_ctx* c, int64_t bytes, fsdp_nvls** out, CUmulticastObjectProp* prop,
+                              unsigned handle_types) {
   if (!c || !out || bytes < 1) return fail(FSDP_ERR_INVALID_ARG, "NULL ctx / out or bytes < 1");
   *out = nullptr;
   const Driver& d = drv();
@@ -108,8 +110,8 @@ static fsdp_status nvls_begin(fsdp_ctx* c, int64_t bytes, fsdp_nvls** out, CUmul
   if (!mc_ok) return fail(FSDP_ERR_UNSUPPORTED, "device does not support multicast (NVLS)");
   std::memset(prop, 0, sizeof(*prop));
   prop->numDevices = static_cast<unsigned>(c->world);
-  // a team of one needs no shareable handle; larger teams export a fabric handle
-  prop->handleTypes = c->world > 1 ? CU_MEM_HANDLE_TYPE_FABRIC : 0;
+  // a team of one needs no shareable handle; larger teams export one (fabric or POSIX fd)
+  prop->handleTypes = c->world > 1 ? handle_types : 0;
   size_t g = 0;
   prop->size = static_cast<size_t>(bytes);
   FSDP_CU_TRY(d.mcGranularity(&g, prop, CU_MULTICAST_GRANULARITY_RECOMMENDED));
@@ -159,25 +161,60 @@ extern "C" fsdp_status fsdp_nvls_destroy(fsdp_nvls* m) {
   return FSDP_OK;
 }
 
+// One attempt at the multicast object with the given shareable handle type;
+// on success the handle is exported into h.
+static CUresult create_exported(fsdp_nvls* m, CUmulticastObjectProp* prop, int world, unsigned type,
+                                fsdp_nvls_handle* h, const char** what) {
+  const Driver& d = drv();
+  prop->handleTypes = world > 1 ? type : 0;
+  *what = "cuMulticastCreate";
+  CUresult r = d.mcCreate(&m->mc, prop);
+  if (r != CUDA_SUCCESS || world == 1) return r;
+  if (type == CU_MEM_HANDLE_TYPE_FABRIC) {
+    CUmemFabricHandle fh;
+    *what = "cuMemExportToShareableHandle(FABRIC)";
+    r = d.exportHandle(&fh, m->mc, CU_MEM_HANDLE_TYPE_FABRIC, 0);
+    if (r == CUDA_SUCCESS) {
+      h->type = FSDP_NVLS_FABRIC;
+      std::memcpy(h->fabric, &fh, sizeof(fh));
+    }
+  } else {
+    int fd = -1;
+    *what = "cuMemExportToShareableHandle(POSIX_FD)";
+    r = d.exportHandle(&fd, m->mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0);
+    if (r == CUDA_SUCCESS) {
+      h->type = FSDP_NVLS_POSIX_FD;
+      h->fd = fd;
+      h->pid = static_cast<int32_t>(getpid());
+    }
+  }
+  if (r != CUDA_SUCCESS) {
+    d.memRelease(m->mc);
+    m->mc = 0;
+  }
+  return r;
+}
+
 extern "C" fsdp_status fsdp_nvls_create(fsdp_ctx* c, int64_t bytes, void* handle_out, fsdp_nvls** out) {
   if (!handle_out) return fail(FSDP_ERR_INVALID_ARG, "NULL handle_out");
   CUmulticastObjectProp prop;
-  FSDP_TRY(nvls_begin(c, bytes, out, &prop));
+  FSDP_TRY(nvls_begin(c, bytes, out, &prop, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
   fsdp_nvls* m = *out;
-  const Driver& d = drv();
-  std::memset(handle_out, 0, FSDP_NVLS_HANDLE_BYTES);
-  CUresult r = d.mcCreate(&m->mc, &prop);
-  const char* what = "cuMulticastCreate";
-  if (r == CUDA_SUCCESS && c->world > 1) {
-    CUmemFabricHandle fh;
-    r = d.exportHandle(&fh, m->mc, CU_MEM_HANDLE_TYPE_FABRIC, 0);
-    what = "cuMemExportToShareableHandle(FABRIC)";
-    if (r == CUDA_SUCCESS) std::memcpy(handle_out, &fh, sizeof(fh));
-  }
+  fsdp_nvls_handle h;
+  std::memset(&h, 0, sizeof h);
+  h.fd = -1;
+  const char* what = "";
+  // a fabric handle where the platform provides one (IMEX / NVSwitch fabric
+  // manager), else a POSIX file descriptor for the caller to pass on
+  CUresult r = create_exported(m, &prop, c->world, CU_MEM_HANDLE_TYPE_FABRIC, &h, &what);
+  if (r != CUDA_SUCCESS && c->world > 1)
+    r = create_exported(m, &prop, c->world, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, &h, &what);
+  std::memcpy(handle_out, &h, sizeof h);
   // A device can report multicast support while the platform refuses the
   // object (e.g. a GPU whose NVSwitch fabric partition holds only itself:
   // CUDA_ERROR_INVALID_VALUE for every property set): unsupported here.
-  const bool refused = r == CUDA_ERROR_NOT_SUPPORTED || (r == CUDA_ERROR_INVALID_VALUE && m->mc == 0);
+  const bool refused = r == CUDA_ERROR_NOT_SUPPORTED || r == CUDA_ERROR_NOT_PERMITTED ||
+                       (r == CUDA_ERROR_INVALID_VALUE && m->mc == 0);
   fsdp_status st = r == CUDA_SUCCESS ? add_device(m)
                                      : fail(refused ? FSDP_ERR_UNSUPPORTED : FSDP_ERR_CUDA,
                                             std::string(what) + ": CUresult " + std::to_string(r) +
@@ -191,12 +228,25 @@ extern "C" fsdp_status fsdp_nvls_create(fsdp_ctx* c, int64_t bytes, void* handle
 
 extern "C" fsdp_status fsdp_nvls_import(fsdp_ctx* c, const void* handle, int64_t bytes, fsdp_nvls** out) {
   if (!handle) return fail(FSDP_ERR_INVALID_ARG, "NULL handle");
+  fsdp_nvls_handle h;
+  std::memcpy(&h, handle, sizeof h);
+  if (h.type != FSDP_NVLS_FABRIC && h.type != FSDP_NVLS_POSIX_FD)
+    return fail(FSDP_ERR_INVALID_ARG, "NVLS handle of unknown type");
+  if (h.type == FSDP_NVLS_POSIX_FD && h.fd < 0) return fail(FSDP_ERR_INVALID_ARG, "NVLS POSIX handle without fd");
   CUmulticastObjectProp prop;
-  FSDP_TRY(nvls_begin(c, bytes, out, &prop));
+  FSDP_TRY(nvls_begin(c, bytes, out, &prop, h.type == FSDP_NVLS_FABRIC ? CU_MEM_HANDLE_TYPE_FABRIC
+                                                                       : CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
   fsdp_nvls* m = *out;
-  CUmemFabricHandle fh;
-  std::memcpy(&fh, handle, sizeof(fh));
-  CUresult r = drv().importHandle(&m->mc, &fh, CU_MEM_HANDLE_TYPE_FABRIC);
+  CUresult r;
+  if (h.type == FSDP_NVLS_FABRIC) {
+    CUmemFabricHandle fh;
+    std::memcpy(&fh, h.fabric, sizeof(fh));
+    r = drv().importHandle(&m->mc, &fh, CU_MEM_HANDLE_TYPE_FABRIC);
+  } else {
+    r = drv().importHandle(&m->mc, reinterpret_cast<void*>(static_cast<intptr_t>(h.fd)),
+                           CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+    close(h.fd);  // ownership taken (include/fsdp.h)
+  }
   fsdp_status st = r == CUDA_SUCCESS ? add_device(m)
                                      : fail(FSDP_ERR_CUDA, "cuMemImportFromShareableHandle: CUresult " + std::to_string(r));
   if (st != FSDP_OK) {

@@ -427,24 +427,85 @@ def register_buffer(ctx, ptr, nbytes, mode=L.REG_LOCAL):
 class Nvls:
     """NVLS multicast team memory (fsdp_nvls_*).  Rank 0: Nvls(ctx, nbytes);
     others: Nvls(ctx, nbytes, handle=<rank 0's .handle>); then, after every
-    rank constructed its object (a host barrier), .bind() -> (uc, mc, nbytes)."""
+    rank constructed its object (a host barrier), .bind() -> (uc, mc, nbytes).
 
-    def __init__(self, ctx, nbytes, handle=None):
+    Where the platform has no fabric handles the library exports a POSIX file
+    descriptor instead; rank 0 then serves it to the peers over an abstract
+    unix socket (SCM_RIGHTS, one connection per peer: ctx world - 1) and each
+    peer writes the descriptor it received into the handle before importing
+    (include/fsdp.h, fsdp_nvls_handle).  Plumbing only: no bytes of the
+    collective pass through here."""
+
+    def __init__(self, ctx, nbytes, handle=None, timeout_s=120.0):
+        import struct
         self.ctx = ctx
         h = C.c_void_p()
+        self._server = None
         if handle is None:
             buf = (C.c_uint8 * L.NVLS_HANDLE_BYTES)()
             check(L.lib.fsdp_nvls_create(ctx.h, int(nbytes), C.cast(buf, C.c_void_p), C.byref(h)))
             self.handle = bytes(buf)
+            kind, fd, _pid, _ = struct.unpack_from("<iiii", self.handle)
+            if kind == L.NVLS_POSIX_FD and ctx.world > 1:
+                self._serve_fd(fd, ctx.world - 1, timeout_s)
         else:
-            buf = (C.c_uint8 * L.NVLS_HANDLE_BYTES).from_buffer_copy(handle)
+            hb = bytearray(handle)
+            kind, fd, pid, _ = struct.unpack_from("<iiii", hb)
+            if kind == L.NVLS_POSIX_FD:
+                struct.pack_into("<i", hb, 4, self._receive_fd(pid, fd, timeout_s))
+            buf = (C.c_uint8 * L.NVLS_HANDLE_BYTES).from_buffer_copy(bytes(hb))
             check(L.lib.fsdp_nvls_import(ctx.h, C.cast(buf, C.c_void_p), int(nbytes), C.byref(h)))
             self.handle = bytes(handle)
         self.h = h
         self.uc = self.mc = None
         self.nbytes = int(nbytes)
 
+    @staticmethod
+    def _sock_name(pid, fd):
+        return "\0fsdp_nvls.%d.%d" % (pid, fd)
+
+    def _serve_fd(self, fd, peers, timeout_s):
+        import os
+        import socket
+        import threading
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(self._sock_name(os.getpid(), fd))
+        srv.listen(peers)
+        srv.settimeout(timeout_s)
+
+        def run():
+            try:
+                for _ in range(peers):
+                    conn, _ = srv.accept()
+                    with conn:
+                        socket.send_fds(conn, [b"fd"], [fd])
+            finally:
+                srv.close()
+                os.close(fd)   # every peer holds its own copy now
+        self._server = threading.Thread(target=run, daemon=True)
+        self._server.start()
+
+    def _receive_fd(self, pid, fd, timeout_s):
+        import socket
+        import time
+        t0 = time.time()
+        while True:
+            s = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            try:
+                s.connect(self._sock_name(pid, fd))
+                _, fds, _, _ = socket.recv_fds(s, 16, 1)
+                return fds[0]
+            except (ConnectionRefusedError, FileNotFoundError):
+                if time.time() - t0 > timeout_s:
+                    raise
+                time.sleep(0.05)
+            finally:
+                s.close()
+
     def bind(self):
+        if self._server is not None:
+            self._server.join()      # every peer took its descriptor
+            self._server = None
         uc, mc, n = C.c_void_p(), C.c_void_p(), C.c_int64()
         check(L.lib.fsdp_nvls_bind(self.h, C.byref(uc), C.byref(mc), C.byref(n)))
         self.uc, self.mc, self.nbytes = uc.value, mc.value, n.value

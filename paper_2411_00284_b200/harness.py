@@ -144,6 +144,10 @@ class RankState:
                               grad_shards=[gp + self.gs_offs[j] for j in m] if phase == 1 else None,
                               param_dtype=param_dtype, grad_dtype=L.BF16, flags=flags)
                 bk.members = m
+                bk.full_offs = offs          # member byte offsets in its full-parameter slot
+                bk.grad_offs = goffs         # member byte offsets in its full-gradient slot
+                bk.full_slot = self.full_slot_index(phase, b)
+                bk.grad_slot = b % self.n_grad_slots if phase == 1 else None
                 out.append(bk)
                 max_ag = max(max_ag, bk.ag_seg)
                 max_rs = max(max_rs, bk.rs_seg)
@@ -492,6 +496,57 @@ def emulation_ctas_p2p(world, bus_gbps=720.0, per_cta_gbps=29.0):
         return 32
     rate = 2.0 * bus_gbps * world / (world - 1)
     return int(min(148, max(32, math.ceil(rate / per_cta_gbps))))
+
+
+def time_bucket_collectives(specs, world, rank, ctx, compute, comm, reps=20, warmup=5, p2p=False,
+                            exchange=None, max_over_ranks=None, seed=11):
+    """One bucket holding all of ``specs``, alone: a forward AG, a backward AG
+    and an RS per step through fsdp_run_schedule with FSDP_SCHED_TIMING -- the
+    AG / RS log entries are CUDA events around the collective alone on the comm
+    stream (NCCL, or K8 / K9 with FSDP_SCHED_P2P).  Median over `reps` steps
+    after `warmup`, max over ranks.  Returns dict(ag_bytes, rs_bytes, ag_ns,
+    rs_ns): full bucket bytes in the planner's definition (G8: N * seg, bf16
+    AG / fp32 RS) and the collective's device time."""
+    plan = [list(range(len(specs)))]
+    st = RankState(specs, world, rank, plan, plan, ctx, seed=seed, ipc=p2p and world > 1)
+    try:
+        if p2p:
+            if world > 1:
+                st.setup_p2p_ipc(exchange)
+            else:
+                st.setup_p2p_simulated()
+        flags = L.SCHED_REORDER | L.SCHED_TIMING | (L.SCHED_P2P if p2p else 0)
+        ag, rs = [], []
+        for i in range(warmup + reps):
+            rep = st.step(flags, compute, comm, want_log=True)
+            if i >= warmup:
+                ag += [e[4] for e in rep["log"] if e[1] == L.OP_AG]
+                rs += [e[4] for e in rep["log"] if e[1] == L.OP_RS]
+        st.check_p2p()
+        t_ag, t_rs = float(np.median(ag)), float(np.median(rs))
+        if max_over_ranks is not None:
+            t_ag, t_rs = max_over_ranks(t_ag), max_over_ranks(t_rs)
+        return dict(ag_bytes=world * st.fwd[0].ag_seg, rs_bytes=world * st.bwd[0].rs_seg, ag_ns=t_ag, rs_ns=t_rs)
+    finally:
+        if p2p:
+            st.close_ipc()
+        del st
+        torch.cuda.empty_cache()
+
+
+def fit_link(rows, key_bytes, key_ns, big=64 << 20):
+    """alpha / beta of T(n) = alpha + beta n from a size sweep (SURVEY
+    §8(d)): alpha = the measured time at the smallest size; beta = the
+    least-squares slope over sizes >= `big`; both rounded to the planner's
+    integer units (ns, fs per byte; G9).  Returns (alpha_ns, beta_fs_per_byte)."""
+    small = min(rows, key=lambda r: r[key_bytes])
+    pts = [(r[key_bytes], r[key_ns]) for r in rows if r[key_bytes] >= big]
+    beta = 0.0
+    if len(pts) >= 2:
+        x = np.array([p[0] for p in pts], dtype=np.float64)
+        y = np.array([p[1] for p in pts], dtype=np.float64)
+        beta = float(np.polyfit(x, y, 1)[0])
+    return int(round(small[key_ns])), max(0, int(round(beta * 1e6)))
 
 
 def calibrate_proxy(ctx, stream, ctas_per_sm=1, smem=0, probe_iters=200000):

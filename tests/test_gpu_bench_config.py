@@ -42,12 +42,23 @@ def test_bench_p2p_two_processes_one_gpu():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"),
            "--gpus", "2", "--collective", "p2p", "--same-device", "--steps", "2", "--warmup", "1",
-           "--layers", "1", "--tokens", "0", "--no-e2e"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+           "--layers", "1", "--no-e2e", "--exposure-tokens", "256"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["p2p_wait_timeouts"] == 0
     assert line["kernels"]["fsdp_p2p_allgather_kernel"]["launches_per_step"] == 2 * line["config"]["buckets_fwd"]
+    # the N > 1 self-checks of the line: K8 / K9 across the two processes' IPC
+    # mappings against the oracle (bit-exact), the isolated-block busbw, the
+    # alpha / beta fit and the measured exposure variants all ran
+    par = line["parity"]
+    assert par["ok"] and par["ag"]["bit_exact"] and par["rs"]["bit_exact"], par
+    assert par["ag"]["elements"] > 0 and par["rs"]["elements"] > 0
+    assert line["value_kind"] == "bus" and line["busbw_block"]["ag_GBps"] > 0
+    assert line["alpha_beta"]["source"].startswith("measured") and len(line["alpha_beta"]["rows"]) == 10
+    assert len(line["exposure"]["variants"]) == 3
+    for v in line["exposure"]["variants"].values():
+        assert v["step_ms"] > 0 and v["compute_only_ms"] > 0
 
 
 @pytest.mark.parametrize("collective", ["nccl", "p2p"])
@@ -72,9 +83,12 @@ def test_bench_distributed_path_world1(collective):
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 1 and line["config"]["layout_world"] == 1 and line["value"] > 0
+    assert line["value_kind"] == "hbm"       # world 1: no bus
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+    assert line["parity"]["ok"], line["parity"]
     if collective == "nccl":
-        assert line["collectives"]["ag_ms_per_step"] > 0 and line["busbw_GBps"] is not None
+        assert line["collectives"]["ag_ms_per_step"] > 0
+        assert line["nccl_info"] is not None and any("NCCL" in x for x in line["nccl_info"]["lines"])
     else:
         assert line["p2p_wait_timeouts"] == 0
 

@@ -22,13 +22,22 @@ run() {  # run <n> <tag> <bench args...>
   echo "N=$n $tag rc=$? $(tail -c 200 $O/bench_${tag}_N$n.json)"
   PORT=$((PORT + 1))
 }
+# correctness first: NCCL / K8-K9 / K10 NVLS parity on real peers (N = min(devices, 8))
+timeout 3600 python -m pytest tests/test_gpu_multi.py -q -rs > $O/pytest_multi.log 2>&1
+echo "pytest multi rc=$? $(tail -n 3 $O/pytest_multi.log)"
 for n in 2 4 8; do
   [ $n -le $MAX ] || continue
+  # the north-star comparison (BASELINE configs[2]); the default line already
+  # carries parity, busbw_block, alpha_beta and the measured exposure variants
   run $n flat
+  run $n p2p --collective p2p
+  run $n vanilla --plan per_param --no-reorder --tokens 1024 --quick      # the unbucketed, unreordered baseline
+  run $n perblock_T1024 --plan manual --tokens 1024 --quick               # + bucket & reorder (manual wrap)
+  run $n greedy_T1024 --plan greedy --tokens 1024 --quick                 # auto-wrap (assumed links; the default
+                                                                          # line's `exposure` plans with fitted ones)
   run $n grouped --ag grouped
   run $n reglocal --nccl-register local
   run $n regsym --nccl-register symmetric
-  run $n p2p --collective p2p
   run $n p2p_fullgrid --collective p2p --p2p-max-ctas 0      # grid cap off (full GPU) vs the default cap
   run $n search --plan search                               # fsdp_plan_search (beyond Algorithm 1)
   run $n search_p2p --plan search --collective p2p
