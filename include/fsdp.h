@@ -613,6 +613,14 @@ typedef struct fsdp_gemm_compute {
  *     WAIT_RS j with a communicator), the d2h stream copies its gradient-shard
  *     segment (rs_seg bytes) to bwd_host_grads[j]; the step's last
  *     compute-stream work waits for every such copy.
+ * The H2D copies (which overwrite the shard storage) are ordered after the
+ * previous fsdp_run_schedule step's last reader of that storage -- its last
+ * UNPACK on the compute stream -- not after its end, so they overlap the
+ * previous step's gradient D2H tail (PCIe is full duplex).  For the first
+ * step on a ctx, after a captured or peer-memory step, and after a step with
+ * no UNPACK, they wait for everything enqueued on `compute` instead.  Work the
+ * caller enqueues between steps that reads the shard storage must be ordered
+ * by the caller (e.g. run it before the previous step).
  * Forward buckets need FSDP_BUCKET_SEGMENT_SHARDS and backward buckets
  * FSDP_BUCKET_SEGMENT_GRAD_SHARDS; host memory should be pinned; NULL entries
  * are skipped; h2d / d2h NULL = library-owned streams. */

@@ -363,6 +363,7 @@ fsdp_status fsdp_ctx_destroy(fsdp_ctx* c) {
   cudaSetDevice(c->device);
   for (cudaEvent_t ev : c->timing_events) cudaEventDestroy(ev);
   for (cudaEvent_t ev : c->io_events) cudaEventDestroy(ev);
+  if (c->ev_shards_released) cudaEventDestroy(c->ev_shards_released);
   if (c->gemm_cache) gemm_cache_destroy(c->gemm_cache);
   if (c->own_comm_stream) cudaStreamDestroy(c->own_comm_stream);
   if (c->own_h2d) cudaStreamDestroy(c->own_h2d);

@@ -214,6 +214,11 @@ struct fsdp_ctx {
   std::vector<cudaEvent_t> timing_events;  // pool for FSDP_SCHED_TIMING
   std::vector<cudaEvent_t> io_events;      // pool for host I/O ordering (fsdp_host_io)
   cudaStream_t own_h2d = nullptr, own_d2h = nullptr;
+  // recorded on the compute stream after the last reader of the shard storage
+  // in a scheduled step (its last UNPACK); the next step's host-I/O H2D waits
+  // on it instead of on the whole previous step (fsdp_host_io)
+  cudaEvent_t ev_shards_released = nullptr;
+  bool shards_released_valid = false;
   void* gemm_cache = nullptr;              // cuBLASLt handle + plans (gemm.cc)
   const fsdp_comm_emulation* emul = nullptr;  // set by fsdp_run_schedule for the call (emulated collectives)
   // NCCL registrations (ncclmem.cc): base pointer -> local handle / window

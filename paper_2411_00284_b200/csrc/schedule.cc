@@ -335,9 +335,17 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
       ctx->io_events.push_back(e);
     }
     iev = ctx->io_events.data();
-    // the previous step's readers of the shard storage are ordered before this point
-    FSDP_CUDA_TRY(cudaEventRecord(iev[0], cs));
-    FSDP_CUDA_TRY(cudaStreamWaitEvent(h2d, iev[0], 0));
+    // the previous step's readers of the shard storage are ordered before the
+    // H2D that overwrites it: after that step's last UNPACK (so this step's
+    // loads overlap the previous step's gradient D2H, PCIe being full duplex),
+    // else -- first step, peer-memory mode (peers read the storage until their
+    // step ends), after a captured step -- after everything enqueued on compute
+    if (!pp && ctx->shards_released_valid) {
+      FSDP_CUDA_TRY(cudaStreamWaitEvent(h2d, ctx->ev_shards_released, 0));
+    } else {
+      FSDP_CUDA_TRY(cudaEventRecord(iev[0], cs));
+      FSDP_CUDA_TRY(cudaStreamWaitEvent(h2d, iev[0], 0));
+    }
     for (int32_t k = 0; k < s->n_fwd; ++k) {
       if (!io->fwd_host_shards || !io->fwd_host_shards[k]) continue;
       FSDP_CUDA_TRY(cudaMemcpyAsync(s->fwd[k]->shard_seg, io->fwd_host_shards[k], static_cast<size_t>(s->fwd[k]->ag_seg),
@@ -348,6 +356,24 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   auto io_before = [&](const Op& o) -> fsdp_status {
     if (io && o.op == FSDP_OP_PACK_AG && o.phase == 0 && io->fwd_host_shards && io->fwd_host_shards[o.bucket])
       FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, iev[1 + o.bucket], 0));
+    return FSDP_OK;
+  };
+  // the step's last reader of the shard storage: its last UNPACK (after its
+  // WAIT_AG, hence after every all-gather that sent from the storage)
+  int64_t last_unpack = -1;
+  for (size_t i = 0; i < seq.size(); ++i)
+    if (seq[i].op == FSDP_OP_UNPACK) last_unpack = static_cast<int64_t>(i);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  FSDP_CUDA_TRY(cudaStreamIsCapturing(cs, &cap));
+  const bool track_release = !pp && cap == cudaStreamCaptureStatusNone;
+  ctx->shards_released_valid = false;
+  if (track_release && !ctx->ev_shards_released)
+    FSDP_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_shards_released, cudaEventDisableTiming));
+  auto mark_release = [&](size_t i) -> fsdp_status {
+    if (track_release && static_cast<int64_t>(i) == last_unpack) {
+      FSDP_CUDA_TRY(cudaEventRecord(ctx->ev_shards_released, cs));
+      ctx->shards_released_valid = true;
+    }
     return FSDP_OK;
   };
   auto io_after = [&](const Op& o) -> fsdp_status {
@@ -496,6 +522,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     }
     if (timing && !skipped) FSDP_CUDA_TRY(cudaEventRecord(ev[3 + 2 * i], on));
     FSDP_TRY(io_after(o));
+    FSDP_TRY(mark_release(i));
   }
   if (io && s->n_bwd > 0) {
     // the step ends when its gradient shards are on the host

@@ -161,6 +161,49 @@ def test_host_io_step():
     del toy_mlp
 
 
+def test_host_io_next_step_loads_after_last_reader():
+    """Two host-I/O steps back to back with different host shards: the second
+    step's H2D (which overlaps the first step's gradient D2H) must not land
+    before the first step's last reader of the shard storage -- the first
+    step's backward re-gathers see the first host buffer, the second step's
+    the second."""
+    world = 2
+    specs = llama("8b", n_layers=2)
+    ctx = F.Ctx(world, 0)
+    fplan, bplan = H.plans_for(specs, world, L.PLAN_MANUAL)
+    st = H.RankState(specs, world, 0, fplan, bplan, ctx, seed=6)
+    dev0 = st.shard_buf.cpu()
+    gaps = torch.ones(st.shard_buf.numel(), dtype=torch.bool)
+    for j, o in enumerate(st.shard_offs):
+        gaps[o:o + st.shard_numel[j] * 2] = False
+    hosts = []
+    for seed in (11, 12):
+        h = torch.randint(0, 256, (st.shard_buf.numel(),), dtype=torch.uint8,
+                          generator=torch.Generator().manual_seed(seed))
+        h[gaps] = dev0[gaps]
+        hosts.append(h.pin_memory())
+    h_gs = torch.zeros(st.gshard_buf.numel(), dtype=torch.uint8).pin_memory()
+    cs, ms = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+    flags = L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT
+    st.step(flags, cs.cuda_stream, ms.cuda_stream, io=st.host_io(hosts[1], h_gs))   # a released event exists
+    snaps = []
+    for h in hosts:
+        st.step(flags, cs.cuda_stream, ms.cuda_stream, io=st.host_io(h, h_gs))
+        with torch.cuda.stream(cs):     # stream-ordered after this step, before the next one
+            snaps.append([t.clone() for t in st.full_slots])
+    cs.synchronize()
+    # the last two backward buckets' gathered parameters: this rank's rows come
+    # from the shards the step loaded
+    for h, snap in zip(hosts, snaps):
+        for b in st.bwd[-2:]:
+            slot = snap[b.full_slot]
+            for j, foff in zip(b.members, b.full_offs):
+                sp = st.specs[j]
+                c = -(-sp.dim0 // world)
+                n = min(c, sp.dim0) * sp.row_numel * 2
+                assert torch.equal(slot[foff:foff + n].cpu(), h[st.shard_offs[j]:st.shard_offs[j] + n])
+
+
 @pytest.mark.parametrize("graph", [False, True])
 def test_llama8b_bench_step_sampled_parity(graph):
     """graph=True: the step as bench.py times it -- captured once into a CUDA
