@@ -511,14 +511,16 @@ def fused_leg(args):
             "how": "bench.py --collective p2p (same workload, own process; the 7 peers simulated in local HBM)"}
 
 
-def kernel_table(st, ctx, names, kbytes, klaunch, op_ns, steps, cs_stream, peak):
+def kernel_table(st, ctx, names, kbytes, klaunch, op_ns, steps, cs_stream, peak, p2p=False):
     """Per data kernel: (a) in-step, event-timed -- an event pair around every
     launch in the profiled steps (FSDP_SCHED_TIMING), which also counts each
     launch's event / launch latency (~8 us per launch, tools/
     launch_overhead_probe.py); (b) back to back -- this step's launches of
     that kernel alone (fsdp_bucket_launch_kernel, same tables, staging slots
     and order), captured into one CUDA graph, timed with CUDA events around
-    three replays on the launching stream."""
+    three replays on the launching stream.  Peer-memory path: (a) covers the RS op,
+    i.e. K9 with the epoch wait / signal kernels around it; (b) K8 / K9 alone
+    (fsdp_p2p_*_bucket, same tables and peer rows)."""
     import torch
     import paper_2411_00284_b200 as F
     from paper_2411_00284_b200 import _lib as L
@@ -531,7 +533,14 @@ def kernel_table(st, ctx, names, kbytes, klaunch, op_ns, steps, cs_stream, peak)
                "ms_per_step_in_step_event": round(op_ns[op] / steps / 1e6, 3),
                "launches_per_step": klaunch[op], "bytes_per_step": kbytes[op]}
         seq = []
-        if op in (L.OP_PACK_AG, L.OP_UNPACK):
+        if p2p:
+            # K8 / K9 alone (fsdp_p2p_*_bucket: the same tables and peer rows as
+            # the step, without its epoch wait / signal kernels)
+            if op == L.OP_AG:
+                seq = [("ag", bk, st.ag_peers[i]) for i, bk in enumerate(st.fwd + st.bwd)]
+            else:
+                seq = [("rs", bk, st.rs_peers[i]) for i, bk in enumerate(st.bwd)]
+        elif op in (L.OP_PACK_AG, L.OP_UNPACK):
             seq = [(bk, st.ag_st[b % 2]) for bs in (st.fwd, st.bwd) for b, bk in enumerate(bs)]
         elif op in (L.OP_PACK_RS, L.OP_COPYOUT_RS):
             seq = [(bk, st.rs_st[b % 2]) for b, bk in enumerate(st.bwd)]
@@ -540,8 +549,15 @@ def kernel_table(st, ctx, names, kbytes, klaunch, op_ns, steps, cs_stream, peak)
             g = torch.cuda.CUDAGraph()
             n = 0
             with torch.cuda.graph(g, stream=s):
-                for bk, stg in seq:
-                    n += F.bucket_launch_kernel(ctx, bk, op, stg.data_ptr(), s.cuda_stream)
+                for item in seq:
+                    if p2p:
+                        kind, bk, peers = item
+                        (F.p2p_allgather_bucket if kind == "ag" else F.p2p_reduce_scatter_bucket)(
+                            ctx, bk, peers, s.cuda_stream)
+                        n += 1
+                    else:
+                        bk, stg = item
+                        n += F.bucket_launch_kernel(ctx, bk, op, stg.data_ptr(), s.cuda_stream)
             with torch.cuda.stream(s):
                 g.replay()
             s.synchronize()
@@ -785,10 +801,9 @@ def main(argv=None):
     live = [op for op in kbytes if kbytes[op] > 0 and op_ns.get(op, 0) > 0]
     dom = max(live, key=lambda op: op_ns[op])
     achieved = kbytes[dom] * args.steps / (op_ns[dom] * 1e-9) / 1e9
-    per_kernel = (kernel_table(st, ctx, names, kbytes, klaunch, op_ns, args.steps, cs, peak) if not p2p else
-                  {names[op]: {"GB/s_in_step_event": round(kbytes[op] * args.steps / (op_ns[op] * 1e-9) / 1e9, 1),
-                               "ms_per_step_in_step_event": round(op_ns[op] / args.steps / 1e6, 3),
-                               "launches_per_step": klaunch[op], "bytes_per_step": kbytes[op]} for op in live})
+    barrier()
+    per_kernel = kernel_table(st, ctx, names, kbytes, klaunch, op_ns, args.steps, cs, peak, p2p=p2p)
+    barrier()
     launches = sum(r["kernel_launches"] for r in reports)
     coll_ms = None
     busbw_step = None

@@ -79,9 +79,11 @@ class RankState:
         self.param_dtype = param_dtype
         ep = 2 if param_dtype == L.BF16 else 4
         self.ep = ep
-        P = len(specs)
-        c = [-(-p.dim0 // world) for p in specs]
-        self.shard_numel = [c[j] * specs[j].row_numel for j in range(P)]
+        # shard rows / valid rows from the library (fsdp_shard metadata, G1)
+        info = [F.shard(world, rank, d, param_dtype) for d in self.descs]
+        c = [x["shard_rows"] for x in info]
+        self.valid_rows = [x["valid_rows"] for x in info]
+        self.shard_numel = [x["shard_numel"] for x in info]
         self.full_numel = [p.dim0 * p.row_numel for p in specs]
         if segment_storage:
             # shards stored in the forward plan's AG segment layout, gradient
@@ -111,7 +113,7 @@ class RankState:
                 self._fill_normal(t, 1e-3, g, L.BF16)
             # shard padding rows hold +0 (fsdp_shard contract)
             for j, p in enumerate(specs):
-                v = max(0, min(p.dim0 - rank * c[j], c[j]))
+                v = self.valid_rows[j]
                 if v < c[j]:
                     o = self.shard_offs[j] + v * p.row_numel * ep
                     self.shard_buf[o:self.shard_offs[j] + self.shard_numel[j] * ep].zero_()
