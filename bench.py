@@ -590,11 +590,13 @@ def main(argv=None):
     multi = args.gpus > 1 or args.dist
     p2p = args.collective == "p2p"
     quick = args.quick
-    if multi and not p2p and os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("", "VERSION", "WARN"):
+    if multi and not p2p:
         # the communicator's own account (version, channels, NVLS, tuning), one file per rank
-        os.environ["NCCL_DEBUG"] = "INFO"
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS,TUNING,ENV")
-        os.environ["NCCL_DEBUG_FILE"] = nccl_log_path(rank)
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("", "VERSION", "WARN"):
+            os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS,TUNING,ENV")
+        if "NCCL_DEBUG_FILE" not in os.environ:
+            os.environ["NCCL_DEBUG_FILE"] = nccl_log_path(rank)
 
     import numpy as np
     import torch

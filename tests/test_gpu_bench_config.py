@@ -233,6 +233,14 @@ def test_llama8b_bench_step_sampled_parity(graph):
     assert rep["kernel_launches"] == 4 * 35, rep["kernel_launches"]
     assert rep["log_len"] == 5 * 35 + 9 * 35, rep["log_len"]
 
+    _sampled_step_checks(st, specs, world)
+
+
+def _sampled_step_checks(st, specs, world):
+    """Rank 0 of a layout-only `world`-way job after one step: every gradient
+    shard = this rank's chunk of its full gradient widened x fl32(1/N) (no
+    other contributor; sampled elements, oracle O1 widen / O5 scale); the last
+    two backward buckets' gathered parameters hold this rank's shard rows."""
     inv = inv_world_f32(world)
     rng = np.random.Generator(np.random.Philox(5))
     gs_u8 = st.gshard_buf
@@ -262,3 +270,28 @@ def test_llama8b_bench_step_sampled_parity(graph):
                 # direct-gather bucket (emb / output / final norm) has no staging:
                 # without a collective its peer rows are simply not written
                 assert int(torch.count_nonzero(full[2 * n:])) == 0, specs[j].name
+
+
+@pytest.mark.parametrize("cfg", ["70b_sizecap500MB", "405b_layer"])
+def test_large_config_step_sampled_parity(cfg):
+    """BASELINE configs[3] (Llama-3-70B shards at N = 8, a 500 MB size-cap
+    plan: 17.6 GB of bf16 shards on this rank) and configs[4] (one Llama-3-405B
+    layer as one 6.4 GB bucket, N = 8), one reordered step on rank 0 of a
+    layout-only job, checked like the 8B bench step on sampled elements."""
+    world = 8
+    if cfg.startswith("70b"):
+        specs = llama("70b")
+        fplan, bplan = H.plans_for(specs, world, L.PLAN_SIZE_CAP, mem_max=500 * 10 ** 6)
+    else:
+        specs = llama("405b", n_layers=1)
+        fplan, bplan = H.plans_for(specs, world, L.PLAN_MANUAL)
+    ctx = F.Ctx(world, 0)
+    st = H.RankState(specs, world, 0, fplan, bplan, ctx, seed=78)
+    st.gshard_buf.fill_(0xAB)
+    cs, ms = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+    st.step(L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT, cs.cuda_stream, ms.cuda_stream)
+    torch.cuda.synchronize()
+    _sampled_step_checks(st, specs, world)
+    del st
+    torch.cuda.empty_cache()
+    ctx.close()

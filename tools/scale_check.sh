@@ -44,6 +44,13 @@ for n in 2 4 8; do
   run $n keeplast --keep-last                               # G42: no re-gather of the boundary bucket
   run $n gemm_p2p_search --compute gemm --collective p2p --plan search   # real GEMMs between the collectives
   run $n nccl_maxctas16 --nccl-max-ctas 16                  # NCCL's SM footprint bounded
+  # BASELINE configs[3]: Llama-3-70B shards, bucket-size sweep 25-500 MB (size cap on the gathered bytes, G30)
+  for cap in 25e6 50e6 100e6 200e6 500e6; do
+    run $n 70b_cap$cap --model 70b --plan size_cap --mem-limit $cap --quick --no-e2e
+  done
+  # BASELINE configs[4]: one Llama-3-405B layer (d 16384, FFN 53248), per-param and one whole-layer bucket
+  run $n 405b_layer --model 405b --layers 1 --quick --no-e2e
+  run $n 405b_layer_pp --model 405b --layers 1 --plan per_param --quick --no-e2e
   for c in nccl p2p; do
     timeout 1800 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
       --master-port $PORT tools/busbw_sweep.py --collective $c --out $O/busbw_${c}_N$n.json > $O/busbw_${c}_N$n.log 2>&1
