@@ -598,7 +598,6 @@ def main(argv=None):
         if "NCCL_DEBUG_FILE" not in os.environ:
             os.environ["NCCL_DEBUG_FILE"] = nccl_log_path(rank)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
