@@ -1008,7 +1008,7 @@ def main(argv=None):
             "dtype": "bf16", "data": "synthetic (seeded N(0, 0.02) bf16 params, N(0, 1e-3) bf16 grads)",
             "config": {
                 "workload": workload,
-                "model": "llama3-8b shapes (Table 2; vocab 128256, 8 KV heads)", "layout_world": world,
+                "shapes": "llama3-%s (Table 2; vocab 128256, 8 KV heads)" % args.model, "layout_world": world,
                 "collective": ("NCCL all-gather / reduce-scatter with copy kernels" if not p2p else
                                "fused peer-memory kernels K8/K9"),
                 "buckets_fwd": n_fwd, "buckets_bwd": n_bwd, "param_dtype": "bf16", "reduce_dtype": "fp32",
