@@ -989,8 +989,8 @@ def main(argv=None):
     if rank == 0 and not multi and not p2p and not args.no_fused_leg and not quick and args.compute == "proxy":
         fused = fused_leg(args)
 
-    workload = "llama3-8b FSDP rank step, %s plan, %s, %s" % (
-        "file:" + os.path.basename(args.plan_file) if args.plan_file else args.plan,
+    workload = "llama3-%s FSDP rank step, %s plan, %s, %s" % (
+        args.model, "file:" + os.path.basename(args.plan_file) if args.plan_file else args.plan,
         "reorder fwd-%s/bwd-%s" % (args.fwd_placement, args.bwd_placement) if not args.no_reorder else "vanilla order",
         "compute: none (the communication path alone)" if not tokens and args.compute == "proxy"
         else "compute: %s at %d tokens/GPU" % (args.compute, tokens or 1024))
