@@ -31,11 +31,9 @@ def main():
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
 
-    import numpy as np
     import torch
     import torch.distributed as dist
     import paper_2411_00284_b200 as F
-    from paper_2411_00284_b200 import _lib as L
     from paper_2411_00284_b200 import harness as H
     from workloads.shapes import ParamSpec
 
@@ -66,51 +64,24 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def exchange(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
     for n in sorted(set(sizes)):
         d = max(world, (n // (2 * R)) // world * world)
-        spec = [ParamSpec("x", d, R, 0)]
-        plan = [[0]]
-        st = H.RankState(spec, world, rank, plan, plan, ctx, ipc=p2p and world > 1)
-        if p2p:
-            if world > 1:
-                def exchange(obj):
-                    out = [None] * world
-                    dist.all_gather_object(out, obj)
-                    return out
-                st.setup_p2p_ipc(exchange)
-            else:
-                st.setup_p2p_simulated()
-        flags = L.SCHED_REORDER | L.SCHED_TIMING | (L.SCHED_P2P if p2p else 0)
-        ag, rs = [], []
-        for i in range(args.reps + 2):
-            rep = st.step(flags, cs.cuda_stream, ms.cuda_stream, want_log=True)
-            if i < 2:
-                continue
-            ag += [e[4] for e in rep["log"] if e[1] == L.OP_AG]
-            rs += [e[4] for e in rep["log"] if e[1] == L.OP_RS]
-        full_ag = world * st.fwd[0].ag_seg
-        full_rs = world * st.bwd[0].rs_seg
-        t_ag = max_over_ranks(float(np.median(ag)))
-        t_rs = max_over_ranks(float(np.median(rs)))
-        rows.append(dict(ag_bytes=full_ag, rs_bytes=full_rs, ag_ns=t_ag, rs_ns=t_rs,
-                         ag_busbw=(world - 1) / world * full_ag / t_ag if world > 1 else None,
-                         rs_busbw=(world - 1) / world * full_rs / t_rs if world > 1 else None,
-                         ag_algbw=full_ag / t_ag, rs_algbw=full_rs / t_rs))
-        if p2p:
-            st.close_ipc()
-        del st
-        torch.cuda.empty_cache()
-
-    def fit(key_b, key_t):
-        small = min(rows, key=lambda r: r[key_b])
-        big = [r for r in rows if r[key_b] >= 64 * 2 ** 20]
-        x = np.array([r[key_b] for r in big], dtype=np.float64)
-        y = np.array([r[key_t] for r in big], dtype=np.float64)
-        beta = float(np.polyfit(x, y, 1)[0]) if len(big) >= 2 else 0.0
-        return dict(alpha_ns=int(round(small[key_t])), beta_fs_per_byte=int(round(beta * 1e6)))
+        r = H.time_bucket_collectives([ParamSpec("x", d, R, 0)], world, rank, ctx, cs.cuda_stream, ms.cuda_stream,
+                                      reps=args.reps, warmup=2, p2p=p2p, exchange=exchange,
+                                      max_over_ranks=max_over_ranks)
+        r.update(ag_busbw=(world - 1) / world * r["ag_bytes"] / r["ag_ns"] if world > 1 else None,
+                 rs_busbw=(world - 1) / world * r["rs_bytes"] / r["rs_ns"] if world > 1 else None,
+                 ag_algbw=r["ag_bytes"] / r["ag_ns"], rs_algbw=r["rs_bytes"] / r["rs_ns"])
+        rows.append(r)
 
     res = dict(world=world, collective=args.collective, rows=rows,
-               fit=dict(ag=fit("ag_bytes", "ag_ns"), rs=fit("rs_bytes", "rs_ns")))
+               fit={op: dict(zip(("alpha_ns", "beta_fs_per_byte"), H.fit_link(rows, op + "_bytes", op + "_ns")))
+                    for op in ("ag", "rs")})
     if rank == 0:
         print(json.dumps(res), flush=True)
         if args.out:
