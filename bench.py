@@ -72,6 +72,8 @@ def parse(argv=None):
     ap.add_argument("--no-reorder", action="store_true")
     ap.add_argument("--grad-slots", type=int, default=2)
     ap.add_argument("--keep-last", action="store_true", help="G42 (beyond the paper): no re-gather of the boundary bucket")
+    ap.add_argument("--copy-stream", action="store_true",
+                    help="FSDP_SCHED_COPY_STREAM: pack / copy-out kernels on a third stream (NCCL path)")
     ap.add_argument("--fwd-placement", default="before", choices=["before", "after"])
     ap.add_argument("--bwd-placement", default="after", choices=["before", "after"])
     ap.add_argument("--mem-limit", type=float, default=2e9)
@@ -686,6 +688,8 @@ def main(argv=None):
         flags |= L.SCHED_BWD_AG_BEFORE_WAIT
     if args.keep_last:
         flags |= L.SCHED_KEEP_LAST_GATHERED
+    if args.copy_stream and not p2p:
+        flags |= L.SCHED_COPY_STREAM
 
     gemm = model = None
     if args.compute == "llama":

@@ -466,8 +466,25 @@ enum {
   FSDP_SCHED_DRY_RUN = 16u,
   FSDP_SCHED_TIMING = 32u,
   FSDP_SCHED_P2P = 64u,
-  FSDP_SCHED_KEEP_LAST_GATHERED = 128u
+  FSDP_SCHED_KEEP_LAST_GATHERED = 128u,
+  FSDP_SCHED_COPY_STREAM = 256u
 };
+/* FSDP_SCHED_COPY_STREAM (beyond the paper's single compute stream):
+ * the pack and copy-out kernels (K1, K3, K4, K6) run on a third, library-
+ * owned, highest-priority stream instead of `compute`, so that they overlap
+ * the compute of neighbouring buckets rather than sit between them -- the
+ * copy-in / copy-out cost the paper blames for bucketing's single-node
+ * regression.  Same op sequence, same kernels, same bytes; the data
+ * dependencies are kept with events: COMPUTE k waits for UNPACK k; PACK_RS j
+ * waits for COMPUTE_B j; an UNPACK (and the all-gather of a direct-gather /
+ * grouped bucket, which writes the full parameters itself) waits for the last
+ * earlier COMPUTE whose bucket's full-parameter memory overlaps it; a
+ * COMPUTE_B waits for the last earlier PACK_RS whose bucket's full-gradient
+ * memory overlaps it (overlaps are found from the bound pointers, so any slot
+ * layout is safe; adjacent buckets in distinct slots are what lets the copies
+ * overlap); the step ends on `compute` after the copy stream's last op.  Log
+ * entries of the copy ops carry stream 2.  Not with FSDP_SCHED_P2P (its
+ * collectives are the copies). */
 /* FSDP_SCHED_KEEP_LAST_GATHERED (reading G42; FSDP2's reshard-after-forward
  * off for the boundary module, which the paper does not describe -- P:137
  * re-gathers every parameter): the first backward bucket reuses the full

@@ -32,6 +32,7 @@ N_OPS = 10
 SCHED_REORDER, SCHED_FWD_AG_BEFORE_WAIT, SCHED_BWD_AG_BEFORE_WAIT = 1, 2, 4
 SCHED_NO_COMM, SCHED_DRY_RUN, SCHED_TIMING, SCHED_P2P = 8, 16, 32, 64
 SCHED_KEEP_LAST_GATHERED = 128
+SCHED_COPY_STREAM = 256
 BUCKET_SEGMENT_SHARDS, BUCKET_SEGMENT_GRAD_SHARDS, BUCKET_FP32_MASTER, BUCKET_GROUPED_AG = 1, 2, 4, 8
 BUCKET_BF16_GRAD_SHARDS = 16
 REG_LOCAL, REG_SYMMETRIC = 0, 1

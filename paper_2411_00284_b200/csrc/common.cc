@@ -366,6 +366,8 @@ fsdp_status fsdp_ctx_destroy(fsdp_ctx* c) {
   if (c->ev_shards_released) cudaEventDestroy(c->ev_shards_released);
   if (c->gemm_cache) gemm_cache_destroy(c->gemm_cache);
   if (c->own_comm_stream) cudaStreamDestroy(c->own_comm_stream);
+  if (c->own_copy_stream) cudaStreamDestroy(c->own_copy_stream);
+  for (cudaEvent_t ev : c->copy_events) cudaEventDestroy(ev);
   if (c->own_h2d) cudaStreamDestroy(c->own_h2d);
   if (c->own_d2h) cudaStreamDestroy(c->own_d2h);
   if (c->sink) cudaFree(c->sink);

@@ -207,6 +207,10 @@ struct fsdp_ctx {
   ncclComm_t comm = nullptr;
   bool owns_comm = false;
   cudaStream_t own_comm_stream = nullptr;
+  // FSDP_SCHED_COPY_STREAM: the pack / copy-out kernels' stream and the
+  // per-call cross-stream events (unpacked / computed / grads packed per bucket)
+  cudaStream_t own_copy_stream = nullptr;
+  std::vector<cudaEvent_t> copy_events;
   int sm_count = 148;
   int max_ctas = 148 * 8;
   float* sink = nullptr;

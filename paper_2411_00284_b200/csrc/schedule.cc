@@ -4,6 +4,8 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <utility>
 #include <vector>
 
 #include "internal.h"
@@ -17,6 +19,30 @@ struct Op {
 };
 
 bool is_comm(int32_t op) { return op == FSDP_OP_AG || op == FSDP_OP_RS; }
+// ops that run on the copy stream with FSDP_SCHED_COPY_STREAM (the waits too:
+// the copy-out after them is what consumes the collective's result)
+bool is_copy_side(int32_t op) {
+  return op == FSDP_OP_PACK_AG || op == FSDP_OP_WAIT_AG || op == FSDP_OP_UNPACK || op == FSDP_OP_PACK_RS ||
+         op == FSDP_OP_WAIT_RS || op == FSDP_OP_COPYOUT_RS;
+}
+// [lo, hi) of the memory a bucket's full parameters (grads = false) or full
+// gradients (grads = true) occupy
+std::pair<uintptr_t, uintptr_t> full_range(const fsdp_bucket* b, bool grads) {
+  uintptr_t lo = UINTPTR_MAX, hi = 0;
+  const std::vector<void*>& ptrs = grads ? b->grads : b->fulls;
+  for (size_t j = 0; j < ptrs.size() && j < b->members.size(); ++j) {
+    if (!ptrs[j]) continue;
+    const uintptr_t p = reinterpret_cast<uintptr_t>(ptrs[j]);
+    const uintptr_t n = static_cast<uintptr_t>(b->members[j].dim0 * b->members[j].row_numel *
+                                               (grads ? b->grad_bytes : b->param_bytes));
+    lo = std::min(lo, p);
+    hi = std::max(hi, p + n);
+  }
+  return {lo, hi};
+}
+bool overlaps(std::pair<uintptr_t, uintptr_t> a, std::pair<uintptr_t, uintptr_t> b) {
+  return a.first < b.second && b.first < a.second;
+}
 
 // NVTX range names (host-side enqueue ranges; visible in nsys / ncu --nvtx).
 const char* const kOpNames[FSDP_N_OPS] = {"fsdp:PACK_AG", "fsdp:AG",        "fsdp:WAIT_AG", "fsdp:UNPACK",
@@ -126,8 +152,11 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   if (!s) return fail(FSDP_ERR_INVALID_ARG, "NULL schedule");
   const uint32_t known = FSDP_SCHED_REORDER | FSDP_SCHED_FWD_AG_BEFORE_WAIT | FSDP_SCHED_BWD_AG_BEFORE_WAIT |
                          FSDP_SCHED_NO_COMM | FSDP_SCHED_DRY_RUN | FSDP_SCHED_TIMING | FSDP_SCHED_P2P |
-                         FSDP_SCHED_KEEP_LAST_GATHERED;
+                         FSDP_SCHED_KEEP_LAST_GATHERED | FSDP_SCHED_COPY_STREAM;
   if (s->flags & ~known) return fail(FSDP_ERR_INVALID_ARG, "unknown schedule flag");
+  const bool copy_stream = s->flags & FSDP_SCHED_COPY_STREAM;
+  if (copy_stream && (s->flags & FSDP_SCHED_P2P))
+    return fail(FSDP_ERR_INVALID_ARG, "FSDP_SCHED_COPY_STREAM is not for FSDP_SCHED_P2P");
   if (s->n_fwd < 0 || s->n_bwd < 0) return fail(FSDP_ERR_INVALID_ARG, "negative bucket count");
   const bool p2p = s->flags & FSDP_SCHED_P2P;
   const bool dry = s->flags & FSDP_SCHED_DRY_RUN;
@@ -161,7 +190,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
         e.phase = seq[i].phase;
         e.op = seq[i].op;
         e.bucket = seq[i].bucket;
-        e.stream = is_comm(seq[i].op) ? 1 : 0;
+        e.stream = is_comm(seq[i].op) ? 1 : (copy_stream && is_copy_side(seq[i].op)) ? 2 : 0;
       }
     }
   }
@@ -313,6 +342,54 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     for (int32_t q = 0; q < ctx->world; ++q) t.p[q] = static_cast<const char*>(rows[row * ctx->world + q]);
     return t;
   };
+  // ---- FSDP_SCHED_COPY_STREAM: pack / copy-out kernels on a third stream
+  // (xs); events per bucket position p (forward k -> k, backward j -> n_fwd + j):
+  // [3p] unpacked (xs), [3p + 1] computed (cs), [3p + 2] grads packed (xs);
+  // [3P] the copy stream's end of step
+  cudaStream_t xs = cs;
+  cudaEvent_t* xev = nullptr;
+  const int32_t P = s->n_fwd + s->n_bwd;
+  if (copy_stream) {
+    if (!ctx->own_copy_stream) {
+      int lo = 0, hi = 0;
+      FSDP_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      FSDP_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->own_copy_stream, cudaStreamNonBlocking, hi));
+    }
+    xs = ctx->own_copy_stream;
+    while (ctx->copy_events.size() < static_cast<size_t>(3 * P + 2)) {
+      cudaEvent_t e;
+      FSDP_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ctx->copy_events.push_back(e);
+    }
+    xev = ctx->copy_events.data();
+    // the copy stream starts where the compute stream stands
+    FSDP_CUDA_TRY(cudaEventRecord(xev[3 * P + 1], cs));
+    FSDP_CUDA_TRY(cudaStreamWaitEvent(xs, xev[3 * P + 1], 0));
+  }
+  auto pos = [&](const Op& o) { return o.phase == 0 ? o.bucket : s->n_fwd + o.bucket; };
+  auto bucket_at = [&](int32_t p) { return p < s->n_fwd ? s->fwd[p] : s->bwd[p - s->n_fwd]; };
+  std::vector<char> computed(copy_stream ? P : 0, 0), grads_packed(copy_stream ? P : 0, 0);
+  // stream `st` waits for the last earlier COMPUTE (grads = false) / PACK_RS
+  // (grads = true) whose bucket's full-parameter / full-gradient memory
+  // overlaps position p's
+  auto wait_last_user = [&](int32_t p, bool grads, cudaStream_t st) -> fsdp_status {
+    const auto mine = full_range(bucket_at(p), grads);
+    for (int32_t q = p - 1; q >= 0; --q) {
+      if (grads && q < s->n_fwd) break;
+      if (!overlaps(mine, full_range(bucket_at(q), grads))) continue;
+      const char done = grads ? grads_packed[q] : computed[q];
+      // an overlapping bucket whose compute is not enqueued yet (the prefetch
+      // of the next bucket into the memory the current one is computing on):
+      // the two-slot contract of the schedule is broken
+      if (!done)
+        return fail(FSDP_ERR_INVALID_ARG,
+                    "FSDP_SCHED_COPY_STREAM: adjacent buckets share full-parameter memory (prefetch needs two slots)");
+      FSDP_CUDA_TRY(cudaStreamWaitEvent(st, xev[3 * q + (grads ? 2 : 1)], 0));
+      break;
+    }
+    return FSDP_OK;
+  };
+
   // ---- host I/O (fsdp_host_io): per-bucket H2D of shards, D2H of gradient shards
   const fsdp_host_io* io = s->io;
   cudaStream_t h2d = nullptr, d2h = nullptr;
@@ -355,7 +432,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   }
   auto io_before = [&](const Op& o) -> fsdp_status {
     if (io && o.op == FSDP_OP_PACK_AG && o.phase == 0 && io->fwd_host_shards && io->fwd_host_shards[o.bucket])
-      FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, iev[1 + o.bucket], 0));
+      FSDP_CUDA_TRY(cudaStreamWaitEvent(xs, iev[1 + o.bucket], 0));
     return FSDP_OK;
   };
   // the step's last reader of the shard storage: its last UNPACK (after its
@@ -371,7 +448,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     FSDP_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_shards_released, cudaEventDisableTiming));
   auto mark_release = [&](size_t i) -> fsdp_status {
     if (track_release && static_cast<int64_t>(i) == last_unpack) {
-      FSDP_CUDA_TRY(cudaEventRecord(ctx->ev_shards_released, cs));
+      FSDP_CUDA_TRY(cudaEventRecord(ctx->ev_shards_released, xs));
       ctx->shards_released_valid = true;
     }
     return FSDP_OK;
@@ -380,7 +457,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     if (io && o.op == FSDP_OP_COPYOUT_RS && io->bwd_host_grads && io->bwd_host_grads[o.bucket]) {
       fsdp_bucket* bb = s->bwd[o.bucket];
       cudaEvent_t e = iev[1 + s->n_fwd + o.bucket];
-      FSDP_CUDA_TRY(cudaEventRecord(e, cs));
+      FSDP_CUDA_TRY(cudaEventRecord(e, xs));
       FSDP_CUDA_TRY(cudaStreamWaitEvent(d2h, e, 0));
       FSDP_CUDA_TRY(cudaMemcpyAsync(io->bwd_host_grads[o.bucket], bb->gshard_seg, static_cast<size_t>(bb->rs_seg),
                                     cudaMemcpyDeviceToHost, d2h));
@@ -497,7 +574,19 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     char* rs_st = static_cast<char*>(s->rs_staging[o.bucket & 1]);
     const bool comm_op = is_comm(o.op);
     const bool skipped = !with_comm && (comm_op || o.op == FSDP_OP_WAIT_AG || o.op == FSDP_OP_WAIT_RS);
-    cudaStream_t on = comm_op ? ms : cs;
+    const int32_t p = pos(o);
+    cudaStream_t on = comm_op ? ms : is_copy_side(o.op) ? xs : cs;
+    if (copy_stream) {
+      // cross-stream data dependencies of the copy stream (include/fsdp.h)
+      if (o.op == FSDP_OP_UNPACK || (o.op == FSDP_OP_PACK_AG && (b->ag_direct || b->ag_grouped)))
+        FSDP_TRY(wait_last_user(p, false, xs));                 // full-parameter memory free
+      if (o.op == FSDP_OP_COMPUTE_F || o.op == FSDP_OP_COMPUTE_B) {
+        const bool has_unpack = !(keep_last && o.phase == 1 && o.bucket == 0);
+        if (has_unpack) FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, xev[3 * p], 0));     // unpacked
+        if (o.op == FSDP_OP_COMPUTE_B) FSDP_TRY(wait_last_user(p, true, cs));      // full-gradient memory free
+      }
+      if (o.op == FSDP_OP_PACK_RS) FSDP_CUDA_TRY(cudaStreamWaitEvent(xs, xev[3 * p + 1], 0));  // computed
+    }
     if (timing && !skipped) {
       if (comm_op) {
         // start after the pack this collective depends on
@@ -506,23 +595,39 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
       FSDP_CUDA_TRY(cudaEventRecord(ev[2 + 2 * i], on));
     }
     switch (o.op) {
-      case FSDP_OP_PACK_AG: FSDP_TRY(ag_pack(ctx, b, ag_st, cs, with_comm, &launches)); break;
+      case FSDP_OP_PACK_AG: FSDP_TRY(ag_pack(ctx, b, ag_st, xs, with_comm, &launches)); break;
       case FSDP_OP_AG: FSDP_TRY(ag_collective(ctx, b, ag_st, ms, with_comm, &colls)); break;
-      case FSDP_OP_WAIT_AG: FSDP_TRY(ag_wait(ctx, b, cs, with_comm)); break;
-      case FSDP_OP_UNPACK: FSDP_TRY(ag_unpack(ctx, b, ag_st, cs, &launches)); break;
+      case FSDP_OP_WAIT_AG: FSDP_TRY(ag_wait(ctx, b, xs, with_comm)); break;
+      case FSDP_OP_UNPACK: FSDP_TRY(ag_unpack(ctx, b, ag_st, xs, &launches)); break;
       case FSDP_OP_COMPUTE_F:
       case FSDP_OP_COMPUTE_B: {
         FSDP_TRY(compute(o, b));
         break;
       }
-      case FSDP_OP_PACK_RS: FSDP_TRY(rs_pack(ctx, b, rs_st, cs, with_comm, &launches)); break;
+      case FSDP_OP_PACK_RS: FSDP_TRY(rs_pack(ctx, b, rs_st, xs, with_comm, &launches)); break;
       case FSDP_OP_RS: FSDP_TRY(rs_collective(ctx, b, rs_st, ms, with_comm, &colls)); break;
-      case FSDP_OP_WAIT_RS: FSDP_TRY(rs_wait(ctx, b, cs, with_comm)); break;
-      case FSDP_OP_COPYOUT_RS: FSDP_TRY(rs_copyout(ctx, b, rs_st, cs, with_comm, &launches)); break;
+      case FSDP_OP_WAIT_RS: FSDP_TRY(rs_wait(ctx, b, xs, with_comm)); break;
+      case FSDP_OP_COPYOUT_RS: FSDP_TRY(rs_copyout(ctx, b, rs_st, xs, with_comm, &launches)); break;
+    }
+    if (copy_stream) {
+      if (o.op == FSDP_OP_UNPACK) FSDP_CUDA_TRY(cudaEventRecord(xev[3 * p], xs));
+      if (o.op == FSDP_OP_COMPUTE_F || o.op == FSDP_OP_COMPUTE_B) {
+        FSDP_CUDA_TRY(cudaEventRecord(xev[3 * p + 1], cs));
+        computed[p] = 1;
+      }
+      if (o.op == FSDP_OP_PACK_RS) {
+        FSDP_CUDA_TRY(cudaEventRecord(xev[3 * p + 2], xs));
+        grads_packed[p] = 1;
+      }
     }
     if (timing && !skipped) FSDP_CUDA_TRY(cudaEventRecord(ev[3 + 2 * i], on));
     FSDP_TRY(io_after(o));
     FSDP_TRY(mark_release(i));
+  }
+  if (copy_stream) {
+    // the step ends on the compute stream after the copy stream's last op
+    FSDP_CUDA_TRY(cudaEventRecord(xev[3 * P], xs));
+    FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, xev[3 * P], 0));
   }
   if (io && s->n_bwd > 0) {
     // the step ends when its gradient shards are on the host
