@@ -933,7 +933,7 @@ def main(argv=None):
     torch.cuda.empty_cache()
 
     # ---- N > 1: isolated 8B-block busbw, alpha / beta fit, measured exposure
-    busbw_block = alpha_beta = exposure = None
+    busbw_block = alpha_beta = exposure = nvls_block = None
     if multi and world > 1 and not quick:
         from workloads.shapes import ParamSpec
         kw = dict(p2p=p2p, exchange=exchange, max_over_ranks=max_over_ranks)
@@ -969,6 +969,7 @@ def main(argv=None):
         if args.exposure_tokens:
             exposure = exposure_leg(args, specs, world, my_rank, ctx, cs, ms, compute, p2p, exchange, barrier,
                                     max_over_ranks, alpha_beta)
+        nvls_block = nvls_leg(world, my_rank, ctx, exchange, barrier, max_over_ranks)
     elif not multi:
         alpha_beta = {"ag": {"alpha_ns": args.alpha_ns, "beta_fs_per_byte": args.beta_fs},
                       "rs": {"alpha_ns": args.alpha_ns, "beta_fs_per_byte": args.beta_fs},
@@ -1029,6 +1030,7 @@ def main(argv=None):
                                          if host_enqueue else None),
             "collectives": coll_ms, "busbw_step": busbw_step, "busbw_block": busbw_block,
             "alpha_beta": alpha_beta, "exposure": exposure, "parity": parity, "nccl_info": nccl_info,
+            "nvls_block": nvls_block,
             "kernels": per_kernel,
             "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
@@ -1046,6 +1048,121 @@ def main(argv=None):
     ctx.close()
     if multi:
         dist.destroy_process_group()
+
+
+def nvls_leg(world, rank, ctx, exchange, barrier, max_over_ranks, reps=20):
+    """N > 1: the NVLS reduce-scatter read-out K10 on one Llama-3-8B block
+    bucket: every rank packs its bf16 gradients (K4)
+    into its unicast mapping of one multicast object over the N GPUs; after a
+    barrier K10 reads this rank's segment through the multicast mapping (the
+    NVSwitch sums the N copies) into the fp32 gradient shards.  K10 alone is
+    timed with events (median of `reps`, max over ranks) -> busbw (N-1)/N x the
+    fp32 bucket / t; the result is checked against the oracle on sampled rows
+    (rs_check: G7 bound).  {"unavailable": why} where the platform refuses
+    multicast objects."""
+    import numpy as np
+    import torch
+    import paper_2411_00284_b200 as F
+    from paper_2411_00284_b200 import _lib as L
+    from workloads import llama
+    specs = llama("8b", n_layers=1, with_embeddings=False)
+    descs = [(p.dim0, p.row_numel, 0) for p in specs]
+    g = torch.Generator(device="cuda").manual_seed(500 + rank)
+    grads = [torch.empty(p.dim0 * p.row_numel, dtype=torch.bfloat16, device="cuda").normal_(0, 1e-3, generator=g)
+             for p in specs]
+    gsh = [torch.zeros(-(-p.dim0 // world) * p.row_numel, dtype=torch.float32, device="cuda") for p in specs]
+    b = F.Bucket(ctx, descs, full_grads=[t.data_ptr() for t in grads], grad_shards=[t.data_ptr() for t in gsh],
+                 param_dtype=L.BF16, grad_dtype=L.BF16)
+    m, err = None, None
+
+    def agree(local_err):
+        """Every rank's error (or None) -> the first one, on every rank: the
+        collective steps below stay in lockstep even when one rank fails."""
+        errs = [e for e in exchange(local_err) if e]
+        return errs[0] if errs else None
+
+    try:
+        if rank == 0:
+            m = F.Nvls(ctx, b.rs_seg)
+    except Exception as e:
+        err = "%s: %s" % (type(e).__name__, e)
+    handle = exchange(m.handle if m is not None else None)[0]
+    err = agree(err)
+    if err is None and rank != 0:
+        try:
+            m = F.Nvls(ctx, b.rs_seg, handle=handle)
+        except Exception as e:
+            err = "%s: %s" % (type(e).__name__, e)
+        err = agree(err)
+    elif err is None:
+        err = agree(None)
+    uc = mc = None
+    if err is None:
+        barrier()                      # every GPU added before any binding
+        try:
+            uc, mc, _ = m.bind()
+        except Exception as e:
+            err = "%s: %s" % (type(e).__name__, e)
+        err = agree(err)
+    t = None
+    members = []
+    if err is None:
+        barrier()
+        s = torch.cuda.Stream()
+        try:
+            F.reduce_scatter_bucket(ctx, b, uc, s.cuda_stream, 0, L.ISSUE | L.NO_COLLECTIVE)   # K4 into uc
+            s.synchronize()
+        except Exception as e:
+            err = "%s: %s" % (type(e).__name__, e)
+        err = agree(err)
+    if err is None:
+        barrier()                      # every rank packed
+        try:
+            ts = []
+            for _ in range(reps + 3):
+                a, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                F.nvls_reduce_scatter_bucket(ctx, b, mc, s.cuda_stream)
+                e_.record(s)
+                e_.synchronize()
+                ts.append(a.elapsed_time(e_) * 1e6)
+            t = float(np.median(ts[3:]))
+            for j, p in enumerate(specs):
+                d, R = p.dim0, p.row_numel
+                c = -(-d // world)
+                loc = sample_local_rows(c, 3000 + j)
+                grows = sorted({q * c + t_ for q in range(world) for t_ in loc if q * c + t_ < d})
+                gv = grads[j].view(torch.int16).view(d, R)
+                gr = gv[torch.tensor(grows, device="cuda")].cpu().numpy().view(np.uint16)
+                own = [t_ for t_ in loc if rank * c + t_ < d]
+                got = (gsh[j].view(c, R)[torch.tensor(own, device="cuda")].cpu().numpy() if own
+                       else np.zeros((0, R), np.float32))
+                members.append({"key": j, "d": d, "R": R, "loc": loc, "own": own,
+                                "grads": {g_: gr[i].copy() for i, g_ in enumerate(grows)}, "got": got})
+        except Exception as e:
+            err = "%s: %s" % (type(e).__name__, e)
+        err = agree(err)
+    out = None
+    if err is None:
+        t = max_over_ranks(t)
+        barrier()                      # every rank done reading before teardown
+        acc = {"elements": 0, "mismatches": 0, "max_err_over_bound": 0.0}
+        rs_check(world, rank, members, exchange, acc)
+        full = world * b.rs_seg
+        bus = (world - 1) / world * full / t
+        out = {"rs_ms": round(t / 1e6, 4), "busbw_GBps": round(bus, 1), "frac_nvlink": round(bus / NVLINK_GBS, 4),
+               "rs_full_bytes": full,
+               "parity": dict(acc, ok=acc["elements"] > 0 and acc["max_err_over_bound"] <= 1.0,
+                              required="G7 bound (the switch's summation order)"),
+               "how": "K10 alone (multimem.ld_reduce.add.v4.f32 through the multicast mapping), events, median "
+                      "of %d, max over ranks; busbw = (N-1)/N x fp32 bucket bytes / t" % reps}
+    barrier()
+    if m is not None:
+        m.close()
+    b.close()
+    if out is not None:
+        return out
+    return {"unavailable" if "refused" in err or "multicast" in err or "UNSUPPORTED" in err else "error": err[:300]}
 
 
 def exposure_leg(args, specs, world, rank, ctx, cs, ms, compute, p2p, exchange, barrier, max_over_ranks, alpha_beta):

@@ -70,6 +70,8 @@ def test_nccl_path_parity_and_measurements():
     assert ab["source"].startswith("measured") and ab["ag"]["beta_fs_per_byte"] > 0
     assert len(line["exposure"]["variants"]) == 3
     assert line["nccl_info"] and line["nccl_info"]["lines"]
+    nv = line["nvls_block"]
+    assert "unavailable" in nv or (nv["parity"]["ok"] and nv["busbw_GBps"] > 0), nv
 
 
 @needs_two
