@@ -52,7 +52,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "AG/RS bus GB/s and exposed-comm ms/step, Llama-3-8B shards, 1/2/4/8 B200"
-NVLINK_GBS = 900.0      # NVLink 5, per direction per GPU (SURVEY §8(d) roofline)
+NVLINK_GBS = 900.0      # NVLink 5 nominal, per direction per GPU (SURVEY §8(d) roofline)
+NVLINK_MEASURED_GBS = 770.0   # peer copy per direction measured on this pool (B200_PROFILING.md)
 ASSUMED_LINK = (20000, 1215)   # 20 us, (N-1)/N / 720 GB/s at N = 8: used only where nothing was measured
 
 
@@ -945,6 +946,9 @@ def main(argv=None):
         bb_rs = (world - 1) / world * wire_rs_block / r["rs_ns"]
         busbw_block = {"ag_GBps": round(bb_ag, 1), "rs_GBps": round(bb_rs, 1),
                        "ag_frac_nvlink": round(bb_ag / NVLINK_GBS, 4), "rs_frac_nvlink": round(bb_rs / NVLINK_GBS, 4),
+                       "ag_frac_measured_peer": round(bb_ag / NVLINK_MEASURED_GBS, 4),
+                       "rs_frac_measured_peer": round(bb_rs / NVLINK_MEASURED_GBS, 4),
+                       "peer_reference_GBps": NVLINK_MEASURED_GBS,
                        "ag_ms": round(r["ag_ns"] / 1e6, 4), "rs_ms": round(r["rs_ns"] / 1e6, 4),
                        "ag_full_bytes": r["ag_bytes"], "rs_full_bytes": r["rs_bytes"],
                        "rs_wire_dtype": "bf16 (K9 pulls the gradients)" if p2p else "fp32",
@@ -1151,6 +1155,7 @@ def nvls_leg(world, rank, ctx, exchange, barrier, max_over_ranks, reps=20):
         full = world * b.rs_seg
         bus = (world - 1) / world * full / t
         out = {"rs_ms": round(t / 1e6, 4), "busbw_GBps": round(bus, 1), "frac_nvlink": round(bus / NVLINK_GBS, 4),
+               "frac_measured_peer": round(bus / NVLINK_MEASURED_GBS, 4),
                "rs_full_bytes": full,
                "parity": dict(acc, ok=acc["elements"] > 0 and acc["max_err_over_bound"] <= 1.0,
                               required="G7 bound (the switch's summation order)"),
