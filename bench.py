@@ -443,7 +443,7 @@ def parity_leg(st, ctx, cs, ms, p2p, world, rank, exchange, barrier):
                             "got": {g: fr[i].tobytes() for i, g in enumerate(grows)}})
         ag_check(world, rank, members, exchange, ag)
         ag["buckets"].append(k)
-    rs = {"buckets": [], "elements": 0, "max_err_over_bound": 0.0, "mismatches": 0}
+    rs = {"buckets": [], "elements": 0, "max_err_over_bound": 0.0, "mismatches": 0, "pad_rows": 0, "pad_nonzero": 0}
     for b in sample_buckets(len(st.bwd)):
         bk = st.bwd[b]
         barrier()
@@ -464,11 +464,25 @@ def parity_leg(st, ctx, cs, ms, p2p, world, rank, exchange, barrier):
             members.append({"key": j, "d": d, "R": R, "loc": loc, "own": own,
                             "grads": {g: gr[i].copy() for i, g in enumerate(grows)},
                             "got": rows_of(st.gshard_buf, st.gs_offs[j], own, R * 4, np.float32)})
+            # pad rows of this rank's gradient shard (uneven dim 0) are exactly +0.0 (O5)
+            pads = [t for t in range(c) if rank * c + t >= d]
+            if pads:
+                pr = rows_of(st.gshard_buf, st.gs_offs[j], pads, R * 4, np.uint32)
+                rs["pad_rows"] += len(pads)
+                rs["pad_nonzero"] += int(np.count_nonzero(pr))
         rs_check(world, rank, members, exchange, rs)
         rs["buckets"].append(b)
     barrier()
     ok, required = parity_verdict(ag, rs, world, p2p)
-    return {"ok": ok, "ag": dict(ag, bit_exact=ag["mismatches"] == 0),
+    ok = ok and rs["pad_nonzero"] == 0
+    # every rank checked its own outputs: the verdict is all of them
+    allr = exchange((ok, ag, rs))
+    ok = all(x[0] for x in allr)
+    ag = dict(ag, elements=sum(x[1]["elements"] for x in allr), mismatches=sum(x[1]["mismatches"] for x in allr))
+    rs = dict(rs, elements=sum(x[2]["elements"] for x in allr), mismatches=sum(x[2]["mismatches"] for x in allr),
+              max_err_over_bound=max(x[2]["max_err_over_bound"] for x in allr),
+              pad_rows=sum(x[2]["pad_rows"] for x in allr), pad_nonzero=sum(x[2]["pad_nonzero"] for x in allr))
+    return {"ok": ok, "ranks_checked": len(allr), "ag": dict(ag, bit_exact=ag["mismatches"] == 0),
             "rs": dict(rs, bit_exact=rs["mismatches"] == 0, required=required),
             "how": ("sampled rows (first / last / seeded) of every member of buckets %s (fwd AG) / %s (bwd RS) of "
                     "the bench's own state, run through the same calls and communicator as the step, compared "
@@ -662,6 +676,8 @@ def main(argv=None):
             pj = json.load(f)["plans"]
         fplan, bplan = pj["fwd"], pj["bwd"]
         assert sorted(j for b in fplan for j in b) == sorted(j for b in bplan for j in b) == list(range(len(specs)))
+    if p2p and not H.same_buckets(fplan, bplan):
+        bplan = H.mirror_plan(fplan)     # one shard layout for both phases (peer-memory path)
     reg = args.nccl_register if (multi and not p2p and args.nccl_register != "none") else None
     st = H.RankState(specs, world, my_rank, fplan, bplan, ctx, seed=1234 + my_rank, ipc=multi and p2p,
                      nccl_register=reg, ag_grouped=args.ag == "grouped", grad_slots=args.grad_slots)
@@ -1152,6 +1168,9 @@ def nvls_leg(world, rank, ctx, exchange, barrier, max_over_ranks, reps=20):
         barrier()                      # every rank done reading before teardown
         acc = {"elements": 0, "mismatches": 0, "max_err_over_bound": 0.0}
         rs_check(world, rank, members, exchange, acc)
+        alla = exchange(acc)           # every rank's own rows
+        acc = {"elements": sum(a_["elements"] for a_ in alla), "mismatches": sum(a_["mismatches"] for a_ in alla),
+               "max_err_over_bound": max(a_["max_err_over_bound"] for a_ in alla), "ranks_checked": len(alla)}
         full = world * b.rs_seg
         bus = (world - 1) / world * full / t
         out = {"rs_ms": round(t / 1e6, 4), "busbw_GBps": round(bus, 1), "frac_nvlink": round(bus / NVLINK_GBS, 4),
@@ -1199,6 +1218,8 @@ def exposure_leg(args, specs, world, rank, ctx, cs, ms, compute, p2p, exchange, 
                                 ("per-block + reorder (manual wrap)", L.PLAN_MANUAL, RF),
                                 ("greedy + reorder (Algorithm 1, fitted links)", L.PLAN_GREEDY, RF)):
         vf, vb = H.plans_for(specs, world, vmode, tf, tb, lag, lrs, int(args.mem_limit))
+        if p2p and not H.same_buckets(vf, vb):
+            vb = H.mirror_plan(vf)           # one shard layout for both phases (peer-memory path)
         vst = H.RankState(specs, world, rank, vf, vb, ctx, seed=77 + rank, ipc=p2p)
         if p2p:
             vst.setup_p2p_ipc(exchange)

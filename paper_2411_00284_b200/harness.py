@@ -446,6 +446,18 @@ def plans_for(specs, world, mode, t_fwd=None, t_bwd=None, ag=(0, 0), rs=(0, 0), 
     return fb, bb
 
 
+def mirror_plan(fwd_plan):
+    """The backward plan that re-gathers the forward plan's buckets in reverse
+    (SPEC's mirrored reading).  The peer-memory path needs it when the
+    two phases' plans differ: peers read this rank's shards in one segment
+    layout, so both phases must bucket the same members together."""
+    return [sorted(b, reverse=True) for b in reversed(fwd_plan)]
+
+
+def same_buckets(fwd_plan, bwd_plan):
+    return sorted(tuple(sorted(b)) for b in fwd_plan) == sorted(tuple(sorted(b)) for b in bwd_plan)
+
+
 # fsdp_plan_search cost model (tools/plan_search.py documents the numbers)
 SEARCH_COST = dict(unpack_bytes_per_us=6470000, pack_rs_bytes_per_us=6680000, copy_launch_ns=6000,
                    compute_overhead_ns=16000, max_moves=0)

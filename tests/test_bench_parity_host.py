@@ -170,3 +170,17 @@ def test_parity_checks_over_gloo(world, case, p2p, want_ok):
         errs.append(errq.get())
     assert not errs, "\n".join(errs)
     assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
+
+
+def test_mirror_plan_for_the_peer_memory_path():
+    """The peer-memory path keeps one shard layout, so when Algorithm 1's two
+    phase plans differ the backward re-gathers the forward's buckets, in the
+    backward execution order (parameters in reverse)."""
+    from paper_2411_00284_b200 import harness as H
+    fwd = [[0], [1, 2], [3, 4, 5], [6]]
+    bwd = [[6, 5], [4, 3, 2], [1, 0]]
+    assert not H.same_buckets(fwd, bwd)
+    m = H.mirror_plan(fwd)
+    assert m == [[6], [5, 4, 3], [2, 1], [0]]
+    assert H.same_buckets(fwd, m)
+    assert [j for b in m for j in b] == list(range(6, -1, -1))

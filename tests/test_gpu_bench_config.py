@@ -25,7 +25,8 @@ from workloads import llama
 pytestmark = pytest.mark.gpu
 
 
-def test_bench_p2p_two_processes_one_gpu():
+@pytest.mark.parametrize("nproc", [2, 3])
+def test_bench_p2p_two_processes_one_gpu(nproc):
     """bench.py's multi-rank peer-memory path (IPC handle exchange over
     torch.distributed, epoch flags across processes) end to end with 2 ranks
     on one GPU (--same-device, time-sliced: the timings mean nothing)."""
@@ -39,14 +40,14 @@ def test_bench_p2p_two_processes_one_gpu():
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(nproc),
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"),
-           "--gpus", "2", "--collective", "p2p", "--same-device", "--steps", "2", "--warmup", "1",
+           "--gpus", str(nproc), "--collective", "p2p", "--same-device", "--steps", "2", "--warmup", "1",
            "--layers", "1", "--no-e2e", "--exposure-tokens", "256"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
-    assert line["n_gpus"] == 2 and line["p2p_wait_timeouts"] == 0
+    assert line["n_gpus"] == nproc and line["p2p_wait_timeouts"] == 0
     assert line["kernels"]["fsdp_p2p_allgather_kernel"]["launches_per_step"] == 2 * line["config"]["buckets_fwd"]
     # the N > 1 self-checks of the line: K8 / K9 across the two processes' IPC
     # mappings against the oracle (bit-exact), the isolated-block busbw, the
@@ -54,6 +55,8 @@ def test_bench_p2p_two_processes_one_gpu():
     par = line["parity"]
     assert par["ok"] and par["ag"]["bit_exact"] and par["rs"]["bit_exact"], par
     assert par["ag"]["elements"] > 0 and par["rs"]["elements"] > 0
+    if nproc == 3:      # 4096 / 14336 / 128256 rows split 3 ways: padded shards, pad rows +0.0
+        assert par["rs"]["pad_rows"] > 0 and par["rs"]["pad_nonzero"] == 0
     assert line["value_kind"] == "bus" and line["busbw_block"]["ag_GBps"] > 0
     assert line["alpha_beta"]["source"].startswith("measured") and len(line["alpha_beta"]["rows"]) == 10
     assert len(line["exposure"]["variants"]) == 3
