@@ -611,7 +611,7 @@ def main(argv=None):
         # the communicator's own account (version, channels, NVLS, tuning), one file per rank
         if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("", "VERSION", "WARN"):
             os.environ["NCCL_DEBUG"] = "INFO"
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS,TUNING,ENV")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS,ENV")   # init-time only: nothing per call
         if "NCCL_DEBUG_FILE" not in os.environ:
             os.environ["NCCL_DEBUG_FILE"] = nccl_log_path(rank)
 
