@@ -87,7 +87,7 @@ def parse(argv=None):
     ap.add_argument("--proxy-smem", type=int, default=0)
     ap.add_argument("--eager", action="store_true", help="time the eager enqueue instead of the CUDA-graph replay")
     ap.add_argument("--trace", default=None, help="Chrome trace of one profiled step")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fused-leg", action="store_true")

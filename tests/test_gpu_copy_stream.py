@@ -108,3 +108,38 @@ def test_copy_stream_rejects_shared_adjacent_slots():
         b.close()
     del st
     ctx.close()
+
+
+def test_copy_stream_with_host_io():
+    """fsdp_host_io with the copy stream: the H2D'd shards feed the gathers
+    and the gradient D2H follows the copy-outs, same host bytes as without."""
+    world = 2
+    specs = llama("8b", n_layers=2)
+    outs = []
+    for flags in (RF, RF | L.SCHED_COPY_STREAM):
+        ctx = F.Ctx(world, 0)
+        fplan, bplan = H.plans_for(specs, world, L.PLAN_MANUAL)
+        st = H.RankState(specs, world, 0, fplan, bplan, ctx, seed=12)
+        h_sh = torch.empty(st.shard_buf.numel(), dtype=torch.uint8).pin_memory()
+        h_sh.copy_(torch.randint(0, 256, (h_sh.numel(),), dtype=torch.uint8,
+                                 generator=torch.Generator().manual_seed(4)))
+        gaps = torch.ones(st.shard_buf.numel(), dtype=torch.bool)
+        for j, o in enumerate(st.shard_offs):
+            gaps[o:o + st.shard_numel[j] * 2] = False
+        h_sh[gaps] = 0
+        h_gs = torch.zeros(st.gshard_buf.numel(), dtype=torch.uint8).pin_memory()
+        cs, ms = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+        for t in st.full_slots:
+            t.zero_()
+        st.shard_buf[gaps.cuda()] = 0
+        torch.cuda.synchronize()
+        for _ in range(2):
+            st.step(flags, cs.cuda_stream, ms.cuda_stream, io=st.host_io(h_sh, h_gs))
+        cs.synchronize()
+        outs.append((h_gs.clone(), [t.cpu() for t in st.full_slots]))
+        assert torch.equal(st.shard_buf.cpu(), h_sh)
+        del st
+        ctx.close()
+    assert torch.equal(outs[0][0], outs[1][0])
+    for x, y in zip(outs[0][1], outs[1][1]):
+        assert torch.equal(x, y)
