@@ -107,6 +107,9 @@ def parse(argv=None):
     ap.add_argument("--dist", action="store_true", help="the N>1 code path at --gpus 1 (world 1, real communicator)")
     ap.add_argument("--nccl-register", default="none", choices=["none", "local", "symmetric"])
     ap.add_argument("--p2p-max-ctas", type=int, default=-1)
+    ap.add_argument("--p2p-transport", default="ipc", choices=["ipc", "window"],
+                    help="N > 1 peer-memory path: peers mapped through CUDA IPC handles, or through NCCL symmetric "
+                         "windows (fsdp_window_peer_pointers; the ctx then holds a communicator)")
     ap.add_argument("--nccl-max-ctas", type=int, default=0)
     ap.add_argument("--ag", default="flat", choices=["flat", "grouped"])
     return ap.parse_args(argv)
@@ -632,9 +635,9 @@ def main(argv=None):
         assert world_env == args.gpus, "launch with torchrun --nproc-per-node %d" % args.gpus
         dist.init_process_group("gloo")      # host plumbing only; the data path is the library's
         world = args.gpus
-        if p2p:
+        if p2p and args.p2p_transport == "ipc":
             ctx = F.Ctx(world, rank, local)  # peer-memory collectives need no NCCL communicator
-        else:
+        else:   # NCCL collectives, or NCCL symmetric windows for the peer-memory path
             uid = [F.nccl_get_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
             cfg = dict(max_ctas=args.nccl_max_ctas) if args.nccl_max_ctas > 0 else None
@@ -679,8 +682,9 @@ def main(argv=None):
     if p2p and not H.same_buckets(fplan, bplan):
         bplan = H.mirror_plan(fplan)     # one shard layout for both phases (peer-memory path)
     reg = args.nccl_register if (multi and not p2p and args.nccl_register != "none") else None
-    st = H.RankState(specs, world, my_rank, fplan, bplan, ctx, seed=1234 + my_rank, ipc=multi and p2p,
-                     nccl_register=reg, ag_grouped=args.ag == "grouped", grad_slots=args.grad_slots)
+    win = multi and p2p and args.p2p_transport == "window"
+    st = H.RankState(specs, world, my_rank, fplan, bplan, ctx, seed=1234 + my_rank, ipc=multi and p2p and not win,
+                     nccl_register=reg, ag_grouped=args.ag == "grouped", grad_slots=args.grad_slots, windows=win)
     compute = torch.cuda.Stream()
     comm = torch.cuda.Stream(priority=-1)
     cs, ms = compute.cuda_stream, comm.cuda_stream
@@ -692,7 +696,10 @@ def main(argv=None):
         pb = H.proxy_iters(H.bucket_times(bplan, t_bwd), nspi)
     if p2p:
         if multi:
-            st.setup_p2p_ipc(exchange)
+            if win:
+                st.setup_p2p_windows()
+            else:
+                st.setup_p2p_ipc(exchange)
             st.p2p_max_ctas = args.p2p_max_ctas if args.p2p_max_ctas >= 0 else H.emulation_ctas_p2p(world)
         else:
             st.setup_p2p_simulated(seed=99)
@@ -953,7 +960,7 @@ def main(argv=None):
     busbw_block = alpha_beta = exposure = nvls_block = None
     if multi and world > 1 and not quick:
         from workloads.shapes import ParamSpec
-        kw = dict(p2p=p2p, exchange=exchange, max_over_ranks=max_over_ranks)
+        kw = dict(p2p=p2p, exchange=exchange, max_over_ranks=max_over_ranks, windows=args.p2p_transport == "window")
         block = [p for p in llama("8b", n_layers=1, with_embeddings=False)]
         barrier()
         r = H.time_bucket_collectives(block, world, my_rank, ctx, cs, ms, reps=20, warmup=5, **kw)
@@ -1093,7 +1100,7 @@ def nvls_leg(world, rank, ctx, exchange, barrier, max_over_ranks, reps=20):
     gsh = [torch.zeros(-(-p.dim0 // world) * p.row_numel, dtype=torch.float32, device="cuda") for p in specs]
     b = F.Bucket(ctx, descs, full_grads=[t.data_ptr() for t in grads], grad_shards=[t.data_ptr() for t in gsh],
                  param_dtype=L.BF16, grad_dtype=L.BF16)
-    m, err = None, None
+    m, err, route, win_ptr = None, None, None, None
 
     def agree(local_err):
         """Every rank's error (or None) -> the first one, on every rank: the
@@ -1101,6 +1108,8 @@ def nvls_leg(world, rank, ctx, exchange, barrier, max_over_ranks, reps=20):
         errs = [e for e in exchange(local_err) if e]
         return errs[0] if errs else None
 
+    # route 1: a multicast object of our own (cuMulticastCreate, fabric or
+    # POSIX-fd handle exchanged by the binding)
     try:
         if rank == 0:
             m = F.Nvls(ctx, b.rs_seg)
@@ -1124,6 +1133,36 @@ def nvls_leg(world, rank, ctx, exchange, barrier, max_over_ranks, reps=20):
         except Exception as e:
             err = "%s: %s" % (type(e).__name__, e)
         err = agree(err)
+    route = "cuMulticast object (fsdp_nvls_*)" if err is None else None
+    # route 2 (needs a communicator): NCCL's own multicast mapping of a
+    # symmetric window (fsdp_window_multimem_pointer, the NCCL device API)
+    has_comm = exchange(bool(getattr(ctx, "has_nccl", False)))
+    if err is not None and all(has_comm):
+        first_err, err = err, None
+        if m is not None:
+            m.close()
+            m = None
+        try:
+            win_ptr = F.mem_alloc(ctx, world * b.rs_seg)
+        except Exception as e:
+            err = "%s: %s" % (type(e).__name__, e)
+        err = agree(err)
+        if err is None:
+            try:
+                F.register_buffer(ctx, win_ptr, world * b.rs_seg, L.REG_SYMMETRIC)   # collective
+            except Exception as e:
+                err = "%s: %s" % (type(e).__name__, e)
+            err = agree(err)
+        if err is None:
+            try:
+                uc, mc = win_ptr, F.window_multimem_pointer(ctx, win_ptr)        # collective on first use
+            except Exception as e:
+                err = "%s: %s" % (type(e).__name__, e)
+            err = agree(err)
+        if err is None:
+            route = "NCCL symmetric window (fsdp_window_multimem_pointer)"
+        else:
+            err = "own multicast object: %s; NCCL window: %s" % (first_err[:150], err[:150])
     t = None
     members = []
     if err is None:
@@ -1183,8 +1222,11 @@ def nvls_leg(world, rank, ctx, exchange, barrier, max_over_ranks, reps=20):
     barrier()
     if m is not None:
         m.close()
+    if win_ptr is not None:
+        F.mem_free(ctx, win_ptr)       # deregisters the window (collective: every rank gets here)
     b.close()
     if out is not None:
+        out["route"] = route
         return out
     return {"unavailable" if "refused" in err or "multicast" in err or "UNSUPPORTED" in err else "error": err[:300]}
 
@@ -1220,8 +1262,11 @@ def exposure_leg(args, specs, world, rank, ctx, cs, ms, compute, p2p, exchange, 
         vf, vb = H.plans_for(specs, world, vmode, tf, tb, lag, lrs, int(args.mem_limit))
         if p2p and not H.same_buckets(vf, vb):
             vb = H.mirror_plan(vf)           # one shard layout for both phases (peer-memory path)
-        vst = H.RankState(specs, world, rank, vf, vb, ctx, seed=77 + rank, ipc=p2p)
-        if p2p:
+        win = p2p and args.p2p_transport == "window"
+        vst = H.RankState(specs, world, rank, vf, vb, ctx, seed=77 + rank, ipc=p2p and not win, windows=win)
+        if win:
+            vst.setup_p2p_windows()
+        elif p2p:
             vst.setup_p2p_ipc(exchange)
             vst.p2p_max_ctas = args.p2p_max_ctas if args.p2p_max_ctas >= 0 else H.emulation_ctas_p2p(world)
         fl = vflags | (L.SCHED_P2P if p2p else 0)
@@ -1253,6 +1298,7 @@ def exposure_leg(args, specs, world, rank, ctx, cs, ms, compute, p2p, exchange, 
         barrier()
         if p2p:
             vst.close_ipc()
+        vst.close_nccl_mem()
         del vst
         gc.collect()
         torch.cuda.empty_cache()

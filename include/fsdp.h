@@ -42,7 +42,7 @@ extern "C" {
 #endif
 
 #define FSDP_ABI_VERSION 5  /* 2: schedule.hook; 3: schedule.emulate; 4: p2p_schedule.max_ctas;
-                              5: fsdp_bucket_launch_kernel */
+                              5: fsdp_bucket_launch_kernel, 80-B NVLS handle, window pointers */
 
 typedef void* fsdp_stream_t; /* cudaStream_t */
 
@@ -854,6 +854,29 @@ enum { FSDP_REG_LOCAL = 0, FSDP_REG_SYMMETRIC = 1 };
 fsdp_status fsdp_mem_alloc(fsdp_ctx* ctx, int64_t bytes, void** dev_ptr);
 fsdp_status fsdp_mem_free(fsdp_ctx* ctx, void* dev_ptr);
 fsdp_status fsdp_register_buffer(fsdp_ctx* ctx, void* dev_ptr, int64_t bytes, int32_t mode);
+
+/* NCCL symmetric windows for the peer-memory path (SURVEY §8(f) NEXT #1,
+ * the NCCL 2.28 device API): a buffer registered with FSDP_REG_SYMMETRIC is
+ * mapped by NCCL in every rank of the NVLink (LSA) domain, so the K8 / K9
+ * peer tables and the K10 multicast staging can come from NCCL instead of
+ * CUDA IPC handles and a caller-built multicast object.
+ *   fsdp_window_peer_pointers(ctx, base, peer_ptrs[world]): peer_ptrs[q] =
+ *       rank q's copy of the window at `base` (ncclGetPeerPointer), valid in
+ *       this process; NCCL maps all ranks' windows into one flat range, so
+ *       peer_ptrs[rank] is an alias of `base` at another address.  Local (no
+ *       communication).
+ *       FSDP_ERR_UNSUPPORTED if some rank is outside this rank's NVLink
+ *       domain.
+ *   fsdp_window_multimem_pointer(ctx, base, &mc): the NVLS multicast address
+ *       of the window (ncclGetLsaMultimemPointer of a device communicator
+ *       created once per ctx with lsaMultimem; that creation is COLLECTIVE --
+ *       the first call must be made by every rank); usable as K10's
+ *       mc_staging with `base` as the unicast staging.  FSDP_ERR_UNSUPPORTED
+ *       where NCCL gives no multicast mapping (no NVLS).
+ * Errors: a ctx without a communicator, `base` not the start of a symmetric
+ * window of this ctx -> FSDP_ERR_INVALID_ARG.  (ABI 5) */
+fsdp_status fsdp_window_peer_pointers(fsdp_ctx* ctx, const void* base, void** peer_ptrs);
+fsdp_status fsdp_window_multimem_pointer(fsdp_ctx* ctx, const void* base, void** mc_ptr);
 
 /* ----------------------------------------------- compute proxy (K7)
  * A measurement device, not a method step: stands in for the layer compute

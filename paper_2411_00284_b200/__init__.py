@@ -13,7 +13,8 @@ _API = ("Bucket", "Ctx", "abi_version", "allgather_bucket", "layout", "nccl_get_
         "shard", "p2p_allgather_bucket", "p2p_reduce_scatter_bucket", "p2p_signal", "p2p_wait",
         "ipc_alloc", "ipc_open", "ipc_close", "ipc_free", "comm_time_ns", "simulate_schedule",
         "mem_alloc", "mem_free", "register_buffer", "Nvls", "nvls_reduce_scatter_bucket",
-        "StepGraph", "simulate_memory", "plan_search", "bucket_launch_kernel")
+        "StepGraph", "simulate_memory", "plan_search", "bucket_launch_kernel",
+        "window_peer_pointers", "window_multimem_pointer")
 
 
 def __getattr__(name):

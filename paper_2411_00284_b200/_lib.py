@@ -45,7 +45,8 @@ EXPORTED = [
     "fsdp_run_schedule", "fsdp_proxy_launch", "fsdp_proxy_calibrate",
     "fsdp_p2p_allgather_bucket", "fsdp_p2p_reduce_scatter_bucket", "fsdp_p2p_signal", "fsdp_p2p_wait",
     "fsdp_ipc_alloc", "fsdp_ipc_open", "fsdp_ipc_close", "fsdp_ipc_free",
-    "fsdp_mem_alloc", "fsdp_mem_free", "fsdp_register_buffer",
+    "fsdp_mem_alloc", "fsdp_mem_free", "fsdp_register_buffer", "fsdp_window_peer_pointers",
+    "fsdp_window_multimem_pointer",
     "fsdp_nvls_create", "fsdp_nvls_import", "fsdp_nvls_bind", "fsdp_nvls_destroy",
     "fsdp_nvls_reduce_scatter_bucket",
     "fsdp_step_graph_create", "fsdp_step_graph_launch", "fsdp_step_graph_info", "fsdp_step_graph_destroy",
@@ -206,6 +207,8 @@ _sigs = {
     "fsdp_mem_alloc": (C.c_int, [_P, C.c_int64, C.POINTER(_P)]),
     "fsdp_mem_free": (C.c_int, [_P, _P]),
     "fsdp_register_buffer": (C.c_int, [_P, _P, C.c_int64, C.c_int32]),
+    "fsdp_window_peer_pointers": (C.c_int, [_P, _P, C.POINTER(C.c_void_p)]),
+    "fsdp_window_multimem_pointer": (C.c_int, [_P, _P, C.POINTER(C.c_void_p)]),
     "fsdp_nvls_create": (C.c_int, [_P, C.c_int64, _P, C.POINTER(_P)]),
     "fsdp_nvls_import": (C.c_int, [_P, _P, C.c_int64, C.POINTER(_P)]),
     "fsdp_nvls_bind": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(C.c_int64)]),

@@ -371,6 +371,7 @@ fsdp_status fsdp_ctx_destroy(fsdp_ctx* c) {
   if (c->own_h2d) cudaStreamDestroy(c->own_h2d);
   if (c->own_d2h) cudaStreamDestroy(c->own_d2h);
   if (c->sink) cudaFree(c->sink);
+  release_devcomm(c);                  // before the windows and the communicator go
   release_registrations(c, nullptr);  // before the communicator goes
   fsdp_status st = FSDP_OK;
   if (c->owns_comm && c->comm) {

@@ -211,6 +211,11 @@ struct fsdp_ctx {
   // per-call cross-stream events (unpacked / computed / grads packed per bucket)
   cudaStream_t own_copy_stream = nullptr;
   std::vector<cudaEvent_t> copy_events;
+  // NCCL device communicator with an LSA multicast mapping (ncclwin.cu,
+  // fsdp_window_multimem_pointer); ncclDevComm_t behind a void*
+  void* devcomm = nullptr;
+  bool devcomm_ready = false;
+  void* devcomm_mc_base = nullptr;
   int sm_count = 148;
   int max_ctas = 148 * 8;
   float* sink = nullptr;
@@ -231,6 +236,7 @@ struct fsdp_ctx {
 };
 namespace fsdp {
 void release_registrations(fsdp_ctx* c, void* base);  // base NULL = all
+void release_devcomm(fsdp_ctx* c);                      // the device communicator, if any
 }
 
 struct fsdp_bucket {

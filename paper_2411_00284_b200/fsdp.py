@@ -109,6 +109,7 @@ class Ctx:
         """nccl_config: dict(min_ctas, max_ctas, nvls_ctas, cta_policy) ->
         fsdp_ctx_create_config (needs nccl_uid)."""
         self.world, self.rank, self.device = world, rank, device
+        self.has_nccl = nccl_uid is not None or bool(borrowed_comm)   # a communicator is held
         h = C.c_void_p()
         uid = None
         if nccl_uid is not None:
@@ -141,6 +142,7 @@ class Ctx:
         n, r = C.c_int32(), C.c_int32()
         check(L.lib.fsdp_ctx_info(h, C.byref(n), C.byref(r)))
         sub.world, sub.rank = n.value, r.value
+        sub.has_nccl = True
         return sub
 
     def close(self):
@@ -422,6 +424,22 @@ def register_buffer(ctx, ptr, nbytes, mode=L.REG_LOCAL):
     """fsdp_register_buffer: REG_LOCAL (ncclCommRegister) or REG_SYMMETRIC
     (collective ncclCommWindowRegister)."""
     check(L.lib.fsdp_register_buffer(ctx.h, ptr, int(nbytes), int(mode)))
+
+
+def window_peer_pointers(ctx, base):
+    """fsdp_window_peer_pointers: every rank's copy of the symmetric window
+    registered at `base` (list of world addresses, this process's VA)."""
+    out = (C.c_void_p * ctx.world)()
+    check(L.lib.fsdp_window_peer_pointers(ctx.h, base, out))
+    return [int(x or 0) for x in out]
+
+
+def window_multimem_pointer(ctx, base):
+    """fsdp_window_multimem_pointer: the window's NVLS multicast address
+    (collective on the first call per ctx)."""
+    mc = C.c_void_p()
+    check(L.lib.fsdp_window_multimem_pointer(ctx.h, base, C.byref(mc)))
+    return mc.value
 
 
 class Nvls:

@@ -35,7 +35,7 @@ def _carve(sizes, align=ALIGN):
 class RankState:
     def __init__(self, specs, world, rank, fwd_plan, bwd_plan, ctx, param_dtype=L.BF16,
                  device="cuda", seed=0, fill=True, segment_storage=True, ipc=False, nccl_register=None,
-                 ag_grouped=False, grad_slots=2):
+                 ag_grouped=False, grad_slots=2, windows=False):
         # ipc=True: the buffers peers read in the peer-memory path (shard
         # storage, gradient slots) come from fsdp_ipc_alloc so that other
         # processes can map them (setup_p2p_ipc).
@@ -43,18 +43,24 @@ class RankState:
         # sends from or receives into (shard storage, full-parameter slots, AG /
         # RS staging, gradient-shard storage) comes from fsdp_mem_alloc and is
         # registered with the ctx's communicator (fsdp_register_buffer).
+        # windows=True: those buffers instead come from fsdp_mem_alloc and are
+        # registered as NCCL symmetric windows (a collective, same sizes and
+        # order on every rank); setup_p2p_windows then takes the peer tables
+        # from NCCL (fsdp_window_peer_pointers) -- no IPC handles.
         self.ipc_handles = {}
         self._ipc_ptrs = []
         self._nccl_ptrs = []
+        self.win_bases = {}
+        self.windows = windows
         reg_mode = {None: None, "none": None, "local": L.REG_LOCAL, "symmetric": L.REG_SYMMETRIC}[nccl_register]
         dev_index = torch.device(device).index or torch.cuda.current_device()
 
-        def nccl_buf(nbytes, zero=False):
+        def nccl_buf(nbytes, zero=False, mode=None):
             from .dlpack_view import uint8_view
             nbytes = max(int(nbytes), 4096)
             ptr = F.mem_alloc(ctx, nbytes)
             self._nccl_ptrs.append(ptr)
-            F.register_buffer(ctx, ptr, nbytes, reg_mode)
+            F.register_buffer(ctx, ptr, nbytes, reg_mode if mode is None else mode)
             t = uint8_view(ptr, nbytes, dev_index)
             if zero:
                 t.zero_()
@@ -62,6 +68,10 @@ class RankState:
 
         def alloc(name, nbytes, zero=False, collective=False, peer=False):
             # collective: an NCCL send / receive buffer; peer: read by peers (K8 / K9)
+            if windows and peer:
+                t = nccl_buf(nbytes, zero, L.REG_SYMMETRIC)
+                self.win_bases[name] = t.data_ptr()
+                return t
             if collective and reg_mode is not None:
                 return nccl_buf(nbytes, zero)
             if not (ipc and peer):
@@ -259,6 +269,33 @@ class RankState:
             shard_base.append(ptrs[0])
             flag_base.append(ptrs[1])
             grad_base.append(ptrs[2:])
+        self.ready_slots = [flag_base[q] + 8 * r for q in range(W)]
+        self.done_slots = [flag_base[q] + 8 * W + 8 * r for q in range(W)]
+        self._p2p_tables(shard_base, grad_base)
+
+    def setup_p2p_windows(self):
+        """Peer-memory state from NCCL symmetric windows (RankState(...,
+        windows=True); the ctx has a communicator): peers' shard storage,
+        gradient slots and flag arrays through fsdp_window_peer_pointers.  The
+        flag array is registered here -- a collective: every rank calls this."""
+        from .dlpack_view import uint8_view
+        W, r = self.world, self.rank
+        nb = max(16 * W, 4096)
+        fptr = F.mem_alloc(self.ctx, nb)
+        self._nccl_ptrs.append(fptr)
+        F.register_buffer(self.ctx, fptr, nb, L.REG_SYMMETRIC)
+        fl = uint8_view(fptr, nb, torch.cuda.current_device())
+        fl.zero_()
+        torch.cuda.synchronize()
+        self.ready = fl[:8 * W].view(torch.int64)
+        self.done = fl[8 * W:16 * W].view(torch.int64)
+        self.p2p_err = torch.zeros(1, dtype=torch.int32, device=self.shard_buf.device)
+        shard_base = F.window_peer_pointers(self.ctx, self.win_bases["shards"])
+        flag_base = F.window_peer_pointers(self.ctx, fptr)
+        gslots = [F.window_peer_pointers(self.ctx, self.win_bases["grads%d" % i]) for i in range(self.n_grad_slots)]
+        grad_base = [[gslots[i][q] for i in range(self.n_grad_slots)] for q in range(W)]
+        # (NCCL maps every rank's window, this rank's too, into one flat VA
+        # range: peer_ptrs[rank] aliases the buffer at a different address)
         self.ready_slots = [flag_base[q] + 8 * r for q in range(W)]
         self.done_slots = [flag_base[q] + 8 * W + 8 * r for q in range(W)]
         self._p2p_tables(shard_base, grad_base)
@@ -513,7 +550,7 @@ def emulation_ctas_p2p(world, bus_gbps=720.0, per_cta_gbps=29.0):
 
 
 def time_bucket_collectives(specs, world, rank, ctx, compute, comm, reps=20, warmup=5, p2p=False,
-                            exchange=None, max_over_ranks=None, seed=11):
+                            exchange=None, max_over_ranks=None, seed=11, windows=False):
     """One bucket holding all of ``specs``, alone: a forward AG, a backward AG
     and an RS per step through fsdp_run_schedule with FSDP_SCHED_TIMING -- the
     AG / RS log entries are CUDA events around the collective alone on the comm
@@ -522,9 +559,13 @@ def time_bucket_collectives(specs, world, rank, ctx, compute, comm, reps=20, war
     rs_ns): full bucket bytes in the planner's definition (G8: N * seg, bf16
     AG / fp32 RS) and the collective's device time."""
     plan = [list(range(len(specs)))]
-    st = RankState(specs, world, rank, plan, plan, ctx, seed=seed, ipc=p2p and world > 1)
+    windows = windows and p2p
+    st = RankState(specs, world, rank, plan, plan, ctx, seed=seed, ipc=p2p and world > 1 and not windows,
+                   windows=windows)
     try:
-        if p2p:
+        if windows:
+            st.setup_p2p_windows()
+        elif p2p:
             if world > 1:
                 st.setup_p2p_ipc(exchange)
             else:
@@ -544,6 +585,7 @@ def time_bucket_collectives(specs, world, rank, ctx, compute, comm, reps=20, war
     finally:
         if p2p:
             st.close_ipc()
+        st.close_nccl_mem()
         del st
         torch.cuda.empty_cache()
 
