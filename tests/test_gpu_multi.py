@@ -11,7 +11,7 @@ devices, 8), one process per GPU under torchrun:
   alpha / beta fit and the measured exposure variants;
 * peer-memory path: the same with --collective p2p -- K8 / K9 reading the
   peers' HBM through CUDA IPC mappings over NVLink, both bit-exact (K9 sums in
-  rank order);
+  rank order); and with the peers mapped through NCCL symmetric windows;
 * NVLS: K10 (multimem.ld_reduce through a multicast object spanning the N
   GPUs) against the oracle's reduce-scatter, within G7's bound; skipped where
   the platform refuses multicast objects.
@@ -85,6 +85,15 @@ def test_p2p_path_parity_over_real_peers(n):
     par = line["parity"]
     assert par["ok"] and par["ag"]["bit_exact"] and par["rs"]["bit_exact"], par
     assert line["p2p_wait_timeouts"] == 0 and line["busbw_block"]["ag_GBps"] > 0
+
+
+@needs_two
+def test_p2p_over_nccl_windows():
+    """K8 / K9 with the peers mapped through NCCL symmetric windows (the NCCL
+    2.28 device API) instead of CUDA IPC: same bit-exact parity."""
+    line = _bench(["--collective", "p2p", "--p2p-transport", "window"])
+    par = line["parity"]
+    assert par["ok"] and par["ag"]["bit_exact"] and par["rs"]["bit_exact"], par
 
 
 @needs_two
