@@ -31,6 +31,7 @@ for n in 2 4 8; do
   # carries parity, busbw_block, alpha_beta and the measured exposure variants
   run $n flat
   run $n p2p --collective p2p
+  run $n p2p_window --collective p2p --p2p-transport window              # peers mapped by NCCL symmetric windows
   run $n vanilla --plan per_param --no-reorder --tokens 1024 --quick      # the unbucketed, unreordered baseline
   run $n perblock_T1024 --plan manual --tokens 1024 --quick               # + bucket & reorder (manual wrap)
   run $n greedy_T1024 --plan greedy --tokens 1024 --quick                 # auto-wrap (assumed links; the default
