@@ -20,11 +20,11 @@ pytestmark = pytest.mark.gpu
 RF = L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT
 
 
-def _run(world, comm, compute, flags, graph=False, seed=21, tokens=256):
+def _run(world, comm, compute, flags, graph=False, seed=21, tokens=256, mode=L.PLAN_MANUAL):
     specs = llama("8b", n_layers=2)
     ctx = F.Ctx(world, 0, 0, nccl_uid=F.nccl_get_unique_id()) if comm else F.Ctx(world, 0)
     tf, tb = per_param_compute_ns(specs, tokens)
-    fplan, bplan = H.plans_for(specs, world, L.PLAN_MANUAL)
+    fplan, bplan = H.plans_for(specs, world, mode, tf, tb, (20000, 1215), (20000, 1215), 2 * 10 ** 9)
     st = H.RankState(specs, world, 0, fplan, bplan, ctx, seed=seed)
     for t in st.full_slots:      # rows no kernel writes (peers' rows of direct-gather
         t.zero_()                # buckets on a layout-only rank) compare equal
@@ -143,3 +143,14 @@ def test_copy_stream_with_host_io():
     assert torch.equal(outs[0][0], outs[1][0])
     for x, y in zip(outs[0][1], outs[1][1]):
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("mode", [L.PLAN_PER_PARAM, L.PLAN_GREEDY])
+def test_copy_stream_other_plans(mode):
+    """Per-parameter buckets (many small copies) and Algorithm 1's greedy
+    buckets (different forward / backward groupings): same bytes."""
+    a = _run(8, False, "gemm", RF, mode=mode)
+    b = _run(8, False, "gemm", RF | L.SCHED_COPY_STREAM, mode=mode)
+    for x, y in zip(a[0], b[0]):
+        assert torch.equal(x, y)
+    assert torch.equal(a[2], b[2]) and all(torch.equal(x, y) for x, y in zip(a[1], b[1]))
