@@ -76,6 +76,32 @@ def test_emulated_step_captures_into_a_graph():
     ctx.close()
 
 
+def test_emulated_gather_writes_this_ranks_rows():
+    """An out-of-place gather (segment-layout shard storage) writes this rank's
+    own slot too, as NCCL's does: after an emulated step the direct-gather
+    buckets' full parameters (embedding, output) hold this rank's shard rows
+    -- no stale rows under the compute."""
+    ctx, st = _state()
+    for t in st.full_slots:
+        t.fill_(0xEE)
+    torch.cuda.synchronize()
+    cs, ms = torch.cuda.Stream(), torch.cuda.Stream()
+    st.step(0, cs.cuda_stream, ms.cuda_stream, emulate=EM)
+    torch.cuda.synchronize()
+    checked = 0
+    for b in st.bwd[-2:]:
+        if not b.query()["ag_direct"]:
+            continue
+        slot = st.full_slots[b.full_slot]
+        for j, o in zip(b.members, b.full_offs):
+            n = st.shard_numel[j] * 2
+            assert torch.equal(slot[o:o + n], st.shard_buf[st.shard_offs[j]:st.shard_offs[j] + n])
+            checked += 1
+    assert checked >= 1
+    del st
+    ctx.close()
+
+
 def test_emulation_rejections():
     specs = llama("8b", n_layers=1)
     fplan, bplan = H.plans_for(specs, 1, L.PLAN_MANUAL)
