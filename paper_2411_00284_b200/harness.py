@@ -319,7 +319,9 @@ class RankState:
         self.epoch = 0   # fixed epoch_base: the epochs advance on the device (epoch_counter)
         self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=self.shard_buf.device)
 
-    def p2p_schedule(self, timeout_ns=10 ** 10):
+    def p2p_schedule(self, timeout_ns=None):
+        if timeout_ns is None:
+            timeout_ns = getattr(self, "p2p_timeout_ns", 10 ** 10)
         return dict(ag_peers=self.ag_peers, rs_peers=self.rs_peers, ready_slots=self.ready_slots,
                     done_slots=self.done_slots, ready_flags=self.ready.data_ptr(), done_flags=self.done.data_ptr(),
                     epoch_base=self.epoch, timeout_ns=timeout_ns, error_flag=self.p2p_err.data_ptr(),

@@ -336,3 +336,31 @@ def test_fused_sync_variant_schedule():
                         os.path.join(root, "tests", "test_gpu_p2p.py")], env=env, cwd=root,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_timed_out_epoch_wait_fails_the_step():
+    """A peer that never signals: the epoch waits time out, the timed step
+    returns an error instead of results computed without the peer (ADVICE
+    round 1), and the harness's check raises."""
+    import torch
+    import paper_2411_00284_b200 as F
+    from paper_2411_00284_b200 import _lib as L
+    from paper_2411_00284_b200 import harness as H
+    from workloads import llama
+    specs = llama("8b", n_layers=1, with_embeddings=False)
+    world = 4
+    ctx = F.Ctx(world, 0)
+    fplan, bplan = H.plans_for(specs, world, L.PLAN_MANUAL)
+    st = H.RankState(specs, world, 0, fplan, bplan, ctx, seed=5)
+    st.setup_p2p_simulated(seed=6)
+    st.ready[2] = 0                      # simulated peer 2 never reports ready
+    st.p2p_timeout_ns = 2_000_000        # 2 ms per wait
+    torch.cuda.synchronize()
+    cs, ms = torch.cuda.Stream(), torch.cuda.Stream()
+    flags = L.SCHED_REORDER | L.SCHED_P2P | L.SCHED_TIMING
+    with pytest.raises(L.FsdpError):
+        st.step(flags, cs.cuda_stream, ms.cuda_stream)
+    with pytest.raises(RuntimeError):
+        st.check_p2p()
+    del st
+    ctx.close()
