@@ -523,7 +523,8 @@ typedef struct {
                                    would hold every SM for the link time, starving the compute
                                    stream; a cap like NCCL's channel count leaves the SMs to
                                    compute (57 CTAs carried an 8B block's traffic at N = 8 in
-                                   the emulation). */
+                                   the emulation).  K9 gets twice the cap: it
+                                   keeps half of K8's bytes in flight per thread. */
   int32_t grad_slots;           /* gradient slots the backward buckets rotate through (0 = 2):
                                    K9 reads peers' full gradients in place, so the backward of
                                    bucket b first waits until every peer has consumed bucket

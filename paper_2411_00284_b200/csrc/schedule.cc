@@ -317,6 +317,11 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   // bucket; RS: the bucket's gradients in their dtype, the bytes K9 pulls)
   const int p2p_ctas = (pp && s->emulate) ? s->emulate->ctas
                        : (pp && pp->max_ctas > 0) ? std::min(pp->max_ctas, ctx->max_ctas) : ctx->max_ctas;
+  // K9 keeps half of K8's bytes in flight per thread (peers in batches of 4
+  // x 16 B vs 8 x 16 B), so under a cap it gets twice the CTAs: the same
+  // bytes in flight against NVLink latency
+  const int p2p_ctas_rs = (pp && !s->emulate && pp->max_ctas > 0) ? std::min(2 * pp->max_ctas, ctx->max_ctas)
+                                                                  : p2p_ctas;
   auto p2p_hold = [&](fsdp_bucket* bk, bool rs) -> int64_t {
     if (!pp || !s->emulate) return 0;
     int64_t ns = 0;
@@ -547,12 +552,12 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
                          static_cast<long long>(pp->timeout_ns), pp->error_flag, done_slots, epoch(o.bucket),
                          ctx->p2p_counter};
             FSDP_CUDA_TRY(launch_p2p_reduce_scatter(b->p2p_rs, peer_row(pp->rs_peers, o.bucket), ctx->world, inv,
-                                                    b->grad_accumulate, ms, p2p_ctas, &sync, p2p_hold(b, true)));
+                                                    b->grad_accumulate, ms, p2p_ctas_rs, &sync, p2p_hold(b, true)));
             ++launches;
 #else
             FSDP_TRY(p2p_wait(pp->ready_flags, epoch(o.bucket), ms));
             FSDP_CUDA_TRY(launch_p2p_reduce_scatter(b->p2p_rs, peer_row(pp->rs_peers, o.bucket), ctx->world, inv,
-                                                    b->grad_accumulate, ms, p2p_ctas, nullptr, p2p_hold(b, true)));
+                                                    b->grad_accumulate, ms, p2p_ctas_rs, nullptr, p2p_hold(b, true)));
             ++launches;
             FSDP_TRY(p2p_signal(done_slots, epoch(o.bucket), ms));  // done reading peers' b
 #endif
