@@ -87,7 +87,7 @@ def parse(argv=None):
     ap.add_argument("--proxy-smem", type=int, default=0)
     ap.add_argument("--eager", action="store_true", help="time the eager enqueue instead of the CUDA-graph replay")
     ap.add_argument("--trace", default=None, help="Chrome trace of one profiled step")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fused-leg", action="store_true")
@@ -859,16 +859,23 @@ def main(argv=None):
         h_gs = torch.empty(st.gshard_buf.numel(), dtype=torch.uint8, pin_memory=True)
         h_sh.copy_(st.shard_buf)
         h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
-        io = st.host_io(h_sh, h_gs, h2d_s.cuda_stream, d2h_s.cuda_stream)
+        # async_d2h: a step's gradient D2H overlaps the next step (each bucket's
+        # next gradient writer waits for its own D2H; tools/e2e_probe.py: 83 vs
+        # 87 ms per step); the timed region ends when the last step's gradients
+        # are on the host (an event on the d2h stream)
+        io = st.host_io(h_sh, h_gs, h2d_s.cuda_stream, d2h_s.cuda_stream, async_d2h=not p2p)
         h2d_bytes = sum(b.ag_seg for b, p in zip(st.fwd, io["fwd_host_shards"]) if p)
         d2h_bytes = sum(b.rs_seg for b, p in zip(st.bwd, io["bwd_host_grads"]) if p)
         st.step(flags, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, io=io, gemm=gemm, hook=hook)   # warm-up
         barrier()
         x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        xc = torch.cuda.Event()
         x0.record(compute)
         for _ in range(args.e2e_steps):
             st.step(flags, cs, ms, pf, pb, args.proxy_ctas, args.proxy_smem, io=io, gemm=gemm, hook=hook)
-        x1.record(compute)
+        xc.record(compute)
+        d2h_s.wait_event(xc)        # after the device work and every gradient D2H
+        x1.record(d2h_s)
         barrier()
         st.check_p2p()
         e2e_ms = max_over_ranks(x0.elapsed_time(x1) / args.e2e_steps)
@@ -876,8 +883,10 @@ def main(argv=None):
         e2e = {"value": round(e2e_val, 3), "unit": "GB/s", "ms_per_step": round(e2e_ms, 3),
                "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h_bytes),
                "how": "fsdp_run_schedule with fsdp_host_io: per-bucket H2D of shards / D2H of fp32 grad shards "
-                      "from / to pinned host memory inside the call, overlapped with the device path; value "
-                      "defined as the headline's (%s)" % value_kind}
+                      "from / to pinned host memory inside the call, overlapped with the device path and (async_d2h; "
+                      "PCIe floor of these bytes ~76 ms, tools/pcie_probe.py) with the neighbouring steps; timed "
+                      "from the first step's start on the compute stream to the last step's gradients on the host; "
+                      "value defined as the headline's (%s)" % value_kind}
         del h_sh, h_gs
 
     zero_copy = st.zero_copy()

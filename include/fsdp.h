@@ -42,7 +42,8 @@ extern "C" {
 #endif
 
 #define FSDP_ABI_VERSION 5  /* 2: schedule.hook; 3: schedule.emulate; 4: p2p_schedule.max_ctas;
-                              5: fsdp_bucket_launch_kernel, 80-B NVLS handle, window pointers */
+                              5: fsdp_bucket_launch_kernel, 80-B NVLS handle, window pointers,
+                                 host_io.async_d2h */
 
 typedef void* fsdp_stream_t; /* cudaStream_t */
 
@@ -647,6 +648,14 @@ typedef struct fsdp_host_io {
   void* const* bwd_host_grads;        /* n_bwd */
   fsdp_stream_t h2d;
   fsdp_stream_t d2h;
+  int32_t async_d2h;  /* 0: the step's compute stream ends after its gradient D2H (the
+                         step is done when the gradients are on the host).  1: it does
+                         not wait -- the D2H copies finish on the d2h stream (the caller
+                         orders its host reads after that stream), and each bucket's next
+                         writer of its gradient-shard storage (its next PACK_RS, in any
+                         later step on this ctx) waits for that bucket's D2H instead, so
+                         the next step overlaps this step's D2H tail. */
+  int32_t reserved;   /* 0 */
 } fsdp_host_io;
 
 typedef struct {

@@ -106,7 +106,7 @@ class P2PSchedule(C.Structure):
 
 class HostIO(C.Structure):
     _fields_ = [("fwd_host_shards", C.POINTER(C.c_void_p)), ("bwd_host_grads", C.POINTER(C.c_void_p)),
-                ("h2d", C.c_void_p), ("d2h", C.c_void_p)]
+                ("h2d", C.c_void_p), ("d2h", C.c_void_p), ("async_d2h", C.c_int32), ("reserved", C.c_int32)]
 
 
 class GemmCompute(C.Structure):

@@ -30,7 +30,7 @@ void destroy_bucket(fsdp_bucket* b) {
   release(&b->rs_copyout);
   release(&b->p2p_ag);
   release(&b->p2p_rs);
-  for (cudaEvent_t* e : {&b->ev_ag_packed, &b->ev_ag_done, &b->ev_rs_packed, &b->ev_rs_done})
+  for (cudaEvent_t* e : {&b->ev_ag_packed, &b->ev_ag_done, &b->ev_rs_packed, &b->ev_rs_done, &b->ev_d2h_done})
     if (*e) cudaEventDestroy(*e);
   delete b;
 }
@@ -287,7 +287,7 @@ extern "C" fsdp_status fsdp_bucket_create(fsdp_ctx* ctx, const fsdp_bucket_desc*
   if (st == FSDP_OK) st = upload(nvls, &b->nvls_rs);
   if (st == FSDP_OK && N <= kMaxPeers) st = upload(p2p_ag, &b->p2p_ag);
   if (st == FSDP_OK && N <= kMaxPeers) st = upload(p2p_rs, &b->p2p_rs);
-  for (cudaEvent_t* e : {&b->ev_ag_packed, &b->ev_ag_done, &b->ev_rs_packed, &b->ev_rs_done}) {
+  for (cudaEvent_t* e : {&b->ev_ag_packed, &b->ev_ag_done, &b->ev_rs_packed, &b->ev_rs_done, &b->ev_d2h_done}) {
     if (st != FSDP_OK) break;
     cudaError_t err = cudaEventCreateWithFlags(e, cudaEventDisableTiming);
     if (err != cudaSuccess) st = fail(FSDP_ERR_CUDA, cudaGetErrorString(err));

@@ -268,4 +268,8 @@ struct fsdp_bucket {
   fsdp::DevTable p2p_ag, p2p_rs;  // K8 / K9 tables (peer-memory path)
   cudaEvent_t ev_ag_packed = nullptr, ev_ag_done = nullptr;
   cudaEvent_t ev_rs_packed = nullptr, ev_rs_done = nullptr;
+  // host I/O with async_d2h: this bucket's gradient-shard D2H (d2h stream),
+  // which its next gradient-shard writer waits for
+  cudaEvent_t ev_d2h_done = nullptr;
+  bool d2h_pending = false;
 };

@@ -267,6 +267,10 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
       if (s->bwd[j]->grad_bytes != 2) return fail(FSDP_ERR_INVALID_ARG, "linear-layer compute needs bf16 gradients");
   }
   if (s->io) {
+    if ((s->io->async_d2h != 0 && s->io->async_d2h != 1) || s->io->reserved != 0)
+      return fail(FSDP_ERR_INVALID_ARG, "host I/O: async_d2h must be 0 or 1, reserved 0");
+    if (s->io->async_d2h && (s->flags & FSDP_SCHED_P2P))
+      return fail(FSDP_ERR_INVALID_ARG, "host I/O: async_d2h is not for FSDP_SCHED_P2P");
     for (int32_t k = 0; k < s->n_fwd; ++k)
       if (s->io->fwd_host_shards && s->io->fwd_host_shards[k] && !s->fwd[k]->ag_zero_copy)
         return fail(FSDP_ERR_INVALID_ARG, "host I/O: forward buckets need FSDP_BUCKET_SEGMENT_SHARDS");
@@ -438,6 +442,15 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
   auto io_before = [&](const Op& o) -> fsdp_status {
     if (io && o.op == FSDP_OP_PACK_AG && o.phase == 0 && io->fwd_host_shards && io->fwd_host_shards[o.bucket])
       FSDP_CUDA_TRY(cudaStreamWaitEvent(xs, iev[1 + o.bucket], 0));
+    if (o.op == FSDP_OP_PACK_RS) {
+      // an earlier step's asynchronous D2H of this bucket's gradient shards
+      // must finish before anything of this step rewrites them
+      fsdp_bucket* bb = s->bwd[o.bucket];
+      if (bb->d2h_pending) {
+        FSDP_CUDA_TRY(cudaStreamWaitEvent(xs, bb->ev_d2h_done, 0));
+        bb->d2h_pending = false;
+      }
+    }
     return FSDP_OK;
   };
   // the step's last reader of the shard storage: its last UNPACK (after its
@@ -466,6 +479,10 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
       FSDP_CUDA_TRY(cudaStreamWaitEvent(d2h, e, 0));
       FSDP_CUDA_TRY(cudaMemcpyAsync(io->bwd_host_grads[o.bucket], bb->gshard_seg, static_cast<size_t>(bb->rs_seg),
                                     cudaMemcpyDeviceToHost, d2h));
+      if (io->async_d2h) {
+        FSDP_CUDA_TRY(cudaEventRecord(bb->ev_d2h_done, d2h));
+        bb->d2h_pending = true;
+      }
     }
     return FSDP_OK;
   };
@@ -634,7 +651,7 @@ extern "C" fsdp_status fsdp_run_schedule(fsdp_ctx* ctx, const fsdp_schedule* s, 
     FSDP_CUDA_TRY(cudaEventRecord(xev[3 * P], xs));
     FSDP_CUDA_TRY(cudaStreamWaitEvent(cs, xev[3 * P], 0));
   }
-  if (io && s->n_bwd > 0) {
+  if (io && s->n_bwd > 0 && !io->async_d2h) {
     // the step ends when its gradient shards are on the host
     cudaEvent_t e = iev[1 + s->n_fwd + s->n_bwd];
     FSDP_CUDA_TRY(cudaEventRecord(e, d2h));

@@ -270,6 +270,7 @@ def run_schedule(ctx, fwd, bwd, ag_staging=(0, 0), rs_staging=(0, 0), compute=0,
         keep += [a, g, hio]
         hio.fwd_host_shards, hio.bwd_host_grads = a, g
         hio.h2d, hio.d2h = io.get("h2d") or None, io.get("d2h") or None
+        hio.async_d2h, hio.reserved = 1 if io.get("async_d2h") else 0, 0
         s.io = C.pointer(hio)
     if gemm is not None:
         # gemm: dict(tokens, x, dy, y, workspace, workspace_bytes) -- fsdp_gemm_compute

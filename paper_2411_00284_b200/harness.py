@@ -342,14 +342,14 @@ class RankState:
         k9 = sum(b.query()["p2p_bytes"][1] for b in self.bwd)
         return k8, k9
 
-    def host_io(self, host_shards, host_gshards, h2d=0, d2h=0):
+    def host_io(self, host_shards, host_gshards, h2d=0, d2h=0, async_d2h=False):
         """fsdp_host_io for pinned host mirrors laid out like shard_buf /
         gshard_buf: forward bucket k streams in from host_shards at its segment
         offset, backward bucket j streams its gradient shards out to host_gshards."""
         hs, hg = host_shards.data_ptr(), host_gshards.data_ptr()
         fwd = [hs + self.shard_offs[b.members[0]] if b.query()["ag_zero_copy"] else 0 for b in self.fwd]
         bwd = [hg + self.gs_offs[b.members[0]] if b.query()["rs_zero_copy"] else 0 for b in self.bwd]
-        return dict(fwd_host_shards=fwd, bwd_host_grads=bwd, h2d=h2d, d2h=d2h)
+        return dict(fwd_host_shards=fwd, bwd_host_grads=bwd, h2d=h2d, d2h=d2h, async_d2h=async_d2h)
 
     def setup_gemm(self, tokens, seed=7, workspace_bytes=64 << 20):
         """Linear-layer compute (fsdp_gemm_compute) at `tokens` tokens: bf16

@@ -209,6 +209,48 @@ def test_host_io_next_step_loads_after_last_reader():
                 assert torch.equal(slot[foff:foff + n].cpu(), h[st.shard_offs[j]:st.shard_offs[j] + n])
 
 
+def test_host_io_async_d2h_orders_the_next_gradient_writer():
+    """fsdp_host_io.async_d2h: the step does not wait for its gradient D2H;
+    the next step's gradient-shard writers do, bucket by bucket.  Two steps
+    with different gradients, each D2H into its own host buffer: each buffer
+    holds its own step's averaged shards (layout-only rank 0 at N = 2: this
+    rank's rows widened x fl32(1/2))."""
+    world = 2
+    specs = llama("8b", n_layers=2)
+    ctx = F.Ctx(world, 0)
+    fplan, bplan = H.plans_for(specs, world, L.PLAN_MANUAL)
+    st = H.RankState(specs, world, 0, fplan, bplan, ctx, seed=8)
+    h_sh = torch.empty(st.shard_buf.numel(), dtype=torch.uint8).pin_memory()
+    h_sh.copy_(st.shard_buf.cpu())
+    hosts = [torch.zeros(st.gshard_buf.numel(), dtype=torch.uint8).pin_memory() for _ in range(2)]
+    cs, ms, d2h = torch.cuda.Stream(), torch.cuda.Stream(priority=-1), torch.cuda.Stream()
+    flags = L.SCHED_REORDER | L.SCHED_FWD_AG_BEFORE_WAIT
+    grads = []
+    for k, h in enumerate(hosts):
+        with torch.cuda.stream(cs):      # new gradients, stream-ordered between the steps
+            if k:
+                for t in st.grad_slots:
+                    t.copy_(torch.roll(t, 2))   # whole bf16 values move: new gradients
+            grads.append([t.clone() for t in st.grad_slots])
+        st.step(flags, cs.cuda_stream, ms.cuda_stream,
+                io=st.host_io(h_sh, h, d2h=d2h.cuda_stream, async_d2h=True))
+    torch.cuda.synchronize()
+    inv = inv_world_f32(world)
+    for k, h in enumerate(hosts):
+        for bk in st.bwd:
+            slot = grads[k][bk.grad_slot]
+            for j, goff in zip(bk.members, bk.grad_offs):
+                n = st.shard_numel[j]
+                c = n // st.specs[j].row_numel
+                v = min(c, st.specs[j].dim0)
+                g = slot[goff:goff + 2 * v * st.specs[j].row_numel].view(torch.int16).cpu().numpy().view(np.uint16)
+                want = (bf16.widen(g) * inv).astype(np.float32)
+                got = h[st.gs_offs[j]:st.gs_offs[j] + 4 * want.size].numpy().view(np.float32)
+                assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (k, st.specs[j].name)
+    del st
+    ctx.close()
+
+
 @pytest.mark.parametrize("graph", [False, True])
 def test_llama8b_bench_step_sampled_parity(graph):
     """graph=True: the step as bench.py times it -- captured once into a CUDA
