@@ -48,6 +48,21 @@ MUTATIONS = [
     ("cost model floor instead of ceil (G9)", "cost.py",
      "return alpha_ns + -(-(nbytes * beta_fs_per_byte) // 10**6)",
      "return alpha_ns + (nbytes * beta_fs_per_byte) // 10**6"),
+    ("prefetch placed after the wait under BEFORE (Table 6)", "schedule.py",
+     "        s += (pre + wait) if placement == BEFORE else (wait + pre)\n        s.append(_e(0, COMPUTE_F, b))",
+     "        s += (wait + pre)\n        s.append(_e(0, COMPUTE_F, b))"),
+    ("Wr(j-1) after RS(j) (P:191)", "schedule.py",
+     """        if b >= 1:
+            s += [_e(1, WAIT_RS, b - 1), _e(1, COPYOUT_RS, b - 1)]
+        s.append(_e(1, RS, b))""",
+     """        s.append(_e(1, RS, b))
+        if b >= 1:
+            s += [_e(1, WAIT_RS, b - 1), _e(1, COPYOUT_RS, b - 1)]"""),
+    ("a wait does not block the compute stream (S:303)", "sim.py",
+     "            if c > t_cmp:", "            if False:"),
+    ("bf16 narrow truncates instead of RNE (O1)", "bf16.py",
+     "    r = ((u + np.uint64(0x7FFF) + lsb) >> np.uint64(16)).astype(np.uint16)",
+     "    r = (u >> np.uint64(16)).astype(np.uint16)"),
 ]
 
 
