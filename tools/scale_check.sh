@@ -59,3 +59,5 @@ for n in 2 4 8; do
     PORT=$((PORT + 1))
   done
 done
+python tools/scale_summary.py $O > $O/scale_summary.md
+echo "summary: $O/scale_summary.md"
