@@ -105,6 +105,9 @@ def parse(argv=None):
     ap.add_argument("--same-device", action="store_true",
                     help="TEST ONLY: every rank on cuda:0 (multi-process p2p path on one GPU; timings meaningless)")
     ap.add_argument("--dist", action="store_true", help="the N>1 code path at --gpus 1 (world 1, real communicator)")
+    ap.add_argument("--n-rank-legs-at-world1", action="store_true",
+                    help="TEST ONLY (with --dist): also run the N > 1 legs (block busbw, alpha/beta sweep, exposure, "
+                         "NVLS) at world 1, to exercise their code with a real communicator on one GPU")
     ap.add_argument("--nccl-register", default="none", choices=["none", "local", "symmetric"])
     ap.add_argument("--p2p-max-ctas", type=int, default=-1)
     ap.add_argument("--p2p-transport", default="ipc", choices=["ipc", "window"],
@@ -967,7 +970,7 @@ def main(argv=None):
 
     # ---- N > 1: isolated 8B-block busbw, alpha / beta fit, measured exposure
     busbw_block = alpha_beta = exposure = nvls_block = None
-    if multi and world > 1 and not quick:
+    if multi and (world > 1 or args.n_rank_legs_at_world1) and not quick:
         from workloads.shapes import ParamSpec
         kw = dict(p2p=p2p, exchange=exchange, max_over_ranks=max_over_ranks, windows=args.p2p_transport == "window")
         block = [p for p in llama("8b", n_layers=1, with_embeddings=False)]

@@ -83,7 +83,8 @@ def test_bench_distributed_path_world1(collective):
     s.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"),
-           "--gpus", "1", "--dist", "--collective", collective, "--steps", "3", "--warmup", "3"]
+           "--gpus", "1", "--dist", "--collective", collective, "--steps", "3", "--warmup", "3",
+           "--n-rank-legs-at-world1", "--exposure-tokens", "256"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
@@ -91,6 +92,11 @@ def test_bench_distributed_path_world1(collective):
     assert line["value_kind"] == "hbm"       # world 1: no bus
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
     assert line["parity"]["ok"], line["parity"]
+    # the N > 1 legs' code with a real communicator (world 1: bus fractions are 0)
+    assert line["busbw_block"]["ag_ms"] > 0 and line["alpha_beta"]["source"].startswith("measured")
+    assert len(line["alpha_beta"]["rows"]) == 10 and len(line["exposure"]["variants"]) == 3
+    nv = line["nvls_block"]
+    assert "unavailable" in nv or nv["parity"]["ok"], nv
     if collective == "nccl":
         assert line["collectives"]["ag_ms_per_step"] > 0
         assert line["nccl_info"] is not None and any("NCCL" in x for x in line["nccl_info"]["lines"])
