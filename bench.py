@@ -963,6 +963,8 @@ def main(argv=None):
     if p2p and multi:
         barrier()
         st.close_ipc()
+        barrier()                    # every rank closed its mappings of ours
+        st.free_ipc()
     st.close_nccl_mem()
     del st
     gc.collect()
@@ -1310,6 +1312,8 @@ def exposure_leg(args, specs, world, rank, ctx, cs, ms, compute, p2p, exchange, 
         barrier()
         if p2p:
             vst.close_ipc()
+            barrier()                # every rank closed its mappings of ours
+            vst.free_ipc()
         vst.close_nccl_mem()
         del vst
         gc.collect()

@@ -308,9 +308,19 @@ class RankState:
         self._nccl_ptrs = []
 
     def close_ipc(self):
+        """Closes this rank's mappings of the peers' buffers.  Its own exported
+        buffers stay until free_ipc -- call that only after EVERY rank has
+        closed its mappings (a barrier between the two)."""
         for p in getattr(self, "_opened", []):
             F.ipc_close(p)
         self._opened = []
+
+    def free_ipc(self):
+        """Frees this rank's IPC-exported buffers (shard storage, gradient
+        slots, flags); their torch views must not be used afterwards."""
+        for p in self._ipc_ptrs:
+            F.ipc_free(p)
+        self._ipc_ptrs = []
 
     def _p2p_tables(self, shard_base, grad_base):
         W = self.world
@@ -585,8 +595,12 @@ def time_bucket_collectives(specs, world, rank, ctx, compute, comm, reps=20, war
             t_ag, t_rs = max_over_ranks(t_ag), max_over_ranks(t_rs)
         return dict(ag_bytes=world * st.fwd[0].ag_seg, rs_bytes=world * st.bwd[0].rs_seg, ag_ns=t_ag, rs_ns=t_rs)
     finally:
+        torch.cuda.synchronize()
         if p2p:
             st.close_ipc()
+            if exchange is not None and world > 1:
+                exchange(None)          # every rank closed its mappings of ours
+            st.free_ipc()
         st.close_nccl_mem()
         del st
         torch.cuda.empty_cache()
