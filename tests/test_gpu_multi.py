@@ -51,17 +51,17 @@ def _torchrun(script_args, timeout=1500, n=None):
     return subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
 
 
-def _bench(extra, n=None):
+def _bench(extra, n=None, e2e=False):
     n = n or N
     r = _torchrun([os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--layers", "2", "--steps", "3",
-                   "--warmup", "3", "--no-e2e", "--exposure-tokens", "512"] + extra, n=n)
+                   "--warmup", "3", "--exposure-tokens", "512"] + ([] if e2e else ["--no-e2e"]) + extra, n=n)
     assert r.returncode == 0, r.stderr[-4000:]
     return json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
 
 
 @pytest.mark.parametrize("n", WORLDS)
 def test_nccl_path_parity_and_measurements(n):
-    line = _bench([], n)
+    line = _bench([], n, e2e=n == 2)      # host I/O (async D2H) over real NCCL once
     par = line["parity"]
     assert par["ok"], par
     assert par["ag"]["bit_exact"] and par["ag"]["elements"] > 0
@@ -77,6 +77,8 @@ def test_nccl_path_parity_and_measurements(n):
     assert line["nccl_info"] and line["nccl_info"]["lines"]
     nv = line["nvls_block"]
     assert "unavailable" in nv or (nv["parity"]["ok"] and nv["busbw_GBps"] > 0), nv
+    if n == 2:
+        assert line["e2e"]["ms_per_step"] > 0
 
 
 @pytest.mark.parametrize("n", WORLDS)
