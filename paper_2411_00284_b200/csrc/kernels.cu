@@ -62,6 +62,9 @@
 #ifndef FSDP_K9_MIN_BLOCKS
 #define FSDP_K9_MIN_BLOCKS FSDP_MIN_BLOCKS
 #endif
+#ifndef FSDP_PDL
+#define FSDP_PDL 1  // K0-K6: programmatic dependent launch (launch overlaps the previous kernel's tail)
+#endif
 #ifndef FSDP_PROXY_WAVES
 #define FSDP_PROXY_WAVES 16  // K7: short CTAs per (SM x ctas_per_sm) slot
 #endif
@@ -501,23 +504,40 @@ __device__ __forceinline__ void run_table_bulk(const Chunk* __restrict__ tab, in
 #define FSDP_LSU_BOUNDS __launch_bounds__(kThreads, FSDP_MIN_BLOCKS)
 
 // K0: full parameter -> padded shard (absolute -> absolute).
+// Programmatic dependent launch (launched with programmaticStreamSerialization,
+// launch_table): every CTA first waits until the kernels it depends on have
+// completed and their writes are visible (griddepcontrol.wait), then lets the
+// next kernel of the stream start launching (griddepcontrol.launch_dependents)
+// -- once every CTA of this grid is resident the next grid's CTAs fill the
+// SM slots this one's tail frees, instead of after a launch gap.
+__device__ __forceinline__ void pdl_enter() {
+#if FSDP_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 __global__ void FSDP_LSU_BOUNDS fsdp_shard_kernel(const Chunk* tab, int n, char* base, float s) {
+  pdl_enter();
   run_table<false, false>(tab, n, base, s);
 }
 // K1: shards -> segment `rank` of the AG staging buffer (absolute -> staging).
 __global__ void FSDP_LSU_BOUNDS fsdp_ag_pack_kernel(const Chunk* tab, int n, char* base, float s) {
+  pdl_enter();
   run_table<false, true>(tab, n, base, s);
 }
 // K3: gathered staging -> full parameters (staging -> absolute).
 __global__ void FSDP_LSU_BOUNDS fsdp_ag_unpack_kernel(const Chunk* tab, int n, char* base, float s) {
+  pdl_enter();
   run_table<true, false>(tab, n, base, s);
 }
 // K4: full gradients -> fp32 rank-major chunks * fl32(1/N) (absolute -> staging).
 __global__ void FSDP_LSU_BOUNDS fsdp_rs_pack_kernel(const Chunk* tab, int n, char* base, float s) {
+  pdl_enter();
   run_table<false, true>(tab, n, base, s);
 }
 // K6: own reduce-scatter segment -> fp32 gradient shards (staging -> absolute).
 __global__ void FSDP_LSU_BOUNDS fsdp_rs_copyout_kernel(const Chunk* tab, int n, char* base, float s) {
+  pdl_enter();
   run_table<true, false>(tab, n, base, s);
 }
 
@@ -911,13 +931,27 @@ cudaError_t launch_table(KernelKind kind, const DevTable& t, char* base, float s
     return cudaGetLastError();
   }
   const int grid = t.n < max_ctas ? t.n : max_ctas;
+  void (*fn)(const Chunk*, int, char*, float) = nullptr;
   switch (kind) {
-    case KK_SHARD: fsdp_shard_kernel<<<grid, kThreads, 0, s>>>(t.d, t.n, base, scale); break;
-    case KK_AG_PACK: fsdp_ag_pack_kernel<<<grid, kThreads, 0, s>>>(t.d, t.n, base, scale); break;
-    case KK_AG_UNPACK: fsdp_ag_unpack_kernel<<<grid, kThreads, 0, s>>>(t.d, t.n, base, scale); break;
-    case KK_RS_PACK: fsdp_rs_pack_kernel<<<grid, kThreads, 0, s>>>(t.d, t.n, base, scale); break;
-    case KK_RS_COPYOUT: fsdp_rs_copyout_kernel<<<grid, kThreads, 0, s>>>(t.d, t.n, base, scale); break;
+    case KK_SHARD: fn = fsdp_shard_kernel; break;
+    case KK_AG_PACK: fn = fsdp_ag_pack_kernel; break;
+    case KK_AG_UNPACK: fn = fsdp_ag_unpack_kernel; break;
+    case KK_RS_PACK: fn = fsdp_rs_pack_kernel; break;
+    case KK_RS_COPYOUT: fn = fsdp_rs_copyout_kernel; break;
   }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = FSDP_PDL ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const Chunk* tab = t.d;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, fn, tab, t.n, base, scale);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
