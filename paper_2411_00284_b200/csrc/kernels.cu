@@ -737,6 +737,7 @@ __device__ __forceinline__ void run_peer_reduce(const Chunk* __restrict__ tab, i
 // K8: fused all-gather + copy-out over peer memory.
 __global__ void FSDP_LSU_BOUNDS fsdp_p2p_allgather_kernel(const Chunk* tab, int n, const __grid_constant__ PeerTable pt,
                                                           long long hold_ns) {
+  pdl_enter();
   const unsigned long long t0 = hold_ns > 0 ? global_ns() : 0ull;
   run_peer_copy(tab, n, pt);
   hold_until(t0, hold_ns);
@@ -783,6 +784,7 @@ __device__ __forceinline__ void store_flags(const PeerTable& slots, int world, u
 __global__ void __launch_bounds__(kThreads, FSDP_K9_MIN_BLOCKS) fsdp_p2p_reduce_scatter_kernel(
     const Chunk* tab, int n, const __grid_constant__ PeerTable pt, int world, float scale, int accum,
     const __grid_constant__ P2PSync sync, long long hold_ns) {
+  pdl_enter();
   if (sync.counter) {
     if (threadIdx.x < 32) wait_flags(sync.wait_flags, world, sync.wait_value, sync.timeout_ns, sync.err);
     __syncthreads();
@@ -909,6 +911,21 @@ cudaError_t launch_bulk(KernelKind kind, K kernel, int grid, const DevTable& t, 
 }
 }  // namespace
 
+// Launch configuration of the PDL kernels (kThreads threads, no dynamic smem,
+// programmatic stream serialization when FSDP_PDL); `attr` is the caller's storage.
+static cudaLaunchConfig_t pdl_config(int grid, cudaStream_t s, cudaLaunchAttribute (&attr)[1]) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = FSDP_PDL ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
 cudaError_t launch_table(KernelKind kind, const DevTable& t, char* base, float scale, cudaStream_t s,
                          int max_ctas) {
   if (t.n == 0) return cudaSuccess;
@@ -939,16 +956,8 @@ cudaError_t launch_table(KernelKind kind, const DevTable& t, char* base, float s
     case KK_RS_PACK: fn = fsdp_rs_pack_kernel; break;
     case KK_RS_COPYOUT: fn = fsdp_rs_copyout_kernel; break;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = FSDP_PDL ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cudaLaunchConfig_t cfg = pdl_config(grid, s, attr);
   const Chunk* tab = t.d;
   cudaError_t e = cudaLaunchKernelEx(&cfg, fn, tab, t.n, base, scale);
   if (e != cudaSuccess) return e;
@@ -959,7 +968,12 @@ cudaError_t launch_p2p_allgather(const DevTable& t, const PeerTable& pt, cudaStr
                                  int64_t hold_ns) {
   if (t.n == 0) return cudaSuccess;
   (void)cudaGetLastError();
-  fsdp_p2p_allgather_kernel<<<t.n < max_ctas ? t.n : max_ctas, kThreads, 0, s>>>(t.d, t.n, pt, hold_ns);
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = pdl_config(t.n < max_ctas ? t.n : max_ctas, s, attr);
+  const Chunk* tab = t.d;
+  const long long hold = hold_ns;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, fsdp_p2p_allgather_kernel, tab, t.n, pt, hold);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -971,8 +985,14 @@ cudaError_t launch_p2p_reduce_scatter(const DevTable& t, const PeerTable& pt, in
   (void)cudaGetLastError();
   // a fused handshake needs >= 1 CTA even for an empty table
   const int grid = t.n == 0 ? 1 : (t.n < max_ctas ? t.n : max_ctas);
-  fsdp_p2p_reduce_scatter_kernel<<<grid, kThreads, 0, s>>>(t.d, t.n, pt, world, scale, accumulate ? 1 : 0,
-                                                           sync ? *sync : none, hold_ns);
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = pdl_config(grid, s, attr);
+  const Chunk* tab = t.d;
+  const int acc = accumulate ? 1 : 0;
+  const P2PSync sy = sync ? *sync : none;
+  const long long hold = hold_ns;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, fsdp_p2p_reduce_scatter_kernel, tab, t.n, pt, world, scale, acc, sy, hold);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
