@@ -2,7 +2,7 @@
 # Validates tools/plan_search.py plans on one B200: the N = 8 step predicted
 # from MEASURED op durations (bench.py's `predicted`) for the manual, greedy
 # (Algorithm 1) and searched plans at T = 1024 / 2048 / 4096 tokens per GPU.
-B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-fused-leg --no-gemm-comparison --no-e2e --no-variants"
+B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-fused-leg --no-gemm-comparison --no-e2e --no-variants --emulate"
 for T in 1024 2048 4096; do
   for v in "manual:--plan manual" "greedy:--plan greedy" "search:--plan-file profiles/r01_plan_search_T$T.json"; do
     name=${v%%:*}; flags=${v#*:}
