@@ -48,3 +48,14 @@ def test_product_never_imports_oracle():
         for f in files:
             if f.endswith(".py"):
                 assert not pat.search(open(os.path.join(dirpath, f)).read()), f
+
+
+def test_reference_arm_multi_gpu_unit():
+    """--impl reference at N > 1 states its value in the multi-GPU headline's
+    unit (bus bytes), at N = 1 in HBM bytes -- the same definitions as ours."""
+    for gpus, kind in (("2", "bus"), ("1", "hbm")):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", gpus,
+                            "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+        assert r.returncode == 0, r.stderr[-2000:]
+        d = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+        assert d["value_kind"] == kind and d["value"] > 0 and d["config"]["world"] == (8 if gpus == "1" else 2)
